@@ -1,0 +1,202 @@
+/*
+ * copris_b200.h — C-ABI of the B200-native CoPRIS IS-corrected loss path.
+ *
+ * Drop-in boundary for the reference's loss entry points
+ * (/root/reference/proj/include/copris). The reference is header-only C++ with
+ * no FFI of its own; each entry point below names the reference function it
+ * replaces. All pointers are caller-owned DEVICE buffers unless a parameter
+ * says "host". `stream` is a cudaStream_t passed as void* (NULL = legacy
+ * default stream). No call allocates on the hot path and no call falls back to
+ * the CPU: every compute entry point launches sm_100a kernels or fails.
+ *
+ * Status: every call returns COPRIS_OK (0) or an error code; the message is in
+ * copris_last_error() (thread-local). COPRIS_E_CONTRACT / COPRIS_E_CONFIG carry
+ * the reference's exception type (ContractViolation / ConfigError,
+ * common.hpp:9-18) and its fixed message. Conditions only the device can see
+ * (token outside the vocabulary, non-finite log-prob) are latched in a device
+ * error word and reported by copris_ctx_check().
+ *
+ * Packed batch layout: trajectories are concatenated in
+ * batch order (groups in batch order, members ascending traj_id,
+ * rollout.hpp:75-95); token t of the packed batch is row t of the logits.
+ *   tok_off[n_traj+1]  int64   token offsets of trajectories
+ *   group_off[P+1]     int64   trajectory offsets of prompt groups
+ *   target[T]          int32   generated token ids
+ *   stage[T]           uint32  policy version of the segment holding token t
+ *   buffered_lp[T]     f32     concat_segments() values (trajectory.hpp:69-75)
+ *   tok_traj[T]        int32   trajectory index of token t
+ *   adv[n_traj]        f64     group-relative advantages
+ */
+#ifndef COPRIS_B200_H
+#define COPRIS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define COPRIS_B200_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define COPRIS_API __attribute__((visibility("default")))
+#else
+#define COPRIS_API
+#endif
+
+enum copris_status {
+  COPRIS_OK = 0,
+  COPRIS_E_CONTRACT = 1, /* copris::ContractViolation */
+  COPRIS_E_CONFIG = 2,   /* copris::ConfigError */
+  COPRIS_E_CUDA = 3,     /* CUDA runtime / launch failure */
+  COPRIS_E_INVALID = 4   /* malformed call (null pointer, bad dtype, ...) */
+};
+
+enum copris_dtype { COPRIS_BF16 = 0, COPRIS_F32 = 1 };
+
+/* Source of the behaviour log-prob of CURRENT-stage tokens when IS is on.
+ * RECOMPUTED (default): the recomputed current log-prob, which the reference's
+ *   sampler records bit-identically (test_policy.cpp:157-172), so the ratio of
+ *   every current-stage token is exactly 1 (acceptance C3).
+ * RECORDED: buffered_lp for every token, i.e. concat_segments() verbatim. */
+enum copris_behav_mode { COPRIS_BEHAV_RECOMPUTED = 0, COPRIS_BEHAV_RECORDED = 1 };
+
+/* bits of the per-token flags byte */
+enum { COPRIS_FLAG_STALE = 1, COPRIS_FLAG_CLIPPED = 2 };
+
+typedef struct copris_ctx copris_ctx;
+
+COPRIS_API int copris_abi_version(void);
+COPRIS_API const char* copris_last_error(void);
+
+/* Context: device binding, SM count, device error word and reduction scratch.
+ * Re-entrant: one context per (thread, device) or shared under the caller's
+ * lock; no global mutable state (SURVEY.md §8(b) Threading). */
+COPRIS_API int copris_ctx_create(int device, copris_ctx** out);
+COPRIS_API int copris_ctx_destroy(copris_ctx* ctx);
+/* Synchronises `stream`, then reports and clears the device error word. */
+COPRIS_API int copris_ctx_check(copris_ctx* ctx, void* stream);
+
+/* ---- K1: streaming log-softmax + gather ------------------------------------
+ * Replaces sequence_logprobs (policy.hpp:160-173) over packed rows:
+ *   out_lp[t] = z[t][target[t]] - logsumexp(z[t]),  out_lse[t] = logsumexp(z[t]).
+ * Rows are logits + r*ld for r in [0,n_tok); target/out indexed by r.
+ * out_lse may be NULL. Token outside [0,vocab) -> device error
+ * "token out of vocabulary" (policy.hpp:169). */
+COPRIS_API int copris_logprob_gather(copris_ctx* ctx, const void* logits, int64_t ld, int32_t dtype,
+                          const int32_t* target, int64_t n_tok, int32_t vocab, float* out_lp,
+                          float* out_lse, void* stream);
+
+/* ---- K2: segmented cross-stage behaviour concat -----------------------------
+ * copris_expand_segments: per-token stage ids from segment tables
+ *   (segments in packed order; seg_off[n_seg+1] token offsets, seg_ver[n_seg]).
+ * copris_behaviour_concat replaces concat_segments (trajectory.hpp:69-75) and
+ *   the IS-off substitution (trainer.hpp:149):
+ *   behav[t] = is_enabled ? (stage[t] < cur_stage || mode == RECORDED
+ *                            ? buffered_lp[t] : cur_lp[t]) : cur_lp[t]
+ *   Bit-exact (a select, no arithmetic). out_flags (optional) gets
+ *   COPRIS_FLAG_STALE where stage[t] < cur_stage (rollout.hpp:105). */
+COPRIS_API int copris_expand_segments(copris_ctx* ctx, const int64_t* seg_off, const uint32_t* seg_ver,
+                           int64_t n_seg, uint32_t* out_stage, void* stream);
+COPRIS_API int copris_behaviour_concat(copris_ctx* ctx, const uint32_t* stage, uint32_t cur_stage,
+                            const float* buffered_lp, const float* cur_lp, int32_t is_enabled,
+                            int32_t behav_mode, int64_t n_tok, float* out_behav,
+                            uint8_t* out_flags, void* stream);
+
+/* ---- K3a: rewards and group-normalised advantages ---------------------------
+ * copris_terminal_rewards replaces terminal_reward (grpo.hpp:35-47);
+ * copris_group_advantages replaces compute_advantages (grpo.hpp:51-65) for all
+ *   groups at once: adv = (R - mean) / (population std + adv_epsilon), fp64.
+ *   A group with fewer than 2 members -> COPRIS_E_CONFIG
+ *   "advantage group size must be >= 2" (checked on the host from group_off,
+ *   which is therefore a HOST array here).
+ * copris_token_traj expands tok_off (device array) into the per-token
+ *   trajectory index tok_traj[T]. */
+COPRIS_API int copris_terminal_rewards(copris_ctx* ctx, const int32_t* tokens, const int64_t* tok_off,
+                            int64_t n_traj, const uint8_t* terminated,
+                            const int32_t* answer_target, int32_t eos_token, double* out_reward,
+                            void* stream);
+COPRIS_API int copris_group_advantages(copris_ctx* ctx, const double* rewards,
+                            const int64_t* group_off_host, const int64_t* group_off,
+                            int64_t n_groups, double adv_epsilon, double* out_adv, void* stream);
+COPRIS_API int copris_token_traj(copris_ctx* ctx, const int64_t* tok_off, int64_t n_traj, int64_t n_tok,
+                      int32_t* out_tok_traj, void* stream);
+
+/* ---- K3: the IS-corrected clipped GRPO loss and its logit gradient ----------
+ * One call processes a CHUNK of n_rows packed rows whose packed token indices
+ * are [row_base, row_base + n_rows): logits/dlogits are chunk-local (row r at
+ * ptr + r*ld), every per-token array is indexed by the packed index. Per token
+ * (grpo.hpp:147-181, policy.hpp:180-196):
+ *   r = exp(cur - behav); c = clamp(r, 1-clip_low, 1+clip_high)
+ *   u = r*A, v = c*A; u <= v ? (obj = u, w = r*A) : (obj = v, w = 0, clipped)
+ *   kl:      d = ref - cur; obj -= kl*(e^d - d - 1); w += kl*(e^d - 1)
+ *   entropy: obj += c_H * H
+ *   dlogits[k] = coef*(1[k=y] - p_k) [+ (c_H/T) p_k (log p_k + H)], coef = -w/T
+ * with T = cfg.total_tokens (the GLOBAL token count, grpo.hpp:135). The loss
+ * is -sum(obj)/T, reduced by copris_loss_reduce (+ an allreduce when sharded).
+ */
+typedef struct {
+  const void* logits;        /* [n_rows x ld] chunk */
+  int64_t ld;                /* elements between rows (>= vocab) */
+  int32_t logits_dtype;      /* copris_dtype */
+  int32_t vocab;
+  int64_t n_rows;
+  int64_t row_base;          /* packed index of chunk row 0 */
+  const int32_t* target;     /* [T] */
+  const uint32_t* stage;     /* [T] */
+  const float* buffered_lp;  /* [T] */
+  const float* ref_lp;       /* [T]; required iff kl_coeff > 0 */
+  const int32_t* tok_traj;   /* [T] */
+  const double* adv;         /* [n_traj] */
+  uint32_t cur_stage;        /* rollout_version of the batch */
+  uint32_t _pad;
+} copris_loss_batch;
+
+typedef struct {
+  double clip_low, clip_high, kl_coeff, entropy_coeff; /* ClipConfig, grpo.hpp:15-28 */
+  int32_t is_enabled;        /* RunConfig::is_enabled, trainer.hpp:23 */
+  int32_t behav_mode;        /* copris_behav_mode */
+  int64_t total_tokens;      /* global T for the 1/T token-mean */
+} copris_loss_cfg;
+
+typedef struct {
+  void* dlogits;             /* [n_rows x ld_dlogits] chunk, or NULL (no backward) */
+  int64_t ld_dlogits;
+  int32_t dlogits_dtype;     /* copris_dtype */
+  int32_t _pad;
+  float* cur_lp;             /* [T] required */
+  float* lse;                /* [T] optional */
+  float* behav;              /* [T] optional */
+  double* obj;               /* [T] required: per-token objective */
+  double* coef;              /* [T] optional: dlogits row scale -w/T */
+  uint8_t* flags;            /* [T] required: COPRIS_FLAG_* */
+} copris_loss_out;
+
+/* Fused single pass: log-softmax+gather, behaviour select, ratio/clip/KL/
+ * entropy, and dlogits from ONE read of each logits row (rows held in shared
+ * memory across a 2-CTA cluster at large vocab, TMA bulk loads). */
+COPRIS_API int copris_is_loss_fused(copris_ctx* ctx, const copris_loss_batch* batch,
+                         const copris_loss_cfg* cfg, const copris_loss_out* out, void* stream);
+
+/* Unfused K3: consumes cur_lp/lse (K1) and behav (K2) and streams the logits
+ * a second time to write dlogits. Same per-token arithmetic as the fused path;
+ * out->cur_lp/lse/behav are ignored (the inputs are passed explicitly). */
+COPRIS_API int copris_is_loss_bwd(copris_ctx* ctx, const copris_loss_batch* batch,
+                       const copris_loss_cfg* cfg, const float* cur_lp, const float* lse,
+                       const float* behav, const copris_loss_out* out, void* stream);
+
+/* Deterministic fixed-order reduction of the per-token outputs:
+ * out4[0] = sum obj (fp64), out4[1] = tokens, out4[2] = stale tokens
+ * (rollout.hpp:99-110), out4[3] = clipped tokens. out4 is a DEVICE f64[4]. */
+COPRIS_API int copris_loss_reduce(copris_ctx* ctx, const double* obj, const uint8_t* flags, int64_t n_tok,
+                       double* out4, void* stream);
+
+/* Introspection (not a reference entry point): cluster size, grid and kernel
+ * name of the last copris_is_loss_* launch on this context. */
+COPRIS_API int copris_ctx_last_launch(const copris_ctx* ctx, int* cluster, int* grid, int* num_sms,
+                           const char** kernel_name);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* COPRIS_B200_H */

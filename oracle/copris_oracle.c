@@ -51,14 +51,15 @@ int oracle_logprob_gather(const double* logits, int64_t ld, const int32_t* targe
 }
 
 void oracle_behaviour(const uint32_t* stage, uint32_t cur_stage, const double* buffered_lp,
-                      const double* cur_lp, int is_enabled, int64_t n_tok, double* out_behav,
-                      int64_t* out_stale) {
+                      const double* cur_lp, int is_enabled, int behav_mode, int64_t n_tok,
+                      double* out_behav, int64_t* out_stale) {
   int64_t stale = 0;
   for (int64_t t = 0; t < n_tok; ++t) {
     int old = stage[t] < cur_stage; /* rollout.hpp:105 */
     stale += old;
-    /* trajectory.hpp:69-75 + trainer.hpp:149 (IS off -> current_lp) */
-    out_behav[t] = (is_enabled && old) ? buffered_lp[t] : cur_lp[t];
+    /* trajectory.hpp:69-75 + trainer.hpp:149 (IS off -> current_lp). Mode 1
+     * (recorded) is concat_segments verbatim for every token. */
+    out_behav[t] = (is_enabled && (old || behav_mode == 1)) ? buffered_lp[t] : cur_lp[t];
   }
   if (out_stale) *out_stale = stale;
 }
@@ -124,8 +125,8 @@ int oracle_is_loss(const oracle_batch* b, const oracle_clip_cfg* cfg, oracle_res
   int rc = oracle_logprob_gather(b->logits, b->ld, b->target, total, V, cur);
   if (rc) goto done;
   int64_t stale = 0;
-  oracle_behaviour(b->stage, b->cur_stage, b->buffered_lp, cur, cfg->is_enabled, total, behav,
-                   &stale);
+  oracle_behaviour(b->stage, b->cur_stage, b->buffered_lp, cur, cfg->is_enabled, cfg->behav_mode,
+                   total, behav, &stale);
 
   const double inv_t = 1.0 / (double)total; /* grpo.hpp:135 */
   if (out->dlogits) memset(out->dlogits, 0, sizeof(double) * (size_t)total * (size_t)V);
@@ -153,16 +154,14 @@ int oracle_is_loss(const oracle_batch* b, const oracle_clip_cfg* cfg, oracle_res
         objective += clipped;
         bind = 1;
       }
+      if (out->obj) out->obj[t] = bind ? clipped : unclipped;
       n_clipped += bind;
       if (out->clipped) out->clipped[t] = (uint8_t)bind;
       if (cfg->kl_coeff > 0.0) { /* grpo.hpp:158-162 */
-        if (!isfinite(b->ref_lp[t])) {
-          rc = fail(ORACLE_E_CONTRACT, "kl_lowvar requires finite log-probs");
-          goto done;
-        }
         double d = b->ref_lp[t] - cur[t];
         objective -= cfg->kl_coeff * (exp(d) - d - 1.0);
         w[t] += cfg->kl_coeff * (exp(d) - 1.0);
+        if (out->obj) out->obj[t] -= cfg->kl_coeff * (exp(d) - d - 1.0);
       }
     }
     /* policy.hpp:180-196 with scale = -inv_t (grpo.hpp:166-167) */
@@ -182,6 +181,7 @@ int oracle_is_loss(const oracle_batch* b, const oracle_clip_cfg* cfg, oracle_res
         double h = 0.0;
         for (int32_t k = 0; k < V; ++k) h -= probs[k] * log(probs[k]);
         objective += cfg->entropy_coeff * h;
+        if (out->obj) out->obj[t] += cfg->entropy_coeff * h;
         if (out->dlogits) {
           double* g = out->dlogits + t * (int64_t)V;
           for (int32_t k = 0; k < V; ++k) {

@@ -41,10 +41,11 @@ int oracle_logprob_gather(const double* logits, int64_t ld, const int32_t* targe
 
 /* trajectory.hpp:69-75 (concat_segments) + trainer.hpp:149 (IS off) expressed
  * per token: behav[t] = (is_enabled && stage[t] < cur_stage) ? buffered_lp[t]
- * : cur_lp[t]. Counts stale tokens as rollout.hpp:99-110 does. */
+ * : cur_lp[t] (behav_mode 0); behav_mode 1 takes buffered_lp for every token
+ * when IS is on. Counts stale tokens as rollout.hpp:99-110 does. */
 void oracle_behaviour(const uint32_t* stage, uint32_t cur_stage, const double* buffered_lp,
-                      const double* cur_lp, int is_enabled, int64_t n_tok, double* out_behav,
-                      int64_t* out_stale);
+                      const double* cur_lp, int is_enabled, int behav_mode, int64_t n_tok,
+                      double* out_behav, int64_t* out_stale);
 
 /* grpo.hpp:51-65 (compute_advantages), applied group by group. Groups are
  * trajectory ranges [group_off[g], group_off[g+1]). G<2 -> ORACLE_E_CONFIG. */
@@ -59,6 +60,7 @@ int oracle_terminal_rewards(const int32_t* tokens, const int64_t* tok_off, int64
 typedef struct {
   double clip_low, clip_high, kl_coeff, entropy_coeff;
   int is_enabled;
+  int behav_mode; /* 0: current-stage tokens use the recomputed lp; 1: recorded */
 } oracle_clip_cfg;
 
 typedef struct {
@@ -84,6 +86,7 @@ typedef struct {
   double* behav;     /* [n_tok] or NULL */
   double* weight;    /* [n_tok] or NULL: w_t of grpo.hpp:150-162 */
   uint8_t* clipped;  /* [n_tok] or NULL: 1 where the clamp branch binds */
+  double* obj;       /* [n_tok] or NULL: the token's objective terms (clip - KL + entropy) */
   int64_t stale_tokens;
   int64_t clipped_tokens;
 } oracle_result;

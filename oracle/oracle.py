@@ -65,12 +65,13 @@ class _oracle_batch(C.Structure):
 
 class _oracle_cfg(C.Structure):
     _fields_ = [("clip_low", D), ("clip_high", D), ("kl_coeff", D), ("entropy_coeff", D),
-                ("is_enabled", C.c_int)]
+                ("is_enabled", C.c_int), ("behav_mode", C.c_int)]
 
 
 class _oracle_result(C.Structure):
     _fields_ = [("loss", D), ("objective", D), ("dlogits", P), ("cur_lp", P), ("behav", P),
-                ("weight", P), ("clipped", P), ("stale_tokens", I64), ("clipped_tokens", I64)]
+                ("weight", P), ("clipped", P), ("obj", P), ("stale_tokens", I64),
+                ("clipped_tokens", I64)]
 
 
 @dataclass
@@ -82,6 +83,7 @@ class LossResult:
     behav: np.ndarray | None = None
     weight: np.ndarray | None = None
     clipped: np.ndarray | None = None
+    obj: np.ndarray | None = None
     stale_tokens: int = 0
     clipped_tokens: int = 0
     seconds: float = 0.0
@@ -102,7 +104,7 @@ class Oracle:
         L = self.lib
         L.oracle_last_error.restype = C.c_char_p
         L.oracle_logprob_gather.argtypes = [P, I64, P, I64, I32, P]
-        L.oracle_behaviour.argtypes = [P, U32, P, P, C.c_int, I64, P, P]
+        L.oracle_behaviour.argtypes = [P, U32, P, P, C.c_int, C.c_int, I64, P, P]
         L.oracle_behaviour.restype = None
         L.oracle_advantages.argtypes = [P, P, I64, D, P]
         L.oracle_terminal_rewards.argtypes = [P, P, I64, P, P, I32, P]
@@ -121,13 +123,14 @@ class Oracle:
         self._check(self.lib.oracle_logprob_gather(_ptr(logits), v, _ptr(target), n, v, _ptr(out)))
         return out
 
-    def behaviour(self, stage, cur_stage, buffered_lp, cur_lp, is_enabled=True):
+    def behaviour(self, stage, cur_stage, buffered_lp, cur_lp, is_enabled=True, behav_mode=0):
         stage = np.ascontiguousarray(stage, dtype=np.uint32)
         buffered_lp, cur_lp = _f64(buffered_lp), _f64(cur_lp)
         out = np.zeros(len(stage), np.float64)
         stale = C.c_int64(0)
         self.lib.oracle_behaviour(_ptr(stage), cur_stage, _ptr(buffered_lp), _ptr(cur_lp),
-                                  int(is_enabled), len(stage), _ptr(out), C.byref(stale))
+                                  int(is_enabled), behav_mode, len(stage), _ptr(out),
+                                  C.byref(stale))
         return out, stale.value
 
     def advantages(self, rewards, group_off, adv_epsilon=1e-6):
@@ -151,7 +154,7 @@ class Oracle:
 
     def is_loss(self, logits, tok_off, target, stage, cur_stage, buffered_lp, adv,
                 clip_low=0.2, clip_high=0.28, kl_coeff=0.0, entropy_coeff=0.0,
-                is_enabled=True, ref_lp=None, want_dlogits=True) -> LossResult:
+                is_enabled=True, ref_lp=None, want_dlogits=True, behav_mode=0) -> LossResult:
         logits = _f64(logits)
         n, v = logits.shape
         tok_off = np.ascontiguousarray(tok_off, dtype=np.int64)
@@ -160,15 +163,16 @@ class Oracle:
         buffered_lp, adv, ref_lp = _f64(buffered_lp), _f64(adv), _f64(ref_lp)
         b = _oracle_batch(_ptr(logits), v, v, n, len(tok_off) - 1, _ptr(tok_off), _ptr(target),
                           _ptr(stage), cur_stage, _ptr(buffered_lp), _ptr(ref_lp), _ptr(adv))
-        cfg = _oracle_cfg(clip_low, clip_high, kl_coeff, entropy_coeff, int(is_enabled))
+        cfg = _oracle_cfg(clip_low, clip_high, kl_coeff, entropy_coeff, int(is_enabled), behav_mode)
         res = LossResult(0.0)
         res.dlogits = np.zeros((n, v), np.float64) if want_dlogits else None
         res.cur_lp = np.zeros(n, np.float64)
         res.behav = np.zeros(n, np.float64)
         res.weight = np.zeros(n, np.float64)
         res.clipped = np.zeros(n, np.uint8)
+        res.obj = np.zeros(n, np.float64)
         out = _oracle_result(0.0, 0.0, _ptr(res.dlogits), _ptr(res.cur_lp), _ptr(res.behav),
-                             _ptr(res.weight), _ptr(res.clipped), 0, 0)
+                             _ptr(res.weight), _ptr(res.clipped), _ptr(res.obj), 0, 0)
         self._check(self.lib.oracle_is_loss(C.byref(b), C.byref(cfg), C.byref(out)))
         res.loss, res.objective = out.loss, out.objective
         res.stale_tokens, res.clipped_tokens = out.stale_tokens, out.clipped_tokens

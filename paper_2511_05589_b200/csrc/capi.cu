@@ -1,0 +1,326 @@
+// capi.cu — the C-ABI (include/copris_b200.h): argument validation with the
+// reference's exception semantics, context/device handling and dispatch to the
+// sm_100a kernels in kernels.cu. No CPU compute path exists behind any entry.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <string>
+
+#include "../../include/copris_b200.h"
+#include "kernels.cuh"
+
+using namespace copris_b200;
+
+struct copris_ctx {
+  int device;
+  int num_sms;
+  uint32_t* d_err;   // device error word (kernels.cuh ERR_*)
+  void* d_scratch;   // reduction scratch
+  LaunchInfo last;   // what the last loss launch did (introspection)
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(COPRIS_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+// Makes ctx->device current for the call and restores the caller's device.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+bool valid_dtype(int32_t d) { return d == COPRIS_BF16 || d == COPRIS_F32; }
+
+// grpo.hpp:120-133 / trainer.hpp:21-48 style validation shared by the loss
+// entry points. Returns COPRIS_OK or an error with the reference's message.
+int validate_loss(const copris_ctx* ctx, const copris_loss_batch* b, const copris_loss_cfg* c,
+                  const copris_loss_out* o) {
+  if (!ctx || !b || !c || !o) return fail(COPRIS_E_INVALID, "null argument");
+  if (c->total_tokens <= 0) return fail(COPRIS_E_CONFIG, "grpo_step_loss batch has no tokens");
+  if (c->clip_low <= 0.0 || c->clip_high <= 0.0)  // grpo.hpp:21-22
+    return fail(COPRIS_E_CONFIG, "grpo.clip_low and grpo.clip_high must be > 0");
+  if (c->kl_coeff < 0.0) return fail(COPRIS_E_CONFIG, "grpo.kl_coeff must be >= 0");
+  if (c->kl_coeff > 0.0 && !b->ref_lp)  // grpo.hpp:126-127
+    return fail(COPRIS_E_CONTRACT, "reference log-probs required when kl_coeff > 0");
+  if (c->behav_mode != COPRIS_BEHAV_RECOMPUTED && c->behav_mode != COPRIS_BEHAV_RECORDED)
+    return fail(COPRIS_E_INVALID, "behav_mode must be COPRIS_BEHAV_RECOMPUTED or _RECORDED");
+  if (b->n_rows < 0 || b->row_base < 0) return fail(COPRIS_E_INVALID, "negative row range");
+  if (b->row_base + b->n_rows > c->total_tokens)
+    return fail(COPRIS_E_CONTRACT, "log-prob vectors must align with token count");
+  if (b->n_rows == 0) return COPRIS_OK;
+  if (b->vocab < 1) return fail(COPRIS_E_CONFIG, "policy.vocab must leave room for answer tokens plus EOS");
+  if (b->ld < b->vocab) return fail(COPRIS_E_INVALID, "ld must be >= vocab");
+  if (!valid_dtype(b->logits_dtype)) return fail(COPRIS_E_INVALID, "unknown logits dtype");
+  if (!b->logits || !b->target || !b->stage || !b->buffered_lp || !b->tok_traj || !b->adv)
+    return fail(COPRIS_E_INVALID, "null batch pointer");
+  if (!o->obj || !o->flags) return fail(COPRIS_E_INVALID, "null output pointer (obj/flags)");
+  if (o->dlogits) {
+    if (!valid_dtype(o->dlogits_dtype)) return fail(COPRIS_E_INVALID, "unknown dlogits dtype");
+    if (o->ld_dlogits < b->vocab) return fail(COPRIS_E_INVALID, "ld_dlogits must be >= vocab");
+  }
+  return COPRIS_OK;
+}
+
+LossParams make_params(const copris_ctx* ctx, const copris_loss_batch* b, const copris_loss_cfg* c,
+                       const copris_loss_out* o) {
+  LossParams p{};
+  p.logits = b->logits;
+  p.ld = b->ld;
+  p.vocab = b->vocab;
+  p.cur_stage = static_cast<int32_t>(b->cur_stage);
+  p.n_rows = b->n_rows;
+  p.row_base = b->row_base;
+  p.target = b->target;
+  p.stage = b->stage;
+  p.buffered_lp = b->buffered_lp;
+  p.ref_lp = c->kl_coeff > 0.0 ? b->ref_lp : nullptr;
+  p.tok_traj = b->tok_traj;
+  p.adv = b->adv;
+  p.clamp_lo = 1.0 - c->clip_low;   // grpo.hpp:149 bounds, same fp64 ops
+  p.clamp_hi = 1.0 + c->clip_high;
+  p.kl_coeff = c->kl_coeff;
+  p.entropy_coeff = c->entropy_coeff;
+  p.inv_t = 1.0 / static_cast<double>(c->total_tokens);  // grpo.hpp:135
+  p.is_enabled = c->is_enabled;
+  p.behav_mode = c->behav_mode;
+  p.dlogits = o->dlogits;
+  p.ld_d = o->ld_dlogits;
+  p.cur_lp = o->cur_lp;
+  p.lse = o->lse;
+  p.behav = o->behav;
+  p.obj = o->obj;
+  p.coef = o->coef;
+  p.flags = o->flags;
+  p.err = ctx->d_err;
+  return p;
+}
+
+DType dt(int32_t d) { return d == COPRIS_BF16 ? DType::BF16 : DType::F32; }
+
+}  // namespace
+
+extern "C" {
+
+int copris_abi_version(void) { return COPRIS_B200_ABI_VERSION; }
+
+const char* copris_last_error(void) { return g_err.c_str(); }
+
+int copris_ctx_create(int device, copris_ctx** out) {
+  if (!out) return fail(COPRIS_E_INVALID, "null out");
+  *out = nullptr;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+  if (device < 0 || device >= n) return fail(COPRIS_E_INVALID, "device out of range");
+  DeviceGuard g(device);
+  cudaDeviceProp prop{};
+  e = cudaGetDeviceProperties(&prop, device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceProperties");
+  if (prop.major != 10)
+    return fail(COPRIS_E_CUDA, "copris_b200 kernels are built for sm_100a (Blackwell B200)");
+  auto* ctx = new copris_ctx{};
+  ctx->device = device;
+  ctx->num_sms = prop.multiProcessorCount;
+  e = cudaMalloc(&ctx->d_err, sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMemset(ctx->d_err, 0, sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->d_scratch, reduce_scratch_bytes());
+  if (e == cudaSuccess) e = cudaMemset(ctx->d_scratch, 0, reduce_scratch_bytes());
+  if (e != cudaSuccess) {
+    cudaFree(ctx->d_err);
+    cudaFree(ctx->d_scratch);
+    delete ctx;
+    return cuda_fail(e, "copris_ctx_create");
+  }
+  *out = ctx;
+  return COPRIS_OK;
+}
+
+int copris_ctx_destroy(copris_ctx* ctx) {
+  if (!ctx) return COPRIS_OK;
+  DeviceGuard g(ctx->device);
+  cudaFree(ctx->d_err);
+  cudaFree(ctx->d_scratch);
+  delete ctx;
+  return COPRIS_OK;
+}
+
+int copris_ctx_check(copris_ctx* ctx, void* stream) {
+  if (!ctx) return fail(COPRIS_E_INVALID, "null ctx");
+  DeviceGuard g(ctx->device);
+  cudaError_t e = cudaStreamSynchronize(as_stream(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+  uint32_t err = 0;
+  e = cudaMemcpy(&err, ctx->d_err, sizeof(err), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, "read error word");
+  if (err == 0) return COPRIS_OK;
+  cudaMemset(ctx->d_err, 0, sizeof(uint32_t));
+  if (err & ERR_TOKEN_OOV) return fail(COPRIS_E_CONTRACT, "token out of vocabulary");
+  if (err & ERR_NONFINITE_ADV) return fail(COPRIS_E_CONTRACT, "advantage must be finite");
+  if (err & ERR_NONFINITE_LP) return fail(COPRIS_E_CONTRACT, "token_ratio requires finite log-probs");
+  if (err & ERR_NOT_TERMINATED)
+    return fail(COPRIS_E_CONTRACT, "terminal_reward requires a terminated trajectory");
+  return fail(COPRIS_E_CUDA, "unknown device error");
+}
+
+int copris_logprob_gather(copris_ctx* ctx, const void* logits, int64_t ld, int32_t dtype,
+                          const int32_t* target, int64_t n_tok, int32_t vocab, float* out_lp,
+                          float* out_lse, void* stream) {
+  if (!ctx) return fail(COPRIS_E_INVALID, "null ctx");
+  if (n_tok < 0) return fail(COPRIS_E_INVALID, "negative n_tok");
+  if (n_tok == 0) return COPRIS_OK;  // test_policy.cpp:151-155
+  if (!logits || !target || !out_lp) return fail(COPRIS_E_INVALID, "null pointer");
+  if (!valid_dtype(dtype)) return fail(COPRIS_E_INVALID, "unknown logits dtype");
+  if (vocab < 1 || ld < vocab) return fail(COPRIS_E_INVALID, "bad vocab/ld");
+  DeviceGuard g(ctx->device);
+  cudaError_t e = launch_logprob_gather(logits, ld, dt(dtype), target, n_tok, vocab, out_lp,
+                                        out_lse, ctx->d_err, ctx->num_sms, as_stream(stream));
+  return e == cudaSuccess ? COPRIS_OK : cuda_fail(e, "logprob_gather launch");
+}
+
+int copris_expand_segments(copris_ctx* ctx, const int64_t* seg_off, const uint32_t* seg_ver,
+                           int64_t n_seg, uint32_t* out_stage, void* stream) {
+  if (!ctx) return fail(COPRIS_E_INVALID, "null ctx");
+  if (n_seg < 0) return fail(COPRIS_E_INVALID, "negative n_seg");
+  if (n_seg == 0) return COPRIS_OK;
+  if (!seg_off || !seg_ver || !out_stage) return fail(COPRIS_E_INVALID, "null pointer");
+  DeviceGuard g(ctx->device);
+  cudaError_t e = launch_expand_segments(seg_off, seg_ver, n_seg, out_stage, as_stream(stream));
+  return e == cudaSuccess ? COPRIS_OK : cuda_fail(e, "expand_segments launch");
+}
+
+int copris_behaviour_concat(copris_ctx* ctx, const uint32_t* stage, uint32_t cur_stage,
+                            const float* buffered_lp, const float* cur_lp, int32_t is_enabled,
+                            int32_t behav_mode, int64_t n_tok, float* out_behav,
+                            uint8_t* out_flags, void* stream) {
+  if (!ctx) return fail(COPRIS_E_INVALID, "null ctx");
+  if (n_tok < 0) return fail(COPRIS_E_INVALID, "negative n_tok");
+  if (n_tok == 0) return COPRIS_OK;
+  if (!stage || !buffered_lp || !cur_lp || !out_behav) return fail(COPRIS_E_INVALID, "null pointer");
+  if (behav_mode != COPRIS_BEHAV_RECOMPUTED && behav_mode != COPRIS_BEHAV_RECORDED)
+    return fail(COPRIS_E_INVALID, "behav_mode must be COPRIS_BEHAV_RECOMPUTED or _RECORDED");
+  DeviceGuard g(ctx->device);
+  cudaError_t e = launch_behaviour(stage, cur_stage, buffered_lp, cur_lp, is_enabled, behav_mode,
+                                   n_tok, out_behav, out_flags, as_stream(stream));
+  return e == cudaSuccess ? COPRIS_OK : cuda_fail(e, "behaviour_concat launch");
+}
+
+int copris_terminal_rewards(copris_ctx* ctx, const int32_t* tokens, const int64_t* tok_off,
+                            int64_t n_traj, const uint8_t* terminated,
+                            const int32_t* answer_target, int32_t eos_token, double* out_reward,
+                            void* stream) {
+  if (!ctx) return fail(COPRIS_E_INVALID, "null ctx");
+  if (n_traj < 0) return fail(COPRIS_E_INVALID, "negative n_traj");
+  if (n_traj == 0) return COPRIS_OK;
+  if (!tokens || !tok_off || !terminated || !answer_target || !out_reward)
+    return fail(COPRIS_E_INVALID, "null pointer");
+  DeviceGuard g(ctx->device);
+  cudaError_t e = launch_terminal_rewards(tokens, tok_off, n_traj, terminated, answer_target,
+                                          eos_token, out_reward, ctx->d_err, as_stream(stream));
+  return e == cudaSuccess ? COPRIS_OK : cuda_fail(e, "terminal_rewards launch");
+}
+
+int copris_group_advantages(copris_ctx* ctx, const double* rewards,
+                            const int64_t* group_off_host, const int64_t* group_off,
+                            int64_t n_groups, double adv_epsilon, double* out_adv, void* stream) {
+  if (!ctx) return fail(COPRIS_E_INVALID, "null ctx");
+  if (n_groups < 0) return fail(COPRIS_E_INVALID, "negative n_groups");
+  if (n_groups == 0) return COPRIS_OK;
+  if (!rewards || !group_off_host || !group_off || !out_adv)
+    return fail(COPRIS_E_INVALID, "null pointer");
+  if (!(adv_epsilon > 0.0)) return fail(COPRIS_E_CONFIG, "grpo.adv_epsilon must be > 0");
+  for (int64_t g = 0; g < n_groups; ++g)  // grpo.hpp:54
+    if (group_off_host[g + 1] - group_off_host[g] < 2)
+      return fail(COPRIS_E_CONFIG, "advantage group size must be >= 2");
+  DeviceGuard g(ctx->device);
+  cudaError_t e = launch_group_advantages(rewards, group_off, n_groups, adv_epsilon, out_adv,
+                                          as_stream(stream));
+  return e == cudaSuccess ? COPRIS_OK : cuda_fail(e, "group_advantages launch");
+}
+
+int copris_token_traj(copris_ctx* ctx, const int64_t* tok_off, int64_t n_traj, int64_t n_tok,
+                      int32_t* out_tok_traj, void* stream) {
+  if (!ctx) return fail(COPRIS_E_INVALID, "null ctx");
+  if (n_traj < 0 || n_tok < 0) return fail(COPRIS_E_INVALID, "negative size");
+  if (n_traj == 0 || n_tok == 0) return COPRIS_OK;
+  if (!tok_off || !out_tok_traj) return fail(COPRIS_E_INVALID, "null pointer");
+  DeviceGuard g(ctx->device);
+  cudaError_t e = launch_token_traj(tok_off, n_traj, out_tok_traj, as_stream(stream));
+  return e == cudaSuccess ? COPRIS_OK : cuda_fail(e, "token_traj launch");
+}
+
+int copris_is_loss_fused(copris_ctx* ctx, const copris_loss_batch* batch,
+                         const copris_loss_cfg* cfg, const copris_loss_out* out, void* stream) {
+  int rc = validate_loss(ctx, batch, cfg, out);
+  if (rc) return rc;
+  if (!out->cur_lp) return fail(COPRIS_E_INVALID, "null output pointer (cur_lp)");
+  if (batch->n_rows == 0) return COPRIS_OK;
+  DeviceGuard g(ctx->device);
+  LossParams p = make_params(ctx, batch, cfg, out);
+  cudaError_t e = launch_fused(p, dt(batch->logits_dtype), dt(out->dlogits_dtype), ctx->num_sms,
+                               as_stream(stream), &ctx->last);
+  return e == cudaSuccess ? COPRIS_OK : cuda_fail(e, "is_loss_fused launch");
+}
+
+int copris_is_loss_bwd(copris_ctx* ctx, const copris_loss_batch* batch,
+                       const copris_loss_cfg* cfg, const float* cur_lp, const float* lse,
+                       const float* behav, const copris_loss_out* out, void* stream) {
+  int rc = validate_loss(ctx, batch, cfg, out);
+  if (rc) return rc;
+  if (!cur_lp || !lse || !behav) return fail(COPRIS_E_INVALID, "null cur_lp/lse/behav input");
+  if (batch->n_rows == 0) return COPRIS_OK;
+  DeviceGuard g(ctx->device);
+  LossParams p = make_params(ctx, batch, cfg, out);
+  p.in_cur_lp = cur_lp;
+  p.in_lse = lse;
+  p.in_behav = behav;
+  p.cur_lp = nullptr;
+  p.lse = nullptr;
+  p.behav = nullptr;
+  cudaError_t e = launch_bwd(p, dt(batch->logits_dtype), dt(out->dlogits_dtype), ctx->num_sms,
+                             as_stream(stream), &ctx->last);
+  return e == cudaSuccess ? COPRIS_OK : cuda_fail(e, "is_loss_bwd launch");
+}
+
+int copris_loss_reduce(copris_ctx* ctx, const double* obj, const uint8_t* flags, int64_t n_tok,
+                       double* out4, void* stream) {
+  if (!ctx) return fail(COPRIS_E_INVALID, "null ctx");
+  if (n_tok < 0) return fail(COPRIS_E_INVALID, "negative n_tok");
+  if (!out4 || (n_tok > 0 && (!obj || !flags))) return fail(COPRIS_E_INVALID, "null pointer");
+  DeviceGuard g(ctx->device);
+  cudaError_t e = launch_reduce(obj, flags, n_tok, out4, ctx->d_scratch, ctx->num_sms,
+                                as_stream(stream));
+  return e == cudaSuccess ? COPRIS_OK : cuda_fail(e, "loss_reduce launch");
+}
+
+/* Introspection (not part of the reference surface): what the last loss
+ * launch on this context ran. kernel_name is a static string. */
+int copris_ctx_last_launch(const copris_ctx* ctx, int* cluster, int* grid, int* num_sms,
+                           const char** kernel_name) {
+  if (!ctx) return fail(COPRIS_E_INVALID, "null ctx");
+  if (cluster) *cluster = ctx->last.cluster;
+  if (grid) *grid = ctx->last.grid;
+  if (num_sms) *num_sms = ctx->num_sms;
+  if (kernel_name) *kernel_name = ctx->last.kernel ? ctx->last.kernel : "";
+  return COPRIS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,100 @@
+// kernels.cuh — device-side parameter blocks and host launchers for the
+// sm_100a kernels of the IS-corrected loss path. Launchers return a
+// cudaError_t; argument validation and error mapping live in capi.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace copris_b200 {
+
+// Bits of the device error word (copris_ctx_check maps them to the
+// reference's exception messages).
+enum : uint32_t {
+  ERR_TOKEN_OOV = 1u,        // policy.hpp:169 "token out of vocabulary"
+  ERR_NONFINITE_LP = 2u,     // grpo.hpp:69-70 "token_ratio requires finite log-probs"
+  ERR_NONFINITE_ADV = 4u,    // grpo.hpp:128 "advantage must be finite"
+  ERR_NOT_TERMINATED = 8u,   // grpo.hpp:36 "terminal_reward requires a terminated trajectory"
+};
+
+// Everything one loss launch needs, by value (kernel parameter space).
+struct LossParams {
+  // batch
+  const void* logits;
+  int64_t ld;
+  int32_t vocab;
+  int32_t cur_stage;
+  int64_t n_rows;
+  int64_t row_base;
+  const int32_t* target;
+  const uint32_t* stage;
+  const float* buffered_lp;
+  const float* ref_lp;
+  const int32_t* tok_traj;
+  const double* adv;
+  // unfused-K3 inputs (nullptr in the fused kernel)
+  const float* in_cur_lp;
+  const float* in_lse;
+  const float* in_behav;
+  // cfg (grpo.hpp:15-28, 135)
+  double clamp_lo;   // 1 - clip_low
+  double clamp_hi;   // 1 + clip_high
+  double kl_coeff;
+  double entropy_coeff;
+  double inv_t;      // 1 / T_global
+  int32_t is_enabled;
+  int32_t behav_mode;
+  // out
+  void* dlogits;
+  int64_t ld_d;
+  float* cur_lp;
+  float* lse;
+  float* behav;
+  double* obj;
+  double* coef;
+  uint8_t* flags;
+  uint32_t* err;
+};
+
+enum class DType : int { BF16 = 0, F32 = 1 };
+
+struct LaunchInfo {
+  int num_sms;
+  int cluster;       // CTAs per row chosen by the dispatcher (fused TMA path)
+  int grid;          // CTAs launched
+  const char* kernel;
+};
+
+// Fused single-pass loss. Chooses the TMA/cluster kernel when rows are 16-byte
+// aligned, otherwise the generic kernel.
+cudaError_t launch_fused(const LossParams& p, DType in, DType out, int num_sms,
+                         cudaStream_t stream, LaunchInfo* info);
+// Unfused K3 (second logits pass from lse).
+cudaError_t launch_bwd(const LossParams& p, DType in, DType out, int num_sms,
+                       cudaStream_t stream, LaunchInfo* info);
+// K1.
+cudaError_t launch_logprob_gather(const void* logits, int64_t ld, DType in, const int32_t* target,
+                                  int64_t n_tok, int32_t vocab, float* out_lp, float* out_lse,
+                                  uint32_t* err, int num_sms, cudaStream_t stream);
+// K2.
+cudaError_t launch_expand_segments(const int64_t* seg_off, const uint32_t* seg_ver, int64_t n_seg,
+                                   uint32_t* out_stage, cudaStream_t stream);
+cudaError_t launch_behaviour(const uint32_t* stage, uint32_t cur_stage, const float* blp,
+                             const float* cur_lp, int is_enabled, int behav_mode, int64_t n_tok,
+                             float* out_behav, uint8_t* out_flags, cudaStream_t stream);
+// K3a and helpers.
+cudaError_t launch_terminal_rewards(const int32_t* tokens, const int64_t* tok_off, int64_t n_traj,
+                                    const uint8_t* terminated, const int32_t* answer_target,
+                                    int32_t eos, double* out, uint32_t* err, cudaStream_t stream);
+cudaError_t launch_group_advantages(const double* rewards, const int64_t* group_off,
+                                    int64_t n_groups, double eps, double* out_adv,
+                                    cudaStream_t stream);
+cudaError_t launch_token_traj(const int64_t* tok_off, int64_t n_traj, int32_t* out,
+                              cudaStream_t stream);
+// Deterministic reduction; scratch holds >= reduce_scratch_bytes() bytes.
+size_t reduce_scratch_bytes();
+cudaError_t launch_reduce(const double* obj, const uint8_t* flags, int64_t n_tok, double* out4,
+                          void* scratch, int num_sms, cudaStream_t stream);
+
+}  // namespace copris_b200

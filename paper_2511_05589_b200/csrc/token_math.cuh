@@ -1,0 +1,153 @@
+// token_math.cuh — per-token scalar semantics shared by every loss kernel, so
+// the fused, generic and unfused paths agree on branch selection and rounding.
+//
+// Restates grpo.hpp:147-181 (ratio, asymmetric clip, KL, entropy objective)
+// and the scale of policy.hpp:180-196 for ONE token, in fp64, with the
+// reference's operation order. The V-length work stays in the kernels.
+#pragma once
+
+#include <cstdint>
+
+#include "kernels.cuh"
+
+namespace copris_b200 {
+
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr double kLog2eD = 1.4426950408889634;
+
+enum : uint8_t { FLAG_STALE = 1, FLAG_CLIPPED = 2 };
+
+// trajectory.hpp:69-75 (concat_segments) + trainer.hpp:149 (IS off) for one
+// token. A select, never arithmetic: bit-exact by construction.
+__device__ __forceinline__ float select_behaviour(uint32_t stage, uint32_t cur_stage, float blp,
+                                                  float cur, int is_enabled, int behav_mode) {
+  return (is_enabled && (stage < cur_stage || behav_mode == 1)) ? blp : cur;
+}
+
+struct TokenResult {
+  double obj;    // this token's objective contribution
+  double coef;   // dlogits row scale: -w/T (policy.hpp:188 with scale -inv_t)
+  uint8_t flags;
+  uint32_t err;
+};
+
+// grpo.hpp:147-162 (+ 170-171 when `ent`): cur/beh are the f32 log-probs,
+// H the row entropy in nats (only read when ent).
+__device__ __forceinline__ TokenResult token_objective(const LossParams& P, float cur, float beh,
+                                                       double adv, float ref, bool stale,
+                                                       double H, bool ent) {
+  TokenResult r{0.0, 0.0, static_cast<uint8_t>(stale ? FLAG_STALE : 0), 0u};
+  if (!isfinite(adv)) {
+    r.err = ERR_NONFINITE_ADV;
+    return r;
+  }
+  const double c = cur, b = beh;
+  if (!isfinite(c) || !isfinite(b)) {  // grpo.hpp:69-70 token_ratio
+    r.err = ERR_NONFINITE_LP;
+    return r;
+  }
+  const double ratio = exp(__dadd_rn(c, -b));
+  // std::clamp(ratio, 1 - clip_low, 1 + clip_high), grpo.hpp:149
+  const double clamped = ratio < P.clamp_lo ? P.clamp_lo : (P.clamp_hi < ratio ? P.clamp_hi : ratio);
+  const double unclipped = __dmul_rn(ratio, adv);
+  const double clipped = __dmul_rn(clamped, adv);
+  double obj, w = 0.0;
+  if (unclipped <= clipped) {  // ties take the unclipped branch (grpo.hpp:152)
+    obj = unclipped;
+    w = __dmul_rn(ratio, adv);
+  } else {
+    obj = clipped;  // binding clamp: zero gradient
+    r.flags |= FLAG_CLIPPED;
+  }
+  if (P.kl_coeff > 0.0) {  // grpo.hpp:158-162
+    const double d = __dadd_rn(static_cast<double>(ref), -c);
+    const double ed = exp(d);
+    obj = __dadd_rn(obj, -__dmul_rn(P.kl_coeff, __dadd_rn(__dadd_rn(ed, -d), -1.0)));
+    w = __dadd_rn(w, __dmul_rn(P.kl_coeff, __dadd_rn(ed, -1.0)));
+  }
+  if (ent) obj = __dadd_rn(obj, __dmul_rn(P.entropy_coeff, H));
+  r.obj = obj;
+  r.coef = __dmul_rn(-P.inv_t, w);
+  return r;
+}
+
+// log-prob and log-sum-exp of one row from the online state (m, s excluding
+// the target column) and the target logit: S = s + e^(z_y - m),
+// lse = m + ln S, cur = (z_y - m) - ln S. fp64 for the O(1) scalar part.
+struct LogProb {
+  float cur;
+  double lse;
+  double ln_s;
+  double S;
+};
+
+__device__ __forceinline__ LogProb finish_logprob(float M, float s_excl, float zy, bool ok) {
+  LogProb r;
+  const double dz = static_cast<double>(zy) - static_cast<double>(M);
+  r.S = static_cast<double>(s_excl) + (ok ? exp(dz) : 0.0);
+  r.ln_s = log(r.S);
+  r.lse = static_cast<double>(M) + r.ln_s;
+  r.cur = ok ? static_cast<float>(dz - r.ln_s) : __int_as_float(0x7fc00000);
+  return r;
+}
+
+// Values pass C of a row needs, broadcast from the scalar phase.
+struct RowBroadcast {
+  float coef;    // dlogits scale of the one-hot/softmax term
+  float dy;      // dlogits of the target column: coef * (1 - p_y)
+  float m;       // row max (pass-B frame)
+  float log2s;   // log2(sum exp(z - m))
+  int32_t y;     // target column
+  float eg;      // entropy gradient scale c_H/T (0 when off or on error)
+  float k0;      // H - ln(S): log p + H = (z - m) + k0
+};
+
+// The scalar phase of one row: given the row's (max, sum exp(z-m), sum
+// exp(z-m)(z-m)) and the target logit, produce cur_lp, behaviour, objective and
+// the dlogits coefficients; write the per-token outputs when `write`.
+template <bool ENT, typename LseT>
+__device__ __forceinline__ RowBroadcast row_scalar_phase(const LossParams& P, int64_t t, int32_t y,
+                                                         uint32_t st, float blp, float rl,
+                                                         double adv, const LseT& tot, float zy,
+                                                         bool write) {
+  const bool oov = static_cast<uint32_t>(y) >= static_cast<uint32_t>(P.vocab);
+  const float M = tot.m;
+  const LogProb lp = finish_logprob(M, tot.s, zy, !oov);
+  const double ln_s = lp.ln_s, lse = lp.lse;
+  const float cur = lp.cur;
+  const bool stale = st < static_cast<uint32_t>(P.cur_stage);
+  const float beh = select_behaviour(st, static_cast<uint32_t>(P.cur_stage), blp, cur, P.is_enabled,
+                                     P.behav_mode);
+  double H = 0.0;
+  if (ENT) H = ln_s - static_cast<double>(tot.u) / static_cast<double>(tot.a);
+  TokenResult tr;
+  if (oov) {
+    tr = TokenResult{0.0, 0.0, static_cast<uint8_t>(stale ? FLAG_STALE : 0), ERR_TOKEN_OOV};
+  } else {
+    tr = token_objective(P, cur, beh, adv, rl, stale, H, ENT);
+  }
+  if (tr.err) {
+    atomicOr(P.err, tr.err);
+    tr.obj = 0.0;
+    tr.coef = 0.0;
+  }
+  if (write) {
+    P.cur_lp[t] = cur;
+    if (P.lse) P.lse[t] = static_cast<float>(lse);
+    if (P.behav) P.behav[t] = beh;
+    P.obj[t] = tr.obj;
+    if (P.coef) P.coef[t] = tr.coef;
+    P.flags[t] = tr.flags;
+  }
+  RowBroadcast b;
+  b.coef = static_cast<float>(tr.coef);
+  b.dy = tr.err ? 0.f : static_cast<float>(tr.coef * -expm1(static_cast<double>(cur)));  // coef*(1-p_y)
+  b.m = M;
+  b.log2s = static_cast<float>(ln_s * kLog2eD);
+  b.y = y;
+  b.eg = (ENT && !tr.err) ? static_cast<float>(P.inv_t * P.entropy_coeff) : 0.f;
+  b.k0 = ENT ? static_cast<float>(H - ln_s) : 0.f;
+  return b;
+}
+
+}  // namespace copris_b200

@@ -1,0 +1,250 @@
+"""GPU parity: the sm_100a path, called through the C-ABI, against the CPU
+oracle (oracle/copris_oracle.c, itself pinned to the reference) on the same
+seeded inputs. Tolerances: tests/parity_util.py."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from parity_util import Case, assert_rows_close, assert_scalar_close, exact_dlogits
+
+pytestmark = pytest.mark.gpu
+
+BF16, F32 = torch.bfloat16, torch.float32
+
+
+def run(ctx, case, dl_dtype=BF16, fused=True, **kw):
+    batch = case.upload(ctx)
+    return case, ctx.grpo_step_loss(case.logits_gpu(), batch, case.clip(), is_enabled=case.is_enabled,
+                                    behav_mode=case.behav_mode, fused=fused,
+                                    dlogits_dtype=dl_dtype, coef=True, **kw)
+
+
+# (V, logits dtype, expected kernel, expected cluster)
+SHAPES = [
+    (151936, BF16, "fused_tma_kernel", 2),   # Qwen2.5 vocab: row split over a CTA pair
+    (32000, BF16, "fused_tma_kernel", 1),    # 64 KB rows: 8-warp CTAs, several per SM
+    (80000, BF16, "fused_tma_kernel", 1),    # 160 KB rows: one 16-warp CTA per row
+    (151936, F32, "fused_tma_kernel", 4),    # 608 KB f32 rows: 4-CTA cluster
+    (32000, F32, "fused_tma_kernel", 1),
+    (256, BF16, "fused_tma_kernel", 1),
+    (4099, BF16, "fused_generic_kernel", 1),  # odd vocab: unaligned rows
+    (100, F32, "fused_generic_kernel", 1),
+    (6, F32, "fused_generic_kernel", 1),      # desk vocab
+]
+
+
+@pytest.mark.parametrize("V,dtype,kernel,cluster", SHAPES)
+@pytest.mark.parametrize("dl_dtype", [BF16, F32])
+def test_fused_matches_oracle(ctx, oracle, V, dtype, kernel, cluster, dl_dtype):
+    P, G = (2, 4) if V > 50000 else (4, 4)
+    case = Case(oracle, seed=V % 97 + 3, P=P, G=G, V=V, dtype=dtype, mu=math.log(10), lmax=24)
+    _, res = run(ctx, case, dl_dtype)
+    info = ctx.last_launch()
+    assert info["kernel"] == kernel and info["cluster"] == cluster, info
+    case.check(res, dl_dtype, what=f"V={V} {dtype}->{dl_dtype}")
+
+
+@pytest.mark.parametrize("V,dtype", [(151936, BF16), (32000, BF16), (4099, BF16), (32000, F32)])
+def test_unfused_matches_oracle(ctx, oracle, V, dtype):
+    case = Case(oracle, seed=11, P=2, G=4, V=V, dtype=dtype, mu=math.log(10), lmax=24)
+    _, res = run(ctx, case, F32, fused=False)
+    assert ctx.last_launch()["kernel"] == "bwd_kernel"
+    case.check(res, F32, what=f"unfused V={V}")
+
+
+@pytest.mark.parametrize("V", [151936, 32000, 4099])
+def test_kl_and_entropy(ctx, oracle, V):
+    case = Case(oracle, seed=5, P=2, G=4, V=V, mu=math.log(10), lmax=24, kl_coeff=0.1,
+                entropy_coeff=0.01)
+    for fused in (True, False):
+        _, res = run(ctx, case, F32, fused=fused)
+        case.check(res, F32, what=f"kl+entropy V={V} fused={fused}")
+
+
+def test_is_off_every_ratio_is_one(ctx, oracle):
+    """trainer.hpp:149 / acceptance C3: with IS off the behaviour IS the
+    recomputed log-prob, bit for bit, so every ratio is exactly 1."""
+    case = Case(oracle, seed=7, P=2, G=4, V=32000, is_enabled=False, stale_prob=1.0)
+    _, res = run(ctx, case, F32)
+    cur, beh = res.cur_lp.cpu().numpy(), res.behav.cpu().numpy()
+    np.testing.assert_array_equal(cur.view(np.uint32), beh.view(np.uint32))
+    assert res.clipped_tokens == 0
+    case.check(res, F32, what="IS off")
+
+
+def test_current_stage_ratio_exactly_one(ctx, oracle):
+    """Current-stage tokens take the recomputed log-prob (RECOMPUTED mode),
+    stale tokens their buffered one; the select is bit-exact."""
+    case = Case(oracle, seed=8, P=4, G=4, V=32000, stages=(2, 4), stale_prob=1.0)
+    _, res = run(ctx, case, F32)
+    cur, beh = res.cur_lp.cpu().numpy(), res.behav.cpu().numpy()
+    stale = case.hb.stage < case.hb.cur_stage
+    np.testing.assert_array_equal(beh[~stale].view(np.uint32), cur[~stale].view(np.uint32))
+    np.testing.assert_array_equal(beh[stale].view(np.uint32), case.blp[stale].view(np.uint32))
+    # weight = ratio * adv = adv exactly for unclipped current tokens
+    coef = res.coef.cpu().numpy()
+    tok_traj = np.repeat(np.arange(case.hb.n_traj), np.diff(case.hb.tok_off))
+    expect = -case.adv[tok_traj] * (1.0 / case.hb.n_tok)
+    np.testing.assert_array_equal(coef[~stale], expect[~stale])
+
+
+def test_recorded_mode(ctx, oracle):
+    case = Case(oracle, seed=9, P=2, G=4, V=32000, behav_mode=1)
+    _, res = run(ctx, case, F32)
+    np.testing.assert_array_equal(res.behav.cpu().numpy().view(np.uint32), case.blp.view(np.uint32))
+    case.check(res, F32, what="recorded")
+
+
+def test_zero_advantages_zero_loss_and_grad(ctx, oracle):
+    """test_grpo.cpp:293-303: A=0 -> loss 0 and gradient exactly 0."""
+    case = Case(oracle, seed=10, P=2, G=4, V=151936, reward=1.0)
+    assert np.all(case.adv == 0.0)
+    _, res = run(ctx, case, BF16)
+    assert res.loss == 0.0
+    assert torch.count_nonzero(res.dlogits).item() == 0
+
+
+def test_advantages_and_rewards_bit_exact(ctx, oracle):
+    from paper_2511_05589_b200.workload import make_host_batch
+    hb = make_host_batch(3, 64, 8, 100, mu=math.log(20), sigma=1.0, lmax=64)
+    rew = torch.from_numpy(hb.reward).cuda()
+    goff = torch.from_numpy(hb.group_off).cuda()
+    adv = ctx.compute_advantages(rew, goff, 1e-6).cpu().numpy()
+    np.testing.assert_array_equal(adv, oracle.advantages(hb.reward, hb.group_off))
+    # terminal rewards (grpo.hpp:35-47) on random EOS placement
+    rng = np.random.default_rng(0)
+    eos = 99
+    toks = hb.target.copy()
+    ends = hb.tok_off[1:] - 1
+    toks[ends[rng.random(len(ends)) < 0.5]] = eos
+    ans = rng.integers(0, 4, hb.n_traj).astype(np.int32)
+    toks[hb.tok_off[:-1]] = rng.integers(0, 4, hb.n_traj)
+    term = np.ones(hb.n_traj, np.uint8)
+    got = ctx.terminal_rewards(torch.from_numpy(toks).cuda(), torch.from_numpy(hb.tok_off).cuda(),
+                               torch.from_numpy(term).cuda(), torch.from_numpy(ans).cuda(), eos)
+    np.testing.assert_array_equal(got.cpu().numpy(),
+                                  oracle.terminal_rewards(toks, hb.tok_off, term, ans, eos))
+
+
+def test_group_of_one_is_config_error(ctx):
+    from paper_2511_05589_b200 import ConfigError
+    rew = torch.zeros(3, dtype=torch.float64, device="cuda")
+    goff = torch.tensor([0, 2, 3], device="cuda")
+    with pytest.raises(ConfigError, match="advantage group size must be >= 2"):
+        ctx.compute_advantages(rew, goff)
+
+
+def test_out_of_vocab_token_is_contract_violation(ctx, oracle):
+    from paper_2511_05589_b200 import ContractViolation
+    case = Case(oracle, seed=12, P=2, G=4, V=32000)
+    batch = case.upload(ctx)
+    batch.target[3] = 32000
+    with pytest.raises(ContractViolation, match="token out of vocabulary"):
+        ctx.grpo_step_loss(case.logits_gpu(), batch, case.clip())
+    ctx.check()  # the error word was cleared
+
+
+def test_nonfinite_buffered_logprob_is_contract_violation(ctx, oracle):
+    from paper_2511_05589_b200 import ContractViolation
+    case = Case(oracle, seed=13, P=2, G=4, V=32000, stale_prob=1.0)
+    batch = case.upload(ctx)
+    stale_idx = int(np.flatnonzero(case.hb.stage < case.hb.cur_stage)[0])
+    batch.buffered_lp[stale_idx] = float("-inf")
+    with pytest.raises(ContractViolation, match="token_ratio requires finite log-probs"):
+        ctx.grpo_step_loss(case.logits_gpu(), batch, case.clip())
+
+
+def test_config_errors(ctx, oracle):
+    from paper_2511_05589_b200 import ClipConfig, ConfigError, ContractViolation
+    case = Case(oracle, seed=14, P=2, G=4, V=256)
+    batch = case.upload(ctx)
+    with pytest.raises(ConfigError):
+        ctx.grpo_step_loss(case.logits_gpu(), batch, ClipConfig(clip_low=0.0))
+    with pytest.raises(ContractViolation, match="reference log-probs required"):
+        ctx.grpo_step_loss(case.logits_gpu(), batch, ClipConfig(kl_coeff=0.1))
+
+
+def test_deterministic_and_chunk_invariant(ctx, oracle):
+    """Reruns are bitwise identical (fixed-order reductions, no float atomics)
+    and processing the batch in chunks changes nothing."""
+    case = Case(oracle, seed=15, P=4, G=4, V=151936, mu=math.log(16), lmax=40)
+    batch = case.upload(ctx)
+    logits = case.logits_gpu()
+    r1 = ctx.grpo_step_loss(logits, batch, case.clip())
+    r2 = ctx.grpo_step_loss(logits, batch, case.clip())
+    assert r1.loss == r2.loss
+    assert torch.equal(r1.dlogits, r2.dlogits)
+    # chunked
+    T = batch.n_tok
+    outs = ctx.alloc_outputs(T, logits.device)
+    dl = torch.empty_like(logits)
+    for a in range(0, T, 37):
+        b = min(T, a + 37)
+        ctx.loss_chunk_fused(logits[a:b], batch, case.clip(), outs, dlogits=dl[a:b], row_base=a,
+                             total_tokens=T)
+    out4 = torch.empty(4, dtype=torch.float64, device="cuda")
+    ctx.reduce(outs, T, out4)
+    ctx.check()
+    assert -out4[0].item() * (1.0 / T) == r1.loss
+    assert torch.equal(dl, r1.dlogits)
+    assert torch.equal(outs["cur_lp"], r1.cur_lp)
+
+
+def test_padded_rows(ctx, oracle):
+    for ld, kernel in ((32008, "fused_tma_kernel"), (32001, "fused_generic_kernel")):
+        case = Case(oracle, seed=16, P=2, G=4, V=32000, ld=ld)
+        _, res = run(ctx, case, F32)
+        assert ctx.last_launch()["kernel"] == kernel
+        case.check(res, F32, what=f"ld={ld}")
+
+
+def test_saturated_rows_one_minus_p(ctx, oracle):
+    """Rows whose target saturates (p_y -> 1) keep 1-p_y accurate (the target
+    is excluded from the running sum): checked on every 64th row."""
+    case = Case(oracle, seed=17, P=4, G=4, V=151936, fixed_len=32)
+    _, res = run(ctx, case, F32)
+    sat = np.arange(case.hb.n_tok) % 64 == 0
+    assert sat.any()
+    dl = res.dlogits.cpu().numpy()[sat]
+    coef = -case.ref.weight / case.hb.n_tok
+    exact = exact_dlogits(case.z64[sat], case.hb.target[sat], coef[sat])
+    assert_rows_close(dl, exact, what="saturated rows vs cancellation-free fp64")
+    assert_scalar_close(res.cur_lp.cpu().numpy()[sat], case.ref.cur_lp[sat], rtol=1e-6,
+                        what="saturated cur_lp")
+
+
+def test_logprob_gather_k1(ctx, oracle):
+    for V, dtype in ((151936, BF16), (4099, F32), (6, F32)):
+        case = Case(oracle, seed=18, P=2, G=4, V=V, dtype=dtype)
+        lp, lse = ctx.sequence_logprobs(case.logits_gpu(), torch.from_numpy(case.hb.target).cuda())
+        ctx.check()
+        assert_scalar_close(lp.cpu().numpy(), case.ref.cur_lp, what=f"K1 V={V}")
+
+
+def test_behaviour_concat_k2_bit_exact(ctx, oracle):
+    rng = np.random.default_rng(1)
+    n = 100_000
+    stage = rng.integers(0, 6, n).astype(np.uint32)
+    blp = rng.standard_normal(n).astype(np.float32)
+    cur = rng.standard_normal(n).astype(np.float32)
+    d = lambda a: torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else a).cuda()
+    for is_on in (True, False):
+        for mode in (0, 1):
+            behav, flags = ctx.concat_segments(d(stage), 5, d(blp), d(cur), is_on, mode)
+            ref, n_stale = oracle.behaviour(stage, 5, blp, cur, is_on, mode)
+            np.testing.assert_array_equal(behav.cpu().numpy(), ref.astype(np.float32))
+            np.testing.assert_array_equal(flags.cpu().numpy(), (stage < 5).astype(np.uint8))
+            assert int(flags.sum().item()) == n_stale
+
+
+def test_expand_segments(ctx):
+    from paper_2511_05589_b200.workload import make_host_batch
+    hb = make_host_batch(4, 8, 4, 100, mu=math.log(30), sigma=1.0, lmax=100, stages=(3, 4),
+                         stale_prob=1.0)
+    st = ctx.expand_segments(torch.from_numpy(hb.seg_off).cuda(),
+                             torch.from_numpy(hb.seg_ver.view(np.int32)).cuda(), hb.n_tok)
+    np.testing.assert_array_equal(st.cpu().numpy().view(np.uint32), hb.stage)
+    tt = ctx.token_traj(torch.from_numpy(hb.tok_off).cuda(), hb.n_tok).cpu().numpy()
+    np.testing.assert_array_equal(tt, np.repeat(np.arange(hb.n_traj), np.diff(hb.tok_off)))
