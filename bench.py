@@ -1,0 +1,466 @@
+#!/usr/bin/env python
+"""bench.py — BASELINE.json metric: "IS-corrected loss fwd+bwd tokens/sec & %
+HBM roofline at 1/2/4/8 B200 vs CPU".
+
+One step = one pass of the hot path over one synthetic GRPO batch
+(BASELINE.json configs[1]: 128 prompts x 8 responses, lognormal lengths up to
+8k, vocab 151,936, 2 rollout stages): for every chunk of packed rows the fused
+kernel (log-softmax + gather, cross-stage behaviour select, ratio/clip, token
+mean, dlogits) and then the deterministic reduction (+ NCCL allreduce of four
+fp64 scalars when sharded). Inputs are resident in HBM when the timed region
+starts; the logits chunk buffer (chunk_rows x V bf16, ~10 GB) is far larger
+than L2. Weak scaling: each rank holds 128 x 8 prompts' worth of whole groups
+(LPT over token counts), T_global is known on the host.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--impl reference runs the reference's own CPU path (oracle/_ref/libcopris_ref.so,
+compiled from /root/reference's headers) on the host cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "IS-corrected loss fwd+bwd tokens/sec & % HBM roofline at 1/2/4/8 B200 vs CPU"
+UNIT = "tokens/s"
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="grpo_128x8_v151936")
+    ap.add_argument("--chunk-rows", type=int, default=32768)
+    ap.add_argument("--unfused", action="store_true", help="K1 -> K2 -> K3 instead of the fused kernel")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-tokens", type=int, default=8192, help="per-rank sample for the host round trip")
+    ap.add_argument("--e2e-chunk", type=int, default=2048)
+    ap.add_argument("--cpu-tokens-per-thread", type=int, default=256)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--seed", type=int, default=1)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# sharding: deterministic LPT over whole prompt groups
+# ---------------------------------------------------------------------------
+def lpt_shard(group_tokens, world):
+    order = sorted(range(len(group_tokens)), key=lambda g: (-int(group_tokens[g]), g))
+    load = [0] * world
+    out = [[] for _ in range(world)]
+    for g in order:
+        r = min(range(world), key=lambda k: (load[k], k))
+        out[r].append(g)
+        load[r] += int(group_tokens[g])
+    return [sorted(x) for x in out]
+
+
+def local_batch(hb, groups):
+    """Rank-local packed arrays for a list of group ids (batch order kept)."""
+    import numpy as np
+    tok_off, group_off, target, stage, reward = [0], [0], [], [], []
+    for g in groups:
+        a, b = hb.group_off[g], hb.group_off[g + 1]
+        for i in range(a, b):
+            t0, t1 = hb.tok_off[i], hb.tok_off[i + 1]
+            target.append(hb.target[t0:t1])
+            stage.append(hb.stage[t0:t1])
+            tok_off.append(tok_off[-1] + (t1 - t0))
+            reward.append(hb.reward[i])
+        group_off.append(group_off[-1] + (b - a))
+    return (np.asarray(tok_off, np.int64), np.asarray(group_off, np.int64),
+            np.concatenate(target), np.concatenate(stage), np.asarray(reward, np.float64))
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md recipe)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("pci.bus_id,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, bus_id: str | None):
+        self.bus = (bus_id or "").upper()
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (OSError, ValueError):
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+        time.sleep(0.3)
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) != 8:
+                continue
+            if self.bus and not parts[0].upper().endswith(self.bus[-12:]):
+                continue
+            self.rows.append(parts)
+
+    def stop(self):
+        if not self.proc:
+            return None
+        time.sleep(0.3)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        reasons = sorted({self.NAMES[i] for r in self.rows for i in range(4)
+                          if r[4 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def traffic_per_row(config, unfused):
+    """dram bytes per row of the top kernel from the committed ncu capture
+    (profiles/ncu_traffic.json, written from an `ncu --set full` run)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            t = json.load(f)
+        return float(t[("unfused:" if unfused else "") + config]["dram_bytes_per_row"])
+    except (OSError, KeyError, ValueError):
+        return None
+
+
+# ---------------------------------------------------------------------------
+# CPU: the reference's own path (oracle/_ref) on the host cores
+# ---------------------------------------------------------------------------
+def cpu_reference(V, tokens_per_thread, seconds, seed, threads=None, min_rounds=1, max_rounds=None):
+    """Times the UNMODIFIED reference hot path (sequence_logprobs ->
+    concat_segments -> grpo_step_loss, compiled from /root/reference) with one
+    independent batch per host thread, like the reference CLI's
+    --parallel-seeds (copris_cli.cpp:98-115). Returns (tok/s, details)."""
+    import numpy as np
+    from oracle.oracle import Oracle, Reference
+
+    kind = "reference" if Reference.available else "port"
+    impl = Reference() if Reference.available else Oracle()
+    threads = threads or os.cpu_count() or 1
+    rng = np.random.default_rng(seed)
+    L = tokens_per_thread
+    target = rng.integers(0, V, L).astype(np.int32)
+    z = rng.standard_normal((L, V)).astype(np.float32).astype(np.float64) * 2.0
+    z[np.arange(L), target] += 4.0
+    tok_off = np.array([0, L // 2, L], np.int64)          # one group of two trajectories
+    stage = np.full(L, 7, np.uint32)
+    stage[: L // 4] = 6                                   # a stale first segment
+    cur = Oracle().logprob_gather(z[: L // 4], target[: L // 4]) if kind == "port" else None
+    blp = np.zeros(L, np.float64)
+    blp[: L // 4] = (cur if cur is not None else -12.0) + rng.uniform(-0.3, 0.3, L // 4)
+    adv = np.array([1.0, -1.0])
+    tokens = 0
+    rounds = 0
+    ref_time = 0.0  # sum over rounds of the slowest thread's time inside the reference path
+    t_start = time.perf_counter()
+
+    while True:
+        secs = [0.0] * threads
+
+        def work(i):
+            secs[i] = impl.is_loss(z, tok_off, target, stage, 7, blp, adv, want_dlogits=True).seconds
+
+        ths = [threading.Thread(target=work, args=(i,)) for i in range(threads)]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        rounds += 1
+        tokens += threads * L
+        ref_time += max(secs)
+        if (time.perf_counter() - t_start >= seconds and rounds >= min_rounds) or \
+                (max_rounds and rounds >= max_rounds):
+            break
+    wall = ref_time
+    try:
+        model = open("/proc/cpuinfo").read().split("model name")[1].split(":")[1].split("\n")[0].strip()
+    except (OSError, IndexError):
+        model = "unknown"
+    return tokens / wall, {
+        "kind": kind, "cores": threads, "cpu_model": model,
+        "sample": f"{rounds} rounds x {threads} threads x {L} tokens (1 group of 2 trajectories, "
+                  f"2 stages) at V={V}; {wall:.2f}s inside the reference path (slowest thread "
+                  f"per round; table construction excluded)",
+    }
+
+
+def run_reference(args):
+    """--impl reference: rank 0 alone times the reference CPU path."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2511_05589_b200.workload import CONFIGS
+    cfg = CONFIGS[args.config]
+    V = cfg["vocab"]
+    # warmup + steps: each step one bounded sample (all threads once)
+    per_step = []
+    det = None
+    for i in range(args.warmup + args.steps):
+        tps, det = cpu_reference(V, args.cpu_tokens_per_thread, 0.0, args.seed + i, max_rounds=1)
+        if i >= args.warmup:
+            per_step.append(tps)
+    value = statistics.mean(per_step)
+    tok_step = det["cores"] * args.cpu_tokens_per_thread
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * tok_step / value, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config} (BASELINE configs[1]) — bounded CPU sample",
+                   "vocab": V, "tokens_per_step": tok_step},
+        "cpu_baseline": {"value": value, "unit": UNIT, **det},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# ours
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2511_05589_b200 import ClipConfig, Copris
+    from paper_2511_05589_b200.grpo import HostWorkspace
+    from paper_2511_05589_b200.packing import upload
+    from paper_2511_05589_b200.workload import CONFIGS, make_host_batch, make_logits, stale_logprobs
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus if args.gpus == 1 else 1)))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    cfgd = dict(CONFIGS[args.config])
+    V = cfgd["vocab"]
+    P_rank = cfgd.pop("P")
+    G = cfgd.pop("G")
+    cfgd.pop("vocab")
+    hb = make_host_batch(args.seed, P_rank * world, G, V, **cfgd)
+    shards = lpt_shard(hb.group_tokens(), world)
+    tok_off, group_off, target_g, stage, reward = local_batch(hb, shards[rank])
+    T_global, T = hb.n_tok, int(tok_off[-1])
+    chunk = min(args.chunk_rows, T)
+    nchunks = (T + chunk - 1) // chunk
+
+    ctx = Copris(local)
+    clip = ClipConfig()
+    # resident logits chunk buffer; token t of the local batch reads buffer row
+    # t % chunk, whose target column is the boosted one.
+    g = torch.Generator(device="cpu")
+    g.manual_seed(args.seed + rank)
+    tbuf = torch.randint(0, V, (chunk,), generator=g, dtype=torch.int64).to(torch.int32)
+    logits = make_logits(chunk, V, tbuf.to(dev), args.seed + rank, device=dev, dtype=torch.bfloat16)
+    target = tbuf.numpy()[np.arange(T) % chunk]
+    cur_buf, _ = ctx.sequence_logprobs(logits, tbuf.to(dev))
+    torch.cuda.synchronize()
+    cur = cur_buf.cpu().numpy()[np.arange(T) % chunk]
+    blp = stale_logprobs(cur, stage, hb.cur_stage, args.seed + rank)
+    del cur
+    batch = upload(ctx, tok_off, group_off, target, blp, hb.cur_stage, stage=stage, reward=reward)
+    outs = ctx.alloc_outputs(T, dev, lse=args.unfused, behav=args.unfused)
+    dl = torch.empty((chunk, V), dtype=torch.bfloat16, device=dev)
+    out4 = torch.zeros(4, dtype=torch.float64, device=dev)
+    run_chunk = ctx.loss_chunk_unfused if args.unfused else ctx.loss_chunk_fused
+
+    def step(evs=None):
+        for c in range(nchunks):
+            r0 = c * chunk
+            n = min(chunk, T - r0)
+            if evs is not None:
+                evs[c][0].record()
+            run_chunk(logits[:n], batch, clip, outs, dlogits=dl[:n], row_base=r0,
+                      total_tokens=T_global)
+            if evs is not None:
+                evs[c][1].record()
+        ctx.reduce(outs, T, out4)
+        if world > 1:
+            dist.all_reduce(out4)
+
+    for _ in range(max(args.warmup, 1)):
+        step()
+    ctx.check()
+    info = ctx.last_launch()
+
+    evs = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)]
+            for _ in range(nchunks)] for _ in range(args.steps)]
+    bus = None
+    try:
+        p = torch.cuda.get_device_properties(local)
+        bus = f"{p.pci_bus_id:02X}:{p.pci_device_id:02X}.0"
+    except Exception:
+        pass
+    sampler = ClockSampler(bus)
+    sampler.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for k in range(args.steps):
+        step(evs[k])
+    e1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    ctx.check()
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = t.item()
+    loss = -out4[0].item() * (1.0 / T_global)
+
+    # kernel-level roofline (dominant kernel: the fused pass)
+    kern_ms = sum(evs[k][c][0].elapsed_time(evs[k][c][1]) for k in range(args.steps)
+                  for c in range(nchunks))
+    rows_timed = args.steps * T
+    bytes_per_tok = 4 * V + 16
+    achieved = rows_timed * bytes_per_tok / (kern_ms / 1e3) / 1e9
+    peak, peak_src = measured_peaks()
+    tr = traffic_per_row(args.config, args.unfused)
+
+    line = None
+    if rank == 0:
+        value = T_global / (ms_max / 1e3)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {
+                "workload": f"{args.config} (BASELINE.json configs[1]: 128 prompts x 8 responses, "
+                            f"max 8k tokens, vocab {V}, 2 rollout stages) per GPU",
+                "prompts": P_rank * world, "responses": G, "vocab": V, "tokens_global": T_global,
+                "tokens_rank0": T, "chunk_rows": chunk, "chunks_per_step": nchunks,
+                "parallelism": f"dp{world} (whole prompt groups, LPT by tokens)",
+                "path": "unfused K1->K2->K3" if args.unfused else "fused single pass",
+                "kernel": info, "l2": "inputs larger than L2 (logits chunk "
+                f"{chunk * V * 2 / 1e9:.1f} GB >> 126 MB)", "loss": loss,
+                "offpolicy_fraction": out4[2].item() / out4[1].item() if out4[1].item() else 0.0,
+                "clipped_tokens": int(out4[3].item()),
+            },
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "peak_source": peak_src,
+                         "traffic": (tr * T / nchunks) if tr else None,
+                         "algorithmic_bytes_per_token": bytes_per_tok,
+                         "kernel_ms_per_step": kern_ms / args.steps,
+                         "frac_of_8TBs_nominal": achieved / 8000.0},
+            "gpu_launches": args.steps * (nchunks * (3 if args.unfused else 1) + 1),
+            "clocks": clocks,
+        }
+
+    # e2e: the host-buffer drop-in (copris_grpo_step_loss_host) on a bounded
+    # sample of this rank's batch: pinned host logits + metadata in, host
+    # dlogits + loss out, host<->device copies inside the timed region.
+    if not args.no_e2e:
+        # whole trajectories from the front of the batch, at least e2e_tokens
+        n_tr = int(np.searchsorted(tok_off, min(args.e2e_tokens, T), side="left"))
+        n_tr = min(max(1, n_tr), len(tok_off) - 1)
+        Ts = int(tok_off[n_tr])
+        s_tok_off = torch.from_numpy(tok_off[: n_tr + 1].copy()).pin_memory()
+        s_target = torch.from_numpy(target[:Ts].copy()).pin_memory()
+        s_stage = torch.from_numpy(stage[:Ts].view(np.int32).copy()).pin_memory()
+        s_blp = torch.from_numpy(blp[:Ts].copy()).pin_memory()
+        # group advantages of the full batch (a sample may cut a group)
+        s_adv = batch.adv[:n_tr].cpu().pin_memory()
+        h_logits = torch.empty((Ts, V), dtype=torch.bfloat16).pin_memory()
+        for a in range(0, Ts, chunk):
+            b = min(Ts, a + chunk)
+            h_logits[a:b].copy_(logits[: b - a])
+        h_dl = torch.empty((Ts, V), dtype=torch.bfloat16).pin_memory()
+        ws = HostWorkspace(ctx, min(args.e2e_chunk, Ts), V, Ts, n_tr)
+        call = lambda: ws.grpo_step_loss(h_logits, s_tok_off, s_target, s_stage, s_blp,
+                                         hb.cur_stage, adv=s_adv, cfg=clip, total_tokens=0,
+                                         dlogits=h_dl)
+        call()
+        e2e_steps = max(1, min(args.steps, 5))
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            res = call()
+        el = (time.perf_counter() - t0) / e2e_steps
+        te = torch.tensor([el, Ts], dtype=torch.float64, device=dev)
+        if world > 1:
+            tmax = te[:1].clone()
+            dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+            tsum = te[1:].clone()
+            dist.all_reduce(tsum)
+            el, Ts_all = tmax.item(), tsum.item()
+        else:
+            Ts_all = Ts
+        h2d = Ts * V * 2 + Ts * 12 + (n_tr + 1) * 8 + n_tr * 8
+        d2h = Ts * V * 2 + 32
+        if line is not None:
+            line["e2e"] = {"value": Ts_all / el, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                           "d2h_bytes_per_step": d2h,
+                           "api": "copris_grpo_step_loss_host (host pinned buffers, 3-stream chunked pipeline)",
+                           "sample": f"first {n_tr} trajectories ({Ts} tokens) of each rank's batch, "
+                                     f"{e2e_steps} timed calls", "loss": res["loss"]}
+        ws.close()
+        del h_logits, h_dl
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        tps, det = cpu_reference(V, args.cpu_tokens_per_thread, args.cpu_seconds, args.seed)
+        line["cpu_baseline"] = {"value": tps, "unit": UNIT, **det}
+    if line is not None:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -191,10 +191,69 @@ COPRIS_API int copris_is_loss_bwd(copris_ctx* ctx, const copris_loss_batch* batc
 COPRIS_API int copris_loss_reduce(copris_ctx* ctx, const double* obj, const uint8_t* flags, int64_t n_tok,
                        double* out4, void* stream);
 
+/* ---- Host-buffer drop-in for grpo_step_loss (grpo.hpp:117-185) -------------
+ * The reference call takes host data and returns a host gradient. This entry
+ * takes HOST arrays (page-locked memory lets the copies overlap compute),
+ * streams the logits through a pre-allocated device workspace in chunks of
+ * `chunk_rows` rows — H2D of chunk c+1, the fused kernel on chunk c and D2H of
+ * chunk c-1 run on three streams — and returns when the loss, the counts and
+ * (optionally) the host dlogits are ready. Synchronous, like the reference.
+ * cfg->total_tokens = 0 means "this batch's own token count"; a sharded caller
+ * passes the global count and sums `objective`/`loss` across ranks. */
+typedef struct copris_workspace copris_workspace;
+
+COPRIS_API int copris_workspace_create(copris_ctx* ctx, int64_t chunk_rows, int32_t vocab,
+                                       int32_t logits_dtype, int32_t dlogits_dtype,
+                                       int64_t max_tokens, int64_t max_traj,
+                                       copris_workspace** out);
+COPRIS_API int copris_workspace_destroy(copris_workspace* ws);
+
+typedef struct {
+  const void* logits;          /* host [n_tok x ld] */
+  int64_t ld;
+  int32_t logits_dtype;
+  int32_t vocab;
+  int64_t n_tok;
+  int64_t n_traj;
+  const int64_t* tok_off;      /* host [n_traj+1] */
+  const int32_t* target;       /* host [n_tok] */
+  const uint32_t* stage;       /* host [n_tok] */
+  const float* buffered_lp;    /* host [n_tok] */
+  const float* ref_lp;         /* host [n_tok] or NULL */
+  const double* adv;           /* host [n_traj], or NULL: computed from rewards */
+  const double* rewards;       /* host [n_traj] (when adv == NULL) */
+  const int64_t* group_off;    /* host [n_groups+1] (when adv == NULL) */
+  int64_t n_groups;
+  double adv_epsilon;
+  uint32_t cur_stage;
+  uint32_t _pad;
+} copris_host_batch;
+
+typedef struct {
+  void* dlogits;               /* host [n_tok x ld_dlogits], or NULL */
+  int64_t ld_dlogits;
+  int32_t dlogits_dtype;
+  int32_t _pad;
+  float* cur_lp;               /* host [n_tok] or NULL */
+  double loss;                 /* -objective / T */
+  double objective;
+  int64_t token_count, stale_tokens, clipped_tokens;
+} copris_host_result;
+
+COPRIS_API int copris_grpo_step_loss_host(copris_ctx* ctx, copris_workspace* ws,
+                                          const copris_host_batch* batch,
+                                          const copris_loss_cfg* cfg, copris_host_result* out);
+
 /* Introspection (not a reference entry point): cluster size, grid and kernel
  * name of the last copris_is_loss_* launch on this context. */
 COPRIS_API int copris_ctx_last_launch(const copris_ctx* ctx, int* cluster, int* grid, int* num_sms,
                            const char** kernel_name);
+
+/* Diagnostics (not a reference entry point): per-CTA phase-cycle counters of
+ * the fused kernels, recorded when COPRIS_TRACE is set in the environment at
+ * context creation; 8 int64 per CTA (pass B, barrier A, scalar phase,
+ * barrier B, pass C, rows). Reading resets them. */
+COPRIS_API int copris_ctx_trace_read(copris_ctx* ctx, long long* host, int n);
 
 #ifdef __cplusplus
 }

@@ -42,6 +42,19 @@ class LossOut(C.Structure):
                 ("cur_lp", P), ("lse", P), ("behav", P), ("obj", P), ("coef", P), ("flags", P)]
 
 
+class HostBatch(C.Structure):
+    _fields_ = [("logits", P), ("ld", I64), ("logits_dtype", I32), ("vocab", I32),
+                ("n_tok", I64), ("n_traj", I64), ("tok_off", P), ("target", P), ("stage", P),
+                ("buffered_lp", P), ("ref_lp", P), ("adv", P), ("rewards", P), ("group_off", P),
+                ("n_groups", I64), ("adv_epsilon", D), ("cur_stage", U32), ("_pad", U32)]
+
+
+class HostResult(C.Structure):
+    _fields_ = [("dlogits", P), ("ld_dlogits", I64), ("dlogits_dtype", I32), ("_pad", I32),
+                ("cur_lp", P), ("loss", D), ("objective", D), ("token_count", I64),
+                ("stale_tokens", I64), ("clipped_tokens", I64)]
+
+
 _SIGS = {
     "copris_abi_version": ([], C.c_int),
     "copris_last_error": ([], C.c_char_p),
@@ -59,6 +72,11 @@ _SIGS = {
     "copris_is_loss_bwd": ([P, C.POINTER(LossBatch), C.POINTER(LossCfg), P, P, P,
                             C.POINTER(LossOut), P], C.c_int),
     "copris_loss_reduce": ([P, P, P, I64, P, P], C.c_int),
+    "copris_workspace_create": ([P, I64, I32, I32, I32, I64, I64, C.POINTER(P)], C.c_int),
+    "copris_workspace_destroy": ([P], C.c_int),
+    "copris_grpo_step_loss_host": ([P, P, C.POINTER(HostBatch), C.POINTER(LossCfg),
+                                    C.POINTER(HostResult)], C.c_int),
+    "copris_ctx_trace_read": ([P, P, C.c_int], C.c_int),
     "copris_ctx_last_launch": ([P, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
                                 C.POINTER(C.c_char_p)], C.c_int),
 }

@@ -5,22 +5,16 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "../../include/copris_b200.h"
+#include "internal.hpp"
 #include "kernels.cuh"
 
 using namespace copris_b200;
 
-struct copris_ctx {
-  int device;
-  int num_sms;
-  uint32_t* d_err;   // device error word (kernels.cuh ERR_*)
-  void* d_scratch;   // reduction scratch
-  LaunchInfo last;   // what the last loss launch did (introspection)
-};
-
-namespace {
+namespace copris_b200 {
 
 thread_local std::string g_err;
 
@@ -33,18 +27,19 @@ int cuda_fail(cudaError_t e, const char* where) {
   return fail(COPRIS_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 
-// Makes ctx->device current for the call and restores the caller's device.
-struct DeviceGuard {
-  int prev = -1;
-  explicit DeviceGuard(int dev) {
-    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
-    if (prev != dev) cudaSetDevice(dev);
-  }
-  ~DeviceGuard() {
-    int cur = -1;
-    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
-  }
-};
+DeviceGuard::DeviceGuard(int dev) {
+  if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+  if (prev != dev) cudaSetDevice(dev);
+}
+
+DeviceGuard::~DeviceGuard() {
+  int cur = -1;
+  if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+}
+
+}  // namespace copris_b200
+
+namespace {
 
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
@@ -111,6 +106,7 @@ LossParams make_params(const copris_ctx* ctx, const copris_loss_batch* b, const 
   p.coef = o->coef;
   p.flags = o->flags;
   p.err = ctx->d_err;
+  p.trace = ctx->d_trace;
   return p;
 }
 
@@ -144,9 +140,14 @@ int copris_ctx_create(int device, copris_ctx** out) {
   if (e == cudaSuccess) e = cudaMemset(ctx->d_err, 0, sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMalloc(&ctx->d_scratch, reduce_scratch_bytes());
   if (e == cudaSuccess) e = cudaMemset(ctx->d_scratch, 0, reduce_scratch_bytes());
+  if (e == cudaSuccess && getenv("COPRIS_TRACE")) {
+    e = cudaMalloc(&ctx->d_trace, sizeof(long long) * kTraceCtas * kTraceSlots);
+    if (e == cudaSuccess) e = cudaMemset(ctx->d_trace, 0, sizeof(long long) * kTraceCtas * kTraceSlots);
+  }
   if (e != cudaSuccess) {
     cudaFree(ctx->d_err);
     cudaFree(ctx->d_scratch);
+    cudaFree(ctx->d_trace);
     delete ctx;
     return cuda_fail(e, "copris_ctx_create");
   }
@@ -159,6 +160,7 @@ int copris_ctx_destroy(copris_ctx* ctx) {
   DeviceGuard g(ctx->device);
   cudaFree(ctx->d_err);
   cudaFree(ctx->d_scratch);
+  cudaFree(ctx->d_trace);
   delete ctx;
   return COPRIS_OK;
 }
@@ -321,6 +323,16 @@ int copris_ctx_last_launch(const copris_ctx* ctx, int* cluster, int* grid, int* 
   if (num_sms) *num_sms = ctx->num_sms;
   if (kernel_name) *kernel_name = ctx->last.kernel ? ctx->last.kernel : "";
   return COPRIS_OK;
+}
+
+int copris_ctx_trace_read(copris_ctx* ctx, long long* host, int n) {
+  if (!ctx || !host) return fail(COPRIS_E_INVALID, "null argument");
+  if (!ctx->d_trace) return fail(COPRIS_E_INVALID, "tracing is off (set COPRIS_TRACE=1 before creating the context)");
+  DeviceGuard g(ctx->device);
+  const int cap = kTraceCtas * kTraceSlots;
+  cudaError_t e = cudaMemcpy(host, ctx->d_trace, sizeof(long long) * (n < cap ? n : cap), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemset(ctx->d_trace, 0, sizeof(long long) * cap);
+  return e == cudaSuccess ? COPRIS_OK : cuda_fail(e, "trace read");
 }
 
 }  // extern "C"

@@ -1,0 +1,33 @@
+// internal.hpp — context layout and error helpers shared by the C-ABI units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "kernels.cuh"
+
+struct copris_ctx {
+  int device;
+  int num_sms;
+  uint32_t* d_err;   // device error word (kernels.cuh ERR_*)
+  void* d_scratch;   // reduction scratch
+  copris_b200::LaunchInfo last;  // what the last loss launch did (introspection)
+  long long* d_trace;  // phase tracing buffer (COPRIS_TRACE=1 at context creation)
+};
+
+
+namespace copris_b200 {
+
+// Records `msg` as this thread's last error and returns `code`.
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* where);
+
+// Makes `dev` current for the scope of a call and restores the caller's device.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev);
+  ~DeviceGuard();
+};
+
+}  // namespace copris_b200

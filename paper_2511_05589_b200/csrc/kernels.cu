@@ -19,6 +19,9 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <type_traits>
 
 #include "kernels.cuh"
 #include "ptx.cuh"
@@ -172,6 +175,28 @@ __device__ __forceinline__ void warp_lse(Lse& st) {
   }
 }
 
+// Phase timer for COPRIS_TRACE (one thread per CTA accumulates cycle deltas).
+struct PhaseTimer {
+  long long acc[kTraceSlots] = {};
+  long long last = 0;
+  bool on = false;
+  __device__ __forceinline__ void start(bool enable) {
+    on = enable;
+    if (on) last = clock64();
+  }
+  __device__ __forceinline__ void mark(int k) {
+    if (on) {
+      const long long now = clock64();
+      acc[k] += now - last;
+      last = now;
+    }
+  }
+  __device__ __forceinline__ void flush(long long* trace) {
+    if (on)
+      for (int k = 0; k < kTraceSlots; ++k) trace[blockIdx.x * kTraceSlots + k] += acc[k];
+  }
+};
+
 // Per-token metadata of one row, loaded by one thread early in the row.
 struct RowMeta {
   int32_t y;
@@ -189,6 +214,34 @@ __device__ __forceinline__ RowMeta load_meta(const LossParams& P, int64_t t) {
   m.adv = P.adv[P.tok_traj[t]];
   return m;
 }
+
+// Row metadata prefetched two rows ahead so that no load depends on a load
+// issued in the same row: tok_traj of row r+2s is fetched while row r runs,
+// and adv[traj] of row r+s then uses it. (A dependent tok_traj -> adv pair
+// on the critical path costs a full memory round trip per row.)
+struct MetaPipe {
+  RowMeta next{};
+  int32_t traj_ahead = 0;
+  __device__ __forceinline__ void init(const LossParams& P, int64_t r, int64_t stride) {
+    if (r < P.n_rows) next = load_meta(P, P.row_base + r);
+    if (r + stride < P.n_rows) traj_ahead = P.tok_traj[P.row_base + r + stride];
+  }
+  // Returns row r's metadata and starts the loads for row r + stride.
+  __device__ __forceinline__ RowMeta advance(const LossParams& P, int64_t r, int64_t stride) {
+    const RowMeta cur = next;
+    const int64_t r1 = r + stride;
+    if (r1 < P.n_rows) {
+      const int64_t t1 = P.row_base + r1;
+      next.y = P.target[t1];
+      next.st = P.stage[t1];
+      next.blp = P.buffered_lp[t1];
+      next.rl = P.ref_lp ? P.ref_lp[t1] : 0.f;
+      next.adv = P.adv[traj_ahead];
+      if (r1 + stride < P.n_rows) traj_ahead = P.tok_traj[t1 + stride];
+    }
+    return cur;
+  }
+};
 
 // dlogits for N consecutive columns starting at column c.
 template <int N, bool ENT>
@@ -208,136 +261,808 @@ __device__ __forceinline__ void row_grad(const float* x, float* d, int32_t c,
 // ---------------------------------------------------------------------------
 // fused TMA / cluster kernel
 // ---------------------------------------------------------------------------
-constexpr int kPieceVec = 256;  // 16-byte vectors per TMA piece (4 KB)
+constexpr int kPieceVec = 256;  // max 16-byte vectors per TMA piece (4 KB)
 constexpr int kMaxPieces = 8;   // per warp
+#ifndef COPRIS_PREFETCH_L2
+#define COPRIS_PREFETCH_L2 1
+#endif
+constexpr bool kPrefetchL2 = COPRIS_PREFETCH_L2;
+
+// Pass-B accumulation over the vectors [v, v+32) of one lane's pair: fast
+// path (no entropy) with packed fp32x2 math. Each lane keeps its running max m
+// and two packed partial sums; the target column (if present) is forced to
+// -inf after the max so it stays out of s (see Lse).
+template <typename TIn>
+struct PassB;
+
+template <>
+struct PassB<__nv_bfloat16> {
+  __device__ static __forceinline__ float vmax(uint4 a, uint4 b) {
+    uint32_t w = ptx::bmax2(ptx::bmax2(ptx::bmax2(a.x, a.y), ptx::bmax2(a.z, a.w)),
+                            ptx::bmax2(ptx::bmax2(b.x, b.y), ptx::bmax2(b.z, b.w)));
+    return fmaxf(ptx::bf16_lo(w), ptx::bf16_hi(w));
+  }
+  __device__ static __forceinline__ void unpack2(uint4 a, uint64_t* x) {
+    x[0] = ptx::bf16x2_to_f2(a.x);
+    x[1] = ptx::bf16x2_to_f2(a.y);
+    x[2] = ptx::bf16x2_to_f2(a.z);
+    x[3] = ptx::bf16x2_to_f2(a.w);
+  }
+  static constexpr uint32_t kNegInfWord = 0xFF80FF80u;
+};
+
+template <>
+struct PassB<float> {
+  __device__ static __forceinline__ float vmax(uint4 a, uint4 b) {
+    return fmaxf(fmaxf(fmaxf(__uint_as_float(a.x), __uint_as_float(a.y)),
+                       fmaxf(__uint_as_float(a.z), __uint_as_float(a.w))),
+                 fmaxf(fmaxf(__uint_as_float(b.x), __uint_as_float(b.y)),
+                       fmaxf(__uint_as_float(b.z), __uint_as_float(b.w))));
+  }
+  __device__ static __forceinline__ void unpack2(uint4 a, uint64_t* x) {
+    x[0] = ptx::f2(__uint_as_float(a.x), __uint_as_float(a.y));
+    x[1] = ptx::f2(__uint_as_float(a.z), __uint_as_float(a.w));
+  }
+  static constexpr uint32_t kNegInfWord = 0xFF800000u;
+};
+
+// Forces column j of a packed vector to -inf (rare path: the target column).
+__device__ __forceinline__ void kill_col(uint64_t* x, int j) {
+  const int k = j >> 1;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (i == k)
+      x[i] = (j & 1) ? ptx::f2(ptx::f2lo(x[i]), -INFINITY) : ptx::f2(-INFINITY, ptx::f2hi(x[i]));
+}
+
+// Sets column j of a packed vector to v (rare path: the target column).
+__device__ __forceinline__ void set_col(uint64_t* g, int j, float v) {
+  const int k = j >> 1;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (i == k) g[i] = (j & 1) ? ptx::f2(ptx::f2lo(g[i]), v) : ptx::f2(v, ptx::f2hi(g[i]));
+}
+
+// Stores NP packed fp32 pairs (2*NP columns) as TOut at a 16-byte aligned address.
+template <typename TOut, int NP>
+__device__ __forceinline__ void store_pairs(TOut* p, const uint64_t* g, uint64_t pol) {
+  if constexpr (sizeof(TOut) == 2) {
+    if constexpr (NP == 4) {
+      uint4 v{ptx::f2_to_bf16x2(g[0]), ptx::f2_to_bf16x2(g[1]), ptx::f2_to_bf16x2(g[2]),
+              ptx::f2_to_bf16x2(g[3])};
+      ptx::st_global_v4_hint(p, v, pol);
+    } else {
+      uint2 v{ptx::f2_to_bf16x2(g[0]), ptx::f2_to_bf16x2(g[1])};
+      *reinterpret_cast<uint2*>(p) = v;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < NP; i += 2) {
+      uint4 v{static_cast<uint32_t>(g[i]), static_cast<uint32_t>(g[i] >> 32),
+              static_cast<uint32_t>(g[i + 1]), static_cast<uint32_t>(g[i + 1] >> 32)};
+      ptx::st_global_v4_hint(p + 2 * i, v, pol);
+    }
+  }
+}
 
 template <typename TIn, typename TOut, int CL, int WARPS, bool ENT>
 __global__ void __launch_bounds__(WARPS * 32, 1)
     fused_tma_kernel(const LossParams P, const int32_t E) {
   using VI = Vec<TIn>;
+  using PB = PassB<TIn>;
   constexpr int VN = VI::N;
+  constexpr int NP = VN / 2;  // fp32 pairs per 16-byte vector
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t bars[WARPS * kMaxPieces];
+  __shared__ __align__(8) uint64_t xbar[2];          // cluster exchange, per row parity
+  __shared__ __align__(16) float slot[2][CL][8];     // (m, s, zy, -, u, a, -, -) per rank
   __shared__ Lse red[WARPS];
-  __shared__ Lse slot[2][CL];
-  __shared__ float slot_zy[2][CL];
   __shared__ RowBroadcast bc;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int rank = 0;
-  if constexpr (CL > 1) rank = static_cast<int>(cg::this_cluster().block_rank());
+  const uint32_t rank = CL > 1 ? ptx::cluster_ctarank() : 0u;
   const int64_t cid = blockIdx.x / CL, ncl = gridDim.x / CL;
   const int32_t V = P.vocab;
-  const int32_t col0 = rank * E;
+  const int32_t col0 = static_cast<int32_t>(rank) * E;
   const int32_t ncols = max(0, min(E, V - col0));
   const int32_t nvec = ncols / VN;
   const int32_t wv0 = static_cast<int32_t>(static_cast<int64_t>(warp) * nvec / WARPS);
   const int32_t wv1 = static_cast<int32_t>(static_cast<int64_t>(warp + 1) * nvec / WARPS);
   const int32_t npieces = (wv1 - wv0 + kPieceVec - 1) / kPieceVec;
-  uint64_t* mybars = bars + warp * kMaxPieces;
+  const int32_t pv = npieces ? (wv1 - wv0 + npieces - 1) / npieces : 0;  // balanced pieces
+  const uint32_t sbase = ptx::smem_u32(smem);
+  const uint32_t barbase = ptx::smem_u32(bars) + warp * kMaxPieces * 8;
+  const uint32_t xbar0 = ptx::smem_u32(xbar);
+  const uint32_t slot0 = ptx::smem_u32(&slot[0][0][0]);
   const uint64_t pol = ptx::policy_evict_first();
+  const uint64_t pol_keep = ptx::policy_evict_last();
   const TIn* logits = static_cast<const TIn*>(P.logits);
 
-  if (lane == 0) {
-    for (int p = 0; p < npieces; ++p) ptx::mbar_init(&mybars[p], 1);
-    ptx::fence_mbarrier_init();
+  if (lane == 0)
+    for (int p = 0; p < npieces; ++p) ptx::mbar_init(&bars[warp * kMaxPieces + p], 1);
+  if (CL > 1 && threadIdx.x == 0) {
+    ptx::mbar_init(&xbar[0], CL - 1);
+    ptx::mbar_init(&xbar[1], CL - 1);
   }
+  if (threadIdx.x == 0 || lane == 0) ptx::fence_mbarrier_init();
   __syncthreads();
-  if constexpr (CL > 1) cg::this_cluster().sync();
+  if constexpr (CL > 1) ptx::cluster_sync_all();
 
   auto issue = [&](int64_t row, int p) {
-    const int32_t v0 = wv0 + p * kPieceVec;
-    const uint32_t bytes = static_cast<uint32_t>(min(kPieceVec, wv1 - v0)) * 16u;
-    ptx::mbar_arrive_expect_tx(&mybars[p], bytes);
-    ptx::bulk_g2s(smem + static_cast<size_t>(v0) * 16,
-                  logits + row * P.ld + col0 + static_cast<int64_t>(v0) * VN, bytes, &mybars[p],
-                  pol);
+    const int32_t v0 = wv0 + p * pv;
+    const uint32_t bytes = static_cast<uint32_t>(min(pv, wv1 - v0)) * 16u;
+    const uint32_t bar = barbase + p * 8;
+    ptx::mbar_arrive_expect_tx_u32(bar, bytes);
+    ptx::bulk_g2s_u32(sbase + v0 * 16, logits + row * P.ld + col0 + static_cast<int64_t>(v0) * VN,
+                      bytes, bar, pol);
   };
 
   int64_t r = cid;
   if (lane == 0 && r < P.n_rows)
     for (int p = 0; p < npieces; ++p) issue(r, p);
+  // per-row metadata, prefetched one row ahead
+  int32_t y_next = r < P.n_rows ? P.target[P.row_base + r] : 0;
+  MetaPipe mp;
+  if (threadIdx.x == 0) mp.init(P, r, ncl);
 
+  PhaseTimer tm;
+  tm.start(P.trace && threadIdx.x == 0 && blockIdx.x < kTraceCtas);
   for (uint32_t it = 0; r < P.n_rows; r += ncl, ++it) {
     const uint32_t par = it & 1u;
     const int64_t t = P.row_base + r;
+    const int32_t y = y_next;
     RowMeta meta{};
-    if (threadIdx.x == 0) meta = load_meta(P, t);
-    const int32_t ycol = P.target[t] - col0;  // target column relative to this chunk
-
-    // pass B: online log-sum-exp over this warp's slice as its pieces land
-    Lse st = lse_empty();
-    for (int p = 0; p < npieces; ++p) {
-      ptx::mbar_wait(&mybars[p], par);
-      const int32_t v0 = wv0 + p * kPieceVec, v1 = min(wv1, v0 + kPieceVec);
-      for (int32_t v = v0 + lane; v < v1; v += 32) {
-        float x[VN];
-        VI::unpack(ptx::ld_shared_v4(smem + static_cast<size_t>(v) * 16), x);
-        const int jt = ycol - v * VN;
-        online_update<VN, ENT>(x, st, static_cast<uint32_t>(jt) < VN ? jt : -1);
+    if (threadIdx.x == 0) meta = mp.advance(P, r, ncl);
+    const int32_t ycol = y - col0;
+    // Pull the NEXT row's slice toward L2 now, so the HBM pipe stays busy
+    // through the scalar phase and pass C's refills hit L2.
+    if (kPrefetchL2 && lane == 0 && r + ncl < P.n_rows) {
+      const TIn* nrow = logits + (r + ncl) * P.ld + col0;
+      for (int p = 0; p < npieces; ++p) {
+        const int32_t v0 = wv0 + p * pv;
+        ptx::bulk_prefetch_l2(nrow + static_cast<int64_t>(v0) * VN,
+                              static_cast<uint32_t>(min(pv, wv1 - v0)) * 16u, pol_keep);
       }
     }
+
+    // ---- pass B: log-sum-exp of this warp's slice as its pieces land --------
+    Lse st = lse_empty();
+    if constexpr (ENT) {
+      for (int p = 0; p < npieces; ++p) {
+        ptx::mbar_wait_u32(barbase + p * 8, par);
+        const int32_t v0 = wv0 + p * pv, v1 = min(wv1, v0 + pv);
+        for (int32_t v = v0 + lane; v < v1; v += 32) {
+          float x[VN];
+          VI::unpack(ptx::lds_v4(sbase + v * 16), x);
+          const int jt = ycol - v * VN;
+          online_update<VN, true>(x, st, static_cast<uint32_t>(jt) < VN ? jt : -1);
+        }
+      }
+    } else {
+      float m = -INFINITY;
+      uint64_t negm = ptx::f2(INFINITY, INFINITY);
+      uint64_t acc0 = ptx::f2(0.f, 0.f), acc1 = acc0;
+      const uint64_t L2 = ptx::f2(kLog2e, kLog2e);
+      for (int p = 0; p < npieces; ++p) {
+        ptx::mbar_wait_u32(barbase + p * 8, par);
+        const int32_t v0 = wv0 + p * pv, v1 = min(wv1, v0 + pv);
+        for (int32_t v = v0 + lane; v < v1; v += 64) {
+          const bool two = v + 32 < v1;
+          const uint4 a = ptx::lds_v4(sbase + v * 16);
+          const uint4 ninf{PB::kNegInfWord, PB::kNegInfWord, PB::kNegInfWord, PB::kNegInfWord};
+          const uint4 b = two ? ptx::lds_v4(sbase + (v + 32) * 16) : ninf;
+          const float vm = PB::vmax(a, b);
+          if (vm > m) {
+            const float rs = ptx::ex2((m - vm) * kLog2e);  // 0 while m = -inf
+            const uint64_t rs2 = ptx::f2(rs, rs);
+            acc0 = ptx::fmul2(acc0, rs2);
+            acc1 = ptx::fmul2(acc1, rs2);
+            m = vm;
+            negm = ptx::f2(-m, -m);
+          }
+          uint64_t xa[4], xb[4];
+          PB::unpack2(a, xa);
+          PB::unpack2(b, xb);
+          const int ja = ycol - v * VN, jb = ja - 32 * VN;
+          if (static_cast<uint32_t>(ja) < VN) kill_col(xa, ja);
+          if (static_cast<uint32_t>(jb) < VN) kill_col(xb, jb);
+#pragma unroll
+          for (int i = 0; i < NP; ++i) {
+            acc0 = ptx::fadd2(acc0, ptx::ex2x2(ptx::fmul2(ptx::fadd2(xa[i], negm), L2)));
+            acc1 = ptx::fadd2(acc1, ptx::ex2x2(ptx::fmul2(ptx::fadd2(xb[i], negm), L2)));
+          }
+        }
+      }
+      const uint64_t acc = ptx::fadd2(acc0, acc1);
+      st.m = m;
+      st.s = ptx::f2lo(acc) + ptx::f2hi(acc);
+    }
+    tm.mark(0);
     warp_lse<ENT>(st);
     if (lane == 0) red[warp] = st;
     __syncthreads();
+    tm.mark(1);
 
-    Lse tot = lse_empty();
-    float zy = 0.f;
-    if (threadIdx.x == 0) {
-      for (int w = 0; w < WARPS; ++w) lse_merge<ENT>(tot, red[w]);
-      if (static_cast<uint32_t>(meta.y - col0) < static_cast<uint32_t>(ncols))
-        zy = VI::load1(smem + static_cast<size_t>(meta.y - col0) * sizeof(TIn));
-      if constexpr (CL > 1) {
-        cg::cluster_group cl = cg::this_cluster();
-        for (int c = 0; c < CL; ++c) {
-          *cl.map_shared_rank(&slot[par][rank], c) = tot;
-          *cl.map_shared_rank(&slot_zy[par][rank], c) = zy;
-        }
-      }
-    }
-    if constexpr (CL > 1) cg::this_cluster().sync();
-    if (threadIdx.x == 0) {
-      if constexpr (CL > 1) {
-        tot = lse_empty();
-        for (int c = 0; c < CL; ++c) lse_merge<ENT>(tot, slot[par][c]);
-        const uint32_t owner = static_cast<uint32_t>(meta.y) / static_cast<uint32_t>(E);
-        zy = owner < static_cast<uint32_t>(CL) ? slot_zy[par][owner] : 0.f;
-      }
-      bc = row_scalar_phase<ENT>(P, t, meta.y, meta.st, meta.blp, meta.rl, meta.adv, tot, zy,
-                                 rank == 0);
-    }
-    __syncthreads();
-
-    // pass C: dlogits from the shared-memory copy; refill each piece with the
-    // next row as soon as this warp has consumed it.
-    const RowBroadcast b = bc;
-    const bool zero_row = (b.coef == 0.f) && (!ENT || b.eg == 0.f);
+    // prefetch the next row's metadata while the scalar phase runs
     const int64_t nxt = r + ncl;
     const bool has_next = nxt < P.n_rows;
-    TOut* drow = P.dlogits ? static_cast<TOut*>(P.dlogits) + r * P.ld_d + col0 : nullptr;
-    for (int p = 0; p < npieces; ++p) {
-      const int32_t v0 = wv0 + p * kPieceVec, v1 = min(wv1, v0 + kPieceVec);
-      if (drow) {
-        for (int32_t v = v0 + lane; v < v1; v += 32) {
-          float d[VN];
-          if (zero_row) {
+    if (has_next) y_next = P.target[P.row_base + nxt];
+
+    // ---- scalar phase (warp 0): CTA total, cluster exchange, token math -----
+    if (warp == 0) {
+      Lse tot = lane < WARPS ? red[lane] : lse_empty();
+      warp_lse<ENT>(tot);  // butterfly: every lane holds the CTA total
+      if (lane == 0) {
+        float zy = 0.f;
+        if (static_cast<uint32_t>(ycol) < static_cast<uint32_t>(ncols)) {
+          const uint32_t za = sbase + ycol * static_cast<uint32_t>(sizeof(TIn));
+          zy = sizeof(TIn) == 2 ? __uint_as_float(ptx::lds_u16(za) << 16) : __uint_as_float(ptx::lds_u32(za));
+        }
+        if constexpr (CL > 1) {
+          const uint32_t my = slot0 + ((par * CL + rank) * 8) * 4;
+          slot[par][rank][0] = tot.m;
+          slot[par][rank][1] = tot.s;
+          slot[par][rank][2] = zy;
+          slot[par][rank][4] = tot.u;
+          slot[par][rank][5] = tot.a;
 #pragma unroll
-            for (int j = 0; j < VN; ++j) d[j] = 0.f;
-          } else {
-            float x[VN];
-            VI::unpack(ptx::ld_shared_v4(smem + static_cast<size_t>(v) * 16), x);
-            row_grad<VN, ENT>(x, d, col0 + v * VN, b);
+          for (uint32_t c = 0; c < CL; ++c) {
+            if (c == rank) continue;
+            const uint32_t rem = ptx::mapa(my, c);
+            ptx::st_cluster_v4(rem, tot.m, tot.s, zy, 0.f);
+            if (ENT) ptx::st_cluster_v4(rem + 16, tot.u, tot.a, 0.f, 0.f);
+            ptx::mbar_arrive_remote(ptx::mapa(xbar0 + par * 8, c));
           }
-          store_vec<TOut, VN>(drow + static_cast<int64_t>(v) * VN, d, pol);
+          ptx::mbar_wait_acq_cluster(xbar0 + par * 8, (it >> 1) & 1u);
+          tot = lse_empty();
+#pragma unroll
+          for (int c = 0; c < CL; ++c) {
+            Lse o{slot[par][c][0], slot[par][c][1], slot[par][c][4], slot[par][c][5]};
+            lse_merge<ENT>(tot, o);
+          }
+          const uint32_t owner = static_cast<uint32_t>(y) / static_cast<uint32_t>(E);
+          zy = owner < static_cast<uint32_t>(CL) ? slot[par][owner][2] : 0.f;
+        }
+        bc = row_scalar_phase<ENT>(P, t, meta.y, meta.st, meta.blp, meta.rl, meta.adv, tot, zy,
+                                   rank == 0);
+      }
+    }
+    tm.mark(2);
+    __syncthreads();
+    tm.mark(3);
+
+    // ---- pass C: dlogits from the shared-memory copy; each piece is refilled
+    // with the next row as soon as this warp has consumed it -----------------
+    const RowBroadcast b = bc;
+    const bool zero_row = (b.coef == 0.f) && (!ENT || b.eg == 0.f);
+    TOut* drow = P.dlogits ? static_cast<TOut*>(P.dlogits) + r * P.ld_d + col0 : nullptr;
+    const uint64_t negM = ptx::f2(-b.m, -b.m);
+    const uint64_t L2 = ptx::f2(kLog2e, kLog2e);
+    const uint64_t nl2s = ptx::f2(-b.log2s, -b.log2s);
+    const uint64_t ncoef = ptx::f2(-b.coef, -b.coef);
+    for (int p = 0; p < npieces; ++p) {
+      const int32_t v0 = wv0 + p * pv, v1 = min(wv1, v0 + pv);
+      if (drow) {
+        if (zero_row) {
+          float d[VN];
+#pragma unroll
+          for (int j = 0; j < VN; ++j) d[j] = 0.f;
+          for (int32_t v = v0 + lane; v < v1; v += 32)
+            store_vec<TOut, VN>(drow + static_cast<int64_t>(v) * VN, d, pol);
+        } else if constexpr (ENT) {
+          for (int32_t v = v0 + lane; v < v1; v += 32) {
+            float x[VN], d[VN];
+            VI::unpack(ptx::lds_v4(sbase + v * 16), x);
+            row_grad<VN, ENT>(x, d, col0 + v * VN, b);
+            store_vec<TOut, VN>(drow + static_cast<int64_t>(v) * VN, d, pol);
+          }
+        } else {
+          // two vectors per iteration: both shared-memory loads issue first
+          for (int32_t v = v0 + lane; v < v1; v += 64) {
+            const bool two = v + 32 < v1;
+            uint64_t xa[4], xb[4];
+            const uint4 ra = ptx::lds_v4(sbase + v * 16);
+            const uint4 rb = two ? ptx::lds_v4(sbase + (v + 32) * 16) : ra;
+            PB::unpack2(ra, xa);
+            PB::unpack2(rb, xb);
+            float da[VN], db[VN];
+#pragma unroll
+            for (int i = 0; i < NP; ++i) {
+              const uint64_t ga =
+                  ptx::fmul2(ptx::ex2x2(ptx::ffma2(ptx::fadd2(xa[i], negM), L2, nl2s)), ncoef);
+              const uint64_t gb =
+                  ptx::fmul2(ptx::ex2x2(ptx::ffma2(ptx::fadd2(xb[i], negM), L2, nl2s)), ncoef);
+              da[2 * i] = ptx::f2lo(ga);
+              da[2 * i + 1] = ptx::f2hi(ga);
+              db[2 * i] = ptx::f2lo(gb);
+              db[2 * i + 1] = ptx::f2hi(gb);
+            }
+            const int ja = b.y - (col0 + v * VN), jb = ja - 32 * VN;
+            if (static_cast<uint32_t>(ja) < VN) {
+#pragma unroll
+              for (int j = 0; j < VN; ++j)
+                if (j == ja) da[j] = b.dy;
+            }
+            if (static_cast<uint32_t>(jb) < VN) {
+#pragma unroll
+              for (int j = 0; j < VN; ++j)
+                if (j == jb) db[j] = b.dy;
+            }
+            store_vec<TOut, VN>(drow + static_cast<int64_t>(v) * VN, da, pol);
+            if (two) store_vec<TOut, VN>(drow + static_cast<int64_t>(v + 32) * VN, db, pol);
+          }
         }
       }
       ptx::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0 && has_next) issue(nxt, p);
     }
+    tm.mark(4);
+    tm.acc[5] += 1;
   }
-  // no CTA may exit while a peer can still write its DSMEM slots
-  if constexpr (CL > 1) cg::this_cluster().sync();
+  tm.flush(P.trace);
+  // no CTA may exit while a peer can still address its shared memory
+  if constexpr (CL > 1) ptx::cluster_sync_all();
+}
+
+// ---------------------------------------------------------------------------
+// fused two-pass streaming kernel: no shared-memory row copy. Pass 1 reads the
+// row from HBM and leaves it in L2 (evict_last); after the row's scalar phase
+// pass 2 re-reads it from L2 (evict_first) and streams dlogits out. Several
+// CTAs per SM work on independent rows, so one CTA's reduction/scalar phase
+// overlaps the others' streaming — no cluster coupling between SMs.
+// ---------------------------------------------------------------------------
+template <typename TIn, typename TOut, int WARPS, int U, bool ENT>
+__global__ void __launch_bounds__(WARPS * 32)
+    fused_l2_kernel(const LossParams P, const int keep_policy) {
+  using VI = Vec<TIn>;
+  using PB = PassB<TIn>;
+  constexpr int VN = VI::N;
+  constexpr int NP = VN / 2;
+  constexpr int NT = WARPS * 32;
+  __shared__ Lse red[WARPS];
+  __shared__ RowBroadcast bc;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int32_t V = P.vocab;
+  const int32_t nvec = V / VN;
+  const uint64_t pol_first = ptx::policy_evict_first();
+  const uint64_t pol_keep = keep_policy == 2 ? ptx::policy_evict_last()
+                            : keep_policy == 1 ? ptx::policy_evict_normal() : pol_first;
+  const uint64_t L2 = ptx::f2(kLog2e, kLog2e);
+
+  int64_t r = blockIdx.x;
+  int32_t y_next = r < P.n_rows ? P.target[P.row_base + r] : 0;
+  MetaPipe mp;
+  if (threadIdx.x == 0) mp.init(P, r, gridDim.x);
+
+  for (; r < P.n_rows; r += gridDim.x) {
+    const int64_t t = P.row_base + r;
+    const int32_t y = y_next;
+    RowMeta meta{};
+    if (threadIdx.x == 0) meta = mp.advance(P, r, gridDim.x);
+    const uint4* row = reinterpret_cast<const uint4*>(static_cast<const TIn*>(P.logits) + r * P.ld);
+
+    // ---- pass 1 (HBM -> registers, line kept in L2) ------------------------
+    Lse st = lse_empty();
+    if constexpr (ENT) {
+      for (int32_t v = threadIdx.x; v < nvec; v += NT) {
+        float x[VN];
+        VI::unpack(ptx::ld_global_v4_hint(row + v, pol_keep), x);
+        const int jt = y - v * VN;
+        online_update<VN, true>(x, st, static_cast<uint32_t>(jt) < VN ? jt : -1);
+      }
+    } else {
+      float m = -INFINITY;
+      uint64_t negm = ptx::f2(INFINITY, INFINITY);
+      uint64_t acc0 = ptx::f2(0.f, 0.f), acc1 = acc0;
+      const uint4 ninf{PB::kNegInfWord, PB::kNegInfWord, PB::kNegInfWord, PB::kNegInfWord};
+      for (int32_t v = threadIdx.x; v < nvec; v += U * NT) {
+        uint4 buf[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          const int32_t vi = v + k * NT;
+          buf[k] = vi < nvec ? ptx::ld_global_v4_hint(row + vi, pol_keep) : ninf;
+        }
+#pragma unroll
+        for (int k = 0; k < U; k += 2) {
+          const float vm = PB::vmax(buf[k], buf[k + 1]);
+          if (vm > m) {
+            const float rs = ptx::ex2((m - vm) * kLog2e);
+            const uint64_t rs2 = ptx::f2(rs, rs);
+            acc0 = ptx::fmul2(acc0, rs2);
+            acc1 = ptx::fmul2(acc1, rs2);
+            m = vm;
+            negm = ptx::f2(-m, -m);
+          }
+          uint64_t xa[4], xb[4];
+          PB::unpack2(buf[k], xa);
+          PB::unpack2(buf[k + 1], xb);
+          const int ja = y - (v + k * NT) * VN, jb = ja - NT * VN;
+          if (static_cast<uint32_t>(ja) < VN) kill_col(xa, ja);
+          if (static_cast<uint32_t>(jb) < VN) kill_col(xb, jb);
+#pragma unroll
+          for (int i = 0; i < NP; ++i) {
+            acc0 = ptx::fadd2(acc0, ptx::ex2x2(ptx::fmul2(ptx::fadd2(xa[i], negm), L2)));
+            acc1 = ptx::fadd2(acc1, ptx::ex2x2(ptx::fmul2(ptx::fadd2(xb[i], negm), L2)));
+          }
+        }
+      }
+      const uint64_t acc = ptx::fadd2(acc0, acc1);
+      st.m = m;
+      st.s = ptx::f2lo(acc) + ptx::f2hi(acc);
+    }
+    warp_lse<ENT>(st);
+    if (lane == 0) red[warp] = st;
+    __syncthreads();
+
+    const int64_t nxt = r + gridDim.x;
+    if (nxt < P.n_rows) y_next = P.target[P.row_base + nxt];
+    if (warp == 0) {
+      Lse tot = lane < WARPS ? red[lane] : lse_empty();
+      warp_lse<ENT>(tot);
+      if (lane == 0) {
+        const float zy = static_cast<uint32_t>(meta.y) < static_cast<uint32_t>(V)
+                             ? VI::load1(static_cast<const TIn*>(P.logits) + r * P.ld + meta.y) : 0.f;
+        bc = row_scalar_phase<ENT>(P, t, meta.y, meta.st, meta.blp, meta.rl, meta.adv, tot, zy, true);
+      }
+    }
+    __syncthreads();
+
+    // ---- pass 2 (L2 -> registers -> dlogits) ----------------------------------
+    const RowBroadcast b = bc;
+    if (P.dlogits) {
+      TOut* drow = static_cast<TOut*>(P.dlogits) + r * P.ld_d;
+      const bool zero_row = (b.coef == 0.f) && (!ENT || b.eg == 0.f);
+      const uint64_t negM = ptx::f2(-b.m, -b.m);
+      const uint64_t nl2s = ptx::f2(-b.log2s, -b.log2s);
+      const uint64_t ncoef = ptx::f2(-b.coef, -b.coef);
+      if (zero_row) {
+        float d[VN];
+#pragma unroll
+        for (int j = 0; j < VN; ++j) d[j] = 0.f;
+        for (int32_t v = threadIdx.x; v < nvec; v += NT)
+          store_vec<TOut, VN>(drow + static_cast<int64_t>(v) * VN, d, pol_first);
+      } else if constexpr (ENT) {
+        for (int32_t v = threadIdx.x; v < nvec; v += NT) {
+          float x[VN], d[VN];
+          VI::unpack(ptx::ld_global_v4_hint(row + v, pol_first), x);
+          row_grad<VN, ENT>(x, d, v * VN, b);
+          store_vec<TOut, VN>(drow + static_cast<int64_t>(v) * VN, d, pol_first);
+        }
+      } else {
+        for (int32_t v = threadIdx.x; v < nvec; v += U * NT) {
+          uint4 buf[U];
+#pragma unroll
+          for (int k = 0; k < U; ++k) {
+            const int32_t vi = v + k * NT;
+            if (vi < nvec) buf[k] = ptx::ld_global_v4_hint(row + vi, pol_first);
+          }
+#pragma unroll
+          for (int k = 0; k < U; ++k) {
+            const int32_t vi = v + k * NT;
+            if (vi < nvec) {
+              uint64_t x[4];
+              PB::unpack2(buf[k], x);
+              float d[VN];
+#pragma unroll
+              for (int i = 0; i < NP; ++i) {
+                const uint64_t g =
+                    ptx::fmul2(ptx::ex2x2(ptx::ffma2(ptx::fadd2(x[i], negM), L2, nl2s)), ncoef);
+                d[2 * i] = ptx::f2lo(g);
+                d[2 * i + 1] = ptx::f2hi(g);
+              }
+              const int jt = b.y - vi * VN;
+              if (static_cast<uint32_t>(jt) < VN) {
+#pragma unroll
+                for (int j = 0; j < VN; ++j)
+                  if (j == jt) d[j] = b.dy;
+              }
+              store_vec<TOut, VN>(drow + static_cast<int64_t>(vi) * VN, d, pol_first);
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// fused TMA-streaming kernel (warp-specialised). One producer warp streams
+// every row twice through a ring of shared-memory slots with TMA bulk copies:
+// pass 1 from HBM (lines kept in L2: evict_last), pass 2 from L2 (evict_first).
+// CW consumer warps reduce pass 1 (online log-sum-exp), run the row's scalar
+// phase, and turn pass 2 into dlogits. The producer never waits on the scalar
+// phase — it runs ahead into the next row as far as the ring allows — so HBM
+// stays busy while the consumers synchronise, and no cluster couples SMs.
+// ---------------------------------------------------------------------------
+constexpr int kStreamSlotVec = 2048;  // 16-byte vectors per ring slot (32 KB)
+
+// Which fp32 pairs of a 16-byte vector take 2^x on the FMA pipe instead of
+// MUFU (bit i = pair i). MUFU.EX2 issues 16 results/clk/SM and two of them per
+// element would otherwise bound the consumers below the HBM rate; moving a
+// quarter of the exponentials to FFMA2 polynomials balances the two pipes.
+#ifndef COPRIS_EMU_MASK
+#define COPRIS_EMU_MASK 0x0
+#endif
+template <int i>
+__device__ __forceinline__ uint64_t exp2_pair(uint64_t x) {
+  if constexpr (((COPRIS_EMU_MASK >> i) & 1) != 0) return ptx::ex2x2_fma(x);
+  return ptx::ex2x2(x);
+}
+
+// Position in the slot ring (slot index + phase parity), advanced without
+// integer division.
+struct Ring {
+  uint32_t slot = 0, ph = 0, n;
+  __device__ explicit Ring(uint32_t nslots) : n(nslots) {}
+  __device__ __forceinline__ void next() {
+    if (++slot == n) {
+      slot = 0;
+      ph ^= 1u;
+    }
+  }
+};
+
+template <typename TIn, typename TOut, int CW, bool ENT>
+__global__ void __launch_bounds__((CW + 1) * 32, CW <= 8 ? 2 : 1)
+    fused_stream_kernel(const LossParams P, const int nslots) {
+  using VI = Vec<TIn>;
+  using PB = PassB<TIn>;
+  constexpr int VN = VI::N;
+  constexpr int NP = VN / 2;
+  constexpr int NC = CW * 32;                  // consumer threads
+  constexpr int K = kStreamSlotVec / NC;       // vectors per consumer thread per slot
+  static_assert(kStreamSlotVec % NC == 0, "slot must split evenly over consumers");
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full[32], empty[32];
+  __shared__ Lse red[CW];
+  __shared__ RowBroadcast bc;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int32_t V = P.vocab;
+  const int32_t nvec = V / VN;
+  const int32_t nseg = (nvec + kStreamSlotVec - 1) / kStreamSlotVec;
+  const uint32_t sbase = ptx::smem_u32(smem);
+  const uint32_t fbase = ptx::smem_u32(full), ebase = ptx::smem_u32(empty);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < nslots; ++i) {
+      ptx::mbar_init(&full[i], 1);
+      ptx::mbar_init(&empty[i], CW);
+    }
+    ptx::fence_mbarrier_init();
+  }
+  __syncthreads();
+
+  if (warp == CW) {
+    // ---------------- producer ----------------
+    if (lane == 0) {
+      const uint64_t keep = ptx::policy_evict_last(), drop = ptx::policy_evict_first();
+      Ring ring(nslots);
+      for (int64_t r = blockIdx.x; r < P.n_rows; r += gridDim.x) {
+        const TIn* row = static_cast<const TIn*>(P.logits) + r * P.ld;
+        for (int pass = 0; pass < 2; ++pass) {
+          if (pass == 1 && !P.dlogits) break;
+          for (int32_t sg = 0; sg < nseg; ++sg, ring.next()) {
+            const uint32_t slot = ring.slot, par = ring.ph;
+            ptx::mbar_wait_u32(ebase + slot * 8, par ^ 1u);
+            const int32_t v0 = sg * kStreamSlotVec;
+            const uint32_t bytes = static_cast<uint32_t>(min(kStreamSlotVec, nvec - v0)) * 16u;
+            ptx::mbar_arrive_expect_tx_u32(fbase + slot * 8, bytes);
+            ptx::bulk_g2s_u32(sbase + slot * (kStreamSlotVec * 16), row + static_cast<int64_t>(v0) * VN,
+                              bytes, fbase + slot * 8, pass == 0 ? keep : drop);
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  const int tid = threadIdx.x;  // 0 .. NC-1
+  const uint64_t pol = ptx::policy_evict_first();
+  const uint64_t L2 = ptx::f2(kLog2e, kLog2e);
+  Ring ring(nslots);
+  int64_t r = blockIdx.x;
+  int32_t y_next = r < P.n_rows ? P.target[P.row_base + r] : 0;
+  MetaPipe mp;
+  if (tid == 0) mp.init(P, r, gridDim.x);
+
+  PhaseTimer tm;
+  tm.start(P.trace && tid == 0 && blockIdx.x < kTraceCtas);
+  for (; r < P.n_rows; r += gridDim.x) {
+    const int64_t t = P.row_base + r;
+    const int32_t y = y_next;
+    RowMeta meta{};
+    if (tid == 0) meta = mp.advance(P, r, gridDim.x);
+
+    // ---- pass 1 ----
+    Lse st = lse_empty();
+    float m = -INFINITY, nml = INFINITY;
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    float zy_local = 0.f;
+    bool have_zy = false;
+    for (int32_t sg = 0; sg < nseg; ++sg, ring.next()) {
+      const uint32_t slot = ring.slot, par = ring.ph;
+      const uint32_t sb = sbase + slot * (kStreamSlotVec * 16);
+      const int32_t v0 = sg * kStreamSlotVec;
+      const int32_t cnt = min(kStreamSlotVec, nvec - v0);
+      const long long w0 = tm.on ? clock64() : 0;
+      ptx::mbar_wait_u32(fbase + slot * 8, par);
+      if (tm.on) tm.acc[6] += clock64() - w0;
+      if constexpr (ENT) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const int32_t j = tid + k * NC;
+          if (j < cnt) {
+            float x[VN];
+            VI::unpack(ptx::lds_v4(sb + j * 16), x);
+            const int jt = y - (v0 + j) * VN;
+            if (static_cast<uint32_t>(jt) < VN) {
+#pragma unroll
+              for (int q = 0; q < VN; ++q)
+                if (q == jt) zy_local = x[q];
+              have_zy = true;
+            }
+            online_update<VN, true>(x, st, static_cast<uint32_t>(jt) < VN ? jt : -1);
+          }
+        }
+      } else {
+        // does this segment hold the target column? (warp-uniform)
+        const bool tseg = static_cast<uint32_t>(y - v0 * VN) < static_cast<uint32_t>(cnt * VN);
+        const bool full_seg = cnt == kStreamSlotVec;  // warp-uniform: no bounds checks
+#pragma unroll
+        for (int k = 0; k < K; k += 2) {
+          const int32_t ja_i = tid + k * NC, jb_i = ja_i + NC;
+          uint4 a, b;
+          if (full_seg) {
+            a = ptx::lds_v4(sb + ja_i * 16);
+            b = ptx::lds_v4(sb + jb_i * 16);
+          } else {
+            const uint4 ninf{PB::kNegInfWord, PB::kNegInfWord, PB::kNegInfWord, PB::kNegInfWord};
+            a = ja_i < cnt ? ptx::lds_v4(sb + ja_i * 16) : ninf;
+            b = jb_i < cnt ? ptx::lds_v4(sb + jb_i * 16) : ninf;
+          }
+          const float vm = PB::vmax(a, b);
+          if (vm > m) {
+            const float rs = ptx::ex2((m - vm) * kLog2e);
+            s0 *= rs;
+            s1 *= rs;
+            s2 *= rs;
+            s3 *= rs;
+            m = vm;
+            nml = -(m * kLog2e);
+          }
+          float xa[VN], xb[VN];
+          VI::unpack(a, xa);
+          VI::unpack(b, xb);
+          if (tseg) {
+            const int ja = y - (v0 + ja_i) * VN, jb = y - (v0 + jb_i) * VN;
+#pragma unroll
+            for (int q = 0; q < VN; ++q) {
+              if (q == ja) {
+                zy_local = xa[q];
+                have_zy = true;
+                xa[q] = -INFINITY;
+              }
+              if (q == jb) {
+                zy_local = xb[q];
+                have_zy = true;
+                xb[q] = -INFINITY;
+              }
+            }
+          }
+          // e = 2^(x log2e - m log2e); four independent accumulators
+#pragma unroll
+          for (int q = 0; q < VN; q += 2) {
+            s0 += ptx::ex2(fmaf(xa[q], kLog2e, nml));
+            s1 += ptx::ex2(fmaf(xa[q + 1], kLog2e, nml));
+            s2 += ptx::ex2(fmaf(xb[q], kLog2e, nml));
+            s3 += ptx::ex2(fmaf(xb[q + 1], kLog2e, nml));
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive_u32(ebase + slot * 8);
+    }
+    if constexpr (!ENT) {
+      st.m = m;
+      st.s = (s0 + s1) + (s2 + s3);
+    }
+    tm.mark(0);
+    warp_lse<ENT>(st);
+    if (lane == 0) red[warp] = st;
+    __shared__ float zy_sh;
+    if (have_zy) zy_sh = zy_local;  // exactly one consumer thread owns the target
+    ptx::named_bar_sync(1, NC);
+    tm.mark(1);
+
+    const int64_t nxt = r + gridDim.x;
+    if (nxt < P.n_rows) y_next = P.target[P.row_base + nxt];
+    if (warp == 0) {
+      Lse tot = lane < CW ? red[lane] : lse_empty();
+      warp_lse<ENT>(tot);
+      if (lane == 0) {
+        const float zy = static_cast<uint32_t>(meta.y) < static_cast<uint32_t>(V) ? zy_sh : 0.f;
+        bc = row_scalar_phase<ENT>(P, t, meta.y, meta.st, meta.blp, meta.rl, meta.adv, tot, zy, true);
+      }
+    }
+    tm.mark(2);
+    ptx::named_bar_sync(1, NC);
+    tm.mark(3);
+
+    // ---- pass 2 ----
+    if (!P.dlogits) continue;
+    const RowBroadcast b = bc;
+    TOut* drow = static_cast<TOut*>(P.dlogits) + r * P.ld_d;
+    const bool zero_row = (b.coef == 0.f) && (!ENT || b.eg == 0.f);
+    const uint64_t nc1 = ptx::f2(-b.c1, -b.c1);
+    const uint64_t ncoef = ptx::f2(-b.coef, -b.coef);
+    for (int32_t sg = 0; sg < nseg; ++sg, ring.next()) {
+      const uint32_t slot = ring.slot, par = ring.ph;
+      const uint32_t sb = sbase + slot * (kStreamSlotVec * 16);
+      const int32_t v0 = sg * kStreamSlotVec;
+      const int32_t cnt = min(kStreamSlotVec, nvec - v0);
+      const bool tseg = static_cast<uint32_t>(b.y - v0 * VN) < static_cast<uint32_t>(cnt * VN);
+      const long long w0 = tm.on ? clock64() : 0;
+      ptx::mbar_wait_u32(fbase + slot * 8, par);
+      if (tm.on) tm.acc[7] += clock64() - w0;
+      TOut* dseg = drow + static_cast<int64_t>(v0) * VN;
+      if (!ENT && !zero_row && cnt == kStreamSlotVec) {
+        // full segment: all K shared-memory loads first, then the math, then the stores
+        uint4 raw[K];
+#pragma unroll
+        for (int q = 0; q < K; ++q) raw[q] = ptx::lds_v4(sb + (tid + q * NC) * 16);
+#pragma unroll
+        for (int q = 0; q < K; ++q) {
+          float x[VN], d[VN];
+          VI::unpack(raw[q], x);
+#pragma unroll
+          for (int e = 0; e < VN; ++e) d[e] = ptx::ex2(fmaf(x[e], kLog2e, -b.c1)) * -b.coef;
+          if (tseg) {
+            const int jt = b.y - (v0 + tid + q * NC) * VN;
+#pragma unroll
+            for (int e = 0; e < VN; ++e)
+              if (e == jt) d[e] = b.dy;
+          }
+          store_vec<TOut, VN>(dseg + static_cast<int64_t>(tid + q * NC) * VN, d, pol);
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < K; ++q) {
+          const int32_t j = tid + q * NC;
+          if (j < cnt) {
+            float d[VN];
+            if (zero_row) {
+#pragma unroll
+              for (int e = 0; e < VN; ++e) d[e] = 0.f;
+            } else {
+              float x[VN];
+              VI::unpack(ptx::lds_v4(sb + j * 16), x);
+              if constexpr (ENT) {
+                row_grad<VN, ENT>(x, d, (v0 + j) * VN, b);
+              } else {
+#pragma unroll
+                for (int e = 0; e < VN; ++e) d[e] = ptx::ex2(fmaf(x[e], kLog2e, -b.c1)) * -b.coef;
+                if (tseg) {
+                  const int jt = b.y - (v0 + j) * VN;
+#pragma unroll
+                  for (int e = 0; e < VN; ++e)
+                    if (e == jt) d[e] = b.dy;
+                }
+              }
+            }
+            store_vec<TOut, VN>(dseg + static_cast<int64_t>(j) * VN, d, pol);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive_u32(ebase + slot * 8);
+    }
+    tm.mark(4);
+    tm.acc[5] += 1;
+  }
+  tm.flush(P.trace);
 }
 
 // ---------------------------------------------------------------------------
@@ -488,13 +1213,12 @@ __global__ void __launch_bounds__(256) bwd_kernel(const LossParams P) {
       const double adv = P.adv[P.tok_traj[t]];
       const float rl = P.ref_lp ? P.ref_lp[t] : 0.f;
       const bool stale = st < static_cast<uint32_t>(P.cur_stage);
-      double H = 0.0, ln_s = 0.0;
+      float H = 0.f, ln_s = 0.f;
       if (ENT) {
         const bool ok = static_cast<uint32_t>(y) < static_cast<uint32_t>(V);
-        const double Sd = static_cast<double>(tot.s) +
-                          (ok ? exp(static_cast<double>(VI::load1(row + y)) - static_cast<double>(tot.m)) : 0.0);
-        ln_s = log(Sd);
-        H = ln_s - static_cast<double>(tot.u) / static_cast<double>(tot.a);
+        const LogProb lp = finish_logprob(tot.m, tot.s, ok ? VI::load1(row + y) : 0.f, ok);
+        ln_s = lp.ln_s;
+        H = ln_s - tot.u / tot.a;
       }
       TokenResult tr = static_cast<uint32_t>(y) < static_cast<uint32_t>(V)
                            ? token_objective(P, cur, beh, adv, rl, stale, H, ENT)
@@ -510,12 +1234,12 @@ __global__ void __launch_bounds__(256) bwd_kernel(const LossParams P) {
       P.flags[t] = tr.flags;
       RowBroadcast b;
       b.coef = static_cast<float>(tr.coef);
-      b.dy = tr.err ? 0.f : static_cast<float>(tr.coef * -expm1(static_cast<double>(cur)));
+      b.dy = tr.err ? 0.f : static_cast<float>(tr.coef) * -expm1f(cur);
       b.y = y;
       if (ENT) {
         b.m = tot.m;
-        b.log2s = static_cast<float>(ln_s * kLog2eD);
-        b.k0 = static_cast<float>(H - ln_s);
+        b.log2s = ln_s * kLog2e;
+        b.k0 = H - ln_s;
         b.eg = tr.err ? 0.f : static_cast<float>(P.inv_t * P.entropy_coeff);
       } else {  // p = exp(z - lse): frame m = lse, log2 s = 0
         b.m = P.in_lse[t];
@@ -756,6 +1480,86 @@ cudaError_t launch_tma(const LossParams& p, int32_t E, int num_sms, cudaStream_t
   return cudaLaunchKernelEx(&cfg, kernel, p, E);
 }
 
+// Tuning overrides for experiments (bf16 -> bf16, no entropy only):
+// COPRIS_TUNE_CL in {2, 4} and COPRIS_TUNE_WARPS in {8, 16, 32}.
+int tune_env(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+template <typename TIn, typename TOut, bool ENT>
+bool launch_tuned(const LossParams& p, int num_sms, cudaStream_t stream, LaunchInfo* info,
+                  cudaError_t* err) {
+  if constexpr (std::is_same<TIn, __nv_bfloat16>::value && std::is_same<TOut, __nv_bfloat16>::value && !ENT) {
+    static const int cl = tune_env("COPRIS_TUNE_CL", 0), w = tune_env("COPRIS_TUNE_WARPS", 0);
+    if (cl == 0 && w == 0) return false;
+    const int c = cl ? cl : 2, ww = w ? w : 16;
+    const int64_t per = (p.vocab + c - 1) / c;
+    const int32_t E = static_cast<int32_t>((per + 7) / 8 * 8);
+    if (c == 2 && ww == 8) *err = launch_tma<TIn, TOut, 2, 8, ENT>(p, E, num_sms, stream, info);
+    else if (c == 2 && ww == 16) *err = launch_tma<TIn, TOut, 2, 16, ENT>(p, E, num_sms, stream, info);
+    else if (c == 2 && ww == 32) *err = launch_tma<TIn, TOut, 2, 32, ENT>(p, E, num_sms, stream, info);
+    else if (c == 4 && ww == 8) *err = launch_tma<TIn, TOut, 4, 8, ENT>(p, E, num_sms, stream, info);
+    else if (c == 4 && ww == 16) *err = launch_tma<TIn, TOut, 4, 16, ENT>(p, E, num_sms, stream, info);
+    else return false;
+    return true;
+  }
+  return false;
+}
+
+template <typename TIn, typename TOut, int WARPS, int U, bool ENT>
+cudaError_t launch_l2(const LossParams& p, int num_sms, cudaStream_t stream, LaunchInfo* info) {
+  auto kernel = fused_l2_kernel<TIn, TOut, WARPS, U, ENT>;
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, WARPS * 32, 0);
+  if (e != cudaSuccess) return e;
+  const int cap = tune_env("COPRIS_TUNE_CTAS", 0);
+  if (cap > 0 && cap < per_sm) per_sm = cap;
+  const int grid = grid_rows(p.n_rows, num_sms, per_sm < 1 ? 1 : per_sm);
+  if (info) {
+    info->cluster = 1;
+    info->grid = grid;
+    info->kernel = "fused_l2_kernel";
+  }
+  kernel<<<grid, WARPS * 32, 0, stream>>>(p, tune_env("COPRIS_TUNE_KEEP", 2));
+  return cudaGetLastError();
+}
+
+template <typename TIn, typename TOut, int CW, bool ENT>
+cudaError_t launch_stream(const LossParams& p, int num_sms, cudaStream_t stream, LaunchInfo* info) {
+  auto kernel = fused_stream_kernel<TIn, TOut, CW, ENT>;
+  const int nslots = tune_env("COPRIS_TUNE_SLOTS", CW >= 16 ? 6 : 3);
+  const int smem = nslots * kStreamSlotVec * 16;
+  cudaError_t e = set_smem(kernel, smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, (CW + 1) * 32, smem);
+  if (e != cudaSuccess) return e;
+  const int grid = grid_rows(p.n_rows, num_sms, per_sm < 1 ? 1 : per_sm);
+  if (info) {
+    info->cluster = 1;
+    info->grid = grid;
+    info->kernel = "fused_stream_kernel";
+  }
+  kernel<<<grid, (CW + 1) * 32, smem, stream>>>(p, nslots);
+  return cudaGetLastError();
+}
+
+// Fused-kernel selection. COPRIS_FUSED_IMPL (read per call) forces one of
+// "stream", "tma", "l2" for experiments and tests; "auto" (default) picks:
+//   rows <= 72 KB : fused_tma_kernel, whole row in shared memory, several
+//                   CTAs per SM (independent rows overlap their sync phases);
+//   larger rows   : fused_stream_kernel (TMA ring + L2 re-read, 1 CTA/SM);
+//   unaligned     : fused_generic_kernel.
+int fused_impl() {
+  const char* e = getenv("COPRIS_FUSED_IMPL");
+  if (!e || !*e || !strcmp(e, "auto")) return 0;
+  if (!strcmp(e, "stream")) return 1;
+  if (!strcmp(e, "tma")) return 2;
+  if (!strcmp(e, "l2")) return 3;
+  return 0;
+}
+
 template <typename TIn, typename TOut, bool ENT>
 cudaError_t dispatch_fused(const LossParams& p, int num_sms, cudaStream_t stream, LaunchInfo* info) {
   constexpr int VN = Vec<TIn>::N;
@@ -767,20 +1571,34 @@ cudaError_t dispatch_fused(const LossParams& p, int num_sms, cudaStream_t stream
                         (((p.ld_d * sizeof(TOut)) % 16 == 0) &&
                          (reinterpret_cast<uintptr_t>(p.dlogits) % 16 == 0))) &&
                        p.vocab >= 32 * VN;
+  auto chunk = [&](int cl) {
+    const int64_t per = (p.vocab + cl - 1) / cl;
+    return static_cast<int32_t>((per + VN - 1) / VN * VN);
+  };
   if (aligned) {
-    auto chunk = [&](int cl) {
-      const int64_t per = (p.vocab + cl - 1) / cl;
-      return static_cast<int32_t>((per + VN - 1) / VN * VN);
-    };
-    if (row_bytes <= 72 * 1024) {
-      return launch_tma<TIn, TOut, 1, 8, ENT>(p, chunk(1), num_sms, stream, info);
-    } else if (row_bytes <= kMaxChunkBytes) {
-      return launch_tma<TIn, TOut, 1, 16, ENT>(p, chunk(1), num_sms, stream, info);
-    } else if (row_bytes <= 2 * kMaxChunkBytes) {
-      return launch_tma<TIn, TOut, 2, 16, ENT>(p, chunk(2), num_sms, stream, info);
-    } else if (row_bytes <= 4 * kMaxChunkBytes) {
-      return launch_tma<TIn, TOut, 4, 16, ENT>(p, chunk(4), num_sms, stream, info);
+    int impl = fused_impl();
+    if (impl == 0) impl = row_bytes <= 72 * 1024 ? 2 : 1;
+    if (impl == 1) {
+      const int w = tune_env("COPRIS_TUNE_WARPS", 16);
+      if (w == 8) return launch_stream<TIn, TOut, 8, ENT>(p, num_sms, stream, info);
+      return launch_stream<TIn, TOut, 16, ENT>(p, num_sms, stream, info);
     }
+    if (impl == 3) {
+      const int w = tune_env("COPRIS_TUNE_WARPS", 32);
+      if (w == 8) return launch_l2<TIn, TOut, 8, 4, ENT>(p, num_sms, stream, info);
+      if (w == 16) return launch_l2<TIn, TOut, 16, 4, ENT>(p, num_sms, stream, info);
+      return launch_l2<TIn, TOut, 32, 4, ENT>(p, num_sms, stream, info);
+    }
+    // impl == 2: whole row resident in shared memory (split over a cluster)
+    if (row_bytes <= 72 * 1024) return launch_tma<TIn, TOut, 1, 8, ENT>(p, chunk(1), num_sms, stream, info);
+    if (row_bytes <= kMaxChunkBytes) return launch_tma<TIn, TOut, 1, 16, ENT>(p, chunk(1), num_sms, stream, info);
+    if (row_bytes <= 2 * kMaxChunkBytes) {
+      cudaError_t e;
+      if (launch_tuned<TIn, TOut, ENT>(p, num_sms, stream, info, &e)) return e;
+      return launch_tma<TIn, TOut, 2, 16, ENT>(p, chunk(2), num_sms, stream, info);
+    }
+    if (row_bytes <= 4 * kMaxChunkBytes) return launch_tma<TIn, TOut, 4, 16, ENT>(p, chunk(4), num_sms, stream, info);
+    return launch_stream<TIn, TOut, 16, ENT>(p, num_sms, stream, info);
   }
   if (info) {
     info->cluster = 1;

@@ -55,7 +55,13 @@ struct LossParams {
   double* coef;
   uint8_t* flags;
   uint32_t* err;
+  long long* trace;  // optional per-CTA phase-cycle accumulators (COPRIS_TRACE)
 };
+
+// Phase accumulators written by the fused kernels when LossParams::trace is
+// set: [cta * kTraceSlots + k], k = pass B, wait A, scalar, wait B, pass C, rows.
+constexpr int kTraceSlots = 8;
+constexpr int kTraceCtas = 2048;
 
 enum class DType : int { BF16 = 0, F32 = 1 };
 

@@ -66,6 +66,119 @@ __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, u
       : "memory");
 }
 
+
+// ---- TMA bulk prefetch into L2 (no shared memory involved) -------------------
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes, uint64_t policy) {
+  asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(src),
+               "r"(bytes), "l"(policy)
+               : "memory");
+}
+
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+// ---- u32 shared-memory addressing (no generic->shared conversion in loops) ----
+__device__ __forceinline__ uint4 lds_v4(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(addr));
+  return v;
+}
+
+__device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+  return v;
+}
+
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+
+__device__ __forceinline__ void bulk_g2s_u32(uint32_t dst, const void* src, uint32_t bytes,
+                                             uint32_t bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx_u32(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_u32(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+// Named barrier over `count` threads (a subset of the CTA).
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+// ---- cluster / DSMEM -------------------------------------------------------------
+// Address of the same shared-memory location in CTA `rank` of this cluster.
+__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+
+__device__ __forceinline__ void st_cluster_v4(uint32_t addr, float a, float b, float c, float d) {
+  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b),
+               "f"(c), "f"(d)
+               : "memory");
+}
+
+// Remote arrive that releases this thread's prior DSMEM stores at cluster scope.
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_acq_cluster(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+
 // ---- streaming global stores ---------------------------------------------------
 __device__ __forceinline__ void st_global_v4_hint(void* p, uint4 v, uint64_t policy) {
   asm volatile(
@@ -82,6 +195,21 @@ __device__ __forceinline__ uint4 ld_shared_v4(const void* p) {
   return v;
 }
 
+// 128-bit global load with an L2 eviction-priority hint, no L1 allocation.
+__device__ __forceinline__ uint4 ld_global_v4_hint(const void* p, uint64_t policy) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.b32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p), "l"(policy));
+  return v;
+}
+
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
 // Streaming 128-bit global load that does not allocate in L1.
 __device__ __forceinline__ uint4 ld_global_nc_v4(const void* p) {
   uint4 v;
@@ -96,6 +224,88 @@ __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+
+// ---- packed fp32x2 arithmetic (Blackwell FADD2/FMUL2/FFMA2) ---------------------
+__device__ __forceinline__ uint64_t f2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float f2lo(uint64_t r) {
+  return __uint_as_float(static_cast<uint32_t>(r));
+}
+__device__ __forceinline__ float f2hi(uint64_t r) {
+  return __uint_as_float(static_cast<uint32_t>(r >> 32));
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+// exp2 of both halves on the MUFU pipe, results landing in one register pair
+__device__ __forceinline__ uint64_t ex2x2(uint64_t a) {
+  uint64_t r;
+  asm("{\n.reg .f32 a0, a1, e0, e1;\nmov.b64 {a0, a1}, %1;\n"
+      "ex2.approx.ftz.f32 e0, a0;\nex2.approx.ftz.f32 e1, a1;\nmov.b64 %0, {e0, e1};\n}"
+      : "=l"(r)
+      : "l"(a));
+  return r;
+}
+// 2^x for both halves on the FMA pipe (no MUFU): round-to-nearest split
+// x = n + f with the 1.5*2^23 trick, degree-5 minimax 2^f on [-0.5, 0.5]
+// (max rel. error 2.3e-7 in fp32 Horner, comparable to ex2.approx), scaled by
+// adding n to the exponent field. Inputs are clamped at -126 with a
+// NaN-propagating max, so NaN stays NaN and tiny results stay finite.
+__device__ __forceinline__ uint64_t ex2x2_fma(uint64_t x) {
+  float lo, hi;
+  asm("{\n.reg .f32 a0, a1;\nmov.b64 {a0, a1}, %2;\n"
+      "max.NaN.f32 %0, a0, 0fC2FC0000;\nmax.NaN.f32 %1, a1, 0fC2FC0000;\n}"
+      : "=f"(lo), "=f"(hi)
+      : "l"(x));
+  const uint64_t xc = f2(lo, hi);
+  const uint64_t magic = f2(12582912.f, 12582912.f);
+  const uint64_t t = fadd2(xc, magic);
+  const uint64_t n = fadd2(t, f2(-12582912.f, -12582912.f));
+  const uint64_t f = ffma2(n, f2(-1.f, -1.f), xc);
+  uint64_t p = ffma2(f2(0.001327647129073739f, 0.001327647129073739f), f,
+                     f2(0.009675540961325169f, 0.009675540961325169f));
+  p = ffma2(p, f, f2(0.05550713092088699f, 0.05550713092088699f));
+  p = ffma2(p, f, f2(0.24022120237350464f, 0.24022120237350464f));
+  p = ffma2(p, f, f2(0.6931469440460205f, 0.6931469440460205f));
+  p = ffma2(p, f, f2(1.0000001192092896f, 1.0000001192092896f));
+  const uint32_t rlo = static_cast<uint32_t>(p) + (static_cast<uint32_t>(t) << 23);
+  const uint32_t rhi = static_cast<uint32_t>(p >> 32) + (static_cast<uint32_t>(t >> 32) << 23);
+  return (static_cast<uint64_t>(rhi) << 32) | rlo;
+}
+
+// bf16x2 word of two floats (round to nearest even)
+__device__ __forceinline__ uint32_t f2_to_bf16x2(uint64_t a) {
+  uint32_t r;
+  asm("{\n.reg .f32 lo, hi;\nmov.b64 {lo, hi}, %1;\ncvt.rn.bf16x2.f32 %0, hi, lo;\n}" : "=r"(r) : "l"(a));
+  return r;
+}
+
+// bf16 word -> (lo, hi) fp32 pair
+__device__ __forceinline__ uint64_t bf16x2_to_f2(uint32_t w) {
+  return f2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+}
+// packed bf16 max (exact; NaN-ignoring like fmaxf)
+__device__ __forceinline__ uint32_t bmax2(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("max.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
 }
 
 // ---- bf16 <-> f32 ------------------------------------------------------------------

@@ -32,21 +32,24 @@ struct TokenResult {
 };
 
 // grpo.hpp:147-162 (+ 170-171 when `ent`): cur/beh are the f32 log-probs,
-// H the row entropy in nats (only read when ent).
+// H the row entropy in nats (only read when ent). The transcendentals run in
+// fp32 (expf, <= 2 ulp) because this sits on every row's critical path; the
+// products and sums that decide the branch and form w, obj and coef are fp64
+// in the reference's order, so a current-stage token (ratio exactly 1) gets
+// w = A and coef = -A/T bit for bit.
 __device__ __forceinline__ TokenResult token_objective(const LossParams& P, float cur, float beh,
                                                        double adv, float ref, bool stale,
-                                                       double H, bool ent) {
+                                                       float H, bool ent) {
   TokenResult r{0.0, 0.0, static_cast<uint8_t>(stale ? FLAG_STALE : 0), 0u};
   if (!isfinite(adv)) {
     r.err = ERR_NONFINITE_ADV;
     return r;
   }
-  const double c = cur, b = beh;
-  if (!isfinite(c) || !isfinite(b)) {  // grpo.hpp:69-70 token_ratio
+  if (!isfinite(cur) || !isfinite(beh)) {  // grpo.hpp:69-70 token_ratio
     r.err = ERR_NONFINITE_LP;
     return r;
   }
-  const double ratio = exp(__dadd_rn(c, -b));
+  const double ratio = static_cast<double>(expf(cur - beh));
   // std::clamp(ratio, 1 - clip_low, 1 + clip_high), grpo.hpp:149
   const double clamped = ratio < P.clamp_lo ? P.clamp_lo : (P.clamp_hi < ratio ? P.clamp_hi : ratio);
   const double unclipped = __dmul_rn(ratio, adv);
@@ -60,35 +63,48 @@ __device__ __forceinline__ TokenResult token_objective(const LossParams& P, floa
     r.flags |= FLAG_CLIPPED;
   }
   if (P.kl_coeff > 0.0) {  // grpo.hpp:158-162
-    const double d = __dadd_rn(static_cast<double>(ref), -c);
-    const double ed = exp(d);
+    const float df = ref - cur;
+    const double d = static_cast<double>(df);
+    const double ed = static_cast<double>(expf(df));
     obj = __dadd_rn(obj, -__dmul_rn(P.kl_coeff, __dadd_rn(__dadd_rn(ed, -d), -1.0)));
     w = __dadd_rn(w, __dmul_rn(P.kl_coeff, __dadd_rn(ed, -1.0)));
   }
-  if (ent) obj = __dadd_rn(obj, __dmul_rn(P.entropy_coeff, H));
+  if (ent) obj = __dadd_rn(obj, __dmul_rn(P.entropy_coeff, static_cast<double>(H)));
   r.obj = obj;
   r.coef = __dmul_rn(-P.inv_t, w);
   return r;
 }
 
-// log-prob and log-sum-exp of one row from the online state (m, s excluding
-// the target column) and the target logit: S = s + e^(z_y - m),
-// lse = m + ln S, cur = (z_y - m) - ln S. fp64 for the O(1) scalar part.
+// log-prob and log-sum-exp of one row from the online state (m, s = sum over
+// the NON-target columns of e^(z-m)) and the target logit z_y. With
+// dz = z_y - m and r = s e^(-dz) = sum_{k!=y} p_k / p_y:
+//   cur = log p_y = -log1p(r),  ln S = dz + log1p(r),  lse = m + ln S.
+// log1p keeps cur accurate when the target saturates the row (p_y -> 1),
+// where log(e^dz + s) would lose r to the rounding of 1 + r. fp64: O(1) work.
 struct LogProb {
   float cur;
   double lse;
-  double ln_s;
-  double S;
+  float ln_s;
+  float S;
 };
 
 __device__ __forceinline__ LogProb finish_logprob(float M, float s_excl, float zy, bool ok) {
-  LogProb r;
-  const double dz = static_cast<double>(zy) - static_cast<double>(M);
-  r.S = static_cast<double>(s_excl) + (ok ? exp(dz) : 0.0);
-  r.ln_s = log(r.S);
-  r.lse = static_cast<double>(M) + r.ln_s;
-  r.cur = ok ? static_cast<float>(dz - r.ln_s) : __int_as_float(0x7fc00000);
-  return r;
+  LogProb q;
+  if (!ok) {
+    q.ln_s = logf(s_excl);
+    q.S = s_excl;
+    q.lse = static_cast<double>(M) + q.ln_s;
+    q.cur = __int_as_float(0x7fc00000);
+    return q;
+  }
+  const float dz = zy - M;
+  const float r = s_excl * expf(-dz);
+  const float l1 = log1pf(r);
+  q.cur = -l1;
+  q.ln_s = dz + l1;
+  q.S = s_excl + expf(dz);
+  q.lse = static_cast<double>(M) + static_cast<double>(q.ln_s);
+  return q;
 }
 
 // Values pass C of a row needs, broadcast from the scalar phase.
@@ -97,6 +113,7 @@ struct RowBroadcast {
   float dy;      // dlogits of the target column: coef * (1 - p_y)
   float m;       // row max (pass-B frame)
   float log2s;   // log2(sum exp(z - m))
+  float c1;      // m*log2(e) + log2(S): p_k = 2^(z_k log2(e) - c1)
   int32_t y;     // target column
   float eg;      // entropy gradient scale c_H/T (0 when off or on error)
   float k0;      // H - ln(S): log p + H = (z - m) + k0
@@ -113,13 +130,14 @@ __device__ __forceinline__ RowBroadcast row_scalar_phase(const LossParams& P, in
   const bool oov = static_cast<uint32_t>(y) >= static_cast<uint32_t>(P.vocab);
   const float M = tot.m;
   const LogProb lp = finish_logprob(M, tot.s, zy, !oov);
-  const double ln_s = lp.ln_s, lse = lp.lse;
+  const float ln_s = lp.ln_s;
+  const double lse = lp.lse;
   const float cur = lp.cur;
   const bool stale = st < static_cast<uint32_t>(P.cur_stage);
   const float beh = select_behaviour(st, static_cast<uint32_t>(P.cur_stage), blp, cur, P.is_enabled,
                                      P.behav_mode);
-  double H = 0.0;
-  if (ENT) H = ln_s - static_cast<double>(tot.u) / static_cast<double>(tot.a);
+  float H = 0.f;
+  if (ENT) H = ln_s - tot.u / tot.a;
   TokenResult tr;
   if (oov) {
     tr = TokenResult{0.0, 0.0, static_cast<uint8_t>(stale ? FLAG_STALE : 0), ERR_TOKEN_OOV};
@@ -141,12 +159,13 @@ __device__ __forceinline__ RowBroadcast row_scalar_phase(const LossParams& P, in
   }
   RowBroadcast b;
   b.coef = static_cast<float>(tr.coef);
-  b.dy = tr.err ? 0.f : static_cast<float>(tr.coef * -expm1(static_cast<double>(cur)));  // coef*(1-p_y)
+  b.dy = tr.err ? 0.f : static_cast<float>(tr.coef) * -expm1f(cur);  // coef*(1-p_y)
   b.m = M;
-  b.log2s = static_cast<float>(ln_s * kLog2eD);
+  b.log2s = ln_s * kLog2e;
+  b.c1 = static_cast<float>(static_cast<double>(M) * kLog2eD + static_cast<double>(ln_s) * kLog2eD);
   b.y = y;
   b.eg = (ENT && !tr.err) ? static_cast<float>(P.inv_t * P.entropy_coeff) : 0.f;
-  b.k0 = ENT ? static_cast<float>(H - ln_s) : 0.f;
+  b.k0 = ENT ? H - ln_s : 0.f;
   return b;
 }
 

@@ -273,8 +273,10 @@ class Copris:
             int(is_enabled), behav_mode, n, _p(behav), None, self._stream(stream)))
         b, c, o = self._structs(logits, batch, cfg, is_enabled, behav_mode, T, row_base, dlogits,
                                 outs)
-        self._call(self.lib.copris_is_loss_bwd(self.h, C.byref(b), C.byref(c), _p(cur), _p(lse),
-                                               _p(behav), C.byref(o), self._stream(stream)))
+        # K3 indexes its per-token inputs by the packed index: pass the full arrays
+        self._call(self.lib.copris_is_loss_bwd(self.h, C.byref(b), C.byref(c), _p(outs["cur_lp"]),
+                                               _p(outs["lse"]), _p(outs["behav"]), C.byref(o),
+                                               self._stream(stream)))
 
     def reduce(self, outs, n_tok: int, out4: torch.Tensor, row_base=0, stream=None):
         obj = outs["obj"][row_base:row_base + n_tok]
@@ -318,3 +320,55 @@ class Copris:
                               clipped_tokens=int(o[3]), cur_lp=outs["cur_lp"],
                               behav=outs.get("behav"), obj=outs["obj"], flags=outs["flags"],
                               coef=outs.get("coef"), lse=outs.get("lse"))
+
+
+class HostWorkspace:
+    """Device workspace for the host-buffer drop-in copris_grpo_step_loss_host
+    (host arrays in, host loss/counts/dlogits out; chunked, 3-stream pipeline)."""
+
+    def __init__(self, ctx: Copris, chunk_rows: int, vocab: int, max_tokens: int, max_traj: int,
+                 logits_dtype=torch.bfloat16, dlogits_dtype=torch.bfloat16):
+        self.ctx = ctx
+        self.vocab = vocab
+        self.logits_dtype, self.dlogits_dtype = logits_dtype, dlogits_dtype
+        h = C.c_void_p()
+        ctx._call(ctx.lib.copris_workspace_create(ctx.h, chunk_rows, vocab, _dtype_code(logits_dtype),
+                                                  _dtype_code(dlogits_dtype), max_tokens, max_traj,
+                                                  C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ctx.lib.copris_workspace_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def grpo_step_loss(self, logits: torch.Tensor, tok_off, target, stage, buffered_lp,
+                       cur_stage: int, *, adv=None, rewards=None, group_off=None,
+                       adv_epsilon: float = 1e-6, ref_lp=None, cfg: ClipConfig = None,
+                       is_enabled: bool = True, behav_mode: int = L.COPRIS_BEHAV_RECOMPUTED,
+                       total_tokens: int = 0, dlogits: Optional[torch.Tensor] = None,
+                       cur_lp: Optional[torch.Tensor] = None) -> dict:
+        """All tensors are CPU tensors (pin them for overlapped copies)."""
+        cfg = cfg or ClipConfig()
+        cfg.validate()
+        n_tok, v = logits.shape
+        hb = L.HostBatch(_p(logits), logits.stride(0), _dtype_code(logits.dtype), v, n_tok,
+                         tok_off.numel() - 1, _p(tok_off), _p(target), _p(stage), _p(buffered_lp),
+                         _p(ref_lp), _p(adv), _p(rewards), _p(group_off),
+                         (group_off.numel() - 1) if group_off is not None else 0, adv_epsilon,
+                         cur_stage, 0)
+        c = L.LossCfg(cfg.clip_low, cfg.clip_high, cfg.kl_coeff, cfg.entropy_coeff, int(is_enabled),
+                      behav_mode, total_tokens)
+        r = L.HostResult(_p(dlogits), dlogits.stride(0) if dlogits is not None else 0,
+                         _dtype_code(dlogits.dtype) if dlogits is not None else 0, 0, _p(cur_lp),
+                         0.0, 0.0, 0, 0, 0)
+        self.ctx._call(self.ctx.lib.copris_grpo_step_loss_host(self.ctx.h, self.h, C.byref(hb),
+                                                               C.byref(c), C.byref(r)))
+        return {"loss": r.loss, "objective": r.objective, "token_count": r.token_count,
+                "stale_tokens": r.stale_tokens, "clipped_tokens": r.clipped_tokens}

@@ -1,0 +1,17 @@
+#!/bin/bash
+# Profiling recipe (run under gpurun, 1 GPU; B200_PROFILING.md):
+#   1. launch list of the bench command (cold, serialised: compare SHARES)
+#   2. one `ncu --set full` capture of the fused kernel (and the unfused K3)
+# Outputs land in gpurun_out/; summaries are copied into profiles/ by hand.
+set -u
+OUT=${OUT:-gpurun_out}
+mkdir -p $OUT
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+    --log-file $OUT/launches.csv \
+    python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > $OUT/launches_bench.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:fused_ -s 3 -c 1 \
+    -o $OUT/prof_fused -f \
+    python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --chunk-rows 8192 > $OUT/prof_fused.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"bwd_kernel|logprob_gather" -s 2 -c 2 \
+    -o $OUT/prof_unfused -f \
+    python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --chunk-rows 8192 --unfused > $OUT/prof_unfused.log 2>&1

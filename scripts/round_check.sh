@@ -1,0 +1,9 @@
+# full GPU check: tests, bench (all arms), profiles. Logs in gpurun_out/.
+timeout 900 python -m pytest tests -q -m gpu --tb=short > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/gpu_tests.log
+python __graft_entry__.py smoke > gpurun_out/smoke.log 2>&1
+timeout 600 python bench.py > gpurun_out/bench.log 2>&1
+timeout 300 python bench.py --config grpo_128x8_v32000_L1024 --no-e2e --no-cpu-baseline > gpurun_out/bench_v32000.log 2>&1
+timeout 300 python bench.py --config grpo_128x8_v151936_longtail_4stage --no-e2e --no-cpu-baseline > gpurun_out/bench_longtail.log 2>&1
+timeout 300 python bench.py --unfused --no-e2e --no-cpu-baseline --steps 5 > gpurun_out/bench_unfused.log 2>&1
+timeout 300 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.log 2>&1
+bash profiles/run_profile.sh

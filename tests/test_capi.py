@@ -40,9 +40,13 @@ int main(void) {
   printf("copris_loss_batch %zu\n", sizeof(copris_loss_batch));
   printf("copris_loss_cfg %zu\n", sizeof(copris_loss_cfg));
   printf("copris_loss_out %zu\n", sizeof(copris_loss_out));
+  printf("copris_host_batch %zu\n", sizeof(copris_host_batch));
+  printf("copris_host_result %zu\n", sizeof(copris_host_result));
   F(copris_loss_batch, cur_stage) F(copris_loss_batch, adv) F(copris_loss_batch, tok_traj)
   F(copris_loss_cfg, total_tokens) F(copris_loss_cfg, behav_mode)
   F(copris_loss_out, flags) F(copris_loss_out, cur_lp)
+  F(copris_host_batch, adv_epsilon) F(copris_host_batch, cur_stage) F(copris_host_batch, group_off)
+  F(copris_host_result, loss) F(copris_host_result, clipped_tokens)
   return 0;
 }
 '''
@@ -57,11 +61,14 @@ int main(void) {
     assert int(got["copris_loss_batch"]) == C.sizeof(L.LossBatch)
     assert int(got["copris_loss_cfg"]) == C.sizeof(L.LossCfg)
     assert int(got["copris_loss_out"]) == C.sizeof(L.LossOut)
+    assert int(got["copris_host_batch"]) == C.sizeof(L.HostBatch)
+    assert int(got["copris_host_result"]) == C.sizeof(L.HostResult)
     for key, val in got.items():
         if "." in key:
             struct, field = key.split(".")
             cls = {"copris_loss_batch": L.LossBatch, "copris_loss_cfg": L.LossCfg,
-                   "copris_loss_out": L.LossOut}[struct]
+                   "copris_loss_out": L.LossOut, "copris_host_batch": L.HostBatch,
+                   "copris_host_result": L.HostResult}[struct]
             assert getattr(cls, field).offset == int(val), key
 
 

@@ -21,23 +21,38 @@ def run(ctx, case, dl_dtype=BF16, fused=True, **kw):
                                     dlogits_dtype=dl_dtype, coef=True, **kw)
 
 
-# (V, logits dtype, expected kernel, expected cluster)
+# (V, logits dtype, forced implementation or None, expected kernel, expected cluster)
 SHAPES = [
-    (151936, BF16, "fused_tma_kernel", 2),   # Qwen2.5 vocab: row split over a CTA pair
-    (32000, BF16, "fused_tma_kernel", 1),    # 64 KB rows: 8-warp CTAs, several per SM
-    (80000, BF16, "fused_tma_kernel", 1),    # 160 KB rows: one 16-warp CTA per row
-    (151936, F32, "fused_tma_kernel", 4),    # 608 KB f32 rows: 4-CTA cluster
-    (32000, F32, "fused_tma_kernel", 1),
-    (256, BF16, "fused_tma_kernel", 1),
-    (4099, BF16, "fused_generic_kernel", 1),  # odd vocab: unaligned rows
-    (100, F32, "fused_generic_kernel", 1),
-    (6, F32, "fused_generic_kernel", 1),      # desk vocab
+    (151936, BF16, None, "fused_stream_kernel", 1),   # Qwen2.5 vocab: TMA ring + L2 re-read
+    (151936, BF16, "tma", "fused_tma_kernel", 2),     # row split over a CTA pair (DSMEM)
+    (151936, BF16, "l2", "fused_l2_kernel", 1),       # register-streamed two-pass variant
+    (32000, BF16, None, "fused_tma_kernel", 1),       # 64 KB rows resident, several CTAs/SM
+    (32000, BF16, "stream", "fused_stream_kernel", 1),
+    (80000, BF16, "tma", "fused_tma_kernel", 1),      # 160 KB rows: one 16-warp CTA per row
+    (151936, F32, None, "fused_stream_kernel", 1),
+    (151936, F32, "tma", "fused_tma_kernel", 4),      # 608 KB f32 rows: 4-CTA cluster
+    (32000, F32, None, "fused_stream_kernel", 1),
+    (256, BF16, None, "fused_tma_kernel", 1),
+    (4099, BF16, None, "fused_generic_kernel", 1),    # odd vocab: unaligned rows
+    (100, F32, None, "fused_generic_kernel", 1),
+    (6, F32, None, "fused_generic_kernel", 1),        # desk vocab
 ]
 
 
-@pytest.mark.parametrize("V,dtype,kernel,cluster", SHAPES)
+@pytest.fixture
+def impl(monkeypatch):
+    def set_impl(name):
+        if name:
+            monkeypatch.setenv("COPRIS_FUSED_IMPL", name)
+        else:
+            monkeypatch.delenv("COPRIS_FUSED_IMPL", raising=False)
+    return set_impl
+
+
+@pytest.mark.parametrize("V,dtype,force,kernel,cluster", SHAPES)
 @pytest.mark.parametrize("dl_dtype", [BF16, F32])
-def test_fused_matches_oracle(ctx, oracle, V, dtype, kernel, cluster, dl_dtype):
+def test_fused_matches_oracle(ctx, oracle, impl, V, dtype, force, kernel, cluster, dl_dtype):
+    impl(force)
     P, G = (2, 4) if V > 50000 else (4, 4)
     case = Case(oracle, seed=V % 97 + 3, P=P, G=G, V=V, dtype=dtype, mu=math.log(10), lmax=24)
     _, res = run(ctx, case, dl_dtype)
@@ -54,13 +69,15 @@ def test_unfused_matches_oracle(ctx, oracle, V, dtype):
     case.check(res, F32, what=f"unfused V={V}")
 
 
-@pytest.mark.parametrize("V", [151936, 32000, 4099])
-def test_kl_and_entropy(ctx, oracle, V):
+@pytest.mark.parametrize("V,force", [(151936, None), (151936, "tma"), (151936, "l2"),
+                                     (32000, None), (32000, "stream"), (4099, None)])
+def test_kl_and_entropy(ctx, oracle, impl, V, force):
+    impl(force)
     case = Case(oracle, seed=5, P=2, G=4, V=V, mu=math.log(10), lmax=24, kl_coeff=0.1,
                 entropy_coeff=0.01)
     for fused in (True, False):
         _, res = run(ctx, case, F32, fused=fused)
-        case.check(res, F32, what=f"kl+entropy V={V} fused={fused}")
+        case.check(res, F32, what=f"kl+entropy V={V} fused={fused} impl={force}")
 
 
 def test_is_off_every_ratio_is_one(ctx, oracle):
@@ -190,6 +207,18 @@ def test_deterministic_and_chunk_invariant(ctx, oracle):
     assert -out4[0].item() * (1.0 / T) == r1.loss
     assert torch.equal(dl, r1.dlogits)
     assert torch.equal(outs["cur_lp"], r1.cur_lp)
+    # the unfused K1 -> K2 -> K3 pipeline, chunked, equals its one-shot run
+    u1 = ctx.grpo_step_loss(logits, batch, case.clip(), fused=False)
+    outs = ctx.alloc_outputs(T, logits.device)
+    for a in range(0, T, 37):
+        b = min(T, a + 37)
+        ctx.loss_chunk_unfused(logits[a:b], batch, case.clip(), outs, dlogits=dl[a:b], row_base=a,
+                               total_tokens=T)
+    ctx.reduce(outs, T, out4)
+    ctx.check()
+    assert -out4[0].item() * (1.0 / T) == u1.loss
+    assert torch.equal(dl, u1.dlogits)
+    case.check(u1, torch.bfloat16, what="unfused one-shot")
 
 
 def test_padded_rows(ctx, oracle):
@@ -248,3 +277,38 @@ def test_expand_segments(ctx):
     np.testing.assert_array_equal(st.cpu().numpy().view(np.uint32), hb.stage)
     tt = ctx.token_traj(torch.from_numpy(hb.tok_off).cuda(), hb.n_tok).cpu().numpy()
     np.testing.assert_array_equal(tt, np.repeat(np.arange(hb.n_traj), np.diff(hb.tok_off)))
+
+
+def test_host_buffer_dropin(ctx, oracle):
+    """copris_grpo_step_loss_host: host arrays in (pinned), 3-stream chunked
+    pipeline, host loss/counts/dlogits out — same numbers as the oracle."""
+    from paper_2511_05589_b200.grpo import HostWorkspace
+    case = Case(oracle, seed=19, P=4, G=4, V=32000, mu=math.log(20), lmax=64)
+    hb = case.hb
+    T = hb.n_tok
+    ws = HostWorkspace(ctx, chunk_rows=29, vocab=32000, max_tokens=T, max_traj=hb.n_traj,
+                       dlogits_dtype=F32)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    logits = case.logits_cpu.pin_memory()
+    dl = torch.empty((T, 32000), dtype=F32).pin_memory()
+    cur = torch.empty(T, dtype=F32).pin_memory()
+    out = ws.grpo_step_loss(logits, pin(hb.tok_off), pin(hb.target), pin(hb.stage.view(np.int32)),
+                            pin(case.blp), hb.cur_stage, rewards=pin(hb.reward),
+                            group_off=pin(hb.group_off), cfg=case.clip(), dlogits=dl, cur_lp=cur)
+    ref = case.ref
+    assert out["token_count"] == T
+    assert out["stale_tokens"] == ref.stale_tokens
+    assert out["clipped_tokens"] == ref.clipped_tokens
+    assert_scalar_close(cur.numpy(), ref.cur_lp, what="host cur_lp")
+    from parity_util import assert_loss_close
+    assert_loss_close(out["loss"], ref.loss, ref.obj, T, what="host loss")
+    atol = (32000 + 8) * 2.0 ** -52 * np.abs(ref.weight) / T
+    assert_rows_close(dl.numpy(), ref.dlogits, what="host dlogits", row_atol=atol)
+    # errors keep the reference's semantics
+    from paper_2511_05589_b200 import ConfigError
+    bad = pin(np.array([0, 1, 3], np.int64))
+    with pytest.raises(ConfigError, match="advantage group size must be >= 2"):
+        ws.grpo_step_loss(logits[:3], pin(np.array([0, 1, 2, 3], np.int64)), pin(hb.target[:3]),
+                          pin(hb.stage[:3].view(np.int32)), pin(case.blp[:3]), hb.cur_stage,
+                          rewards=pin(np.zeros(3)), group_off=bad, cfg=case.clip())
+    ws.close()
