@@ -57,37 +57,6 @@ def parse_args():
 
 
 # ---------------------------------------------------------------------------
-# sharding: deterministic LPT over whole prompt groups
-# ---------------------------------------------------------------------------
-def lpt_shard(group_tokens, world):
-    order = sorted(range(len(group_tokens)), key=lambda g: (-int(group_tokens[g]), g))
-    load = [0] * world
-    out = [[] for _ in range(world)]
-    for g in order:
-        r = min(range(world), key=lambda k: (load[k], k))
-        out[r].append(g)
-        load[r] += int(group_tokens[g])
-    return [sorted(x) for x in out]
-
-
-def local_batch(hb, groups):
-    """Rank-local packed arrays for a list of group ids (batch order kept)."""
-    import numpy as np
-    tok_off, group_off, target, stage, reward = [0], [0], [], [], []
-    for g in groups:
-        a, b = hb.group_off[g], hb.group_off[g + 1]
-        for i in range(a, b):
-            t0, t1 = hb.tok_off[i], hb.tok_off[i + 1]
-            target.append(hb.target[t0:t1])
-            stage.append(hb.stage[t0:t1])
-            tok_off.append(tok_off[-1] + (t1 - t0))
-            reward.append(hb.reward[i])
-        group_off.append(group_off[-1] + (b - a))
-    return (np.asarray(tok_off, np.int64), np.asarray(group_off, np.int64),
-            np.concatenate(target), np.concatenate(stage), np.asarray(reward, np.float64))
-
-
-# ---------------------------------------------------------------------------
 # clocks during the timed region (B200_PROFILING.md recipe)
 # ---------------------------------------------------------------------------
 class ClockSampler:
@@ -264,6 +233,7 @@ def run_ours(args):
     from paper_2511_05589_b200 import ClipConfig, Copris
     from paper_2511_05589_b200.grpo import HostWorkspace
     from paper_2511_05589_b200.packing import upload
+    from paper_2511_05589_b200.sharding import allreduce_scalars, lpt_shard, shard_arrays
     from paper_2511_05589_b200.workload import CONFIGS, make_host_batch, make_logits, stale_logprobs
 
     rank = int(os.environ.get("RANK", "0"))
@@ -281,7 +251,9 @@ def run_ours(args):
     cfgd.pop("vocab")
     hb = make_host_batch(args.seed, P_rank * world, G, V, **cfgd)
     shards = lpt_shard(hb.group_tokens(), world)
-    tok_off, group_off, target_g, stage, reward = local_batch(hb, shards[rank])
+    tok_off, group_off, pt, pj, _ = shard_arrays(hb.tok_off, hb.group_off, {"stage": hb.stage},
+                                                 {"reward": hb.reward}, shards[rank])
+    stage, reward = pt["stage"], pj["reward"]
     T_global, T = hb.n_tok, int(tok_off[-1])
     chunk = min(args.chunk_rows, T)
     nchunks = (T + chunk - 1) // chunk
@@ -317,8 +289,7 @@ def run_ours(args):
             if evs is not None:
                 evs[c][1].record()
         ctx.reduce(outs, T, out4)
-        if world > 1:
-            dist.all_reduce(out4)
+        allreduce_scalars(out4)
 
     for _ in range(max(args.warmup, 1)):
         step()

@@ -775,7 +775,7 @@ __global__ void __launch_bounds__(WARPS * 32)
 // phase — it runs ahead into the next row as far as the ring allows — so HBM
 // stays busy while the consumers synchronise, and no cluster couples SMs.
 // ---------------------------------------------------------------------------
-constexpr int kStreamSlotVec = 2048;  // 16-byte vectors per ring slot (32 KB)
+constexpr int kStreamK = 4;  // 16-byte vectors per consumer thread per ring slot
 
 // Which fp32 pairs of a 16-byte vector take 2^x on the FMA pipe instead of
 // MUFU (bit i = pair i). MUFU.EX2 issues 16 results/clk/SM and two of them per
@@ -806,13 +806,13 @@ struct Ring {
 template <typename TIn, typename TOut, int CW, bool ENT>
 __global__ void __launch_bounds__((CW + 1) * 32, CW <= 8 ? 2 : 1)
     fused_stream_kernel(const LossParams P, const int nslots) {
+  constexpr int kStreamSlotVec = CW * 32 * kStreamK;  // vectors per ring slot
   using VI = Vec<TIn>;
   using PB = PassB<TIn>;
   constexpr int VN = VI::N;
   constexpr int NP = VN / 2;
   constexpr int NC = CW * 32;                  // consumer threads
-  constexpr int K = kStreamSlotVec / NC;       // vectors per consumer thread per slot
-  static_assert(kStreamSlotVec % NC == 0, "slot must split evenly over consumers");
+  constexpr int K = kStreamK;                  // vectors per consumer thread per slot
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[32], empty[32];
   __shared__ Lse red[CW];
@@ -1528,8 +1528,9 @@ cudaError_t launch_l2(const LossParams& p, int num_sms, cudaStream_t stream, Lau
 template <typename TIn, typename TOut, int CW, bool ENT>
 cudaError_t launch_stream(const LossParams& p, int num_sms, cudaStream_t stream, LaunchInfo* info) {
   auto kernel = fused_stream_kernel<TIn, TOut, CW, ENT>;
-  const int nslots = tune_env("COPRIS_TUNE_SLOTS", CW >= 16 ? 6 : 3);
-  const int smem = nslots * kStreamSlotVec * 16;
+  constexpr int slot_bytes = CW * 32 * kStreamK * 16;
+  const int nslots = tune_env("COPRIS_TUNE_SLOTS", (CW >= 16 ? 196608 : 98304) / slot_bytes);
+  const int smem = nslots * slot_bytes;
   cudaError_t e = set_smem(kernel, smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
@@ -1581,6 +1582,7 @@ cudaError_t dispatch_fused(const LossParams& p, int num_sms, cudaStream_t stream
     if (impl == 1) {
       const int w = tune_env("COPRIS_TUNE_WARPS", 16);
       if (w == 8) return launch_stream<TIn, TOut, 8, ENT>(p, num_sms, stream, info);
+      if (w == 24) return launch_stream<TIn, TOut, 24, ENT>(p, num_sms, stream, info);
       return launch_stream<TIn, TOut, 16, ENT>(p, num_sms, stream, info);
     }
     if (impl == 3) {

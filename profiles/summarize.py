@@ -1,0 +1,111 @@
+"""Summarise a profiling run (profiles/run_profile.sh output in gpurun_out/)
+into committed, reviewable files under profiles/:
+
+  <tag>_launches.csv     kernel, launches, total/avg device time, share of the
+                         bench command (ncu --metrics gpu__time_duration.sum)
+  <tag>_ncu_<kernel>.txt key metrics + stall breakdown of one `ncu --set full`
+                         capture per kernel
+  ncu_traffic.json       dram bytes per row of the top kernel (read by bench.py
+                         for roofline.traffic)
+
+usage: python profiles/summarize.py <tag> [gpurun_out]
+"""
+import collections
+import csv
+import json
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "dram__bytes.sum.per_second", "launch__grid_size", "launch__block_size",
+        "launch__registers_per_thread", "launch__cluster_dim_x", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+        "lts__t_sector_hit_rate.pct", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
+
+
+def launches(src, dst):
+    rows = list(csv.reader(open(src)))
+    start = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
+    hdr = rows[start]
+    ix = {h: j for j, h in enumerate(hdr)}
+    tot, cnt = collections.defaultdict(float), collections.Counter()
+    for r in rows[start + 1:]:
+        if len(r) < len(hdr):
+            continue
+        name = r[ix["Kernel Name"]].split("(")[0].replace("void ", "")
+        tot[name] += float(r[ix["Metric Value"]].replace(",", ""))
+        cnt[name] += 1
+    s = sum(tot.values())
+    with open(dst, "w") as f:
+        f.write("kernel,launches,total_ns,avg_ns,share\n")
+        for k, v in sorted(tot.items(), key=lambda x: -x[1]):
+            f.write(f"\"{k}\",{cnt[k]},{v:.0f},{v / cnt[k]:.0f},{v / s:.4f}\n")
+
+
+def ncu_summary(rep, dst_prefix, rows_per_launch):
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(raw.splitlines()))
+    hdr, units = rows[0], rows[1]
+    out = {}
+    for r in rows[2:]:
+        name = r[hdr.index("Kernel Name")]
+        short = name.split("<")[0].split("::")[-1].strip()
+        lines = [f"kernel: {name}"]
+        for k in KEYS:
+            if k in hdr:
+                lines.append(f"{k:70s} {r[hdr.index(k)]} {units[hdr.index(k)]}")
+        stalls = []
+        for i, h in enumerate(hdr):
+            if "warps_issue_stalled" in h and "not_issued" not in h:
+                try:
+                    stalls.append((float(r[i].replace(",", "")), h.replace("smsp__pcsamp_warps_issue_stalled_", "")))
+                except ValueError:
+                    pass
+        tot = sum(v for v, _ in stalls) or 1.0
+        lines.append("stall samples: " + ", ".join(f"{h}={100 * v / tot:.1f}%" for v, h in
+                                                   sorted(stalls, reverse=True)[:10]))
+        rd = float(r[hdr.index("dram__bytes_read.sum")].replace(",", ""))
+        wr = float(r[hdr.index("dram__bytes_write.sum")].replace(",", ""))
+        scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
+        rd *= scale.get(units[hdr.index("dram__bytes_read.sum")], 1.0)
+        wr *= scale.get(units[hdr.index("dram__bytes_write.sum")], 1.0)
+        lines.append(f"dram bytes per row (read+write) over {rows_per_launch} rows: "
+                     f"{(rd + wr) / rows_per_launch:.0f}")
+        out[short] = (rd + wr) / rows_per_launch
+        with open(f"{dst_prefix}_{short}.txt", "w") as f:
+            f.write("\n".join(lines) + "\n")
+    return out
+
+
+def main():
+    tag = sys.argv[1]
+    src = sys.argv[2] if len(sys.argv) > 2 else os.path.join(os.path.dirname(HERE), "gpurun_out")
+    if os.path.exists(os.path.join(src, "launches.csv")):
+        launches(os.path.join(src, "launches.csv"), os.path.join(HERE, f"{tag}_launches.csv"))
+    traffic = {}
+    rows = 8192  # run_profile.sh captures with --chunk-rows 8192
+    if os.path.exists(os.path.join(src, "prof_fused.ncu-rep")):
+        t = ncu_summary(os.path.join(src, "prof_fused.ncu-rep"), os.path.join(HERE, f"{tag}_ncu"), rows)
+        for k, v in t.items():
+            traffic["grpo_128x8_v151936"] = {"dram_bytes_per_row": v, "kernel": k,
+                                             "source": f"profiles/{tag}_ncu_{k}.txt"}
+    if os.path.exists(os.path.join(src, "prof_unfused.ncu-rep")):
+        t = ncu_summary(os.path.join(src, "prof_unfused.ncu-rep"), os.path.join(HERE, f"{tag}_ncu"), rows)
+        if t:
+            traffic["unfused:grpo_128x8_v151936"] = {"dram_bytes_per_row": sum(t.values()),
+                                                     "kernel": "+".join(t),
+                                                     "source": "sum of the unfused kernels"}
+    if traffic:
+        with open(os.path.join(HERE, "ncu_traffic.json"), "w") as f:
+            json.dump(traffic, f, indent=1)
+    print("wrote", sorted(os.listdir(HERE)))
+
+
+if __name__ == "__main__":
+    main()

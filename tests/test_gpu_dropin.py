@@ -1,0 +1,28 @@
+"""GPU: the reference Trainer with the C++ drop-in at its grpo_step_loss seam.
+
+oracle/_ref/dropin_check (built from the UNMODIFIED reference headers plus
+include/copris_b200/grpo_dropin.hpp, linked against libcopris_b200.so) runs
+reference Trainer steps and, with the exact arguments trainer.hpp:176 passes,
+compares the reference grpo_step_loss with the GPU path: loss within 1e-5 and
+the table gradient within 1e-5 of its max, on every captured step."""
+import json
+import os
+import subprocess
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+EXE = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref",
+                   "dropin_check")
+
+
+@pytest.mark.skipif(not os.path.exists(EXE), reason="oracle/_ref/dropin_check not built")
+def test_reference_trainer_with_gpu_dropin():
+    p = subprocess.run([EXE], capture_output=True, text=True, timeout=600)
+    lines = [json.loads(l) for l in p.stdout.splitlines() if l.startswith("{")]
+    assert lines, p.stderr
+    bad = [l for l in lines if not l["ok"]]
+    assert not bad, bad[:3]
+    assert p.returncode == 0, p.stderr
+    assert {l["case"] for l in lines} >= {"desk", "b16_c48", "b16_c48_is_off", "b16_c48_kl_entropy"}
