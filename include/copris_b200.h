@@ -244,6 +244,61 @@ COPRIS_API int copris_grpo_step_loss_host(copris_ctx* ctx, copris_workspace* ws,
                                           const copris_host_batch* batch,
                                           const copris_loss_cfg* cfg, copris_host_result* out);
 
+/* ---- Host rollout buffer / scheduler (rollout.hpp:125-386) -----------------
+ * The concurrency-controlled scheduler stays host-side bookkeeping
+ * (include/copris_b200/rollout.hpp, bit-exact decisions); these entry points
+ * expose it to non-C++ callers. `ids` outputs are caller buffers of `cap`
+ * entries; `*n` receives the count (COPRIS_E_INVALID if cap is too small). */
+typedef struct copris_engine copris_engine;
+
+enum copris_sched_mode { COPRIS_SYNCHRONOUS = 0, COPRIS_NAIVE_PARTIAL = 1, COPRIS_COPRIS = 2 };
+enum copris_engine_list {
+  COPRIS_LIST_IN_FLIGHT = 0, COPRIS_LIST_RESUME_QUEUE = 1, COPRIS_LIST_BUFFERED = 2,
+  COPRIS_LIST_CONSUMED = 3, COPRIS_LIST_EVICTED = 4
+};
+
+typedef struct {
+  int32_t mode;                /* copris_sched_mode */
+  int32_t concurrency, batch_prompts, rollouts_per_prompt, max_response_len, max_staleness;
+  int32_t num_classes, horizon, vocab, answer_vocab;
+  uint64_t seed;               /* question classes come from stream (seed, "prompt") */
+} copris_engine_cfg;
+
+/* A formed training batch in the packed layout (caller-owned host buffers,
+ * sized from copris_engine_early_terminate's sizes[] = {groups, trajectories,
+ * tokens, segments}). */
+typedef struct {
+  uint64_t rollout_version;    /* out */
+  int64_t* group_off;          /* [groups+1] */
+  uint64_t* group_ids;         /* [groups] */
+  int32_t* group_class;        /* [groups] */
+  uint64_t* traj_ids;          /* [traj] */
+  int64_t* tok_off;            /* [traj+1] */
+  int32_t* tokens;             /* [tokens] */
+  int64_t* seg_off;            /* [segments+1] */
+  uint32_t* seg_ver;           /* [segments] */
+  float* buffered_lp;          /* [tokens] concat_segments */
+  uint32_t* stage;             /* [tokens] */
+  uint8_t* terminated;         /* [traj] */
+  int32_t* answer_target;      /* [traj] */
+} copris_packed_host;
+
+COPRIS_API int copris_engine_create(const copris_engine_cfg* cfg, copris_engine** out);
+COPRIS_API int copris_engine_destroy(copris_engine* e);
+COPRIS_API int copris_engine_begin_stage(copris_engine* e, uint64_t version, uint64_t* ids,
+                                         int64_t cap, int64_t* n);
+COPRIS_API int copris_engine_refill_active(copris_engine* e, uint64_t* ids, int64_t cap, int64_t* n);
+COPRIS_API int copris_engine_append_token(copris_engine* e, uint64_t id, int32_t token, double logprob,
+                                          int32_t* terminated);
+COPRIS_API int copris_engine_complete(copris_engine* e, uint64_t id, int32_t* batch_ready);
+COPRIS_API int copris_engine_early_terminate(copris_engine* e, int64_t sizes[4]);
+COPRIS_API int copris_engine_batch_copy(const copris_engine* e, copris_packed_host* out);
+COPRIS_API int copris_engine_list(const copris_engine* e, int32_t which, uint64_t* ids, int64_t cap,
+                                  int64_t* n);
+/* out[7] = {in_flight, buffered partials, buffered completes, total admitted,
+ *           stage version, batch ready, stage tokens in buffer} */
+COPRIS_API int copris_engine_stats(const copris_engine* e, int64_t out[7]);
+
 /* Introspection (not a reference entry point): cluster size, grid and kernel
  * name of the last copris_is_loss_* launch on this context. */
 COPRIS_API int copris_ctx_last_launch(const copris_ctx* ctx, int* cluster, int* grid, int* num_sms,

@@ -55,6 +55,20 @@ class HostResult(C.Structure):
                 ("stale_tokens", I64), ("clipped_tokens", I64)]
 
 
+class EngineCfg(C.Structure):
+    _fields_ = [("mode", I32), ("concurrency", I32), ("batch_prompts", I32),
+                ("rollouts_per_prompt", I32), ("max_response_len", I32), ("max_staleness", I32),
+                ("num_classes", I32), ("horizon", I32), ("vocab", I32), ("answer_vocab", I32),
+                ("seed", C.c_uint64)]
+
+
+class PackedHostC(C.Structure):
+    _fields_ = [("rollout_version", C.c_uint64), ("group_off", P), ("group_ids", P),
+                ("group_class", P), ("traj_ids", P), ("tok_off", P), ("tokens", P), ("seg_off", P),
+                ("seg_ver", P), ("buffered_lp", P), ("stage", P), ("terminated", P),
+                ("answer_target", P)]
+
+
 _SIGS = {
     "copris_abi_version": ([], C.c_int),
     "copris_last_error": ([], C.c_char_p),
@@ -77,6 +91,16 @@ _SIGS = {
     "copris_grpo_step_loss_host": ([P, P, C.POINTER(HostBatch), C.POINTER(LossCfg),
                                     C.POINTER(HostResult)], C.c_int),
     "copris_ctx_trace_read": ([P, P, C.c_int], C.c_int),
+    "copris_engine_create": ([C.POINTER(EngineCfg), C.POINTER(P)], C.c_int),
+    "copris_engine_destroy": ([P], C.c_int),
+    "copris_engine_begin_stage": ([P, C.c_uint64, P, I64, C.POINTER(I64)], C.c_int),
+    "copris_engine_refill_active": ([P, P, I64, C.POINTER(I64)], C.c_int),
+    "copris_engine_append_token": ([P, C.c_uint64, I32, D, C.POINTER(I32)], C.c_int),
+    "copris_engine_complete": ([P, C.c_uint64, C.POINTER(I32)], C.c_int),
+    "copris_engine_early_terminate": ([P, P], C.c_int),
+    "copris_engine_batch_copy": ([P, C.POINTER(PackedHostC)], C.c_int),
+    "copris_engine_list": ([P, I32, P, I64, C.POINTER(I64)], C.c_int),
+    "copris_engine_stats": ([P, P], C.c_int),
     "copris_ctx_last_launch": ([P, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
                                 C.POINTER(C.c_char_p)], C.c_int),
 }
