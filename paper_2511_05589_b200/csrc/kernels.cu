@@ -346,7 +346,7 @@ __device__ __forceinline__ void store_pairs(TOut* p, const uint64_t* g, uint64_t
 }
 
 template <typename TIn, typename TOut, int CL, int WARPS, bool ENT>
-__global__ void __launch_bounds__(WARPS * 32, 1)
+__global__ void __launch_bounds__(WARPS * 32, (WARPS == 8 && CL == 1) ? 3 : 1)
     fused_tma_kernel(const LossParams P, const int32_t E) {
   using VI = Vec<TIn>;
   using PB = PassB<TIn>;
@@ -439,43 +439,54 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
         }
       }
     } else {
-      float m = -INFINITY;
-      uint64_t negm = ptx::f2(INFINITY, INFINITY);
-      uint64_t acc0 = ptx::f2(0.f, 0.f), acc1 = acc0;
-      const uint64_t L2 = ptx::f2(kLog2e, kLog2e);
+      float m = -INFINITY, nml = INFINITY;
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
       for (int p = 0; p < npieces; ++p) {
         ptx::mbar_wait_u32(barbase + p * 8, par);
         const int32_t v0 = wv0 + p * pv, v1 = min(wv1, v0 + pv);
+        // does this piece hold the target column? (warp-uniform)
+        const bool tpiece = static_cast<uint32_t>(ycol - v0 * VN) < static_cast<uint32_t>((v1 - v0) * VN);
         for (int32_t v = v0 + lane; v < v1; v += 64) {
           const bool two = v + 32 < v1;
           const uint4 a = ptx::lds_v4(sbase + v * 16);
-          const uint4 ninf{PB::kNegInfWord, PB::kNegInfWord, PB::kNegInfWord, PB::kNegInfWord};
-          const uint4 b = two ? ptx::lds_v4(sbase + (v + 32) * 16) : ninf;
+          uint4 b;
+          if (two) {
+            b = ptx::lds_v4(sbase + (v + 32) * 16);
+          } else {
+            b = uint4{PB::kNegInfWord, PB::kNegInfWord, PB::kNegInfWord, PB::kNegInfWord};
+          }
           const float vm = PB::vmax(a, b);
           if (vm > m) {
             const float rs = ptx::ex2((m - vm) * kLog2e);  // 0 while m = -inf
-            const uint64_t rs2 = ptx::f2(rs, rs);
-            acc0 = ptx::fmul2(acc0, rs2);
-            acc1 = ptx::fmul2(acc1, rs2);
+            s0 *= rs;
+            s1 *= rs;
+            s2 *= rs;
+            s3 *= rs;
             m = vm;
-            negm = ptx::f2(-m, -m);
+            nml = -(m * kLog2e);
           }
-          uint64_t xa[4], xb[4];
-          PB::unpack2(a, xa);
-          PB::unpack2(b, xb);
-          const int ja = ycol - v * VN, jb = ja - 32 * VN;
-          if (static_cast<uint32_t>(ja) < VN) kill_col(xa, ja);
-          if (static_cast<uint32_t>(jb) < VN) kill_col(xb, jb);
+          float xa[VN], xb[VN];
+          VI::unpack(a, xa);
+          VI::unpack(b, xb);
+          if (tpiece) {  // keep the target column out of s (see Lse)
+            const int ja = ycol - v * VN, jb = ja - 32 * VN;
 #pragma unroll
-          for (int i = 0; i < NP; ++i) {
-            acc0 = ptx::fadd2(acc0, ptx::ex2x2(ptx::fmul2(ptx::fadd2(xa[i], negm), L2)));
-            acc1 = ptx::fadd2(acc1, ptx::ex2x2(ptx::fmul2(ptx::fadd2(xb[i], negm), L2)));
+            for (int q = 0; q < VN; ++q) {
+              if (q == ja) xa[q] = -INFINITY;
+              if (q == jb) xb[q] = -INFINITY;
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < VN; q += 2) {
+            s0 += ptx::ex2(fmaf(xa[q], kLog2e, nml));
+            s1 += ptx::ex2(fmaf(xa[q + 1], kLog2e, nml));
+            s2 += ptx::ex2(fmaf(xb[q], kLog2e, nml));
+            s3 += ptx::ex2(fmaf(xb[q + 1], kLog2e, nml));
           }
         }
       }
-      const uint64_t acc = ptx::fadd2(acc0, acc1);
       st.m = m;
-      st.s = ptx::f2lo(acc) + ptx::f2hi(acc);
+      st.s = (s0 + s1) + (s2 + s3);
     }
     tm.mark(0);
     warp_lse<ENT>(st);
@@ -536,10 +547,6 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
     const RowBroadcast b = bc;
     const bool zero_row = (b.coef == 0.f) && (!ENT || b.eg == 0.f);
     TOut* drow = P.dlogits ? static_cast<TOut*>(P.dlogits) + r * P.ld_d + col0 : nullptr;
-    const uint64_t negM = ptx::f2(-b.m, -b.m);
-    const uint64_t L2 = ptx::f2(kLog2e, kLog2e);
-    const uint64_t nl2s = ptx::f2(-b.log2s, -b.log2s);
-    const uint64_t ncoef = ptx::f2(-b.coef, -b.coef);
     for (int p = 0; p < npieces; ++p) {
       const int32_t v0 = wv0 + p * pv, v1 = min(wv1, v0 + pv);
       if (drow) {
@@ -558,35 +565,26 @@ __global__ void __launch_bounds__(WARPS * 32, 1)
           }
         } else {
           // two vectors per iteration: both shared-memory loads issue first
+          const bool tpiece = static_cast<uint32_t>(b.y - (col0 + v0 * VN)) < static_cast<uint32_t>((v1 - v0) * VN);
           for (int32_t v = v0 + lane; v < v1; v += 64) {
             const bool two = v + 32 < v1;
-            uint64_t xa[4], xb[4];
             const uint4 ra = ptx::lds_v4(sbase + v * 16);
             const uint4 rb = two ? ptx::lds_v4(sbase + (v + 32) * 16) : ra;
-            PB::unpack2(ra, xa);
-            PB::unpack2(rb, xb);
-            float da[VN], db[VN];
+            float xa[VN], xb[VN], da[VN], db[VN];
+            VI::unpack(ra, xa);
+            VI::unpack(rb, xb);
 #pragma unroll
-            for (int i = 0; i < NP; ++i) {
-              const uint64_t ga =
-                  ptx::fmul2(ptx::ex2x2(ptx::ffma2(ptx::fadd2(xa[i], negM), L2, nl2s)), ncoef);
-              const uint64_t gb =
-                  ptx::fmul2(ptx::ex2x2(ptx::ffma2(ptx::fadd2(xb[i], negM), L2, nl2s)), ncoef);
-              da[2 * i] = ptx::f2lo(ga);
-              da[2 * i + 1] = ptx::f2hi(ga);
-              db[2 * i] = ptx::f2lo(gb);
-              db[2 * i + 1] = ptx::f2hi(gb);
+            for (int q = 0; q < VN; ++q) {
+              da[q] = ptx::ex2(fmaf(xa[q], kLog2e, -b.c1)) * -b.coef;
+              db[q] = ptx::ex2(fmaf(xb[q], kLog2e, -b.c1)) * -b.coef;
             }
-            const int ja = b.y - (col0 + v * VN), jb = ja - 32 * VN;
-            if (static_cast<uint32_t>(ja) < VN) {
+            if (tpiece) {
+              const int ja = b.y - (col0 + v * VN), jb = ja - 32 * VN;
 #pragma unroll
-              for (int j = 0; j < VN; ++j)
-                if (j == ja) da[j] = b.dy;
-            }
-            if (static_cast<uint32_t>(jb) < VN) {
-#pragma unroll
-              for (int j = 0; j < VN; ++j)
-                if (j == jb) db[j] = b.dy;
+              for (int q = 0; q < VN; ++q) {
+                if (q == ja) da[q] = b.dy;
+                if (q == jb) db[q] = b.dy;
+              }
             }
             store_vec<TOut, VN>(drow + static_cast<int64_t>(v) * VN, da, pol);
             if (two) store_vec<TOut, VN>(drow + static_cast<int64_t>(v + 32) * VN, db, pol);
