@@ -239,10 +239,19 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus if args.gpus == 1 else 1)))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # control-flow rehearsal of the multi-rank path on a single GPU (not a
+    # measurement): COPRIS_BENCH_ONE_GPU=1 puts every rank on cuda:0 and
+    # COPRIS_BENCH_BACKEND=gloo replaces NCCL (which refuses shared devices)
+    if os.environ.get("COPRIS_BENCH_ONE_GPU"):
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("COPRIS_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     cfgd = dict(CONFIGS[args.config])
     V = cfgd["vocab"]

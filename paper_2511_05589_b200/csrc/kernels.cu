@@ -801,16 +801,16 @@ struct Ring {
   }
 };
 
-template <typename TIn, typename TOut, int CW, bool ENT>
+template <typename TIn, typename TOut, int CW, int KV, bool ENT>
 __global__ void __launch_bounds__((CW + 1) * 32, CW <= 8 ? 2 : 1)
     fused_stream_kernel(const LossParams P, const int nslots) {
-  constexpr int kStreamSlotVec = CW * 32 * kStreamK;  // vectors per ring slot
+  constexpr int kStreamSlotVec = CW * 32 * KV;  // vectors per ring slot
   using VI = Vec<TIn>;
   using PB = PassB<TIn>;
   constexpr int VN = VI::N;
   constexpr int NP = VN / 2;
   constexpr int NC = CW * 32;                  // consumer threads
-  constexpr int K = kStreamK;                  // vectors per consumer thread per slot
+  constexpr int K = KV;                        // vectors per consumer thread per slot
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[32], empty[32];
   __shared__ Lse red[CW];
@@ -1523,10 +1523,10 @@ cudaError_t launch_l2(const LossParams& p, int num_sms, cudaStream_t stream, Lau
   return cudaGetLastError();
 }
 
-template <typename TIn, typename TOut, int CW, bool ENT>
+template <typename TIn, typename TOut, int CW, bool ENT, int KV = kStreamK>
 cudaError_t launch_stream(const LossParams& p, int num_sms, cudaStream_t stream, LaunchInfo* info) {
-  auto kernel = fused_stream_kernel<TIn, TOut, CW, ENT>;
-  constexpr int slot_bytes = CW * 32 * kStreamK * 16;
+  auto kernel = fused_stream_kernel<TIn, TOut, CW, KV, ENT>;
+  constexpr int slot_bytes = CW * 32 * KV * 16;
   const int nslots = tune_env("COPRIS_TUNE_SLOTS", (CW >= 16 ? 196608 : 98304) / slot_bytes);
   const int smem = nslots * slot_bytes;
   cudaError_t e = set_smem(kernel, smem);
@@ -1581,6 +1581,8 @@ cudaError_t dispatch_fused(const LossParams& p, int num_sms, cudaStream_t stream
       const int w = tune_env("COPRIS_TUNE_WARPS", 16);
       if (w == 8) return launch_stream<TIn, TOut, 8, ENT>(p, num_sms, stream, info);
       if (w == 24) return launch_stream<TIn, TOut, 24, ENT>(p, num_sms, stream, info);
+      if (tune_env("COPRIS_TUNE_K", 4) == 8) return launch_stream<TIn, TOut, 16, ENT, 8>(p, num_sms, stream, info);
+      if (tune_env("COPRIS_TUNE_K", 4) == 2) return launch_stream<TIn, TOut, 16, ENT, 2>(p, num_sms, stream, info);
       return launch_stream<TIn, TOut, 16, ENT>(p, num_sms, stream, info);
     }
     if (impl == 3) {

@@ -1,2 +1,3 @@
-python scripts/trace_phases.py 32000 65536 > gpurun_out/trace_tma32k.log 2>&1
-timeout 300 python bench.py --config grpo_128x8_v32000_L1024 --no-e2e --no-cpu-baseline > gpurun_out/bench_v32000.log 2>&1
+for k in 2 4 8; do COPRIS_TUNE_K=$k python scripts/trace_phases.py 151936 16384 > gpurun_out/trace_k$k.log 2>&1; done
+COPRIS_TUNE_K=8 COPRIS_TUNE_SLOTS=2 python scripts/trace_phases.py 151936 16384 > gpurun_out/trace_k8s2.log 2>&1
+COPRIS_TUNE_K=2 COPRIS_TUNE_SLOTS=12 python scripts/trace_phases.py 151936 16384 > gpurun_out/trace_k2s12.log 2>&1
