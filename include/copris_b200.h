@@ -244,6 +244,28 @@ COPRIS_API int copris_grpo_step_loss_host(copris_ctx* ctx, copris_workspace* ws,
                                           const copris_host_batch* batch,
                                           const copris_loss_cfg* cfg, copris_host_result* out);
 
+/* ---- After the gradient: Adam and checkpoints ----
+ * copris_adam_update replaces AdamOptimizer::update (grpo.hpp:205-227) on
+ * DEVICE fp64 params/grad/moments of n elements: `step` is the update count
+ * AFTER this update (t in the reference), bias corrections use the host's
+ * pow() exactly as the reference does, and the per-element arithmetic is
+ * unfused fp64 — bit-identical to the reference. The caller bumps the policy
+ * version. copris_checkpoint_write/read implement the CPRSCKPT format of
+ * io.hpp:397-438 byte for byte (HOST pointers; dims = {Q, H, V, answer_vocab}). */
+typedef struct {
+  double lr, beta1, beta2, eps, weight_decay; /* AdamConfig, grpo.hpp:187-201 */
+} copris_adam_cfg;
+
+COPRIS_API int copris_adam_update(copris_ctx* ctx, double* params, const double* grad, double* m,
+                                  double* v, int64_t n, int64_t step, const copris_adam_cfg* cfg,
+                                  void* stream);
+COPRIS_API int copris_checkpoint_write(const char* path, const double* logits, const int32_t dims[4],
+                                       uint64_t version, uint64_t seed);
+/* Reads the header first: call with logits == NULL to get dims/version/seed,
+ * then again with a buffer of Q*H*V doubles. */
+COPRIS_API int copris_checkpoint_read(const char* path, double* logits, int32_t dims[4],
+                                      uint64_t* version, uint64_t* seed);
+
 /* ---- Host rollout buffer / scheduler (rollout.hpp:125-386) -----------------
  * The concurrency-controlled scheduler stays host-side bookkeeping
  * (include/copris_b200/rollout.hpp, bit-exact decisions); these entry points

@@ -193,6 +193,10 @@ class Reference:
         L.ref_terminal_rewards.argtypes = [P, P, I64, P, P, I32, P]
         L.ref_is_loss.argtypes = [P, I64, I32, I64, P, P, P, U32, P, P, P, D, D, D, D, C.c_int,
                                   C.c_int, P, P, P, P, P]
+        L.ref_adam.argtypes = [P, P, P, C.c_int, D, D, D, D, D]
+        L.ref_write_checkpoint.argtypes = [C.c_char_p, P, P, C.c_uint64, C.c_uint64]
+        L.ref_read_checkpoint.argtypes = [C.c_char_p, P, P, C.POINTER(C.c_uint64),
+                                          C.POINTER(C.c_uint64)]
 
     def _check(self, rc):
         if rc:
@@ -248,3 +252,24 @@ class Reference:
             C.byref(loss), _ptr(res.dlogits), _ptr(res.cur_lp), _ptr(res.behav), C.byref(secs)))
         res.loss, res.seconds = loss.value, secs.value
         return res
+
+    def adam(self, dims, params, grads, lr=5e-2, b1=0.9, b2=0.999, eps=1e-8, wd=0.01):
+        """AdamOptimizer::update applied len(grads) times (grpo.hpp:203-233)."""
+        d = np.ascontiguousarray(dims, np.int32)
+        p = np.array(params, np.float64)
+        g = np.ascontiguousarray(grads, np.float64)
+        self._check(self.lib.ref_adam(_ptr(d), _ptr(p), _ptr(g), len(g), lr, b1, b2, eps, wd))
+        return p
+
+    def write_checkpoint(self, path, dims, logits, version, seed):
+        d = np.ascontiguousarray(dims, np.int32)
+        a = np.ascontiguousarray(logits, np.float64)
+        self._check(self.lib.ref_write_checkpoint(path.encode(), _ptr(d), _ptr(a), version, seed))
+
+    def read_checkpoint(self, path, n):
+        d = np.zeros(4, np.int32)
+        out = np.zeros(n, np.float64)
+        ver, seed = C.c_uint64(), C.c_uint64()
+        self._check(self.lib.ref_read_checkpoint(path.encode(), _ptr(d), _ptr(out), C.byref(ver),
+                                                 C.byref(seed)))
+        return out, tuple(int(x) for x in d), ver.value, seed.value

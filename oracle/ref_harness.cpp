@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "copris/grpo.hpp"
+#include "copris/io.hpp"
 #include "copris/policy.hpp"
 #include "copris/trajectory.hpp"
 
@@ -187,6 +188,45 @@ int ref_is_loss(const double* logits, int64_t ld, int32_t vocab, int64_t n_traj,
         if (out_stored_lp) out_stored_lp[j] = items[i].stored_lp[pos];
       }
     }
+  });
+}
+
+// AdamOptimizer (grpo.hpp:203-233): `k` updates with grads[k][n] on a table of
+// n = Q*H*V parameters.
+int ref_adam(const int32_t dims[4], double* params, const double* grads, int k, double lr,
+             double b1, double b2, double eps, double wd) {
+  return guarded([&] {
+    copris::PolicyParams p(copris::PolicyShape{dims[0], dims[1], dims[2], dims[3]});
+    const size_t n = p.logits.size();
+    std::memcpy(p.logits.data(), params, n * sizeof(double));
+    copris::AdamOptimizer opt(copris::AdamConfig{lr, b1, b2, eps, wd});
+    for (int i = 0; i < k; ++i)
+      opt.update(p, std::span<const double>(grads + static_cast<size_t>(i) * n, n));
+    std::memcpy(params, p.logits.data(), n * sizeof(double));
+  });
+}
+
+// io.hpp:397-438
+int ref_write_checkpoint(const char* path, const int32_t dims[4], const double* logits,
+                         uint64_t version, uint64_t seed) {
+  return guarded([&] {
+    copris::PolicyParams p(copris::PolicyShape{dims[0], dims[1], dims[2], dims[3]});
+    std::memcpy(p.logits.data(), logits, p.logits.size() * sizeof(double));
+    p.version = version;
+    copris::write_checkpoint(path, p, seed);
+  });
+}
+
+int ref_read_checkpoint(const char* path, int32_t dims[4], double* logits, uint64_t* version,
+                        uint64_t* seed) {
+  return guarded([&] {
+    copris::PolicyParams p = copris::read_checkpoint(path, seed);
+    dims[0] = p.shape.num_classes;
+    dims[1] = p.shape.horizon;
+    dims[2] = p.shape.vocab;
+    dims[3] = p.shape.answer_vocab;
+    if (logits) std::memcpy(logits, p.logits.data(), p.logits.size() * sizeof(double));
+    *version = p.version;
   });
 }
 

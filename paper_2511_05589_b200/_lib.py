@@ -55,6 +55,10 @@ class HostResult(C.Structure):
                 ("stale_tokens", I64), ("clipped_tokens", I64)]
 
 
+class AdamCfg(C.Structure):
+    _fields_ = [("lr", D), ("beta1", D), ("beta2", D), ("eps", D), ("weight_decay", D)]
+
+
 class EngineCfg(C.Structure):
     _fields_ = [("mode", I32), ("concurrency", I32), ("batch_prompts", I32),
                 ("rollouts_per_prompt", I32), ("max_response_len", I32), ("max_staleness", I32),
@@ -91,6 +95,9 @@ _SIGS = {
     "copris_grpo_step_loss_host": ([P, P, C.POINTER(HostBatch), C.POINTER(LossCfg),
                                     C.POINTER(HostResult)], C.c_int),
     "copris_ctx_trace_read": ([P, P, C.c_int], C.c_int),
+    "copris_adam_update": ([P, P, P, P, P, I64, I64, C.POINTER(AdamCfg), P], C.c_int),
+    "copris_checkpoint_write": ([C.c_char_p, P, P, C.c_uint64, C.c_uint64], C.c_int),
+    "copris_checkpoint_read": ([C.c_char_p, P, P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)], C.c_int),
     "copris_engine_create": ([C.POINTER(EngineCfg), C.POINTER(P)], C.c_int),
     "copris_engine_destroy": ([P], C.c_int),
     "copris_engine_begin_stage": ([P, C.c_uint64, P, I64, C.POINTER(I64)], C.c_int),

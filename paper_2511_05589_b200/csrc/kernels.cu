@@ -17,6 +17,7 @@
 #include <cooperative_groups.h>
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
@@ -1356,6 +1357,26 @@ __global__ void group_advantages_kernel(const double* __restrict__ r, const int6
   }
 }
 
+// AdamOptimizer::update (grpo.hpp:209-227) per element in fp64, unfused and in
+// the reference's order so the result is bit-identical.
+__global__ void adam_kernel(double* __restrict__ p, const double* __restrict__ g,
+                            double* __restrict__ m, double* __restrict__ v, int64_t n, double lr,
+                            double b1, double b2, double eps, double wd, double bc1, double bc2) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double gi = g[i];
+    const double mi = __dadd_rn(__dmul_rn(b1, m[i]), __dmul_rn(__dadd_rn(1.0, -b1), gi));
+    const double vi = __dadd_rn(__dmul_rn(b2, v[i]), __dmul_rn(__dmul_rn(__dadd_rn(1.0, -b2), gi), gi));
+    m[i] = mi;
+    v[i] = vi;
+    const double mhat = __ddiv_rn(mi, bc1);
+    const double vhat = __ddiv_rn(vi, bc2);
+    const double pi = p[i];
+    const double upd = __dadd_rn(__ddiv_rn(mhat, __dadd_rn(__dsqrt_rn(vhat), eps)), __dmul_rn(wd, pi));
+    p[i] = __dadd_rn(pi, -__dmul_rn(lr, upd));
+  }
+}
+
 // Deterministic two-level reduction: fixed block partition, fixed in-block
 // tree, and the last block sums block partials in index order.
 constexpr int kReduceBlocks = 512;
@@ -1742,6 +1763,16 @@ cudaError_t launch_group_advantages(const double* rewards, const int64_t* group_
 }
 
 size_t reduce_scratch_bytes() { return sizeof(ReduceScratch); }
+
+cudaError_t launch_adam(double* p, const double* g, double* m, double* v, int64_t n, double lr,
+                        double b1, double b2, double eps, double wd, double bc1, double bc2,
+                        int num_sms, cudaStream_t stream) {
+  if (n == 0) return cudaSuccess;
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, static_cast<int64_t>(num_sms) * 8);
+  adam_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(p, g, m, v, n, lr, b1, b2, eps, wd,
+                                                                 bc1, bc2);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_reduce(const double* obj, const uint8_t* flags, int64_t n_tok, double* out4,
                           void* scratch, int num_sms, cudaStream_t stream) {

@@ -98,6 +98,9 @@ cudaError_t launch_group_advantages(const double* rewards, const int64_t* group_
                                     cudaStream_t stream);
 cudaError_t launch_token_traj(const int64_t* tok_off, int64_t n_traj, int32_t* out,
                               cudaStream_t stream);
+cudaError_t launch_adam(double* p, const double* g, double* m, double* v, int64_t n, double lr,
+                        double b1, double b2, double eps, double wd, double bc1, double bc2,
+                        int num_sms, cudaStream_t stream);
 // Deterministic reduction; scratch holds >= reduce_scratch_bytes() bytes.
 size_t reduce_scratch_bytes();
 cudaError_t launch_reduce(const double* obj, const uint8_t* flags, int64_t n_tok, double* out4,
