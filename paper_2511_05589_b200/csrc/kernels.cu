@@ -789,6 +789,17 @@ __device__ __forceinline__ uint64_t exp2_pair(uint64_t x) {
   return ptx::ex2x2(x);
 }
 
+// Element j of a 16-byte vector: 2^x on MUFU, or on the FMA pipe for the
+// columns selected by COPRIS_EMU_COLS (bit j) — balances the two pipes.
+#ifndef COPRIS_EMU_COLS
+#define COPRIS_EMU_COLS 0x00
+#endif
+template <int j>
+__device__ __forceinline__ float exp2_col(float x) {
+  if constexpr (((COPRIS_EMU_COLS >> j) & 1) != 0) return ptx::ex2_fma(x);
+  return ptx::ex2(x);
+}
+
 // Position in the slot ring (slot index + phase parity), advanced without
 // integer division.
 struct Ring {
@@ -952,12 +963,23 @@ __global__ void __launch_bounds__((CW + 1) * 32, CW <= 8 ? 2 : 1)
             }
           }
           // e = 2^(x log2e - m log2e); four independent accumulators
-#pragma unroll
-          for (int q = 0; q < VN; q += 2) {
-            s0 += ptx::ex2(fmaf(xa[q], kLog2e, nml));
-            s1 += ptx::ex2(fmaf(xa[q + 1], kLog2e, nml));
-            s2 += ptx::ex2(fmaf(xb[q], kLog2e, nml));
-            s3 += ptx::ex2(fmaf(xb[q + 1], kLog2e, nml));
+          s0 += exp2_col<0>(fmaf(xa[0], kLog2e, nml));
+          s1 += exp2_col<1>(fmaf(xa[1], kLog2e, nml));
+          s2 += exp2_col<0>(fmaf(xb[0], kLog2e, nml));
+          s3 += exp2_col<1>(fmaf(xb[1], kLog2e, nml));
+          s0 += exp2_col<2>(fmaf(xa[2], kLog2e, nml));
+          s1 += exp2_col<3>(fmaf(xa[3], kLog2e, nml));
+          s2 += exp2_col<2>(fmaf(xb[2], kLog2e, nml));
+          s3 += exp2_col<3>(fmaf(xb[3], kLog2e, nml));
+          if constexpr (VN == 8) {
+            s0 += exp2_col<4>(fmaf(xa[4], kLog2e, nml));
+            s1 += exp2_col<5>(fmaf(xa[5], kLog2e, nml));
+            s2 += exp2_col<4>(fmaf(xb[4], kLog2e, nml));
+            s3 += exp2_col<5>(fmaf(xb[5], kLog2e, nml));
+            s0 += exp2_col<6>(fmaf(xa[6], kLog2e, nml));
+            s1 += exp2_col<7>(fmaf(xa[7], kLog2e, nml));
+            s2 += exp2_col<6>(fmaf(xb[6], kLog2e, nml));
+            s3 += exp2_col<7>(fmaf(xb[7], kLog2e, nml));
           }
         }
       }
@@ -1016,8 +1038,16 @@ __global__ void __launch_bounds__((CW + 1) * 32, CW <= 8 ? 2 : 1)
         for (int q = 0; q < K; ++q) {
           float x[VN], d[VN];
           VI::unpack(raw[q], x);
-#pragma unroll
-          for (int e = 0; e < VN; ++e) d[e] = ptx::ex2(fmaf(x[e], kLog2e, -b.c1)) * -b.coef;
+          d[0] = exp2_col<0>(fmaf(x[0], kLog2e, -b.c1)) * -b.coef;
+          d[1] = exp2_col<1>(fmaf(x[1], kLog2e, -b.c1)) * -b.coef;
+          d[2] = exp2_col<2>(fmaf(x[2], kLog2e, -b.c1)) * -b.coef;
+          d[3] = exp2_col<3>(fmaf(x[3], kLog2e, -b.c1)) * -b.coef;
+          if constexpr (VN == 8) {
+            d[4] = exp2_col<4>(fmaf(x[4], kLog2e, -b.c1)) * -b.coef;
+            d[5] = exp2_col<5>(fmaf(x[5], kLog2e, -b.c1)) * -b.coef;
+            d[6] = exp2_col<6>(fmaf(x[6], kLog2e, -b.c1)) * -b.coef;
+            d[7] = exp2_col<7>(fmaf(x[7], kLog2e, -b.c1)) * -b.coef;
+          }
           if (tseg) {
             const int jt = b.y - (v0 + tid + q * NC) * VN;
 #pragma unroll

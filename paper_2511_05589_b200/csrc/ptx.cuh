@@ -290,6 +290,21 @@ __device__ __forceinline__ uint64_t ex2x2_fma(uint64_t x) {
   return (static_cast<uint64_t>(rhi) << 32) | rlo;
 }
 
+// Scalar 2^x on the FMA pipe (same construction as ex2x2_fma): 1 ALU max,
+// 3 FADD, 5 FFMA, 1 IMAD — no MUFU.
+__device__ __forceinline__ float ex2_fma(float x) {
+  float xc;
+  asm("max.NaN.f32 %0, %1, 0fC2FC0000;" : "=f"(xc) : "f"(x));
+  const float t = xc + 12582912.f;
+  const float f = xc - (t - 12582912.f);
+  float p = fmaf(0.001327647129073739f, f, 0.009675540961325169f);
+  p = fmaf(p, f, 0.05550713092088699f);
+  p = fmaf(p, f, 0.24022120237350464f);
+  p = fmaf(p, f, 0.6931469440460205f);
+  p = fmaf(p, f, 1.0000001192092896f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
 // bf16x2 word of two floats (round to nearest even)
 __device__ __forceinline__ uint32_t f2_to_bf16x2(uint64_t a) {
   uint32_t r;
