@@ -775,6 +775,10 @@ __global__ void __launch_bounds__(WARPS * 32)
 // stays busy while the consumers synchronise, and no cluster couples SMs.
 // ---------------------------------------------------------------------------
 constexpr int kStreamK = 4;  // 16-byte vectors per consumer thread per ring slot
+#ifndef COPRIS_STREAM_PREFETCH
+#define COPRIS_STREAM_PREFETCH 0  // 1|2 = L2-prefetch next row before pass 1|2; measured slower (L2 thrash)
+#endif
+__device__ __forceinline__ int tune_prefetch() { return COPRIS_STREAM_PREFETCH; }
 
 // Which fp32 pairs of a 16-byte vector take 2^x on the FMA pipe instead of
 // MUFU (bit i = pair i). MUFU.EX2 issues 16 results/clk/SM and two of them per
@@ -849,10 +853,19 @@ __global__ void __launch_bounds__((CW + 1) * 32, CW <= 8 ? 2 : 1)
     if (lane == 0) {
       const uint64_t keep = ptx::policy_evict_last(), drop = ptx::policy_evict_first();
       Ring ring(nslots);
+      const int pf = tune_prefetch();
       for (int64_t r = blockIdx.x; r < P.n_rows; r += gridDim.x) {
         const TIn* row = static_cast<const TIn*>(P.logits) + r * P.ld;
         for (int pass = 0; pass < 2; ++pass) {
           if (pass == 1 && !P.dlogits) break;
+          // Before the (L2-resident) second pass of row r, pull the next row
+          // toward L2 so its HBM reads overlap this row's dlogits writes.
+          if (pass == pf - 1 && r + gridDim.x < P.n_rows) {
+            const TIn* nrow = static_cast<const TIn*>(P.logits) + (r + gridDim.x) * P.ld;
+            for (int32_t v0 = 0; v0 < nvec; v0 += kStreamSlotVec)
+              ptx::bulk_prefetch_l2(nrow + static_cast<int64_t>(v0) * VN,
+                                    static_cast<uint32_t>(min(kStreamSlotVec, nvec - v0)) * 16u, keep);
+          }
           for (int32_t sg = 0; sg < nseg; ++sg, ring.next()) {
             const uint32_t slot = ring.slot, par = ring.ph;
             ptx::mbar_wait_u32(ebase + slot * 8, par ^ 1u);

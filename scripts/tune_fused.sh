@@ -1,2 +1,4 @@
-python scripts/trace_phases.py 151936 16384 > gpurun_out/trace_emu.log 2>&1
-timeout 300 python -m pytest tests/test_gpu_parity.py -q -x -k "151936 or saturated or deterministic or kl" > gpurun_out/tune_tests.log 2>&1
+python scripts/trace_phases.py 151936 16384 > gpurun_out/trace_pf2.log 2>&1
+cp paper_2511_05589_b200/libcopris_b200.so /tmp/keep.so; cp scripts/micro/lib_pf1.so paper_2511_05589_b200/libcopris_b200.so
+python scripts/trace_phases.py 151936 16384 > gpurun_out/trace_pf1.log 2>&1
+cp /tmp/keep.so paper_2511_05589_b200/libcopris_b200.so
