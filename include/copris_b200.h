@@ -87,6 +87,30 @@ COPRIS_API int copris_logprob_gather(copris_ctx* ctx, const void* logits, int64_
                           const int32_t* target, int64_t n_tok, int32_t vocab, float* out_lp,
                           float* out_lse, void* stream);
 
+/* ---- LM-head forward fused with the log-softmax statistics -----------------
+ * SURVEY.md §8(f) rank 3 (producer of a8, trainer.hpp:146). On tcgen05 tensor
+ * cores: logits[t][k] = bf16( sum_h hidden[t][h] * weight[k][h] ) (fp32
+ * accumulate) for t < n_rows, k < vocab, written with row stride ld_logits,
+ * plus partials[t][j] = {max, sum_{k in tile j, k != target[t]} exp(z - max)}
+ * (float2, n_vt = copris_lmhead_num_vtiles(vocab) per row) of the ROUNDED
+ * logits. hidden [n_rows x hidden_dim] and weight [vocab x hidden_dim]
+ * (nn.Linear layout) are bf16 with 16-byte aligned row strides ld_hidden /
+ * ld_weight (elements); ld_logits % 8 == 0.
+ * copris_lse_merge then yields exactly what copris_logprob_gather computes
+ * from the stored logits — (cur_lp, lse) — reading only the partials and the
+ * target logit; the loss continues with copris_behaviour_concat +
+ * copris_is_loss_bwd (one streaming pass). */
+COPRIS_API int32_t copris_lmhead_num_vtiles(int32_t vocab);
+COPRIS_API int copris_lmhead_logits(copris_ctx* ctx, const void* hidden, int64_t ld_hidden,
+                                    const void* weight, int64_t ld_weight, int64_t n_rows,
+                                    int32_t hidden_dim, int32_t vocab, const int32_t* target,
+                                    void* logits, int64_t ld_logits, float* partials,
+                                    void* stream);
+COPRIS_API int copris_lse_merge(copris_ctx* ctx, const float* partials, int32_t n_vt,
+                                const void* logits, int64_t ld, const int32_t* target,
+                                int64_t n_rows, int32_t vocab, float* out_lp, float* out_lse,
+                                void* stream);
+
 /* ---- K2: segmented cross-stage behaviour concat -----------------------------
  * copris_expand_segments: per-token stage ids from segment tables
  *   (segments in packed order; seg_off[n_seg+1] token offsets, seg_ver[n_seg]).

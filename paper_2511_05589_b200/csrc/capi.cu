@@ -10,6 +10,7 @@
 
 #include "../../include/copris_b200.h"
 #include "internal.hpp"
+#include "lmhead.cuh"
 #include "kernels.cuh"
 
 using namespace copris_b200;
@@ -196,6 +197,49 @@ int copris_logprob_gather(copris_ctx* ctx, const void* logits, int64_t ld, int32
   cudaError_t e = launch_logprob_gather(logits, ld, dt(dtype), target, n_tok, vocab, out_lp,
                                         out_lse, ctx->d_err, ctx->num_sms, as_stream(stream));
   return e == cudaSuccess ? COPRIS_OK : cuda_fail(e, "logprob_gather launch");
+}
+
+int32_t copris_lmhead_num_vtiles(int32_t vocab) {
+  return vocab > 0 ? lmhead_num_vtiles(vocab) : 0;
+}
+
+int copris_lmhead_logits(copris_ctx* ctx, const void* hidden, int64_t ld_hidden,
+                         const void* weight, int64_t ld_weight, int64_t n_rows,
+                         int32_t hidden_dim, int32_t vocab, const int32_t* target, void* logits,
+                         int64_t ld_logits, float* partials, void* stream) {
+  if (!ctx) return fail(COPRIS_E_INVALID, "null ctx");
+  if (n_rows < 0) return fail(COPRIS_E_INVALID, "negative n_rows");
+  if (n_rows == 0) return COPRIS_OK;
+  if (!hidden || !weight || !target || !logits || !partials)
+    return fail(COPRIS_E_INVALID, "null pointer");
+  if (vocab < 1 || hidden_dim < 1) return fail(COPRIS_E_INVALID, "bad vocab/hidden_dim");
+  if (ld_hidden < hidden_dim || ld_weight < hidden_dim || ld_hidden % 8 || ld_weight % 8)
+    return fail(COPRIS_E_INVALID, "hidden/weight row strides must be >= hidden_dim and 16-byte aligned");
+  if (ld_logits < vocab || ld_logits % 8) return fail(COPRIS_E_INVALID, "bad ld_logits");
+  if ((reinterpret_cast<uintptr_t>(hidden) | reinterpret_cast<uintptr_t>(weight) |
+       reinterpret_cast<uintptr_t>(logits)) & 15)
+    return fail(COPRIS_E_INVALID, "hidden/weight/logits must be 16-byte aligned");
+  if (n_rows > INT32_MAX || vocab > INT32_MAX - 256) return fail(COPRIS_E_INVALID, "too many rows");
+  DeviceGuard g(ctx->device);
+  cudaError_t e = launch_lmhead_fwd(hidden, ld_hidden, weight, ld_weight, n_rows, hidden_dim, vocab,
+                                    target, logits, ld_logits, partials, ctx->num_sms,
+                                    as_stream(stream), &ctx->last);
+  return e == cudaSuccess ? COPRIS_OK : cuda_fail(e, "lmhead_logits launch");
+}
+
+int copris_lse_merge(copris_ctx* ctx, const float* partials, int32_t n_vt, const void* logits,
+                     int64_t ld, const int32_t* target, int64_t n_rows, int32_t vocab,
+                     float* out_lp, float* out_lse, void* stream) {
+  if (!ctx) return fail(COPRIS_E_INVALID, "null ctx");
+  if (n_rows < 0) return fail(COPRIS_E_INVALID, "negative n_rows");
+  if (n_rows == 0) return COPRIS_OK;
+  if (!partials || !logits || !target || !out_lp) return fail(COPRIS_E_INVALID, "null pointer");
+  if (vocab < 1 || ld < vocab) return fail(COPRIS_E_INVALID, "bad vocab/ld");
+  if (n_vt != lmhead_num_vtiles(vocab)) return fail(COPRIS_E_INVALID, "n_vt does not match vocab");
+  DeviceGuard g(ctx->device);
+  cudaError_t e = launch_lse_merge(partials, n_vt, logits, ld, target, n_rows, vocab, out_lp,
+                                   out_lse, ctx->d_err, ctx->num_sms, as_stream(stream));
+  return e == cudaSuccess ? COPRIS_OK : cuda_fail(e, "lse_merge launch");
 }
 
 int copris_expand_segments(copris_ctx* ctx, const int64_t* seg_off, const uint32_t* seg_ver,

@@ -1,0 +1,359 @@
+// lmhead.cu — the LM-head forward fused with the log-softmax statistics
+// (the producer side of a8, trainer.hpp:146).
+//
+//   logits[T x V] = hidden[T x H] * weight[V x H]^T      (bf16 in, fp32 accumulate)
+//
+// is computed on the 5th-generation tensor cores (tcgen05.mma, accumulators in
+// TMEM, operands staged by 2-D TMA with 128-byte swizzle) and the epilogue —
+// while the tile is still on chip — rounds it to bf16, stores it, and emits the
+// per-(token, 256-column tile) log-sum-exp partial {max, sum exp(z - max)} of
+// the ROUNDED values with the target column left out of the sum. A tiny merge
+// kernel then yields (cur_lp, lse) exactly as K1 (logprob_gather) would from
+// the stored logits, without K1's full read of the [T x V] logits: the loss
+// path that follows becomes a single streaming pass (bwd_kernel).
+//
+// Kernel anatomy (one CTA per SM, persistent over output tiles):
+//   warp 0      TMA producer: A = hidden[128 x 64], B = weight[256 x 64] per
+//               k-step into a kStages-deep shared-memory ring (48 KB / stage).
+//   warp 1      TMEM owner (allocates 512 columns = two 128 x 256 fp32
+//               accumulators) and MMA issuer (one thread; 4 x K=16 MMAs per
+//               k-step, tcgen05.commit frees the ring slot).
+//   warps 2..5  epilogue: tcgen05.ld 32 rows x 32 columns at a time; each
+//               thread owns one token row of the tile. Double-buffered TMEM lets
+//               the epilogue of tile i overlap the MMAs of tile i + 1.
+// Tile order is vocab-tile-major, so CTAs running concurrently share weight
+// tiles through L2 while the hidden block (T_chunk x H) stays L2-resident.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <mutex>
+
+#include "lmhead.cuh"
+#include "ptx.cuh"
+#include "tc.cuh"
+
+namespace copris_b200 {
+
+namespace {
+
+constexpr int kBM = 128;       // tokens per tile (TMEM lanes)
+constexpr int kBN = kLmTileN;  // vocab columns per tile (fp32 TMEM columns)
+constexpr int kBK = 64;        // K per stage: one 128-byte swizzle row of bf16
+constexpr int kStages = 4;
+constexpr int kABytes = kBM * kBK * 2;  // 16 KB
+constexpr int kBBytes = kBN * kBK * 2;  // 32 KB
+constexpr int kStageBytes = kABytes + kBBytes;
+constexpr int kTmemCols = 2 * kBN;      // double-buffered accumulator
+constexpr int kThreads = 192;
+constexpr int kEpiThreads = 128;
+constexpr size_t kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + 256 /*barriers*/;
+
+struct LmParams {
+  int64_t n_rows;
+  int32_t H, V;
+  int32_t n_mblk, n_vt;
+  int64_t n_tiles;
+  __nv_bfloat16* logits;
+  int64_t ld;
+  float2* partials;  // [n_rows][n_vt]
+  const int32_t* target;
+};
+
+__device__ __forceinline__ float bf16_round(float x) {
+  return __bfloat162float(__float2bfloat16_rn(x));
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    lmhead_fwd_kernel(const __grid_constant__ CUtensorMap tm_x,
+                      const __grid_constant__ CUtensorMap tm_w, const LmParams P) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t base = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t sA = base;                         // kStages x 16 KB
+  const uint32_t sB = base + kStages * kABytes;     // kStages x 32 KB
+  const uint32_t bars = base + kStages * kStageBytes;
+  auto full_bar = [&](int s) { return bars + 8u * s; };
+  auto empty_bar = [&](int s) { return bars + 8u * (kStages + s); };
+  auto tfull_bar = [&](int b) { return bars + 8u * (2 * kStages + b); };
+  auto tempty_bar = [&](int b) { return bars + 8u * (2 * kStages + 2 + b); };
+  const uint32_t tmem_slot = bars + 8u * (2 * kStages + 4);
+  uint8_t* generic_base = smem_raw + (base - ptx::smem_u32(smem_raw));
+  volatile uint32_t* tmem_slot_ptr =
+      reinterpret_cast<volatile uint32_t*>(generic_base + (tmem_slot - base));
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full_bar(s)));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(empty_bar(s)));
+    }
+    for (int b = 0; b < 2; ++b) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tfull_bar(b)));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tempty_bar(b)),
+                   "r"(kEpiThreads));
+    }
+    ptx::fence_mbarrier_init();
+    tc::prefetch_tensormap(&tm_x);
+    tc::prefetch_tensormap(&tm_w);
+  }
+  if (warp == 1) tc::tmem_alloc<kTmemCols>(tmem_slot);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem_base = *tmem_slot_ptr;
+
+  const int nk = (P.H + kBK - 1) / kBK;
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===== TMA producer =====
+      const uint64_t pol_w = ptx::policy_evict_first();  // weight tiles: used by concurrent CTAs only
+      const uint64_t pol_x = ptx::policy_evict_last();   // hidden block: re-read for every vocab tile
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
+        const int32_t m0 = static_cast<int32_t>(t % P.n_mblk) * kBM;
+        const int32_t n0 = static_cast<int32_t>(t / P.n_mblk) * kBN;
+        for (int kb = 0; kb < nk; ++kb) {
+          ptx::mbar_wait_u32(empty_bar(stage), phase ^ 1u);
+          ptx::mbar_arrive_expect_tx_u32(full_bar(stage), kStageBytes);
+          tc::tma_load_2d(sA + stage * kABytes, &tm_x, full_bar(stage), kb * kBK, m0, pol_x);
+          tc::tma_load_2d(sB + stage * kBBytes, &tm_w, full_bar(stage), kb * kBK, n0, pol_w);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ===== MMA issuer =====
+      constexpr uint32_t idesc = tc::idesc_bf16_f32<kBM, kBN>();
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int64_t t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
+        ptx::mbar_wait_u32(tempty_bar(acc), acc_phase ^ 1u);
+        tc::fence_after_sync();
+        const uint32_t d = tmem_base + static_cast<uint32_t>(acc * kBN);
+        for (int kb = 0; kb < nk; ++kb) {
+          ptx::mbar_wait_u32(full_bar(stage), phase);
+          tc::fence_after_sync();
+          const uint32_t a = sA + stage * kABytes, b = sB + stage * kBBytes;
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k)  // K = 16 per MMA: +32 bytes along the swizzled row
+            tc::mma_bf16_ss(d, tc::smem_desc_sw128(a + 32 * k), tc::smem_desc_sw128(b + 32 * k),
+                            idesc, (kb | k) != 0);
+          tc::commit(empty_bar(stage));
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+        tc::commit(tfull_bar(acc));
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1u;
+        }
+      }
+    }
+  } else {
+    // ===== epilogue: TMEM -> bf16 logits + LSE partials =====
+    const int sub = warp & 3;  // TMEM lane quarter this warp may access
+    const int r_in = sub * 32 + lane;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int64_t t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
+      const int64_t row = static_cast<int64_t>(t % P.n_mblk) * kBM + r_in;
+      const int32_t vt = static_cast<int32_t>(t / P.n_mblk);
+      const int32_t n0 = vt * kBN;
+      const bool row_ok = row < P.n_rows;
+      const int32_t yrel = row_ok ? P.target[row] - n0 : -1;
+      const int32_t ncols = min(kBN, P.V - n0);
+      ptx::mbar_wait_u32(tfull_bar(acc), acc_phase);
+      tc::fence_after_sync();
+      float m = -INFINITY, s = 0.f;
+      __nv_bfloat16* out = P.logits + row * P.ld + n0;
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(sub * 32) << 16) +
+                             static_cast<uint32_t>(acc * kBN);
+#pragma unroll 1
+      for (int c = 0; c < kBN; c += 32) {
+        uint32_t r[32];
+        tc::tmem_ld_32x32b_x32(taddr + c, r);
+        tc::tmem_wait_ld();
+        if (c >= ncols) break;  // uniform across the warp (tile-level)
+        float z[32];
+        float cm = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          z[j] = bf16_round(__uint_as_float(r[j]));
+          if (c + j < ncols) cm = fmaxf(cm, z[j]);
+        }
+        if (cm > m) {
+          s *= ptx::ex2((m - cm) * kLog2e);
+          m = cm;
+        }
+        const float mb = m * kLog2e;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float e = ptx::ex2(fmaf(z[j], kLog2e, -mb));
+          if (c + j < ncols && c + j != yrel) s += e;
+        }
+        if (row_ok) {
+          if (c + 32 <= ncols) {
+            uint4* o = reinterpret_cast<uint4*>(out + c);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              o[q] = make_uint4(ptx::pack_bf16x2(z[8 * q + 0], z[8 * q + 1]),
+                                ptx::pack_bf16x2(z[8 * q + 2], z[8 * q + 3]),
+                                ptx::pack_bf16x2(z[8 * q + 4], z[8 * q + 5]),
+                                ptx::pack_bf16x2(z[8 * q + 6], z[8 * q + 7]));
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (c + j < ncols) out[c + j] = __float2bfloat16_rn(z[j]);
+          }
+        }
+      }
+      tc::fence_before_sync();
+      ptx::mbar_arrive_u32(tempty_bar(acc));
+      if (row_ok) P.partials[row * P.n_vt + vt] = make_float2(m, s);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1u;
+      }
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 1) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc<kTmemCols>(tmem_base);
+  }
+}
+
+// (cur_lp, lse) per token from the tile partials: one warp per token; the
+// target logit is read back from the stored (rounded) logits.
+__global__ void __launch_bounds__(256)
+    lse_merge_kernel(const float2* __restrict__ partials, int32_t n_vt,
+                     const __nv_bfloat16* __restrict__ logits, int64_t ld,
+                     const int32_t* __restrict__ target, int64_t n_rows, int32_t V,
+                     float* __restrict__ out_lp, float* __restrict__ out_lse, uint32_t* err) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < n_rows;
+       r += warps) {
+    const float2* pr = partials + r * n_vt;
+    float m = -INFINITY, s = 0.f;
+    for (int i = lane; i < n_vt; i += 32) {
+      const float2 p = pr[i];
+      if (p.x > m) {
+        s = s * ptx::ex2((m - p.x) * kLog2e) + p.y;
+        m = p.x;
+      } else {
+        s += p.y * ptx::ex2((p.x - m) * kLog2e);
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const float om = __shfl_xor_sync(0xffffffffu, m, off);
+      const float os = __shfl_xor_sync(0xffffffffu, s, off);
+      const float M = fmaxf(m, om);
+      if (M != -INFINITY) {
+        s = s * ptx::ex2((m - M) * kLog2e) + os * ptx::ex2((om - M) * kLog2e);
+        m = M;
+      }
+    }
+    if (lane == 0) {
+      const int32_t y = target[r];
+      const bool ok = static_cast<uint32_t>(y) < static_cast<uint32_t>(V);
+      const float zy = ok ? __bfloat162float(logits[r * ld + y]) : 0.f;
+      const LogProb lp = finish_logprob(m, s, zy, ok);
+      if (!ok) atomicOr(err, ERR_TOKEN_OOV);
+      out_lp[r] = lp.cur;
+      if (out_lse) out_lse[r] = static_cast<float>(lp.lse);
+    }
+  }
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// K-major bf16 matrix [rows x k] with row stride ld elements, box [box_rows x 64].
+bool make_map(CUtensorMap* map, const void* ptr, int64_t rows, int32_t k, int64_t ld,
+              uint32_t box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+int32_t lmhead_num_vtiles(int32_t vocab) { return (vocab + kBN - 1) / kBN; }
+
+cudaError_t launch_lmhead_fwd(const void* hidden, int64_t ld_h, const void* weight, int64_t ld_w,
+                              int64_t n_rows, int32_t H, int32_t V, const int32_t* target,
+                              void* logits, int64_t ld, float* partials, int num_sms,
+                              cudaStream_t stream, LaunchInfo* info) {
+  CUtensorMap tx, tw;
+  if (!make_map(&tx, hidden, n_rows, H, ld_h, kBM) || !make_map(&tw, weight, V, H, ld_w, kBN))
+    return cudaErrorInvalidValue;
+  static bool attr = [] {
+    return cudaFuncSetAttribute(lmhead_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(kSmemBytes)) == cudaSuccess;
+  }();
+  if (!attr) return cudaErrorInvalidValue;
+  LmParams p;
+  p.n_rows = n_rows;
+  p.H = H;
+  p.V = V;
+  p.n_mblk = static_cast<int32_t>((n_rows + kBM - 1) / kBM);
+  p.n_vt = lmhead_num_vtiles(V);
+  p.n_tiles = static_cast<int64_t>(p.n_mblk) * p.n_vt;
+  p.logits = static_cast<__nv_bfloat16*>(logits);
+  p.ld = ld;
+  p.partials = reinterpret_cast<float2*>(partials);
+  p.target = target;
+  const int grid = static_cast<int>(std::min<int64_t>(p.n_tiles, num_sms));
+  lmhead_fwd_kernel<<<grid, kThreads, kSmemBytes, stream>>>(tx, tw, p);
+  if (info) *info = LaunchInfo{num_sms, 1, grid, "lmhead_fwd_kernel"};
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lse_merge(const float* partials, int32_t n_vt, const void* logits, int64_t ld,
+                             const int32_t* target, int64_t n_rows, int32_t V, float* out_lp,
+                             float* out_lse, uint32_t* err, int num_sms, cudaStream_t stream) {
+  const int64_t blocks = std::min<int64_t>((n_rows + 7) / 8, static_cast<int64_t>(num_sms) * 8);
+  lse_merge_kernel<<<static_cast<int>(blocks), 256, 0, stream>>>(
+      reinterpret_cast<const float2*>(partials), n_vt,
+      static_cast<const __nv_bfloat16*>(logits), ld, target, n_rows, V, out_lp, out_lse, err);
+  return cudaGetLastError();
+}
+
+}  // namespace copris_b200

@@ -1,0 +1,28 @@
+// lmhead.cuh — host launchers of the tensor-core LM-head forward with fused
+// log-softmax partials (lmhead.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.cuh"
+#include "token_math.cuh"
+
+namespace copris_b200 {
+
+constexpr int kLmTileN = 256;  // vocab columns per output tile = one LSE partial
+
+int32_t lmhead_num_vtiles(int32_t vocab);
+
+// logits = hidden * weight^T (bf16, row stride ld) + partials[n_rows][n_vt] float2.
+cudaError_t launch_lmhead_fwd(const void* hidden, int64_t ld_h, const void* weight, int64_t ld_w,
+                              int64_t n_rows, int32_t H, int32_t V, const int32_t* target,
+                              void* logits, int64_t ld, float* partials, int num_sms,
+                              cudaStream_t stream, LaunchInfo* info);
+
+cudaError_t launch_lse_merge(const float* partials, int32_t n_vt, const void* logits, int64_t ld,
+                             const int32_t* target, int64_t n_rows, int32_t V, float* out_lp,
+                             float* out_lse, uint32_t* err, int num_sms, cudaStream_t stream);
+
+}  // namespace copris_b200

@@ -175,6 +175,38 @@ class Copris:
             _p(lp), _p(lse), self._stream(stream)))
         return lp, lse
 
+    # -- LM-head forward + log-softmax partials (tcgen05) ---------------------------
+    def lmhead_logits(self, hidden: torch.Tensor, weight: torch.Tensor, target: torch.Tensor,
+                      logits: Optional[torch.Tensor] = None,
+                      partials: Optional[torch.Tensor] = None, stream=None):
+        """logits = bf16(hidden @ weight^T) and per-256-column LSE partials
+        (float2 per (token, tile), target column excluded)."""
+        n, h = hidden.shape
+        v = weight.shape[0]
+        if hidden.dtype != torch.bfloat16 or weight.dtype != torch.bfloat16:
+            raise ValueError("hidden and weight must be bf16")
+        nvt = int(self.lib.copris_lmhead_num_vtiles(v))
+        if logits is None:
+            ld = (v + 7) // 8 * 8
+            logits = torch.empty((n, ld), dtype=torch.bfloat16, device=hidden.device)[:, :v]
+        if partials is None:
+            partials = torch.empty((n, nvt, 2), dtype=torch.float32, device=hidden.device)
+        self._call(self.lib.copris_lmhead_logits(
+            self.h, _p(hidden), hidden.stride(0), _p(weight), weight.stride(0), n, h, v,
+            _p(target), _p(logits), logits.stride(0), _p(partials), self._stream(stream)))
+        return logits, partials
+
+    def lse_merge(self, partials: torch.Tensor, logits: torch.Tensor, target: torch.Tensor,
+                  out_lp=None, out_lse=None, stream=None):
+        """(cur_lp, lse) from lmhead partials — what sequence_logprobs gives on the logits."""
+        n, v = logits.shape
+        lp = out_lp if out_lp is not None else torch.empty(n, dtype=torch.float32, device=logits.device)
+        lse = out_lse if out_lse is not None else torch.empty(n, dtype=torch.float32, device=logits.device)
+        self._call(self.lib.copris_lse_merge(
+            self.h, _p(partials), partials.shape[1], _p(logits), logits.stride(0), _p(target), n, v,
+            _p(lp), _p(lse), self._stream(stream)))
+        return lp, lse
+
     # -- K2 -----------------------------------------------------------------------
     def expand_segments(self, seg_off: torch.Tensor, seg_ver: torch.Tensor, n_tok: int,
                         stream=None) -> torch.Tensor:

@@ -1,0 +1,120 @@
+"""LM-head + IS-corrected GRPO loss over hidden states.
+
+The reference's policy is a table (policy.hpp:110-121: the logits row of token
+t is ``row(class, t)``); in an LLM the same row is ``hidden[t] @ W^T``. This
+module runs the loss path of grpo.hpp:117-185 with that producer in front and
+its backward behind, chunked over tokens so the [T x V] logits exist only one
+chunk at a time:
+
+  per chunk of rows
+    copris_lmhead_logits   tcgen05 GEMM -> bf16 logits + LSE partials   (fwd, fused)
+    copris_lse_merge       (cur_lp, lse) from partials                   (replaces K1's read)
+    copris_behaviour_concat                                             (K2)
+    copris_is_loss_bwd     objective/coef + dlogits IN PLACE over logits (one pass)
+    dhidden = dlogits @ W  and  dW += dlogits^T @ hidden                 (cuBLAS: plain GEMMs)
+  copris_loss_reduce -> loss, counts
+
+Every step is a kernel in libcopris_b200.so except the two backward GEMMs,
+which are plain library GEMMs.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+
+from . import _lib as L
+from .errors import ConfigError, ContractViolation
+from .grpo import ClipConfig, Copris, PackedBatch, _p
+
+
+@dataclass
+class LmHeadStepResult:
+    loss: float
+    token_count: int
+    objective: float
+    stale_tokens: int
+    clipped_tokens: int
+    cur_lp: torch.Tensor
+    lse: torch.Tensor
+    obj: torch.Tensor
+    flags: torch.Tensor
+    dhidden: Optional[torch.Tensor]
+    dweight: Optional[torch.Tensor]
+    coef: Optional[torch.Tensor] = None
+
+
+def lmhead_grpo_step_loss(ctx: Copris, hidden: torch.Tensor, weight: torch.Tensor,
+                          batch: PackedBatch, cfg: ClipConfig = None, *, chunk_rows: int = 8192,
+                          is_enabled: bool = True, behav_mode: int = L.COPRIS_BEHAV_RECOMPUTED,
+                          total_tokens: Optional[int] = None, want_grad: bool = True,
+                          dweight: Optional[torch.Tensor] = None, coef: bool = False,
+                          stream=None) -> LmHeadStepResult:
+    """grpo.hpp:117-185 with logits = hidden @ weight^T (bf16 in, fp32 accumulate).
+
+    ``dweight`` (fp32 [V x H]) is accumulated into when given (zeros otherwise).
+    """
+    cfg = cfg or ClipConfig()
+    cfg.validate()
+    if batch.n_traj == 0:
+        raise ConfigError("grpo_step_loss requires a non-empty batch")
+    if batch.n_tok == 0:
+        raise ConfigError("grpo_step_loss batch has no tokens")
+    T, H = hidden.shape
+    V = weight.shape[0]
+    if T != batch.n_tok:
+        raise ContractViolation("log-prob vectors must align with token count")
+    if weight.shape[1] != H:
+        raise ContractViolation("hidden and weight disagree on the hidden size")
+    T_glob = total_tokens if total_tokens is not None else T
+    dev = hidden.device
+    chunk = max(1, min(chunk_rows, T))
+    ldv = (V + 7) // 8 * 8
+    buf = torch.empty((chunk, ldv), dtype=torch.bfloat16, device=dev)[:, :V]
+    nvt = int(ctx.lib.copris_lmhead_num_vtiles(V))
+    part = torch.empty((chunk, nvt, 2), dtype=torch.float32, device=dev)
+    outs = ctx.alloc_outputs(T, dev, coef=coef)
+    dhidden = torch.empty_like(hidden) if want_grad else None
+    if want_grad and dweight is None:
+        dweight = torch.zeros((V, H), dtype=torch.float32, device=dev)
+    s = ctx._stream(stream)
+    for a in range(0, T, chunk):
+        n = min(chunk, T - a)
+        sl = slice(a, a + n)
+        lg = buf[:n]
+        ctx.lmhead_logits(hidden[sl], weight, batch.target[sl], logits=lg, partials=part[:n],
+                          stream=stream)
+        ctx.lse_merge(part[:n], lg, batch.target[sl], out_lp=outs["cur_lp"][sl],
+                      out_lse=outs["lse"][sl], stream=stream)
+        ctx._call(ctx.lib.copris_behaviour_concat(
+            ctx.h, _p(batch.stage[sl]), batch.cur_stage, _p(batch.buffered_lp[sl]),
+            _p(outs["cur_lp"][sl]), int(is_enabled), behav_mode, n, _p(outs["behav"][sl]), None, s))
+        b, c, o = ctx._structs(lg, batch, cfg, is_enabled, behav_mode, T_glob, a,
+                               lg if want_grad else None, outs)
+        ctx._call(ctx.lib.copris_is_loss_bwd(ctx.h, C.byref(b), C.byref(c), _p(outs["cur_lp"]),
+                                             _p(outs["lse"]), _p(outs["behav"]), C.byref(o), s))
+        if want_grad:
+            # dlogits now sits in `lg`: the LM-head backward (plain GEMMs)
+            with torch.cuda.stream(stream) if stream is not None else _null():
+                torch.mm(lg, weight, out=dhidden[sl])
+                torch.addmm(dweight, lg.t(), hidden[sl], out_dtype=torch.float32, out=dweight)
+    out4 = torch.empty(4, dtype=torch.float64, device=dev)
+    ctx.reduce(outs, T, out4, stream=stream)
+    ctx.check(stream)
+    o4 = out4.cpu().tolist()
+    res = LmHeadStepResult(loss=-o4[0] * (1.0 / T_glob), token_count=int(o4[1]), objective=o4[0],
+                           stale_tokens=int(o4[2]), clipped_tokens=int(o4[3]),
+                           cur_lp=outs["cur_lp"], lse=outs["lse"], obj=outs["obj"],
+                           flags=outs["flags"], dhidden=dhidden, dweight=dweight,
+                           coef=outs.get("coef"))
+    return res
+
+
+class _null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False

@@ -1,0 +1,136 @@
+"""GPU: LM-head forward on tcgen05 with fused log-softmax partials
+ and the loss path behind it.
+
+Parity is split at the bf16 logits the GEMM stores:
+  * GEMM: stored logits vs the fp64 product of the same bf16 inputs, within
+    bf16 rounding + fp32-accumulation error (|err| <= 2^-8 |z| + H 2^-23 sum|x w|);
+  * statistics: (cur_lp, lse) from the partials vs K1 (sequence_logprobs) on the
+    stored logits, and the whole loss path vs the CPU oracle on the stored logits
+    (the usual 1e-5 relative bar);
+  * backward: dhidden / dweight vs fp64 products of the kernel's own dlogits.
+"""
+import numpy as np
+import pytest
+import torch
+
+from parity_util import assert_loss_close, assert_rows_close, assert_scalar_close
+
+pytestmark = pytest.mark.gpu
+
+
+def _inputs(T, H, V, seed, scale=1.0):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    x = (torch.randn(T, H, generator=g) * scale).to(torch.bfloat16)
+    w = (torch.randn(V, H, generator=g) / H ** 0.5 * 2.0).to(torch.bfloat16)
+    tgt = torch.randint(0, V, (T,), generator=g, dtype=torch.int32)
+    return x.cuda(), w.cuda(), tgt.cuda()
+
+
+def _check_logits(lg, x, w):
+    ref = x.double() @ w.double().t()
+    bound = (x.double().abs() @ w.double().abs().t()) * x.shape[1] * 2.0 ** -23
+    err = (lg.double() - ref).abs()
+    assert torch.all(err <= 2.0 ** -8 * ref.abs() + bound + 1e-30), float((err - 2.0 ** -8 * ref.abs() - bound).max())
+
+
+@pytest.mark.parametrize("T,H,V", [(1, 64, 256), (130, 64, 300), (257, 192, 1000), (300, 520, 4099),
+                                   (512, 1024, 32000), (129, 4096, 151936)])
+def test_lmhead_logits_and_partials(ctx, T, H, V):
+    x, w, tgt = _inputs(T, H, V, T + H + V)
+    lg, part = ctx.lmhead_logits(x, w, tgt)
+    torch.cuda.synchronize()
+    rows = torch.arange(T, device="cuda") if T * V <= 2 ** 26 else torch.randperm(T, device="cuda")[:32]
+    _check_logits(lg[rows], x[rows], w)
+    lp, lse = ctx.lse_merge(part, lg, tgt)
+    ref_lp, ref_lse = ctx.sequence_logprobs(lg, tgt)
+    ctx.check()
+    assert_scalar_close(lp.cpu().numpy(), ref_lp.cpu().numpy(), what="cur_lp (partials vs K1)")
+    assert_scalar_close(lse.cpu().numpy(), ref_lse.cpu().numpy(), what="lse (partials vs K1)")
+
+
+def test_lmhead_saturated_rows(ctx):
+    """A dominant target logit (p_y -> 1): cur_lp stays accurate (target excluded from sums)."""
+    T, H, V = 64, 128, 2048
+    x, w, tgt = _inputs(T, H, V, 5)
+    w = w.clone()
+    x = x.clone()
+    # row r points along the target's weight row, scaled so z_y - max_other ~ 20..40
+    wy = w[tgt.long()].float()
+    x = (wy / wy.norm(dim=1, keepdim=True) * torch.linspace(8, 16, T, device="cuda")[:, None] *
+         (H ** 0.5) / 2.0).to(torch.bfloat16)
+    lg, part = ctx.lmhead_logits(x, w, tgt)
+    lp, lse = ctx.lse_merge(part, lg, tgt)
+    ref_lp, _ = ctx.sequence_logprobs(lg, tgt)
+    ctx.check()
+    assert float(lp.abs().max()) < 1e-3
+    assert_scalar_close(lp.cpu().numpy(), ref_lp.cpu().numpy(), what="saturated cur_lp")
+
+
+@pytest.mark.parametrize("chunk", [4096, 100])
+def test_lmhead_loss_path_against_oracle(ctx, oracle, chunk):
+    from paper_2511_05589_b200 import ClipConfig
+    from paper_2511_05589_b200.lmhead import lmhead_grpo_step_loss
+    from paper_2511_05589_b200.packing import upload
+    from paper_2511_05589_b200.workload import stale_logprobs
+    rng = np.random.default_rng(3)
+    n_traj, G = 8, 4
+    lens = rng.integers(5, 60, n_traj)
+    tok_off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    T = int(tok_off[-1])
+    H, V = 256, 1000
+    x, w, tgt = _inputs(T, H, V, 11)
+    target = tgt.cpu().numpy()
+    stage = np.zeros(T, np.uint32)
+    for i in range(n_traj):
+        a, b = tok_off[i], tok_off[i + 1]
+        stage[a:a + (b - a) // 2] = 1 if i % 2 else 2
+        stage[a + (b - a) // 2:b] = 2
+    lg_full, _ = ctx.lmhead_logits(x, w, tgt)
+    cur, _ = ctx.sequence_logprobs(lg_full, tgt)
+    blp = stale_logprobs(cur.cpu().numpy(), stage, 2, 7)
+    reward = (rng.random(n_traj) < 0.5).astype(np.float64)
+    group_off = np.arange(0, n_traj + 1, G, dtype=np.int64)
+    batch = upload(ctx, tok_off, group_off, target, blp, 2, stage=stage, reward=reward)
+    res = lmhead_grpo_step_loss(ctx, x, w, batch, ClipConfig(), chunk_rows=chunk, coef=True)
+    z = lg_full.double().cpu().numpy()
+    adv = batch.adv.cpu().numpy()
+    ref = oracle.is_loss(z, tok_off, target, stage, 2, blp.astype(np.float64), adv)
+    assert res.stale_tokens == ref.stale_tokens
+    assert_scalar_close(res.cur_lp.cpu().numpy(), ref.cur_lp, what="cur_lp")
+    np.testing.assert_array_equal((res.flags.cpu().numpy() >> 1) & 1, ref.clipped)
+    assert_loss_close(res.loss, ref.loss, ref.obj, T)
+    # backward: dlogits (oracle, fp64) -> dhidden, dweight
+    dl = torch.from_numpy(ref.dlogits)
+    xd, wd = x.double().cpu(), w.double().cpu()
+    dh_ref = dl @ wd
+    dw_ref = dl.t() @ xd
+    # the kernel's dlogits are bf16 (2^-9 relative) and the GEMMs accumulate in fp32
+    tol_h = 2.0 ** -7 * (dl.abs() @ wd.abs()) + 1e-12
+    tol_w = 2.0 ** -7 * (dl.abs().t() @ xd.abs()) + 1e-12
+    assert torch.all((res.dhidden.double().cpu() - dh_ref).abs() <= tol_h)
+    assert torch.all((res.dweight.double().cpu() - dw_ref).abs() <= tol_w)
+
+
+def test_lmhead_matches_logits_path(ctx):
+    """Same batch through (a) lmhead path and (b) grpo_step_loss on the stored
+    logits: identical objective terms within fp32 rounding, dlogits within bf16."""
+    from paper_2511_05589_b200 import ClipConfig
+    from paper_2511_05589_b200.lmhead import lmhead_grpo_step_loss
+    from paper_2511_05589_b200.packing import upload
+    from paper_2511_05589_b200.workload import stale_logprobs
+    T, H, V = 2000, 512, 32000
+    x, w, tgt = _inputs(T, H, V, 2)
+    tok_off = np.linspace(0, T, 17).astype(np.int64)
+    group_off = np.arange(0, 17, 4, dtype=np.int64)
+    stage = (np.arange(T) % 3 == 0).astype(np.uint32) + 1
+    lg, _ = ctx.lmhead_logits(x, w, tgt)
+    cur, _ = ctx.sequence_logprobs(lg, tgt)
+    blp = stale_logprobs(cur.cpu().numpy(), stage, 2, 3)
+    reward = (np.arange(16) % 3 == 0).astype(np.float64)
+    batch = upload(ctx, tok_off, group_off, tgt.cpu().numpy(), blp, 2, stage=stage, reward=reward)
+    a = lmhead_grpo_step_loss(ctx, x, w, batch, ClipConfig(), chunk_rows=777)
+    b = ctx.grpo_step_loss(lg.contiguous(), batch, ClipConfig())
+    assert a.stale_tokens == b.stale_tokens and a.clipped_tokens == b.clipped_tokens
+    assert abs(a.loss - b.loss) <= 1e-6 * max(1e-12, float(b.obj.abs().sum()) / T)
+    dh = b.dlogits.float() @ w.float()
+    assert torch.allclose(a.dhidden.float(), dh, rtol=2e-2, atol=1e-3 * float(dh.abs().max()))
