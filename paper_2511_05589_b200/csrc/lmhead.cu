@@ -29,6 +29,8 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "lmhead.cuh"
@@ -64,6 +66,56 @@ struct LmParams {
 
 __device__ __forceinline__ float bf16_round(float x) {
   return __bfloat162float(__float2bfloat16_rn(x));
+}
+
+// One thread = one token row of a 128 x kBN accumulator tile in TMEM: round
+// to bf16, store, and reduce {max, sum exp(z - max)} over the tile's valid
+// columns with the target column left out. Returns the partial.
+__device__ __forceinline__ float2 epilogue_row(uint32_t taddr, int64_t row, bool row_ok,
+                                               int32_t n0, int32_t ncols, int32_t yrel,
+                                               const LmParams& P) {
+  float m = -INFINITY, s = 0.f;
+  __nv_bfloat16* out = P.logits + row * P.ld + n0;
+#pragma unroll 1
+  for (int c = 0; c < kBN; c += 32) {
+    uint32_t r[32];
+    tc::tmem_ld_32x32b_x32(taddr + c, r);
+    tc::tmem_wait_ld();
+    if (c >= ncols) break;  // uniform across the warp (tile-level)
+    float z[32];
+    float cm = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      z[j] = bf16_round(__uint_as_float(r[j]));
+      if (c + j < ncols) cm = fmaxf(cm, z[j]);
+    }
+    if (cm > m) {
+      s *= ptx::ex2((m - cm) * kLog2e);
+      m = cm;
+    }
+    const float mb = m * kLog2e;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const float e = ptx::ex2(fmaf(z[j], kLog2e, -mb));
+      if (c + j < ncols && c + j != yrel) s += e;
+    }
+    if (row_ok) {
+      if (c + 32 <= ncols) {
+        uint4* o = reinterpret_cast<uint4*>(out + c);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          o[q] = make_uint4(ptx::pack_bf16x2(z[8 * q + 0], z[8 * q + 1]),
+                            ptx::pack_bf16x2(z[8 * q + 2], z[8 * q + 3]),
+                            ptx::pack_bf16x2(z[8 * q + 4], z[8 * q + 5]),
+                            ptx::pack_bf16x2(z[8 * q + 6], z[8 * q + 7]));
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (c + j < ncols) out[c + j] = __float2bfloat16_rn(z[j]);
+      }
+    }
+  }
+  return make_float2(m, s);
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -175,52 +227,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int32_t ncols = min(kBN, P.V - n0);
       ptx::mbar_wait_u32(tfull_bar(acc), acc_phase);
       tc::fence_after_sync();
-      float m = -INFINITY, s = 0.f;
-      __nv_bfloat16* out = P.logits + row * P.ld + n0;
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(sub * 32) << 16) +
                              static_cast<uint32_t>(acc * kBN);
-#pragma unroll 1
-      for (int c = 0; c < kBN; c += 32) {
-        uint32_t r[32];
-        tc::tmem_ld_32x32b_x32(taddr + c, r);
-        tc::tmem_wait_ld();
-        if (c >= ncols) break;  // uniform across the warp (tile-level)
-        float z[32];
-        float cm = -INFINITY;
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          z[j] = bf16_round(__uint_as_float(r[j]));
-          if (c + j < ncols) cm = fmaxf(cm, z[j]);
-        }
-        if (cm > m) {
-          s *= ptx::ex2((m - cm) * kLog2e);
-          m = cm;
-        }
-        const float mb = m * kLog2e;
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float e = ptx::ex2(fmaf(z[j], kLog2e, -mb));
-          if (c + j < ncols && c + j != yrel) s += e;
-        }
-        if (row_ok) {
-          if (c + 32 <= ncols) {
-            uint4* o = reinterpret_cast<uint4*>(out + c);
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              o[q] = make_uint4(ptx::pack_bf16x2(z[8 * q + 0], z[8 * q + 1]),
-                                ptx::pack_bf16x2(z[8 * q + 2], z[8 * q + 3]),
-                                ptx::pack_bf16x2(z[8 * q + 4], z[8 * q + 5]),
-                                ptx::pack_bf16x2(z[8 * q + 6], z[8 * q + 7]));
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (c + j < ncols) out[c + j] = __float2bfloat16_rn(z[j]);
-          }
-        }
-      }
+      const float2 part = epilogue_row(taddr, row, row_ok, n0, ncols, yrel, P);
       tc::fence_before_sync();
       ptx::mbar_arrive_u32(tempty_bar(acc));
-      if (row_ok) P.partials[row * P.n_vt + vt] = make_float2(m, s);
+      if (row_ok) P.partials[row * P.n_vt + vt] = part;
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1u;
@@ -232,6 +244,160 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) {
     tc::fence_after_sync();
     tc::tmem_dealloc<kTmemCols>(tmem_base);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2): a cluster of two CTAs on one TPC computes a
+// 256-token x 256-column tile. Each CTA stages its 128 token rows of hidden
+// and its 128-row half of the weight tile; the leader's single thread issues
+// M=256 MMAs that read both CTAs' shared memory and write each CTA's half of
+// the accumulator into its own TMEM. Per SM this halves the weight-operand
+// traffic of the 1-SM kernel (32 KB instead of 48 KB staged per k-step for the
+// same MMA work).
+//   full[s]   leader only; both CTAs' TMA bytes complete on it
+//   empty[s]  both CTAs; multicast tcgen05.commit from the leader
+//   tfull[b]  both CTAs; multicast commit after the tile's last k-step
+//   tempty[b] leader only; one arrive per epilogue warp of either CTA (8)
+// ---------------------------------------------------------------------------
+constexpr int kPStages = 6;
+constexpr int kPABytes = 128 * kBK * 2;  // 16 KB: this CTA's 128 token rows
+constexpr int kPBBytes = 128 * kBK * 2;  // 16 KB: this CTA's half of the weight tile
+constexpr int kPStageBytes = kPABytes + kPBBytes;
+constexpr size_t kPSmemBytes = 1024 + kPStages * kPStageBytes + 256;
+
+__global__ void __launch_bounds__(kThreads, 1)
+    lmhead_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_x,
+                           const __grid_constant__ CUtensorMap tm_w, const LmParams P) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t base = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t sA = base;
+  const uint32_t sB = base + kPStages * kPABytes;
+  const uint32_t bars = base + kPStages * kPStageBytes;
+  auto full_bar = [&](int s) { return bars + 8u * s; };
+  auto empty_bar = [&](int s) { return bars + 8u * (kPStages + s); };
+  auto tfull_bar = [&](int b) { return bars + 8u * (2 * kPStages + b); };
+  auto tempty_bar = [&](int b) { return bars + 8u * (2 * kPStages + 2 + b); };
+  const uint32_t tmem_slot = bars + 8u * (2 * kPStages + 4);
+  volatile uint32_t* tmem_slot_ptr = reinterpret_cast<volatile uint32_t*>(
+      smem_raw + (tmem_slot - ptx::smem_u32(smem_raw)));
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = ptx::cluster_ctarank();
+  const bool leader = rank == 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kPStages; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full_bar(s)));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(empty_bar(s)));
+    }
+    for (int b = 0; b < 2; ++b) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tfull_bar(b)));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;" ::"r"(tempty_bar(b)));
+    }
+    ptx::fence_mbarrier_init();
+    tc::prefetch_tensormap(&tm_x);
+    tc::prefetch_tensormap(&tm_w);
+  }
+  if (warp == 1) tc::tmem_alloc_pair<kTmemCols>(tmem_slot);
+  tc::fence_before_sync();
+  ptx::cluster_sync_all();
+  tc::fence_after_sync();
+  const uint32_t tmem_base = *tmem_slot_ptr;
+
+  const int nk = (P.H + kBK - 1) / kBK;
+  const int64_t n_mpair = (P.n_rows + 255) / 256;
+  const int64_t n_units = n_mpair * P.n_vt;
+  const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===== TMA producer (both CTAs) =====
+      const uint64_t pol_w = ptx::policy_evict_first();
+      const uint64_t pol_x = ptx::policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t u = cid; u < n_units; u += ncl) {
+        const int32_t m0 = static_cast<int32_t>(u % n_mpair) * 256 + 128 * rank;
+        const int32_t n0 = static_cast<int32_t>(u / n_mpair) * kBN + 128 * rank;
+        for (int kb = 0; kb < nk; ++kb) {
+          ptx::mbar_wait_u32(empty_bar(stage), phase ^ 1u);
+          const uint32_t fb = ptx::mapa(full_bar(stage), 0);
+          if (leader) ptx::mbar_arrive_expect_tx_u32(full_bar(stage), 2 * kPStageBytes);
+          tc::tma_load_2d_pair(sA + stage * kPABytes, &tm_x, fb, kb * kBK, m0, pol_x);
+          tc::tma_load_2d_pair(sB + stage * kPBBytes, &tm_w, fb, kb * kBK, n0, pol_w);
+          if (++stage == kPStages) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      // ===== MMA issuer (leader CTA) =====
+      constexpr uint32_t idesc = tc::idesc_bf16_f32<256, kBN>();
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int64_t u = cid; u < n_units; u += ncl) {
+        ptx::mbar_wait_u32(tempty_bar(acc), acc_phase ^ 1u);
+        tc::fence_after_sync();
+        const uint32_t d = tmem_base + static_cast<uint32_t>(acc * kBN);
+        for (int kb = 0; kb < nk; ++kb) {
+          ptx::mbar_wait_u32(full_bar(stage), phase);
+          tc::fence_after_sync();
+          const uint32_t a = sA + stage * kPABytes, b = sB + stage * kPBBytes;
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k)
+            tc::mma_bf16_ss_pair(d, tc::smem_desc_sw128(a + 32 * k),
+                                 tc::smem_desc_sw128(b + 32 * k), idesc, (kb | k) != 0);
+          tc::commit_pair(empty_bar(stage), 0x3);
+          if (++stage == kPStages) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+        tc::commit_pair(tfull_bar(acc), 0x3);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1u;
+        }
+      }
+    }
+  } else {
+    // ===== epilogue (both CTAs): this CTA's 128 token rows x 256 columns =====
+    const int sub = warp & 3;
+    const int r_in = sub * 32 + lane;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int64_t u = cid; u < n_units; u += ncl) {
+      const int64_t row = (u % n_mpair) * 256 + 128 * rank + r_in;
+      const int32_t vt = static_cast<int32_t>(u / n_mpair);
+      const int32_t n0 = vt * kBN;
+      const bool row_ok = row < P.n_rows;
+      const int32_t yrel = row_ok ? P.target[row] - n0 : -1;
+      const int32_t ncols = min(kBN, P.V - n0);
+      ptx::mbar_wait_u32(tfull_bar(acc), acc_phase);
+      tc::fence_after_sync();
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(sub * 32) << 16) +
+                             static_cast<uint32_t>(acc * kBN);
+      const float2 part = epilogue_row(taddr, row, row_ok, n0, ncols, yrel, P);
+      tc::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive_remote(ptx::mapa(tempty_bar(acc), 0));
+      if (row_ok) P.partials[row * P.n_vt + vt] = part;
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1u;
+      }
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  ptx::cluster_sync_all();
+  if (warp == 1) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc_pair<kTmemCols>(tmem_base);
   }
 }
 
@@ -340,10 +506,38 @@ cudaError_t launch_lmhead_fwd(const void* hidden, int64_t ld_h, const void* weig
   p.ld = ld;
   p.partials = reinterpret_cast<float2*>(partials);
   p.target = target;
-  const int grid = static_cast<int>(std::min<int64_t>(p.n_tiles, num_sms));
-  lmhead_fwd_kernel<<<grid, kThreads, kSmemBytes, stream>>>(tx, tw, p);
-  if (info) *info = LaunchInfo{num_sms, 1, grid, "lmhead_fwd_kernel"};
-  return cudaGetLastError();
+  const char* impl = std::getenv("COPRIS_LMHEAD_IMPL");
+  if (impl && std::strcmp(impl, "1sm") == 0) {
+    const int grid = static_cast<int>(std::min<int64_t>(p.n_tiles, num_sms));
+    lmhead_fwd_kernel<<<grid, kThreads, kSmemBytes, stream>>>(tx, tw, p);
+    if (info) *info = LaunchInfo{num_sms, 1, grid, "lmhead_fwd_kernel"};
+    return cudaGetLastError();
+  }
+  // the pair kernel stages half of the weight tile per CTA: 128-row boxes
+  if (!make_map(&tw, weight, V, H, ld_w, 128)) return cudaErrorInvalidValue;
+  static bool pattr = [] {
+    return cudaFuncSetAttribute(lmhead_fwd_pair_kernel,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(kPSmemBytes)) == cudaSuccess;
+  }();
+  if (!pattr) return cudaErrorInvalidValue;
+  const int64_t units = (n_rows + 255) / 256 * p.n_vt;
+  const int grid = static_cast<int>(std::min<int64_t>(2 * units, num_sms & ~1));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kPSmemBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr_cl[1];
+  attr_cl[0].id = cudaLaunchAttributeClusterDimension;
+  attr_cl[0].val.clusterDim.x = 2;
+  attr_cl[0].val.clusterDim.y = 1;
+  attr_cl[0].val.clusterDim.z = 1;
+  cfg.attrs = attr_cl;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, lmhead_fwd_pair_kernel, tx, tw, p);
+  if (info) *info = LaunchInfo{num_sms, 2, grid, "lmhead_fwd_pair_kernel"};
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_lse_merge(const float* partials, int32_t n_vt, const void* logits, int64_t ld,

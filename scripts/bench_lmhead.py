@@ -1,0 +1,81 @@
+"""LM-head forward (tcgen05 + fused LSE partials) vs cuBLAS, and the chunked
+LM-head IS-loss step vs the composition cuBLAS GEMM -> fused loss -> cuBLAS."""
+import json
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+from paper_2511_05589_b200 import ClipConfig, Copris
+from paper_2511_05589_b200.lmhead import lmhead_grpo_step_loss
+from paper_2511_05589_b200.packing import upload
+
+
+def timeit(fn, iters=10, warm=3):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(iters):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / iters
+
+
+def main():
+    T = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
+    H = int(sys.argv[2]) if len(sys.argv) > 2 else 4096
+    V = int(sys.argv[3]) if len(sys.argv) > 3 else 151936
+    ctx = Copris(0)
+    g = torch.Generator(device="cuda").manual_seed(0)
+    x = torch.randn(T, H, device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn(V, H, device="cuda", generator=g) / H ** 0.5).to(torch.bfloat16)
+    tgt = torch.randint(0, V, (T,), device="cuda", dtype=torch.int32, generator=g)
+    ldv = (V + 7) // 8 * 8
+    buf = torch.empty((T, ldv), dtype=torch.bfloat16, device="cuda")[:, :V]
+    part = torch.empty((T, ctx.lib.copris_lmhead_num_vtiles(V), 2), dtype=torch.float32, device="cuda")
+    flops = 2.0 * T * H * V
+    t_ours = timeit(lambda: ctx.lmhead_logits(x, w, tgt, logits=buf, partials=part))
+    t_cublas = timeit(lambda: torch.mm(x, w.t(), out=buf))
+    out = {"T": T, "H": H, "V": V,
+           "lmhead_fwd_ms": t_ours, "lmhead_fwd_tflops": flops / t_ours / 1e9,
+           "cublas_fwd_ms": t_cublas, "cublas_fwd_tflops": flops / t_cublas / 1e9}
+    # full step
+    n_traj = T // 512
+    tok_off = np.arange(0, T + 1, 512, dtype=np.int64)
+    group_off = np.arange(0, n_traj + 1, 8, dtype=np.int64)
+    stage = (np.arange(T) % 2).astype(np.uint32) + 1
+    blp = np.full(T, -10.0, np.float32)
+    reward = (np.arange(n_traj) % 2).astype(np.float64)
+    batch = upload(ctx, tok_off, group_off, tgt.cpu().numpy(), blp, 2, stage=stage, reward=reward)
+    dW = torch.zeros((V, H), dtype=torch.float32, device="cuda")
+    chunk = int(sys.argv[4]) if len(sys.argv) > 4 else 8192
+    t_step = timeit(lambda: lmhead_grpo_step_loss(ctx, x, w, batch, ClipConfig(), chunk_rows=chunk,
+                                                  dweight=dW), iters=3, warm=1)
+    dh = torch.empty_like(x)
+    outs = ctx.alloc_outputs(T, x.device)
+    out4 = torch.empty(4, dtype=torch.float64, device="cuda")
+
+    def composed():
+        for a in range(0, T, chunk):
+            n = min(chunk, T - a)
+            lg = buf[:n]
+            torch.mm(x[a:a + n], w.t(), out=lg)
+            ctx.loss_chunk_fused(lg, batch, ClipConfig(), outs, dlogits=lg, row_base=a, total_tokens=T)
+            torch.mm(lg, w, out=dh[a:a + n])
+            torch.addmm(dW, lg.t(), x[a:a + n], out_dtype=torch.float32, out=dW)
+        ctx.reduce(outs, T, out4)
+        ctx.check()
+        return out4.cpu()
+
+    t_comp = timeit(composed, iters=3, warm=1)
+    out.update({"step_ms": t_step, "composed_step_ms": t_comp, "chunk": chunk,
+                "step_tflops": 6 * T * H * V / t_step / 1e9})
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
