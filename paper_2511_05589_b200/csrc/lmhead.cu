@@ -62,6 +62,7 @@ struct LmParams {
   int64_t ld;
   float2* partials;  // [n_rows][n_vt]
   const int32_t* target;
+  int32_t group;     // token-pair blocks per raster group (pair kernel)
 };
 
 __device__ __forceinline__ float bf16_round(float x) {
@@ -73,7 +74,7 @@ __device__ __forceinline__ float bf16_round(float x) {
 // columns with the target column left out. Returns the partial.
 __device__ __forceinline__ float2 epilogue_row(uint32_t taddr, int64_t row, bool row_ok,
                                                int32_t n0, int32_t ncols, int32_t yrel,
-                                               const LmParams& P) {
+                                               const LmParams& P, uint64_t st_pol) {
   float m = -INFINITY, s = 0.f;
   __nv_bfloat16* out = P.logits + row * P.ld + n0;
 #pragma unroll 1
@@ -104,10 +105,12 @@ __device__ __forceinline__ float2 epilogue_row(uint32_t taddr, int64_t row, bool
         uint4* o = reinterpret_cast<uint4*>(out + c);
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          o[q] = make_uint4(ptx::pack_bf16x2(z[8 * q + 0], z[8 * q + 1]),
-                            ptx::pack_bf16x2(z[8 * q + 2], z[8 * q + 3]),
-                            ptx::pack_bf16x2(z[8 * q + 4], z[8 * q + 5]),
-                            ptx::pack_bf16x2(z[8 * q + 6], z[8 * q + 7]));
+          ptx::st_global_v4_hint(o + q,
+                                 make_uint4(ptx::pack_bf16x2(z[8 * q + 0], z[8 * q + 1]),
+                                            ptx::pack_bf16x2(z[8 * q + 2], z[8 * q + 3]),
+                                            ptx::pack_bf16x2(z[8 * q + 4], z[8 * q + 5]),
+                                            ptx::pack_bf16x2(z[8 * q + 6], z[8 * q + 7])),
+                                 st_pol);
       } else {
 #pragma unroll
         for (int j = 0; j < 32; ++j)
@@ -160,7 +163,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ===== TMA producer =====
-      const uint64_t pol_w = ptx::policy_evict_first();  // weight tiles: used by concurrent CTAs only
+      const uint64_t pol_w = ptx::policy_evict_normal();  // weight tiles: shared by concurrent CTAs
       const uint64_t pol_x = ptx::policy_evict_last();   // hidden block: re-read for every vocab tile
       int stage = 0;
       uint32_t phase = 0;
@@ -216,6 +219,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ===== epilogue: TMEM -> bf16 logits + LSE partials =====
     const int sub = warp & 3;  // TMEM lane quarter this warp may access
     const int r_in = sub * 32 + lane;
+    // logits are streamed out: keep L2 for the operand tiles
+    const uint64_t st_pol = ptx::policy_evict_first();
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int64_t t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
@@ -229,7 +234,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::fence_after_sync();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(sub * 32) << 16) +
                              static_cast<uint32_t>(acc * kBN);
-      const float2 part = epilogue_row(taddr, row, row_ok, n0, ncols, yrel, P);
+      const float2 part = epilogue_row(taddr, row, row_ok, n0, ncols, yrel, P, st_pol);
       tc::fence_before_sync();
       ptx::mbar_arrive_u32(tempty_bar(acc));
       if (row_ok) P.partials[row * P.n_vt + vt] = part;
@@ -260,7 +265,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 //   tfull[b]  both CTAs; multicast commit after the tile's last k-step
 //   tempty[b] leader only; one arrive per epilogue warp of either CTA (8)
 // ---------------------------------------------------------------------------
-constexpr int kPStages = 6;
+constexpr int kPStages = 7;
 constexpr int kPABytes = 128 * kBK * 2;  // 16 KB: this CTA's 128 token rows
 constexpr int kPBBytes = 128 * kBK * 2;  // 16 KB: this CTA's half of the weight tile
 constexpr int kPStageBytes = kPABytes + kPBBytes;
@@ -307,17 +312,31 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nk = (P.H + kBK - 1) / kBK;
   const int64_t n_mpair = (P.n_rows + 255) / 256;
   const int64_t n_units = n_mpair * P.n_vt;
+  // Grouped raster: units sweep every vocab tile for a group of `grp` token
+  // pairs before moving on, so the group's hidden rows stay L2-resident while
+  // each weight tile is shared by the group's concurrently running clusters.
+  const int64_t grp = P.group < n_mpair ? static_cast<int64_t>(P.group) : n_mpair;
+  auto unit_coords = [&](int64_t u, int64_t& mp, int32_t& vt) {
+    const int64_t per = grp * P.n_vt;
+    const int64_t g = u / per, w = u % per;
+    const int64_t gsz = grp < n_mpair - g * grp ? grp : n_mpair - g * grp;  // last group may be short
+    vt = static_cast<int32_t>(w / gsz);
+    mp = g * grp + w % gsz;
+  };
   const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   if (warp == 0) {
     if (lane == 0) {
       // ===== TMA producer (both CTAs) =====
-      const uint64_t pol_w = ptx::policy_evict_first();
+      const uint64_t pol_w = ptx::policy_evict_normal();
       const uint64_t pol_x = ptx::policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t u = cid; u < n_units; u += ncl) {
-        const int32_t m0 = static_cast<int32_t>(u % n_mpair) * 256 + 128 * rank;
-        const int32_t n0 = static_cast<int32_t>(u / n_mpair) * kBN + 128 * rank;
+        int64_t mp;
+        int32_t vt;
+        unit_coords(u, mp, vt);
+        const int32_t m0 = static_cast<int32_t>(mp) * 256 + 128 * rank;
+        const int32_t n0 = vt * kBN + 128 * rank;
         for (int kb = 0; kb < nk; ++kb) {
           ptx::mbar_wait_u32(empty_bar(stage), phase ^ 1u);
           const uint32_t fb = ptx::mapa(full_bar(stage), 0);
@@ -368,11 +387,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ===== epilogue (both CTAs): this CTA's 128 token rows x 256 columns =====
     const int sub = warp & 3;
     const int r_in = sub * 32 + lane;
+    // logits are streamed out: keep L2 for the operand tiles
+    const uint64_t st_pol = ptx::policy_evict_first();
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int64_t u = cid; u < n_units; u += ncl) {
-      const int64_t row = (u % n_mpair) * 256 + 128 * rank + r_in;
-      const int32_t vt = static_cast<int32_t>(u / n_mpair);
+      int64_t mp;
+      int32_t vt;
+      unit_coords(u, mp, vt);
+      const int64_t row = mp * 256 + 128 * rank + r_in;
       const int32_t n0 = vt * kBN;
       const bool row_ok = row < P.n_rows;
       const int32_t yrel = row_ok ? P.target[row] - n0 : -1;
@@ -381,7 +404,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::fence_after_sync();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(sub * 32) << 16) +
                              static_cast<uint32_t>(acc * kBN);
-      const float2 part = epilogue_row(taddr, row, row_ok, n0, ncols, yrel, P);
+      const float2 part = epilogue_row(taddr, row, row_ok, n0, ncols, yrel, P, st_pol);
       tc::fence_before_sync();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive_remote(ptx::mapa(tempty_bar(acc), 0));
@@ -506,6 +529,10 @@ cudaError_t launch_lmhead_fwd(const void* hidden, int64_t ld_h, const void* weig
   p.ld = ld;
   p.partials = reinterpret_cast<float2*>(partials);
   p.target = target;
+  {
+    const char* g = std::getenv("COPRIS_LMHEAD_GROUP");
+    p.group = g ? std::max(1, std::atoi(g)) : 16;
+  }
   const char* impl = std::getenv("COPRIS_LMHEAD_IMPL");
   if (impl && std::strcmp(impl, "1sm") == 0) {
     const int grid = static_cast<int>(std::min<int64_t>(p.n_tiles, num_sms));

@@ -1,4 +1,2 @@
-python scripts/trace_phases.py 151936 16384 > gpurun_out/trace_pf2.log 2>&1
-cp paper_2511_05589_b200/libcopris_b200.so /tmp/keep.so; cp scripts/micro/lib_pf1.so paper_2511_05589_b200/libcopris_b200.so
-python scripts/trace_phases.py 151936 16384 > gpurun_out/trace_pf1.log 2>&1
-cp /tmp/keep.so paper_2511_05589_b200/libcopris_b200.so
+for i in 1 2; do COPRIS_LMHEAD_GROUP=16 timeout 120 python scripts/bench_lmhead.py 4096 >> gpurun_out/lmb.log 2>&1; done
+COPRIS_LMHEAD_GROUP=16 timeout 600 ncu --set full --import-source on -k regex:lmhead_fwd_pair -c 1 -o gpurun_out/lmhead_pair python scripts/bench_lmhead.py 4096 > /dev/null 2>&1

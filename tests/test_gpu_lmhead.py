@@ -18,6 +18,16 @@ from parity_util import assert_loss_close, assert_rows_close, assert_scalar_clos
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(params=["pair", "1sm"], autouse=True)
+def impl(request, monkeypatch):
+    """Both kernels: the CTA-pair (cta_group::2) default and the 1-SM variant."""
+    if request.param == "1sm":
+        monkeypatch.setenv("COPRIS_LMHEAD_IMPL", "1sm")
+    else:
+        monkeypatch.delenv("COPRIS_LMHEAD_IMPL", raising=False)
+    return request.param
+
+
 def _inputs(T, H, V, seed, scale=1.0):
     g = torch.Generator(device="cpu").manual_seed(seed)
     x = (torch.randn(T, H, generator=g) * scale).to(torch.bfloat16)
@@ -35,9 +45,10 @@ def _check_logits(lg, x, w):
 
 @pytest.mark.parametrize("T,H,V", [(1, 64, 256), (130, 64, 300), (257, 192, 1000), (300, 520, 4099),
                                    (512, 1024, 32000), (129, 4096, 151936)])
-def test_lmhead_logits_and_partials(ctx, T, H, V):
+def test_lmhead_logits_and_partials(ctx, impl, T, H, V):
     x, w, tgt = _inputs(T, H, V, T + H + V)
     lg, part = ctx.lmhead_logits(x, w, tgt)
+    assert ctx.last_launch()["kernel"] == ("lmhead_fwd_pair_kernel" if impl == "pair" else "lmhead_fwd_kernel")
     torch.cuda.synchronize()
     rows = torch.arange(T, device="cuda") if T * V <= 2 ** 26 else torch.randperm(T, device="cuda")[:32]
     _check_logits(lg[rows], x[rows], w)
