@@ -48,8 +48,8 @@ def parse_args():
     ap.add_argument("--unfused", action="store_true", help="K1 -> K2 -> K3 instead of the fused kernel")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-tokens", type=int, default=8192, help="per-rank sample for the host round trip")
-    ap.add_argument("--e2e-chunk", type=int, default=2048)
+    ap.add_argument("--e2e-tokens", type=int, default=16384, help="per-rank sample for the host round trip")
+    ap.add_argument("--e2e-chunk", type=int, default=512)
     ap.add_argument("--cpu-tokens-per-thread", type=int, default=256)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--seed", type=int, default=1)
