@@ -775,6 +775,7 @@ __global__ void __launch_bounds__(WARPS * 32)
 // stays busy while the consumers synchronise, and no cluster couples SMs.
 // ---------------------------------------------------------------------------
 constexpr int kStreamK = 4;  // 16-byte vectors per consumer thread per ring slot
+constexpr int kStreamLookahead = 2;  // ring segments of row r+1 consumed before pass 2 of row r
 #ifndef COPRIS_STREAM_PREFETCH
 #define COPRIS_STREAM_PREFETCH 0  // 1|2 = L2-prefetch next row before pass 1|2; measured slower (L2 thrash)
 #endif
@@ -1102,6 +1103,344 @@ __global__ void __launch_bounds__((CW + 1) * 32, CW <= 8 ? 2 : 1)
       if (lane == 0) ptx::mbar_arrive_u32(ebase + slot * 8);
     }
     tm.mark(4);
+    tm.acc[5] += 1;
+  }
+  tm.flush(P.trace);
+}
+
+// ---------------------------------------------------------------------------
+// fused_stream_la_kernel: the streaming kernel with a one-row lookahead that
+// takes the per-row scalar phase off the consumers' critical path.
+//
+// Segment order through the ring (producer and consumers agree on it):
+//   P1(r0) | P1(r1)[0,L) P2(r0) P1(r1)[L,n) | P1(r2)[0,L) P2(r1) P1(r2)[L,n) | ...
+// After pass 1 of row r the consumers hand their partials to a dedicated
+// scalar warp (mbarrier p1done) and continue with the first L segments of the
+// next row; the scalar warp merges the partials, runs the token math and
+// publishes the row broadcast (mbarrier sdone) while they do. Rows stay in L2
+// between their two passes for about one row plus L segments.
+// ---------------------------------------------------------------------------
+struct P1Acc {
+  float m = -INFINITY, nml = INFINITY;
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  float zy = 0.f;
+  bool have_zy = false;
+  Lse st = lse_empty();  // entropy path
+};
+
+// Pass-1 work of one consumer thread on one ring segment.
+template <typename TIn, int NC, int K, int kSlotVec, bool ENT>
+__device__ __forceinline__ void p1_segment(P1Acc& a, uint32_t sb, int32_t v0, int32_t cnt,
+                                           int32_t y, int tid) {
+  using VI = Vec<TIn>;
+  using PB = PassB<TIn>;
+  constexpr int VN = VI::N;
+  if constexpr (ENT) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int32_t j = tid + k * NC;
+      if (j < cnt) {
+        float x[VN];
+        VI::unpack(ptx::lds_v4(sb + j * 16), x);
+        const int jt = y - (v0 + j) * VN;
+        if (static_cast<uint32_t>(jt) < VN) {
+#pragma unroll
+          for (int q = 0; q < VN; ++q)
+            if (q == jt) a.zy = x[q];
+          a.have_zy = true;
+        }
+        online_update<VN, true>(x, a.st, static_cast<uint32_t>(jt) < VN ? jt : -1);
+      }
+    }
+  } else {
+    const bool tseg = static_cast<uint32_t>(y - v0 * VN) < static_cast<uint32_t>(cnt * VN);
+    const bool full_seg = cnt == kSlotVec;
+#pragma unroll
+    for (int k = 0; k < K; k += 2) {
+      const int32_t ja_i = tid + k * NC, jb_i = ja_i + NC;
+      uint4 va, vb;
+      if (full_seg) {
+        va = ptx::lds_v4(sb + ja_i * 16);
+        vb = ptx::lds_v4(sb + jb_i * 16);
+      } else {
+        const uint4 ninf{PB::kNegInfWord, PB::kNegInfWord, PB::kNegInfWord, PB::kNegInfWord};
+        va = ja_i < cnt ? ptx::lds_v4(sb + ja_i * 16) : ninf;
+        vb = jb_i < cnt ? ptx::lds_v4(sb + jb_i * 16) : ninf;
+      }
+      const float vm = PB::vmax(va, vb);
+      if (vm > a.m) {
+        const float rs = ptx::ex2((a.m - vm) * kLog2e);
+        a.s0 *= rs;
+        a.s1 *= rs;
+        a.s2 *= rs;
+        a.s3 *= rs;
+        a.m = vm;
+        a.nml = -(a.m * kLog2e);
+      }
+      float xa[VN], xb[VN];
+      VI::unpack(va, xa);
+      VI::unpack(vb, xb);
+      if (tseg) {
+        const int ja = y - (v0 + ja_i) * VN, jb = y - (v0 + jb_i) * VN;
+#pragma unroll
+        for (int q = 0; q < VN; ++q) {
+          if (q == ja) {
+            a.zy = xa[q];
+            a.have_zy = true;
+            xa[q] = -INFINITY;
+          }
+          if (q == jb) {
+            a.zy = xb[q];
+            a.have_zy = true;
+            xb[q] = -INFINITY;
+          }
+        }
+      }
+      const float nml = a.nml;
+      a.s0 += ptx::ex2(fmaf(xa[0], kLog2e, nml));
+      a.s1 += ptx::ex2(fmaf(xa[1], kLog2e, nml));
+      a.s2 += ptx::ex2(fmaf(xb[0], kLog2e, nml));
+      a.s3 += ptx::ex2(fmaf(xb[1], kLog2e, nml));
+      a.s0 += ptx::ex2(fmaf(xa[2], kLog2e, nml));
+      a.s1 += ptx::ex2(fmaf(xa[3], kLog2e, nml));
+      a.s2 += ptx::ex2(fmaf(xb[2], kLog2e, nml));
+      a.s3 += ptx::ex2(fmaf(xb[3], kLog2e, nml));
+      if constexpr (VN == 8) {
+        a.s0 += ptx::ex2(fmaf(xa[4], kLog2e, nml));
+        a.s1 += ptx::ex2(fmaf(xa[5], kLog2e, nml));
+        a.s2 += ptx::ex2(fmaf(xb[4], kLog2e, nml));
+        a.s3 += ptx::ex2(fmaf(xb[5], kLog2e, nml));
+        a.s0 += ptx::ex2(fmaf(xa[6], kLog2e, nml));
+        a.s1 += ptx::ex2(fmaf(xa[7], kLog2e, nml));
+        a.s2 += ptx::ex2(fmaf(xb[6], kLog2e, nml));
+        a.s3 += ptx::ex2(fmaf(xb[7], kLog2e, nml));
+      }
+    }
+  }
+}
+
+// Pass-2 work (dlogits) of one consumer thread on one ring segment.
+template <typename TIn, typename TOut, int NC, int K, int kSlotVec, bool ENT>
+__device__ __forceinline__ void p2_segment(const RowBroadcast& b, bool zero_row, uint32_t sb,
+                                           int32_t v0, int32_t cnt, TOut* dseg, int tid,
+                                           uint64_t pol) {
+  using VI = Vec<TIn>;
+  constexpr int VN = VI::N;
+  const bool tseg = static_cast<uint32_t>(b.y - v0 * VN) < static_cast<uint32_t>(cnt * VN);
+  if (!ENT && !zero_row && cnt == kSlotVec) {
+    uint4 raw[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) raw[q] = ptx::lds_v4(sb + (tid + q * NC) * 16);
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+      float x[VN], d[VN];
+      VI::unpack(raw[q], x);
+#pragma unroll
+      for (int e = 0; e < VN; ++e) d[e] = ptx::ex2(fmaf(x[e], kLog2e, -b.c1)) * -b.coef;
+      if (tseg) {
+        const int jt = b.y - (v0 + tid + q * NC) * VN;
+#pragma unroll
+        for (int e = 0; e < VN; ++e)
+          if (e == jt) d[e] = b.dy;
+      }
+      store_vec<TOut, VN>(dseg + static_cast<int64_t>(tid + q * NC) * VN, d, pol);
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+      const int32_t j = tid + q * NC;
+      if (j < cnt) {
+        float d[VN];
+        if (zero_row) {
+#pragma unroll
+          for (int e = 0; e < VN; ++e) d[e] = 0.f;
+        } else {
+          float x[VN];
+          VI::unpack(ptx::lds_v4(sb + j * 16), x);
+          if constexpr (ENT) {
+            row_grad<VN, ENT>(x, d, (v0 + j) * VN, b);
+          } else {
+#pragma unroll
+            for (int e = 0; e < VN; ++e) d[e] = ptx::ex2(fmaf(x[e], kLog2e, -b.c1)) * -b.coef;
+            if (tseg) {
+              const int jt = b.y - (v0 + j) * VN;
+#pragma unroll
+              for (int e = 0; e < VN; ++e)
+                if (e == jt) d[e] = b.dy;
+            }
+          }
+        }
+        store_vec<TOut, VN>(dseg + static_cast<int64_t>(j) * VN, d, pol);
+      }
+    }
+  }
+}
+
+template <typename TIn, typename TOut, int CW, int KV, bool ENT>
+__global__ void __launch_bounds__((CW + 2) * 32, 1)
+    fused_stream_la_kernel(const LossParams P, const int nslots, const int look) {
+  constexpr int kSlotVec = CW * 32 * KV;
+  using VI = Vec<TIn>;
+  constexpr int VN = VI::N;
+  constexpr int NC = CW * 32;
+  constexpr int K = KV;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full[32], empty[32], p1done[2], sdone[2];
+  __shared__ Lse red[2][CW];
+  __shared__ float zy_sh[2];
+  __shared__ RowBroadcast bc[2];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int32_t V = P.vocab;
+  const int32_t nvec = V / VN;
+  const int32_t nseg = (nvec + kSlotVec - 1) / kSlotVec;
+  const int32_t L = min(look, nseg);
+  const uint32_t sbase = ptx::smem_u32(smem);
+  const uint32_t fbase = ptx::smem_u32(full), ebase = ptx::smem_u32(empty);
+  const uint32_t p1b = ptx::smem_u32(p1done), sdb = ptx::smem_u32(sdone);
+  const int64_t G = gridDim.x;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < nslots; ++i) {
+      ptx::mbar_init(&full[i], 1);
+      ptx::mbar_init(&empty[i], CW);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&p1done[i], CW);
+      ptx::mbar_init(&sdone[i], 1);
+    }
+    ptx::fence_mbarrier_init();
+  }
+  __syncthreads();
+
+  if (warp == CW) {
+    // ---------------- producer: same segment order as the consumers ----------
+    if (lane == 0) {
+      const uint64_t keep = ptx::policy_evict_last(), drop = ptx::policy_evict_first();
+      Ring ring(nslots);
+      auto issue = [&](const TIn* row, int32_t sg0, int32_t sg1, uint64_t pol) {
+        for (int32_t sg = sg0; sg < sg1; ++sg, ring.next()) {
+          const uint32_t slot = ring.slot, par = ring.ph;
+          ptx::mbar_wait_u32(ebase + slot * 8, par ^ 1u);
+          const int32_t v0 = sg * kSlotVec;
+          const uint32_t bytes = static_cast<uint32_t>(min(kSlotVec, nvec - v0)) * 16u;
+          ptx::mbar_arrive_expect_tx_u32(fbase + slot * 8, bytes);
+          ptx::bulk_g2s_u32(sbase + slot * (kSlotVec * 16), row + static_cast<int64_t>(v0) * VN,
+                            bytes, fbase + slot * 8, pol);
+        }
+      };
+      auto rowp = [&](int64_t r) { return static_cast<const TIn*>(P.logits) + r * P.ld; };
+      int64_t r = blockIdx.x;
+      if (r < P.n_rows) issue(rowp(r), 0, nseg, keep);
+      for (; r < P.n_rows; r += G) {
+        const bool nx = r + G < P.n_rows;
+        if (nx) issue(rowp(r + G), 0, L, keep);
+        if (P.dlogits) issue(rowp(r), 0, nseg, drop);
+        if (nx) issue(rowp(r + G), L, nseg, keep);
+      }
+    }
+    return;
+  }
+
+  if (warp == CW + 1) {
+    // ---------------- scalar warp: merge partials, token math, broadcast -----
+    MetaPipe mp;
+    if (lane == 0) mp.init(P, blockIdx.x, G);
+    uint32_t i = 0;
+    for (int64_t r = blockIdx.x; r < P.n_rows; r += G, ++i) {
+      RowMeta meta{};
+      if (lane == 0) meta = mp.advance(P, r, G);
+      const uint32_t bsel = i & 1u, par = (i >> 1) & 1u;
+      ptx::mbar_wait_u32(p1b + bsel * 8, par);
+      Lse tot = lane < CW ? red[bsel][lane] : lse_empty();
+      warp_lse<ENT>(tot);
+      if (lane == 0) {
+        const float zy = static_cast<uint32_t>(meta.y) < static_cast<uint32_t>(V) ? zy_sh[bsel] : 0.f;
+        bc[bsel] = row_scalar_phase<ENT>(P, P.row_base + r, meta.y, meta.st, meta.blp, meta.rl,
+                                         meta.adv, tot, zy, true);
+        ptx::mbar_arrive_u32(sdb + bsel * 8);
+      }
+      __syncwarp();
+    }
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  const int tid = threadIdx.x;
+  const uint64_t pol = ptx::policy_evict_first();
+  Ring ring(nslots);
+  PhaseTimer tm;
+  tm.start(P.trace && tid == 0 && blockIdx.x < kTraceCtas);
+
+  auto run_p1 = [&](P1Acc& a, int32_t y, int32_t sg0, int32_t sg1) {
+    for (int32_t sg = sg0; sg < sg1; ++sg, ring.next()) {
+      const uint32_t slot = ring.slot, par = ring.ph;
+      const int32_t v0 = sg * kSlotVec;
+      const long long w0 = tm.on ? clock64() : 0;
+      ptx::mbar_wait_u32(fbase + slot * 8, par);
+      if (tm.on) tm.acc[6] += clock64() - w0;
+      p1_segment<TIn, NC, K, kSlotVec, ENT>(a, sbase + slot * (kSlotVec * 16), v0,
+                                            min(kSlotVec, nvec - v0), y, tid);
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive_u32(ebase + slot * 8);
+    }
+  };
+  // hand row i's pass-1 partials to the scalar warp
+  auto finish_p1 = [&](P1Acc& a, uint32_t i) {
+    Lse st = a.st;
+    if constexpr (!ENT) {
+      st.m = a.m;
+      st.s = (a.s0 + a.s1) + (a.s2 + a.s3);
+    }
+    warp_lse<ENT>(st);
+    const uint32_t bsel = i & 1u;
+    if (a.have_zy) zy_sh[bsel] = a.zy;  // exactly one consumer thread owns the target
+    if (lane == 0) red[bsel][warp] = st;
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive_u32(p1b + bsel * 8);
+  };
+
+  int64_t r = blockIdx.x;
+  uint32_t i = 0;
+  if (r < P.n_rows) {
+    P1Acc a0;
+    run_p1(a0, P.target[P.row_base + r], 0, nseg);
+    finish_p1(a0, 0);
+  }
+  tm.mark(0);
+  for (; r < P.n_rows; r += G, ++i) {
+    const int64_t rn = r + G;
+    const bool nx = rn < P.n_rows;
+    P1Acc an;
+    const int32_t yn = nx ? P.target[P.row_base + rn] : 0;
+    if (nx) run_p1(an, yn, 0, L);
+    tm.mark(0);
+    const uint32_t bsel = i & 1u, par = (i >> 1) & 1u;
+    ptx::mbar_wait_u32(sdb + bsel * 8, par);  // row i's broadcast (also frees red/zy_sh[bsel])
+    tm.mark(2);
+    if (P.dlogits) {
+      const RowBroadcast b = bc[bsel];
+      const bool zero_row = (b.coef == 0.f) && (!ENT || b.eg == 0.f);
+      TOut* drow = static_cast<TOut*>(P.dlogits) + r * P.ld_d;
+      for (int32_t sg = 0; sg < nseg; ++sg, ring.next()) {
+        const uint32_t slot = ring.slot, ph = ring.ph;
+        const int32_t v0 = sg * kSlotVec;
+        const long long w0 = tm.on ? clock64() : 0;
+        ptx::mbar_wait_u32(fbase + slot * 8, ph);
+        if (tm.on) tm.acc[7] += clock64() - w0;
+        p2_segment<TIn, TOut, NC, K, kSlotVec, ENT>(b, zero_row, sbase + slot * (kSlotVec * 16), v0,
+                                                    min(kSlotVec, nvec - v0),
+                                                    drow + static_cast<int64_t>(v0) * VN, tid, pol);
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_u32(ebase + slot * 8);
+      }
+    }
+    tm.mark(4);
+    if (nx) {
+      run_p1(an, yn, L, nseg);
+      finish_p1(an, i + 1);
+    }
+    tm.mark(0);
     tm.acc[5] += 1;
   }
   tm.flush(P.trace);
@@ -1589,6 +1928,23 @@ cudaError_t launch_l2(const LossParams& p, int num_sms, cudaStream_t stream, Lau
 
 template <typename TIn, typename TOut, int CW, bool ENT, int KV = kStreamK>
 cudaError_t launch_stream(const LossParams& p, int num_sms, cudaStream_t stream, LaunchInfo* info) {
+  const int look = tune_env("COPRIS_TUNE_LOOKAHEAD", kStreamLookahead);
+  if (look > 0) {
+    auto kernel = fused_stream_la_kernel<TIn, TOut, CW, KV, ENT>;
+    constexpr int slot_bytes = CW * 32 * KV * 16;
+    const int nslots = tune_env("COPRIS_TUNE_SLOTS", (CW >= 16 ? 196608 : 98304) / slot_bytes);
+    const int smem = nslots * slot_bytes;
+    cudaError_t e = set_smem(kernel, smem);
+    if (e != cudaSuccess) return e;
+    const int grid = grid_rows(p.n_rows, num_sms, 1);
+    if (info) {
+      info->cluster = 1;
+      info->grid = grid;
+      info->kernel = "fused_stream_la_kernel";
+    }
+    kernel<<<grid, (CW + 2) * 32, smem, stream>>>(p, nslots, look);
+    return cudaGetLastError();
+  }
   auto kernel = fused_stream_kernel<TIn, TOut, CW, KV, ENT>;
   constexpr int slot_bytes = CW * 32 * KV * 16;
   const int nslots = tune_env("COPRIS_TUNE_SLOTS", (CW >= 16 ? 196608 : 98304) / slot_bytes);

@@ -23,15 +23,20 @@ def run(ctx, case, dl_dtype=BF16, fused=True, **kw):
 
 # (V, logits dtype, forced implementation or None, expected kernel, expected cluster)
 SHAPES = [
-    (151936, BF16, None, "fused_stream_kernel", 1),   # Qwen2.5 vocab: TMA ring + L2 re-read
+    (151936, BF16, None, "fused_stream_la_kernel", 1),  # Qwen2.5 vocab: TMA ring + L2 re-read, lookahead
+    (151936, BF16, "stream+la0", "fused_stream_kernel", 1),  # same without the lookahead
+    (151936, BF16, "stream+la5", "fused_stream_la_kernel", 1),
     (151936, BF16, "tma", "fused_tma_kernel", 2),     # row split over a CTA pair (DSMEM)
     (151936, BF16, "l2", "fused_l2_kernel", 1),       # register-streamed two-pass variant
     (32000, BF16, None, "fused_tma_kernel", 1),       # 64 KB rows resident, several CTAs/SM
-    (32000, BF16, "stream", "fused_stream_kernel", 1),
+    (32000, BF16, "stream", "fused_stream_la_kernel", 1),  # 2 segments/row: lookahead = whole row
+    (32000, BF16, "stream+la1", "fused_stream_la_kernel", 1),
+    (32000, BF16, "stream+la0", "fused_stream_kernel", 1),
     (80000, BF16, "tma", "fused_tma_kernel", 1),      # 160 KB rows: one 16-warp CTA per row
-    (151936, F32, None, "fused_stream_kernel", 1),
+    (151936, F32, None, "fused_stream_la_kernel", 1),
+    (151936, F32, "stream+la0", "fused_stream_kernel", 1),
     (151936, F32, "tma", "fused_tma_kernel", 4),      # 608 KB f32 rows: 4-CTA cluster
-    (32000, F32, None, "fused_stream_kernel", 1),
+    (32000, F32, None, "fused_stream_la_kernel", 1),
     (256, BF16, None, "fused_tma_kernel", 1),
     (4099, BF16, None, "fused_generic_kernel", 1),    # odd vocab: unaligned rows
     (100, F32, None, "fused_generic_kernel", 1),
@@ -42,6 +47,12 @@ SHAPES = [
 @pytest.fixture
 def impl(monkeypatch):
     def set_impl(name):
+        """name = implementation[+laN]: COPRIS_FUSED_IMPL and the stream
+        kernel's lookahead (COPRIS_TUNE_LOOKAHEAD, 0 = the kernel without it)."""
+        monkeypatch.delenv("COPRIS_TUNE_LOOKAHEAD", raising=False)
+        if name and "+la" in name:
+            name, la = name.split("+la")
+            monkeypatch.setenv("COPRIS_TUNE_LOOKAHEAD", la)
         if name:
             monkeypatch.setenv("COPRIS_FUSED_IMPL", name)
         else:
@@ -69,8 +80,9 @@ def test_unfused_matches_oracle(ctx, oracle, V, dtype):
     case.check(res, F32, what=f"unfused V={V}")
 
 
-@pytest.mark.parametrize("V,force", [(151936, None), (151936, "tma"), (151936, "l2"),
-                                     (32000, None), (32000, "stream"), (4099, None)])
+@pytest.mark.parametrize("V,force", [(151936, None), (151936, "stream+la0"), (151936, "tma"),
+                                     (151936, "l2"), (32000, None), (32000, "stream"),
+                                     (4099, None)])
 def test_kl_and_entropy(ctx, oracle, impl, V, force):
     impl(force)
     case = Case(oracle, seed=5, P=2, G=4, V=V, mu=math.log(10), lmax=24, kl_coeff=0.1,
