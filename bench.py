@@ -107,8 +107,10 @@ class ClockSampler:
         mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
         reasons = sorted({self.NAMES[i] for r in self.rows for i in range(4)
                           if r[4 + i].lower().startswith("active")})
+        pw = [float(r[3]) for r in self.rows if r[3].replace(".", "").isdigit()]
         return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows),
+                "power_w": statistics.median(pw) if pw else None}
 
 
 def measured_peaks():

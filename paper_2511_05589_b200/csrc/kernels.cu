@@ -1227,6 +1227,34 @@ __device__ __forceinline__ void p2_segment(const RowBroadcast& b, bool zero_row,
   using VI = Vec<TIn>;
   constexpr int VN = VI::N;
   const bool tseg = static_cast<uint32_t>(b.y - v0 * VN) < static_cast<uint32_t>(cnt * VN);
+  if constexpr (!ENT && sizeof(TOut) == 2 && VN == 8) {
+    if (!zero_row && cnt == kSlotVec) {
+      // |coef| folded into the exponent and the sign applied to the packed
+      // bf16 pair: d_k = -coef p_k = sign * 2^(z_k log2(e) - c2)
+      const float nc2 = -b.c2;
+      const float sdy = b.smask ? -b.dy : b.dy;
+      uint4 raw[K];
+#pragma unroll
+      for (int q = 0; q < K; ++q) raw[q] = ptx::lds_v4(sb + (tid + q * NC) * 16);
+#pragma unroll
+      for (int q = 0; q < K; ++q) {
+        float x[VN], e[VN];
+        VI::unpack(raw[q], x);
+#pragma unroll
+        for (int j = 0; j < VN; ++j) e[j] = ptx::ex2(fmaf(x[j], kLog2e, nc2));
+        if (tseg) {
+          const int jt = b.y - (v0 + tid + q * NC) * VN;
+#pragma unroll
+          for (int j = 0; j < VN; ++j)
+            if (j == jt) e[j] = sdy;
+        }
+        const uint4 v{ptx::pack_bf16x2(e[0], e[1]) ^ b.smask, ptx::pack_bf16x2(e[2], e[3]) ^ b.smask,
+                      ptx::pack_bf16x2(e[4], e[5]) ^ b.smask, ptx::pack_bf16x2(e[6], e[7]) ^ b.smask};
+        ptx::st_global_v4_hint(dseg + static_cast<int64_t>(tid + q * NC) * VN, v, pol);
+      }
+      return;
+    }
+  }
   if (!ENT && !zero_row && cnt == kSlotVec) {
     uint4 raw[K];
 #pragma unroll

@@ -117,6 +117,8 @@ struct RowBroadcast {
   int32_t y;     // target column
   float eg;      // entropy gradient scale c_H/T (0 when off or on error)
   float k0;      // H - ln(S): log p + H = (z - m) + k0
+  float c2;      // c1 - log2|coef|: |dlogits_k| = 2^(z_k log2(e) - c2) off the target
+  uint32_t smask;  // bf16x2 sign mask of -coef (0x80008000 when coef > 0)
 };
 
 // The scalar phase of one row: given the row's (max, sum exp(z-m), sum
@@ -166,6 +168,11 @@ __device__ __forceinline__ RowBroadcast row_scalar_phase(const LossParams& P, in
   b.y = y;
   b.eg = (ENT && !tr.err) ? static_cast<float>(P.inv_t * P.entropy_coeff) : 0.f;
   b.k0 = ENT ? H - ln_s : 0.f;
+  const double ac = fabs(static_cast<double>(b.coef));
+  b.c2 = ac > 0.0 ? static_cast<float>(static_cast<double>(M) * kLog2eD +
+                                       static_cast<double>(ln_s) * kLog2eD - log2(ac))
+                  : 0.f;
+  b.smask = b.coef > 0.f ? 0x80008000u : 0u;
   return b;
 }
 

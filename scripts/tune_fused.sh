@@ -1,3 +1,3 @@
-COPRIS_FUSED_IMPL=tma timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_tma.log 2>&1
-timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_la2_3.log 2>&1
-COPRIS_FUSED_IMPL=tma COPRIS_TUNE_CL=4 timeout 600 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_tma4.log 2>&1
+timeout 900 python -m pytest tests -q -m gpu --tb=short -x 2>&1 | tail -5 > gpurun_out/la_tests.log
+timeout 300 python scripts/micro/power_probe.py > gpurun_out/power.log 2>&1
+python scripts/trace_phases.py 151936 16384 > gpurun_out/la2.log 2>&1
