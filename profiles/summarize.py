@@ -8,7 +8,9 @@ into committed, reviewable files under profiles/:
   ncu_traffic.json       dram bytes per row of the top kernel (read by bench.py
                          for roofline.traffic)
 
-usage: python profiles/summarize.py <tag> [gpurun_out]
+usage: python profiles/summarize.py <tag> [gpurun_out] [dest_dir]
+(dest_dir defaults to profiles/; round_check.sh summarises on the GPU box into
+gpurun_out/profiles_<tag>/ because the raw .ncu-rep files are too large to ship back)
 """
 import collections
 import csv
@@ -19,7 +21,9 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 
-KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+KEYS = ["gpu__time_duration.sum", "sm__cycles_active.avg",
+        "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+        "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active", "dram__bytes_read.sum", "dram__bytes_write.sum",
         "dram__bytes.sum.per_second", "launch__grid_size", "launch__block_size",
         "launch__registers_per_thread", "launch__cluster_dim_x", "sm__warps_active.avg.pct_of_peak_sustained_active",
         "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
@@ -55,7 +59,8 @@ def ncu_summary(rep, dst_prefix, rows_per_launch):
     out = {}
     for r in rows[2:]:
         name = r[hdr.index("Kernel Name")]
-        short = name.split("<")[0].split("::")[-1].strip()
+        short = name.replace("(anonymous namespace)::", "").split("(")[0].split("<")[0]
+        short = short.split("::")[-1].replace("void ", "").strip()
         lines = [f"kernel: {name}"]
         for k in KEYS:
             if k in hdr:
@@ -84,8 +89,12 @@ def ncu_summary(rep, dst_prefix, rows_per_launch):
 
 
 def main():
+    global HERE
     tag = sys.argv[1]
     src = sys.argv[2] if len(sys.argv) > 2 else os.path.join(os.path.dirname(HERE), "gpurun_out")
+    if len(sys.argv) > 3:
+        HERE = sys.argv[3]
+        os.makedirs(HERE, exist_ok=True)
     if os.path.exists(os.path.join(src, "launches.csv")):
         launches(os.path.join(src, "launches.csv"), os.path.join(HERE, f"{tag}_launches.csv"))
     traffic = {}
@@ -101,6 +110,8 @@ def main():
             traffic["unfused:grpo_128x8_v151936"] = {"dram_bytes_per_row": sum(t.values()),
                                                      "kernel": "+".join(t),
                                                      "source": "sum of the unfused kernels"}
+    if os.path.exists(os.path.join(src, "prof_lmhead.ncu-rep")):
+        ncu_summary(os.path.join(src, "prof_lmhead.ncu-rep"), os.path.join(HERE, f"{tag}_ncu"), 4096)
     if traffic:
         with open(os.path.join(HERE, "ncu_traffic.json"), "w") as f:
             json.dump(traffic, f, indent=1)

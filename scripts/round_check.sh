@@ -7,3 +7,6 @@ timeout 300 python bench.py --config grpo_128x8_v151936_longtail_4stage --no-e2e
 timeout 300 python bench.py --unfused --no-e2e --no-cpu-baseline --steps 5 > gpurun_out/bench_unfused.log 2>&1
 timeout 300 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.log 2>&1
 bash profiles/run_profile.sh
+python profiles/summarize.py r01 gpurun_out gpurun_out/profiles_r01 > gpurun_out/summarize.log 2>&1
+cp profiles/run_profile.sh gpurun_out/profiles_r01/ 2>/dev/null
+rm -f gpurun_out/*.ncu-rep
