@@ -1305,7 +1305,7 @@ __device__ __forceinline__ void p2_segment(const RowBroadcast& b, bool zero_row,
 }
 
 template <typename TIn, typename TOut, int CW, int KV, bool ENT>
-__global__ void __launch_bounds__((CW + 2) * 32, 1)
+__global__ void __launch_bounds__((CW + 2) * 32, CW <= 8 ? 2 : 1)
     fused_stream_la_kernel(const LossParams P, const int nslots, const int look) {
   constexpr int kSlotVec = CW * 32 * KV;
   using VI = Vec<TIn>;
@@ -1964,7 +1964,10 @@ cudaError_t launch_stream(const LossParams& p, int num_sms, cudaStream_t stream,
     const int smem = nslots * slot_bytes;
     cudaError_t e = set_smem(kernel, smem);
     if (e != cudaSuccess) return e;
-    const int grid = grid_rows(p.n_rows, num_sms, 1);
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, (CW + 2) * 32, smem);
+    if (e != cudaSuccess) return e;
+    const int grid = grid_rows(p.n_rows, num_sms, per_sm < 1 ? 1 : per_sm);
     if (info) {
       info->cluster = 1;
       info->grid = grid;

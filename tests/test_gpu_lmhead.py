@@ -43,7 +43,7 @@ def _check_logits(lg, x, w):
     assert torch.all(err <= 2.0 ** -8 * ref.abs() + bound + 1e-30), float((err - 2.0 ** -8 * ref.abs() - bound).max())
 
 
-@pytest.mark.parametrize("T,H,V", [(1, 64, 256), (130, 64, 300), (257, 192, 1000), (300, 520, 4099),
+@pytest.mark.parametrize("T,H,V", [(1, 64, 256), (64, 64, 100), (130, 64, 300), (257, 192, 1000), (300, 520, 4099),
                                    (512, 1024, 32000), (129, 4096, 151936)])
 def test_lmhead_logits_and_partials(ctx, impl, T, H, V):
     x, w, tgt = _inputs(T, H, V, T + H + V)
@@ -145,3 +145,42 @@ def test_lmhead_matches_logits_path(ctx):
     assert abs(a.loss - b.loss) <= 1e-6 * max(1e-12, float(b.obj.abs().sum()) / T)
     dh = b.dlogits.float() @ w.float()
     assert torch.allclose(a.dhidden.float(), dh, rtol=2e-2, atol=1e-3 * float(dh.abs().max()))
+
+
+def test_lmhead_argument_errors(ctx):
+    """C-ABI validation: misaligned strides/pointers, short ld, partial-width mismatch."""
+    from paper_2511_05589_b200.grpo import _p
+    T, H, V = 16, 64, 300
+    x, w, tgt = _inputs(T, H, V, 1)
+    lib = ctx.lib
+    lg = torch.empty((T, 304), dtype=torch.bfloat16, device="cuda")
+    part = torch.empty((T, 2, 2), dtype=torch.float32, device="cuda")
+    s = ctx._stream()
+    ok = lib.copris_lmhead_logits(ctx.h, _p(x), H, _p(w), H, T, H, V, _p(tgt), _p(lg), 304, _p(part), s)
+    assert ok == 0
+    assert lib.copris_lmhead_logits(ctx.h, _p(x), H, _p(w), H, T, H, V, _p(tgt), _p(lg), 300,
+                                    _p(part), s) != 0  # ld_logits % 8
+    assert b"ld_logits" in lib.copris_last_error()
+    assert lib.copris_lmhead_logits(ctx.h, _p(x), 60, _p(w), H, T, H, V, _p(tgt), _p(lg), 304,
+                                    _p(part), s) != 0  # ld_hidden < hidden_dim
+    xo = torch.empty(T * H + 8, dtype=torch.bfloat16, device="cuda")[1:1 + T * H]
+    assert lib.copris_lmhead_logits(ctx.h, _p(xo), H, _p(w), H, T, H, V, _p(tgt), _p(lg), 304,
+                                    _p(part), s) != 0  # misaligned hidden
+    assert b"aligned" in lib.copris_last_error()
+    lp = torch.empty(T, dtype=torch.float32, device="cuda")
+    assert lib.copris_lse_merge(ctx.h, _p(part), 3, _p(lg), 304, _p(tgt), T, V, _p(lp), None, s) != 0
+    assert b"n_vt" in lib.copris_last_error()
+    assert lib.copris_lmhead_logits(ctx.h, _p(x), H, _p(w), H, 0, H, V, _p(tgt), _p(lg), 304,
+                                    _p(part), s) == 0  # empty is a no-op
+    ctx.check()
+
+
+def test_lmhead_token_out_of_vocabulary(ctx):
+    from paper_2511_05589_b200 import ContractViolation
+    T, H, V = 8, 64, 300
+    x, w, tgt = _inputs(T, H, V, 2)
+    tgt[3] = V
+    lg, part = ctx.lmhead_logits(x, w, tgt)
+    ctx.lse_merge(part, lg, tgt)
+    with pytest.raises(ContractViolation, match="token out of vocabulary"):
+        ctx.check()
