@@ -324,3 +324,29 @@ def test_host_buffer_dropin(ctx, oracle):
                           pin(hb.stage[:3].view(np.int32)), pin(case.blp[:3]), hb.cur_stage,
                           rewards=pin(np.zeros(3)), group_off=bad, cfg=case.clip())
     ws.close()
+
+
+@pytest.mark.parametrize("V,force", [(151936, None), (151936, "stream+la0"), (151936, "stream+la5"),
+                                     (32000, None), (32000, "stream")])
+def test_forward_only_matches_forward_backward(ctx, oracle, impl, V, force):
+    """want_grad=False skips the dlogits pass (the producer drops pass 2 from the
+    ring): the forward outputs must be bitwise those of the full call."""
+    impl(force)
+    case = Case(oracle, seed=21, P=2, G=4, V=V, mu=math.log(10), lmax=24)
+    batch = case.upload(ctx)
+    full = ctx.grpo_step_loss(case.logits_gpu(), batch, case.clip(), coef=True)
+    fwd = ctx.grpo_step_loss(case.logits_gpu(), batch, case.clip(), coef=True, want_grad=False)
+    assert fwd.dlogits is None
+    assert fwd.loss == full.loss and fwd.clipped_tokens == full.clipped_tokens
+    assert torch.equal(fwd.cur_lp, full.cur_lp) and torch.equal(fwd.coef, full.coef)
+
+
+@pytest.mark.parametrize("half", [37, 74, 75, 148, 150])
+def test_stream_rows_around_the_grid(ctx, oracle, impl, half):
+    """Row counts around the persistent grid (148 SMs): 74 .. 300 rows, i.e. CTAs
+    with one row (no lookahead row) next to CTAs with two; all against the oracle."""
+    impl("stream")
+    case = Case(oracle, seed=half, P=1, G=2, V=151936, fixed_len=half)
+    _, res = run(ctx, case, F32)
+    assert ctx.last_launch()["kernel"] == "fused_stream_la_kernel"
+    case.check(res, F32, what=f"rows={case.hb.n_tok}")
