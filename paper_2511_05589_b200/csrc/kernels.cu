@@ -316,14 +316,6 @@ __device__ __forceinline__ void kill_col(uint64_t* x, int j) {
       x[i] = (j & 1) ? ptx::f2(ptx::f2lo(x[i]), -INFINITY) : ptx::f2(-INFINITY, ptx::f2hi(x[i]));
 }
 
-// Sets column j of a packed vector to v (rare path: the target column).
-__device__ __forceinline__ void set_col(uint64_t* g, int j, float v) {
-  const int k = j >> 1;
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-    if (i == k) g[i] = (j & 1) ? ptx::f2(ptx::f2lo(g[i]), v) : ptx::f2(v, ptx::f2hi(g[i]));
-}
-
 // Stores NP packed fp32 pairs (2*NP columns) as TOut at a 16-byte aligned address.
 template <typename TOut, int NP>
 __device__ __forceinline__ void store_pairs(TOut* p, const uint64_t* g, uint64_t pol) {
@@ -352,7 +344,6 @@ __global__ void __launch_bounds__(WARPS * 32, (WARPS == 8 && CL == 1) ? 3 : 1)
   using VI = Vec<TIn>;
   using PB = PassB<TIn>;
   constexpr int VN = VI::N;
-  constexpr int NP = VN / 2;  // fp32 pairs per 16-byte vector
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t bars[WARPS * kMaxPieces];
   __shared__ __align__(8) uint64_t xbar[2];          // cluster exchange, per row parity
@@ -825,7 +816,6 @@ __global__ void __launch_bounds__((CW + 1) * 32, CW <= 8 ? 2 : 1)
   using VI = Vec<TIn>;
   using PB = PassB<TIn>;
   constexpr int VN = VI::N;
-  constexpr int NP = VN / 2;
   constexpr int NC = CW * 32;                  // consumer threads
   constexpr int K = KV;                        // vectors per consumer thread per slot
   extern __shared__ __align__(128) uint8_t smem[];

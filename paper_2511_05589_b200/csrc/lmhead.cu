@@ -513,11 +513,7 @@ cudaError_t launch_lmhead_fwd(const void* hidden, int64_t ld_h, const void* weig
   CUtensorMap tx, tw;
   if (!make_map(&tx, hidden, n_rows, H, ld_h, kBM) || !make_map(&tw, weight, V, H, ld_w, kBN))
     return cudaErrorInvalidValue;
-  static bool attr = [] {
-    return cudaFuncSetAttribute(lmhead_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(kSmemBytes)) == cudaSuccess;
-  }();
-  if (!attr) return cudaErrorInvalidValue;
+
   LmParams p;
   p.n_rows = n_rows;
   p.H = H;
@@ -535,6 +531,9 @@ cudaError_t launch_lmhead_fwd(const void* hidden, int64_t ld_h, const void* weig
   }
   const char* impl = std::getenv("COPRIS_LMHEAD_IMPL");
   if (impl && std::strcmp(impl, "1sm") == 0) {
+    cudaError_t ea = cudaFuncSetAttribute(lmhead_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(kSmemBytes));
+    if (ea != cudaSuccess) return ea;
     const int grid = static_cast<int>(std::min<int64_t>(p.n_tiles, num_sms));
     lmhead_fwd_kernel<<<grid, kThreads, kSmemBytes, stream>>>(tx, tw, p);
     if (info) *info = LaunchInfo{num_sms, 1, grid, "lmhead_fwd_kernel"};
@@ -542,12 +541,11 @@ cudaError_t launch_lmhead_fwd(const void* hidden, int64_t ld_h, const void* weig
   }
   // the pair kernel stages half of the weight tile per CTA: 128-row boxes
   if (!make_map(&tw, weight, V, H, ld_w, 128)) return cudaErrorInvalidValue;
-  static bool pattr = [] {
-    return cudaFuncSetAttribute(lmhead_fwd_pair_kernel,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(kPSmemBytes)) == cudaSuccess;
-  }();
-  if (!pattr) return cudaErrorInvalidValue;
+  // per call: the attribute is per device, and one process may drive several
+  cudaError_t ea = cudaFuncSetAttribute(lmhead_fwd_pair_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(kPSmemBytes));
+  if (ea != cudaSuccess) return ea;
   const int64_t units = (n_rows + 255) / 256 * p.n_vt;
   const int grid = static_cast<int>(std::min<int64_t>(2 * units, num_sms & ~1));
   cudaLaunchConfig_t cfg = {};
