@@ -199,7 +199,7 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from paper_2511_05589_b200.workload import CONFIGS
+    from paper_2511_05589_b200.workload import CONFIGS, describe
     cfg = CONFIGS[args.config]
     V = cfg["vocab"]
     # warmup + steps: each step one bounded sample (all threads once)
@@ -214,9 +214,10 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1000.0 * tok_step / value, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1000.0 * tok_step / value, "higher_is_better": True,
+        "scaling": "strong" if cfg.get("strong") else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config} (BASELINE configs[1]) — bounded CPU sample",
+        "config": {"workload": f"{describe(args.config)} — bounded CPU sample",
                    "vocab": V, "tokens_per_step": tok_step},
         "cpu_baseline": {"value": value, "unit": UNIT, **det},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -236,7 +237,8 @@ def run_ours(args):
     from paper_2511_05589_b200.grpo import HostWorkspace
     from paper_2511_05589_b200.packing import upload
     from paper_2511_05589_b200.sharding import allreduce_scalars, lpt_shard, shard_arrays
-    from paper_2511_05589_b200.workload import CONFIGS, make_host_batch, make_logits, stale_logprobs
+    from paper_2511_05589_b200.workload import (CONFIGS, describe, make_host_batch, make_logits,
+                                                 stale_logprobs)
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus if args.gpus == 1 else 1)))
@@ -257,10 +259,12 @@ def run_ours(args):
 
     cfgd = dict(CONFIGS[args.config])
     V = cfgd["vocab"]
-    P_rank = cfgd.pop("P")
+    strong = cfgd.pop("strong", False)
+    P_cfg = cfgd.pop("P")
+    P_global = P_cfg if strong else P_cfg * world   # strong: one global batch, sharded
     G = cfgd.pop("G")
     cfgd.pop("vocab")
-    hb = make_host_batch(args.seed, P_rank * world, G, V, **cfgd)
+    hb = make_host_batch(args.seed, P_global, G, V, **cfgd)
     shards = lpt_shard(hb.group_tokens(), world)
     tok_off, group_off, pt, pj, _ = shard_arrays(hb.tok_off, hb.group_off, {"stage": hb.stage},
                                                  {"reward": hb.reward}, shards[rank])
@@ -352,11 +356,11 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic",
             "config": {
-                "workload": f"{args.config} (BASELINE.json configs[1]: 128 prompts x 8 responses, "
-                            f"max 8k tokens, vocab {V}, 2 rollout stages) per GPU",
-                "prompts": P_rank * world, "responses": G, "vocab": V, "tokens_global": T_global,
+                "workload": describe(args.config),
+                "prompts": P_global, "responses": G, "vocab": V, "tokens_global": T_global,
                 "tokens_rank0": T, "chunk_rows": chunk, "chunks_per_step": nchunks,
                 "parallelism": f"dp{world} (whole prompt groups, LPT by tokens)",
                 "path": "unfused K1->K2->K3" if args.unfused else "fused single pass",

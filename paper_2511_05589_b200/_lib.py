@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcopris_b200.so")
+LIB_PATH = os.environ.get("COPRIS_LIB_PATH") or os.path.join(HERE, "libcopris_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "copris_b200.h")
 
 COPRIS_OK, COPRIS_E_CONTRACT, COPRIS_E_CONFIG, COPRIS_E_CUDA, COPRIS_E_INVALID = range(5)

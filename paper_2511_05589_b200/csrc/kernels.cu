@@ -555,6 +555,42 @@ __global__ void __launch_bounds__(WARPS * 32, (WARPS == 8 && CL == 1) ? 3 : 1)
             row_grad<VN, ENT>(x, d, col0 + v * VN, b);
             store_vec<TOut, VN>(drow + static_cast<int64_t>(v) * VN, d, pol);
           }
+        } else if constexpr (sizeof(TOut) == 2 && VN == 8) {
+          // |coef| folded into the exponent, sign applied to the packed bf16
+          // pair (as in p2_segment): d_k = sign * 2^(z_k log2(e) - c2)
+          const bool tpiece = static_cast<uint32_t>(b.y - (col0 + v0 * VN)) < static_cast<uint32_t>((v1 - v0) * VN);
+          const float nc2 = -b.c2;
+          const float sdy = b.smask ? -b.dy : b.dy;
+          for (int32_t v = v0 + lane; v < v1; v += 64) {
+            const bool two = v + 32 < v1;
+            const uint4 ra = ptx::lds_v4(sbase + v * 16);
+            const uint4 rb = two ? ptx::lds_v4(sbase + (v + 32) * 16) : ra;
+            float xa[VN], xb[VN], ea[VN], eb[VN];
+            VI::unpack(ra, xa);
+            VI::unpack(rb, xb);
+#pragma unroll
+            for (int q = 0; q < VN; ++q) {
+              ea[q] = ptx::ex2(fmaf(xa[q], kLog2e, nc2));
+              eb[q] = ptx::ex2(fmaf(xb[q], kLog2e, nc2));
+            }
+            if (tpiece) {
+              const int ja = b.y - (col0 + v * VN), jb = ja - 32 * VN;
+#pragma unroll
+              for (int q = 0; q < VN; ++q) {
+                if (q == ja) ea[q] = sdy;
+                if (q == jb) eb[q] = sdy;
+              }
+            }
+            const uint32_t sm = b.smask;
+            const uint4 wa{ptx::pack_bf16x2(ea[0], ea[1]) ^ sm, ptx::pack_bf16x2(ea[2], ea[3]) ^ sm,
+                           ptx::pack_bf16x2(ea[4], ea[5]) ^ sm, ptx::pack_bf16x2(ea[6], ea[7]) ^ sm};
+            ptx::st_global_v4_hint(drow + static_cast<int64_t>(v) * VN, wa, pol);
+            if (two) {
+              const uint4 wb{ptx::pack_bf16x2(eb[0], eb[1]) ^ sm, ptx::pack_bf16x2(eb[2], eb[3]) ^ sm,
+                             ptx::pack_bf16x2(eb[4], eb[5]) ^ sm, ptx::pack_bf16x2(eb[6], eb[7]) ^ sm};
+              ptx::st_global_v4_hint(drow + static_cast<int64_t>(v + 32) * VN, wb, pol);
+            }
+          }
         } else {
           // two vectors per iteration: both shared-memory loads issue first
           const bool tpiece = static_cast<uint32_t>(b.y - (col0 + v0 * VN)) < static_cast<uint32_t>((v1 - v0) * VN);
@@ -1296,7 +1332,7 @@ __device__ __forceinline__ void p2_segment(const RowBroadcast& b, bool zero_row,
 
 template <typename TIn, typename TOut, int CW, int KV, bool ENT>
 __global__ void __launch_bounds__((CW + 2) * 32, CW <= 8 ? 2 : 1)
-    fused_stream_la_kernel(const LossParams P, const int nslots, const int look) {
+    fused_stream_la_kernel(const LossParams P, const int nslots, const int look, const int resident) {
   constexpr int kSlotVec = CW * 32 * KV;
   using VI = Vec<TIn>;
   constexpr int VN = VI::N;
@@ -1349,6 +1385,11 @@ __global__ void __launch_bounds__((CW + 2) * 32, CW <= 8 ? 2 : 1)
       };
       auto rowp = [&](int64_t r) { return static_cast<const TIn*>(P.logits) + r * P.ld; };
       int64_t r = blockIdx.x;
+      if (resident) {
+        // rows stay in the ring between their two passes: one load per row
+        for (; r < P.n_rows; r += G) issue(rowp(r), 0, nseg, drop);
+        return;
+      }
       if (r < P.n_rows) issue(rowp(r), 0, nseg, keep);
       for (; r < P.n_rows; r += G) {
         const bool nx = r + G < P.n_rows;
@@ -1386,7 +1427,10 @@ __global__ void __launch_bounds__((CW + 2) * 32, CW <= 8 ? 2 : 1)
   // ---------------- consumers ----------------
   const int tid = threadIdx.x;
   const uint64_t pol = ptx::policy_evict_first();
-  Ring ring(nslots);
+  // Resident mode (3 rows fit in the ring): pass 2 reads the row from the
+  // segments pass 1 consumed, which stay allocated until pass 2 releases them;
+  // `ring2` walks the same slot sequence one row behind `ring`.
+  Ring ring(nslots), ring2(nslots);
   PhaseTimer tm;
   tm.start(P.trace && tid == 0 && blockIdx.x < kTraceCtas);
 
@@ -1400,7 +1444,7 @@ __global__ void __launch_bounds__((CW + 2) * 32, CW <= 8 ? 2 : 1)
       p1_segment<TIn, NC, K, kSlotVec, ENT>(a, sbase + slot * (kSlotVec * 16), v0,
                                             min(kSlotVec, nvec - v0), y, tid);
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive_u32(ebase + slot * 8);
+      if (lane == 0 && !resident) ptx::mbar_arrive_u32(ebase + slot * 8);
     }
   };
   // hand row i's pass-1 partials to the scalar warp
@@ -1431,11 +1475,33 @@ __global__ void __launch_bounds__((CW + 2) * 32, CW <= 8 ? 2 : 1)
     const bool nx = rn < P.n_rows;
     P1Acc an;
     const int32_t yn = nx ? P.target[P.row_base + rn] : 0;
-    if (nx) run_p1(an, yn, 0, L);
+    if (nx) run_p1(an, yn, 0, resident ? nseg : L);
+    // resident: hand row i+1 over at once (its red/zy_sh buffer was freed by
+    // row i-1's broadcast), so its scalar phase overlaps pass 2 of row i
+    if (resident && nx) finish_p1(an, i + 1);
     tm.mark(0);
     const uint32_t bsel = i & 1u, par = (i >> 1) & 1u;
     ptx::mbar_wait_u32(sdb + bsel * 8, par);  // row i's broadcast (also frees red/zy_sh[bsel])
     tm.mark(2);
+    if (resident) {
+      // pass 2 of row i from its resident segments, then release them
+      const RowBroadcast b = bc[bsel];
+      const bool zero_row = (b.coef == 0.f) && (!ENT || b.eg == 0.f);
+      TOut* drow = P.dlogits ? static_cast<TOut*>(P.dlogits) + r * P.ld_d : nullptr;
+      for (int32_t sg = 0; sg < nseg; ++sg, ring2.next()) {
+        const uint32_t slot = ring2.slot;
+        const int32_t v0 = sg * kSlotVec;
+        if (drow)
+          p2_segment<TIn, TOut, NC, K, kSlotVec, ENT>(b, zero_row, sbase + slot * (kSlotVec * 16), v0,
+                                                      min(kSlotVec, nvec - v0),
+                                                      drow + static_cast<int64_t>(v0) * VN, tid, pol);
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_u32(ebase + slot * 8);
+      }
+      tm.mark(4);
+      tm.acc[5] += 1;
+      continue;
+    }
     if (P.dlogits) {
       const RowBroadcast b = bc[bsel];
       const bool zero_row = (b.coef == 0.f) && (!ENT || b.eg == 0.f);
@@ -1963,7 +2029,13 @@ cudaError_t launch_stream(const LossParams& p, int num_sms, cudaStream_t stream,
       info->grid = grid;
       info->kernel = "fused_stream_la_kernel";
     }
-    kernel<<<grid, (CW + 2) * 32, smem, stream>>>(p, nslots, look);
+    // resident rows: three whole rows fit in the ring (pass 2 reuses pass 1's
+    // segments instead of re-reading the row from L2)
+    const int64_t nseg = (p.vocab / Vec<TIn>::N + CW * 32 * KV - 1) / (CW * 32 * KV);
+    const int resident = tune_env("COPRIS_TUNE_RESIDENT", 1) && p.dlogits != nullptr &&
+                         3 * nseg <= nslots;
+    if (info) info->kernel = resident ? "fused_stream_la_kernel[resident]" : "fused_stream_la_kernel";
+    kernel<<<grid, (CW + 2) * 32, smem, stream>>>(p, nslots, look, resident);
     return cudaGetLastError();
   }
   auto kernel = fused_stream_kernel<TIn, TOut, CW, KV, ENT>;

@@ -56,13 +56,36 @@ CONFIGS = {
     "grpo_128x8_v151936_longtail_4stage": dict(P=128, G=8, mu=math.log(2048), sigma=1.5,
                                                lmax=8192, vocab=151936, stages=(3, 4),
                                                stale_prob=1.0),
-    # configs[3]: 512 x 16, max 16k (sharded over 2/4/8 GPUs)
+    # configs[3]: 512 x 16, max 16k, ONE global batch sharded over 1/2/4/8 GPUs
+    # (strong scaling: P is the global prompt count, not per rank)
     "grpo_512x16_v151936": dict(P=512, G=16, mu=math.log(4096), sigma=1.0, lmax=16384,
-                                vocab=151936, stages=(1, 2), stale_prob=0.5),
-    # configs[4]: vocab 32,000 fixed-length sweep
-    "grpo_128x8_v32000_L1024": dict(P=128, G=8, fixed_len=1024, vocab=32000, stages=(1, 2),
-                                    stale_prob=0.5),
+                                vocab=151936, stages=(1, 2), stale_prob=0.5, strong=True),
 }
+# configs[4]: vocab 32,000 short-response sweep (fixed lengths 256 .. 4k) at
+# 128 x 8 per GPU, plus a one-group variant (8 trajectories) that exposes the
+# per-step launch and reduction overhead
+for _L in (256, 512, 1024, 2048, 4096):
+    CONFIGS[f"grpo_128x8_v32000_L{_L}"] = dict(P=128, G=8, fixed_len=_L, vocab=32000,
+                                                stages=(1, 2), stale_prob=0.5)
+    CONFIGS[f"grpo_1x8_v32000_L{_L}"] = dict(P=1, G=8, fixed_len=_L, vocab=32000,
+                                              stages=(1, 2), stale_prob=0.5)
+
+BASELINE_INDEX = {"grpo_128x8_v151936": 1, "grpo_128x8_v151936_longtail_4stage": 2,
+                  "grpo_512x16_v151936": 3}
+
+
+def describe(name: str) -> str:
+    """One-line workload description for bench output (BASELINE.json configs[i])."""
+    c = CONFIGS[name]
+    idx = BASELINE_INDEX.get(name, 4)
+    if "fixed_len" in c:
+        shape = f"{c['P']} prompts x {c['G']} responses, fixed length {c['fixed_len']}"
+    else:
+        shape = f"{c['P']} prompts x {c['G']} responses, lognormal lengths max {c['lmax']}"
+    k0, k1 = c["stages"]
+    stages = f"{k0}-{k1} rollout stages" if k0 != k1 else f"{k0} rollout stages"
+    per = "global batch sharded by prompt group" if c.get("strong") else "per GPU"
+    return f"{name} (BASELINE.json configs[{idx}]: {shape}, vocab {c['vocab']}, {stages}) {per}"
 
 
 def make_host_batch(seed: int, P: int, G: int, vocab: int, mu: float = 0.0, sigma: float = 0.0,

@@ -29,8 +29,11 @@ SHAPES = [
     (151936, BF16, "tma", "fused_tma_kernel", 2),     # row split over a CTA pair (DSMEM)
     (151936, BF16, "l2", "fused_l2_kernel", 1),       # register-streamed two-pass variant
     (32000, BF16, None, "fused_tma_kernel", 1),       # 64 KB rows resident, several CTAs/SM
-    (32000, BF16, "stream", "fused_stream_la_kernel", 1),  # 2 segments/row: lookahead = whole row
-    (32000, BF16, "stream+la1", "fused_stream_la_kernel", 1),
+    (32000, BF16, "stream", "fused_stream_la_kernel[resident]", 1),  # 3 rows fit the ring: no L2 re-read
+    (32000, BF16, "stream+res0", "fused_stream_la_kernel", 1),  # 2 segments/row: lookahead = whole row
+    (32000, BF16, "stream+la1+res0", "fused_stream_la_kernel", 1),
+    (20000, BF16, "stream", "fused_stream_la_kernel[resident]", 1),  # partial last segment
+
     (32000, BF16, "stream+la0", "fused_stream_kernel", 1),
     (80000, BF16, "tma", "fused_tma_kernel", 1),      # 160 KB rows: one 16-warp CTA per row
     (151936, F32, None, "fused_stream_la_kernel", 1),
@@ -50,9 +53,14 @@ def impl(monkeypatch):
         """name = implementation[+laN]: COPRIS_FUSED_IMPL and the stream
         kernel's lookahead (COPRIS_TUNE_LOOKAHEAD, 0 = the kernel without it)."""
         monkeypatch.delenv("COPRIS_TUNE_LOOKAHEAD", raising=False)
-        if name and "+la" in name:
-            name, la = name.split("+la")
-            monkeypatch.setenv("COPRIS_TUNE_LOOKAHEAD", la)
+        monkeypatch.delenv("COPRIS_TUNE_RESIDENT", raising=False)
+        if name and "+" in name:
+            name, *opts = name.split("+")
+            for o in opts:
+                if o.startswith("la"):
+                    monkeypatch.setenv("COPRIS_TUNE_LOOKAHEAD", o[2:])
+                elif o.startswith("res"):
+                    monkeypatch.setenv("COPRIS_TUNE_RESIDENT", o[3:])
         if name:
             monkeypatch.setenv("COPRIS_FUSED_IMPL", name)
         else:
