@@ -53,6 +53,9 @@ def parse_args():
     ap.add_argument("--cpu-tokens-per-thread", type=int, default=256)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--graph", action="store_true",
+                    help="capture one step (all chunk launches + the reduction) in a CUDA graph "
+                         "and replay it; the allreduce stays outside the graph")
     return ap.parse_args()
 
 
@@ -293,7 +296,7 @@ def run_ours(args):
     out4 = torch.zeros(4, dtype=torch.float64, device=dev)
     run_chunk = ctx.loss_chunk_unfused if args.unfused else ctx.loss_chunk_fused
 
-    def step(evs=None):
+    def launches(evs=None):
         for c in range(nchunks):
             r0 = c * chunk
             n = min(chunk, T - r0)
@@ -304,12 +307,34 @@ def run_ours(args):
             if evs is not None:
                 evs[c][1].record()
         ctx.reduce(outs, T, out4)
+
+    graph = None
+
+    def step(evs=None):
+        if graph is not None:
+            graph.replay()
+        else:
+            launches(evs)
         allreduce_scalars(out4)
 
     for _ in range(max(args.warmup, 1)):
         step()
     ctx.check()
     info = ctx.last_launch()
+    if args.graph:
+        # CUDA graph of one step: the per-launch host cost (Python + C-ABI)
+        # leaves the loop; replays are bitwise identical to eager steps
+        graph = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            launches()
+        torch.cuda.current_stream().wait_stream(side)
+        with torch.cuda.graph(graph):
+            launches()
+        for _ in range(max(args.warmup, 1)):
+            step()
+        ctx.check()
 
     evs = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)]
             for _ in range(nchunks)] for _ in range(args.steps)]
@@ -341,9 +366,13 @@ def run_ours(args):
     ms_max = t.item()
     loss = -out4[0].item() * (1.0 / T_global)
 
-    # kernel-level roofline (dominant kernel: the fused pass)
-    kern_ms = sum(evs[k][c][0].elapsed_time(evs[k][c][1]) for k in range(args.steps)
-                  for c in range(nchunks))
+    # kernel-level roofline (dominant kernel: the fused pass); under --graph
+    # the per-chunk events are not recorded and the whole step is charged
+    if graph is None:
+        kern_ms = sum(evs[k][c][0].elapsed_time(evs[k][c][1]) for k in range(args.steps)
+                      for c in range(nchunks))
+    else:
+        kern_ms = ms * args.steps
     rows_timed = args.steps * T
     bytes_per_tok = 4 * V + 16
     achieved = rows_timed * bytes_per_tok / (kern_ms / 1e3) / 1e9
@@ -363,7 +392,8 @@ def run_ours(args):
                 "prompts": P_global, "responses": G, "vocab": V, "tokens_global": T_global,
                 "tokens_rank0": T, "chunk_rows": chunk, "chunks_per_step": nchunks,
                 "parallelism": f"dp{world} (whole prompt groups, LPT by tokens)",
-                "path": "unfused K1->K2->K3" if args.unfused else "fused single pass",
+                "path": ("unfused K1->K2->K3" if args.unfused else "fused single pass")
+                        + (" (CUDA graph replay)" if graph is not None else ""),
                 "kernel": info, "l2": "inputs larger than L2 (logits chunk "
                 f"{chunk * V * 2 / 1e9:.1f} GB >> 126 MB)", "loss": loss,
                 "offpolicy_fraction": out4[2].item() / out4[1].item() if out4[1].item() else 0.0,

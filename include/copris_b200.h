@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define COPRIS_B200_ABI_VERSION 1
+#define COPRIS_B200_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define COPRIS_API __attribute__((visibility("default")))
@@ -62,7 +62,7 @@ enum copris_dtype { COPRIS_BF16 = 0, COPRIS_F32 = 1 };
 enum copris_behav_mode { COPRIS_BEHAV_RECOMPUTED = 0, COPRIS_BEHAV_RECORDED = 1 };
 
 /* bits of the per-token flags byte */
-enum { COPRIS_FLAG_STALE = 1, COPRIS_FLAG_CLIPPED = 2 };
+enum { COPRIS_FLAG_STALE = 1, COPRIS_FLAG_CLIPPED = 2, COPRIS_FLAG_MASKED = 4 };
 
 typedef struct copris_ctx copris_ctx;
 
@@ -174,6 +174,12 @@ typedef struct {
   const double* adv;         /* [n_traj] */
   uint32_t cur_stage;        /* rollout_version of the batch */
   uint32_t _pad;
+  /* [T] optional token mask (NULL: every token counts). A token with mask 0 is
+   * left out of the loss as if it were not in the batch: obj 0, dlogits row 0,
+   * no error checks, flags = COPRIS_FLAG_MASKED only, not counted by
+   * copris_loss_reduce; cur_lp/lse are still written. total_tokens is then the
+   * global count of UNMASKED tokens (the masked token mean). */
+  const uint8_t* loss_mask;
 } copris_loss_batch;
 
 typedef struct {
@@ -210,8 +216,9 @@ COPRIS_API int copris_is_loss_bwd(copris_ctx* ctx, const copris_loss_batch* batc
                        const float* behav, const copris_loss_out* out, void* stream);
 
 /* Deterministic fixed-order reduction of the per-token outputs:
- * out4[0] = sum obj (fp64), out4[1] = tokens, out4[2] = stale tokens
- * (rollout.hpp:99-110), out4[3] = clipped tokens. out4 is a DEVICE f64[4]. */
+ * out4[0] = sum obj (fp64), out4[1] = tokens (without COPRIS_FLAG_MASKED ones),
+ * out4[2] = stale tokens (rollout.hpp:99-110), out4[3] = clipped tokens.
+ * out4 is a DEVICE f64[4]. */
 COPRIS_API int copris_loss_reduce(copris_ctx* ctx, const double* obj, const uint8_t* flags, int64_t n_tok,
                        double* out4, void* stream);
 

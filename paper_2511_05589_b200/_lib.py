@@ -16,7 +16,7 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "copris_b200.h")
 COPRIS_OK, COPRIS_E_CONTRACT, COPRIS_E_CONFIG, COPRIS_E_CUDA, COPRIS_E_INVALID = range(5)
 COPRIS_BF16, COPRIS_F32 = 0, 1
 COPRIS_BEHAV_RECOMPUTED, COPRIS_BEHAV_RECORDED = 0, 1
-COPRIS_FLAG_STALE, COPRIS_FLAG_CLIPPED = 1, 2
+COPRIS_FLAG_STALE, COPRIS_FLAG_CLIPPED, COPRIS_FLAG_MASKED = 1, 2, 4
 
 P = C.c_void_p
 I32 = C.c_int32
@@ -29,7 +29,7 @@ class LossBatch(C.Structure):
     _fields_ = [("logits", P), ("ld", I64), ("logits_dtype", I32), ("vocab", I32),
                 ("n_rows", I64), ("row_base", I64), ("target", P), ("stage", P),
                 ("buffered_lp", P), ("ref_lp", P), ("tok_traj", P), ("adv", P),
-                ("cur_stage", U32), ("_pad", U32)]
+                ("cur_stage", U32), ("_pad", U32), ("loss_mask", P)]
 
 
 class LossCfg(C.Structure):

@@ -60,7 +60,8 @@ int validate_loss(const copris_ctx* ctx, const copris_loss_batch* b, const copri
   if (c->behav_mode != COPRIS_BEHAV_RECOMPUTED && c->behav_mode != COPRIS_BEHAV_RECORDED)
     return fail(COPRIS_E_INVALID, "behav_mode must be COPRIS_BEHAV_RECOMPUTED or _RECORDED");
   if (b->n_rows < 0 || b->row_base < 0) return fail(COPRIS_E_INVALID, "negative row range");
-  if (b->row_base + b->n_rows > c->total_tokens)
+  // with a mask total_tokens counts the unmasked tokens only
+  if (!b->loss_mask && b->row_base + b->n_rows > c->total_tokens)
     return fail(COPRIS_E_CONTRACT, "log-prob vectors must align with token count");
   if (b->n_rows == 0) return COPRIS_OK;
   if (b->vocab < 1) return fail(COPRIS_E_CONFIG, "policy.vocab must leave room for answer tokens plus EOS");
@@ -91,6 +92,7 @@ LossParams make_params(const copris_ctx* ctx, const copris_loss_batch* b, const 
   p.ref_lp = c->kl_coeff > 0.0 ? b->ref_lp : nullptr;
   p.tok_traj = b->tok_traj;
   p.adv = b->adv;
+  p.loss_mask = b->loss_mask;
   p.clamp_lo = 1.0 - c->clip_low;   // grpo.hpp:149 bounds, same fp64 ops
   p.clamp_hi = 1.0 + c->clip_high;
   p.kl_coeff = c->kl_coeff;

@@ -204,6 +204,7 @@ struct RowMeta {
   uint32_t st;
   float blp, rl;
   double adv;
+  bool keep;  // loss_mask[t] != 0 (true without a mask)
 };
 
 __device__ __forceinline__ RowMeta load_meta(const LossParams& P, int64_t t) {
@@ -213,6 +214,7 @@ __device__ __forceinline__ RowMeta load_meta(const LossParams& P, int64_t t) {
   m.blp = P.buffered_lp[t];
   m.rl = P.ref_lp ? P.ref_lp[t] : 0.f;
   m.adv = P.adv[P.tok_traj[t]];
+  m.keep = P.loss_mask ? P.loss_mask[t] != 0 : true;
   return m;
 }
 
@@ -238,6 +240,7 @@ struct MetaPipe {
       next.blp = P.buffered_lp[t1];
       next.rl = P.ref_lp ? P.ref_lp[t1] : 0.f;
       next.adv = P.adv[traj_ahead];
+      next.keep = P.loss_mask ? P.loss_mask[t1] != 0 : true;
       if (r1 + stride < P.n_rows) traj_ahead = P.tok_traj[t1 + stride];
     }
     return cur;
@@ -527,7 +530,7 @@ __global__ void __launch_bounds__(WARPS * 32, (WARPS == 8 && CL == 1) ? 3 : 1)
           zy = owner < static_cast<uint32_t>(CL) ? slot[par][owner][2] : 0.f;
         }
         bc = row_scalar_phase<ENT>(P, t, meta.y, meta.st, meta.blp, meta.rl, meta.adv, tot, zy,
-                                   rank == 0);
+                                   rank == 0, meta.keep);
       }
     }
     tm.mark(2);
@@ -729,7 +732,7 @@ __global__ void __launch_bounds__(WARPS * 32)
       if (lane == 0) {
         const float zy = static_cast<uint32_t>(meta.y) < static_cast<uint32_t>(V)
                              ? VI::load1(static_cast<const TIn*>(P.logits) + r * P.ld + meta.y) : 0.f;
-        bc = row_scalar_phase<ENT>(P, t, meta.y, meta.st, meta.blp, meta.rl, meta.adv, tot, zy, true);
+        bc = row_scalar_phase<ENT>(P, t, meta.y, meta.st, meta.blp, meta.rl, meta.adv, tot, zy, true, meta.keep);
       }
     }
     __syncthreads();
@@ -1045,7 +1048,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, CW <= 8 ? 2 : 1)
       warp_lse<ENT>(tot);
       if (lane == 0) {
         const float zy = static_cast<uint32_t>(meta.y) < static_cast<uint32_t>(V) ? zy_sh : 0.f;
-        bc = row_scalar_phase<ENT>(P, t, meta.y, meta.st, meta.blp, meta.rl, meta.adv, tot, zy, true);
+        bc = row_scalar_phase<ENT>(P, t, meta.y, meta.st, meta.blp, meta.rl, meta.adv, tot, zy, true, meta.keep);
       }
     }
     tm.mark(2);
@@ -1416,7 +1419,7 @@ __global__ void __launch_bounds__((CW + 2) * 32, CW <= 8 ? 2 : 1)
       if (lane == 0) {
         const float zy = static_cast<uint32_t>(meta.y) < static_cast<uint32_t>(V) ? zy_sh[bsel] : 0.f;
         bc[bsel] = row_scalar_phase<ENT>(P, P.row_base + r, meta.y, meta.st, meta.blp, meta.rl,
-                                         meta.adv, tot, zy, true);
+                                         meta.adv, tot, zy, true, meta.keep);
         ptx::mbar_arrive_u32(sdb + bsel * 8);
       }
       __syncwarp();
@@ -1559,7 +1562,7 @@ __global__ void __launch_bounds__(256) fused_generic_kernel(const LossParams P) 
       for (int w = 0; w < nw; ++w) lse_merge<ENT>(tot, red[w]);
       const float zy = static_cast<uint32_t>(meta.y) < static_cast<uint32_t>(V)
                            ? Vec<TIn>::load1(row + meta.y) : 0.f;
-      bc = row_scalar_phase<ENT>(P, t, meta.y, meta.st, meta.blp, meta.rl, meta.adv, tot, zy, true);
+      bc = row_scalar_phase<ENT>(P, t, meta.y, meta.st, meta.blp, meta.rl, meta.adv, tot, zy, true, meta.keep);
     }
     __syncthreads();
     const RowBroadcast b = bc;
@@ -1685,7 +1688,9 @@ __global__ void __launch_bounds__(256) bwd_kernel(const LossParams P) {
         ln_s = lp.ln_s;
         H = ln_s - tot.u / tot.a;
       }
-      TokenResult tr = static_cast<uint32_t>(y) < static_cast<uint32_t>(V)
+      const bool keep = P.loss_mask ? P.loss_mask[t] != 0 : true;
+      TokenResult tr = !keep ? TokenResult{0.0, 0.0, FLAG_MASKED, 0u}
+                       : static_cast<uint32_t>(y) < static_cast<uint32_t>(V)
                            ? token_objective(P, cur, beh, adv, rl, stale, H, ENT)
                            : TokenResult{0.0, 0.0, static_cast<uint8_t>(stale ? FLAG_STALE : 0),
                                          ERR_TOKEN_OOV};
@@ -1863,15 +1868,17 @@ __global__ void __launch_bounds__(kReduceThreads)
   const int64_t nb = gridDim.x;
   const int64_t b0 = n * blockIdx.x / nb, b1 = n * (blockIdx.x + 1) / nb;
   double o = 0.0;
-  unsigned long long st = 0, cl = 0;
+  unsigned long long st = 0, cl = 0, mk = 0;
   for (int64_t t = b0 + threadIdx.x; t < b1; t += blockDim.x) {
     o += obj[t];
     const uint8_t f = flags[t];
     st += f & FLAG_STALE;
     cl += (f >> 1) & 1u;
+    mk += (f >> 2) & 1u;
   }
+  // stale/clipped counts < 2^32 per block: pack them with the masked count
   so[threadIdx.x] = o;
-  ss[threadIdx.x] = st;
+  ss[threadIdx.x] = st | (mk << 32);
   sk[threadIdx.x] = cl;
   __syncthreads();
   for (int h = blockDim.x / 2; h > 0; h >>= 1) {
@@ -1893,14 +1900,16 @@ __global__ void __launch_bounds__(kReduceThreads)
   if (last && threadIdx.x == 0) {
     __threadfence();
     double O = 0.0;
-    unsigned long long Sx = 0, Cx = 0;
+    unsigned long long Sx = 0, Cx = 0, Mx = 0;
     for (int i = 0; i < gridDim.x; ++i) {
       O += *reinterpret_cast<volatile double*>(&sc->obj[i]);
-      Sx += *reinterpret_cast<volatile unsigned long long*>(&sc->stale[i]);
+      const unsigned long long sm = *reinterpret_cast<volatile unsigned long long*>(&sc->stale[i]);
+      Sx += sm & 0xFFFFFFFFull;
+      Mx += sm >> 32;
       Cx += *reinterpret_cast<volatile unsigned long long*>(&sc->clipped[i]);
     }
     out4[0] = O;
-    out4[1] = static_cast<double>(n);
+    out4[1] = static_cast<double>(n - static_cast<int64_t>(Mx));
     out4[2] = static_cast<double>(Sx);
     out4[3] = static_cast<double>(Cx);
     sc->ticket = 0;

@@ -33,6 +33,7 @@ struct LossParams {
   const float* ref_lp;
   const int32_t* tok_traj;
   const double* adv;
+  const uint8_t* loss_mask;  // optional: 0 = token left out of the loss
   // unfused-K3 inputs (nullptr in the fused kernel)
   const float* in_cur_lp;
   const float* in_lse;

@@ -15,7 +15,7 @@ namespace copris_b200 {
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr double kLog2eD = 1.4426950408889634;
 
-enum : uint8_t { FLAG_STALE = 1, FLAG_CLIPPED = 2 };
+enum : uint8_t { FLAG_STALE = 1, FLAG_CLIPPED = 2, FLAG_MASKED = 4 };
 
 // trajectory.hpp:69-75 (concat_segments) + trainer.hpp:149 (IS off) for one
 // token. A select, never arithmetic: bit-exact by construction.
@@ -128,7 +128,7 @@ template <bool ENT, typename LseT>
 __device__ __forceinline__ RowBroadcast row_scalar_phase(const LossParams& P, int64_t t, int32_t y,
                                                          uint32_t st, float blp, float rl,
                                                          double adv, const LseT& tot, float zy,
-                                                         bool write) {
+                                                         bool write, bool keep = true) {
   const bool oov = static_cast<uint32_t>(y) >= static_cast<uint32_t>(P.vocab);
   const float M = tot.m;
   const LogProb lp = finish_logprob(M, tot.s, zy, !oov);
@@ -141,7 +141,9 @@ __device__ __forceinline__ RowBroadcast row_scalar_phase(const LossParams& P, in
   float H = 0.f;
   if (ENT) H = ln_s - tot.u / tot.a;
   TokenResult tr;
-  if (oov) {
+  if (!keep) {  // masked token: out of the loss as if absent from the batch
+    tr = TokenResult{0.0, 0.0, FLAG_MASKED, 0u};
+  } else if (oov) {
     tr = TokenResult{0.0, 0.0, static_cast<uint8_t>(stale ? FLAG_STALE : 0), ERR_TOKEN_OOV};
   } else {
     tr = token_objective(P, cur, beh, adv, rl, stale, H, ENT);

@@ -84,6 +84,11 @@ class PackedBatch:
     cur_stage: int
     ref_lp: Optional[torch.Tensor] = None  # [T] f32, for kl_coeff > 0
     group_off_host: Optional[list] = None
+    loss_mask: Optional[torch.Tensor] = None  # [T] uint8, 0 = token left out of the loss
+
+    def loss_tokens(self) -> int:
+        """Tokens the loss averages over (the masked token mean)."""
+        return self.n_tok if self.loss_mask is None else int(self.loss_mask.count_nonzero())
 
     @property
     def n_tok(self) -> int:
@@ -260,7 +265,8 @@ class Copris:
         n_rows, v = logits.shape
         b = L.LossBatch(_p(logits), logits.stride(0), _dtype_code(logits.dtype), v, n_rows,
                         row_base, _p(batch.target), _p(batch.stage), _p(batch.buffered_lp),
-                        _p(batch.ref_lp), _p(batch.tok_traj), _p(batch.adv), batch.cur_stage, 0)
+                        _p(batch.ref_lp), _p(batch.tok_traj), _p(batch.adv), batch.cur_stage, 0,
+                        _p(batch.loss_mask))
         c = L.LossCfg(cfg.clip_low, cfg.clip_high, cfg.kl_coeff, cfg.entropy_coeff,
                       int(is_enabled), behav_mode, total_tokens)
         o = L.LossOut(_p(dlogits), dlogits.stride(0) if dlogits is not None else 0,
@@ -284,7 +290,7 @@ class Copris:
                          total_tokens=None, is_enabled=True,
                          behav_mode=L.COPRIS_BEHAV_RECOMPUTED, stream=None):
         """Launch the fused kernel on one chunk of rows (no sync)."""
-        T = total_tokens if total_tokens is not None else batch.n_tok
+        T = total_tokens if total_tokens is not None else batch.loss_tokens()
         b, c, o = self._structs(logits, batch, cfg, is_enabled, behav_mode, T, row_base, dlogits,
                                 outs)
         self._call(self.lib.copris_is_loss_fused(self.h, C.byref(b), C.byref(c), C.byref(o),
@@ -294,7 +300,7 @@ class Copris:
                            total_tokens=None, is_enabled=True,
                            behav_mode=L.COPRIS_BEHAV_RECOMPUTED, stream=None):
         """K1 -> K2 -> K3 on one chunk of rows (no sync)."""
-        T = total_tokens if total_tokens is not None else batch.n_tok
+        T = total_tokens if total_tokens is not None else batch.loss_tokens()
         n = logits.shape[0]
         sl = slice(row_base, row_base + n)
         cur, lse = outs["cur_lp"][sl], outs["lse"][sl]
@@ -325,7 +331,9 @@ class Copris:
         """grpo.hpp:117-185 over a resident [T x V] logits tensor.
 
         loss = -(1/T) sum_t obj_t; dlogits rows = d loss / d logits. ``total_tokens``
-        overrides T (the GLOBAL token count when the batch is a shard).
+        overrides T (the GLOBAL token count when the batch is a shard). With
+        ``batch.loss_mask`` T counts the unmasked tokens and masked tokens are
+        left out as if absent (obj 0, zero dlogits row, not counted).
         """
         cfg = cfg or ClipConfig()
         cfg.validate()
@@ -335,7 +343,9 @@ class Copris:
             raise ConfigError("grpo_step_loss batch has no tokens")
         if logits.shape[0] != batch.n_tok:
             raise ContractViolation("log-prob vectors must align with token count")
-        T = total_tokens if total_tokens is not None else batch.n_tok
+        T = total_tokens if total_tokens is not None else batch.loss_tokens()
+        if T == 0:
+            raise ConfigError("grpo_step_loss batch has no tokens")
         if want_grad and dlogits is None:
             dlogits = torch.empty(logits.shape, dtype=dlogits_dtype or logits.dtype,
                                   device=logits.device)

@@ -8,8 +8,10 @@ mkdir -p $OUT
 : > $OUT/sweep_v32000.jsonl
 for L in 256 512 1024 2048 4096; do
   for P in 128 1; do
-    steps=10; [ $P = 1 ] && steps=200
+    steps=10; extra=""
+    # one group: launch-bound, so the step is replayed as a CUDA graph
+    [ $P = 1 ] && { steps=300; extra="--graph"; }
     timeout 300 python bench.py --config grpo_${P}x8_v32000_L$L --steps $steps --no-e2e \
-      --no-cpu-baseline "$@" 2>>$OUT/sweep_v32000.err | tail -1 >> $OUT/sweep_v32000.jsonl
+      --no-cpu-baseline $extra "$@" 2>>$OUT/sweep_v32000.err | tail -1 >> $OUT/sweep_v32000.jsonl
   done
 done

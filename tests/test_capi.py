@@ -20,7 +20,7 @@ def test_library_loads_and_exports_every_declared_symbol():
     for name in declared:
         assert hasattr(lib, name), f"{name} declared in include/copris_b200.h but not exported"
     assert set(declared) == set(L._SIGS), "ctypes signatures out of sync with the header"
-    assert lib.copris_abi_version() == 1
+    assert lib.copris_abi_version() == 2
 
 
 def test_exports_nothing_else():

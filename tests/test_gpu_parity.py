@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 import torch
 
-from parity_util import Case, assert_rows_close, assert_scalar_close, exact_dlogits
+from parity_util import Case, assert_loss_close, assert_rows_close, assert_scalar_close, exact_dlogits
 
 pytestmark = pytest.mark.gpu
 
@@ -358,3 +358,92 @@ def test_stream_rows_around_the_grid(ctx, oracle, impl, half):
     _, res = run(ctx, case, F32)
     assert ctx.last_launch()["kernel"] == "fused_stream_la_kernel"
     case.check(res, F32, what=f"rows={case.hb.n_tok}")
+
+
+@pytest.mark.parametrize("V,force", [(151936, None), (151936, "tma"), (32000, None),
+                                     (32000, "stream"), (4099, None)])
+@pytest.mark.parametrize("fused", [True, False])
+def test_loss_mask_equals_deletion(ctx, oracle, impl, V, force, fused):
+    """copris_loss_batch.loss_mask: a masked token is left out of the loss as
+    if it were not in the batch. Checked against the oracle run on the batch
+    with the masked tokens deleted (advantages come from the rewards, so they
+    do not change), with one trajectory masked entirely."""
+    impl(force)
+    case = Case(oracle, seed=13, P=2, G=4, V=V, mu=math.log(10), lmax=24)
+    hb = case.hb
+    rng = np.random.default_rng(5)
+    keep = rng.random(hb.n_tok) > 0.3
+    keep[hb.tok_off[1]:hb.tok_off[2]] = False
+    csum = np.concatenate([[0], np.cumsum(keep)])
+    tok_off2 = csum[hb.tok_off].astype(np.int64)
+    T2 = int(keep.sum())
+    ref = oracle.is_loss(case.z64[keep], tok_off2, hb.target[keep], hb.stage[keep], hb.cur_stage,
+                         case.blp[keep].astype(np.float64), case.adv, **case.cfg)
+    batch = case.upload(ctx)
+    batch.loss_mask = torch.from_numpy(keep.astype(np.uint8)).cuda()
+    res = ctx.grpo_step_loss(case.logits_gpu(), batch, case.clip(), fused=fused,
+                             dlogits_dtype=torch.float32)
+    assert res.token_count == T2
+    assert res.stale_tokens == ref.stale_tokens and res.clipped_tokens == ref.clipped_tokens
+    flags = res.flags.cpu().numpy()
+    np.testing.assert_array_equal(flags[~keep], 4)
+    np.testing.assert_array_equal(flags[keep] & 1, (hb.stage[keep] < hb.cur_stage).astype(np.uint8))
+    np.testing.assert_array_equal((flags[keep] >> 1) & 1, ref.clipped)
+    # log-probs are still produced for every token
+    assert_scalar_close(res.cur_lp.cpu().numpy(), case.ref.cur_lp, what="masked cur_lp")
+    obj = res.obj.cpu().numpy()
+    assert np.all(obj[~keep] == 0.0)
+    assert_scalar_close(obj[keep], ref.obj, what="masked obj")
+    assert_loss_close(res.loss, ref.loss, ref.obj, T2, what="masked loss")
+    dl = res.dlogits.cpu().numpy()
+    assert np.all(dl[~keep] == 0.0)
+    atol = (V + 8) * 2.0 ** -52 * np.abs(ref.weight) / T2
+    assert_rows_close(dl[keep], ref.dlogits, what="masked dlogits", row_atol=atol)
+
+
+@pytest.mark.parametrize("V", [151936, 32000])
+def test_cuda_graph_replay_bitwise(ctx, oracle, V):
+    """The chunk launches and the reduction are capturable in a CUDA graph (no
+    host sync, no allocation inside the C-ABI calls); replaying the graph
+    gives bitwise the eager results."""
+    case = Case(oracle, seed=17, P=2, G=4, V=V, mu=math.log(10), lmax=24)
+    batch = case.upload(ctx)
+    logits = case.logits_gpu()
+    T = batch.n_tok
+    chunk = max(1, T // 3)
+
+    def launches(outs, dl, out4):
+        for r0 in range(0, T, chunk):
+            n = min(chunk, T - r0)
+            ctx.loss_chunk_fused(logits[r0:r0 + n], batch, case.clip(), outs, dlogits=dl[r0:r0 + n],
+                                 row_base=r0, total_tokens=T)
+        ctx.reduce(outs, T, out4)
+
+    eager = ctx.alloc_outputs(T, logits.device)
+    dl_e = torch.empty_like(logits)
+    o4_e = torch.empty(4, dtype=torch.float64, device=logits.device)
+    launches(eager, dl_e, o4_e)
+    ctx.check()
+
+    outs = ctx.alloc_outputs(T, logits.device)
+    dl = torch.zeros_like(logits)
+    o4 = torch.zeros(4, dtype=torch.float64, device=logits.device)
+    g = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        launches(outs, dl, o4)
+    torch.cuda.current_stream().wait_stream(side)
+    with torch.cuda.graph(g):
+        launches(outs, dl, o4)
+    for _ in range(3):
+        dl.zero_()
+        o4.zero_()
+        g.replay()
+    torch.cuda.synchronize()
+    ctx.check()
+    assert torch.equal(dl.view(torch.int16), dl_e.view(torch.int16))
+    assert torch.equal(o4, o4_e)
+    for k in ("cur_lp", "obj", "flags"):
+        assert torch.equal(outs[k], eager[k]), k
+    assert_loss_close(-o4[0].item() / T, case.ref.loss, case.ref.obj, T, what="graph loss")
