@@ -110,6 +110,7 @@ LossParams make_params(const copris_ctx* ctx, const copris_loss_batch* b, const 
   p.flags = o->flags;
   p.err = ctx->d_err;
   p.trace = ctx->d_trace;
+  p.row_ctr = ctx->d_rowctr;
   return p;
 }
 
@@ -141,6 +142,7 @@ int copris_ctx_create(int device, copris_ctx** out) {
   ctx->num_sms = prop.multiProcessorCount;
   e = cudaMalloc(&ctx->d_err, sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMemset(ctx->d_err, 0, sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->d_rowctr, sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMalloc(&ctx->d_scratch, reduce_scratch_bytes());
   if (e == cudaSuccess) e = cudaMemset(ctx->d_scratch, 0, reduce_scratch_bytes());
   if (e == cudaSuccess && getenv("COPRIS_TRACE")) {
@@ -149,6 +151,7 @@ int copris_ctx_create(int device, copris_ctx** out) {
   }
   if (e != cudaSuccess) {
     cudaFree(ctx->d_err);
+    cudaFree(ctx->d_rowctr);
     cudaFree(ctx->d_scratch);
     cudaFree(ctx->d_trace);
     delete ctx;
@@ -162,6 +165,7 @@ int copris_ctx_destroy(copris_ctx* ctx) {
   if (!ctx) return COPRIS_OK;
   DeviceGuard g(ctx->device);
   cudaFree(ctx->d_err);
+  cudaFree(ctx->d_rowctr);
   cudaFree(ctx->d_scratch);
   cudaFree(ctx->d_trace);
   delete ctx;

@@ -11,6 +11,7 @@ struct copris_ctx {
   int device;
   int num_sms;
   uint32_t* d_err;   // device error word (kernels.cuh ERR_*)
+  unsigned long long* d_rowctr;  // row-claim counter of the fused kernels (one launch at a time)
   void* d_scratch;   // reduction scratch
   copris_b200::LaunchInfo last;  // what the last loss launch did (introspection)
   long long* d_trace;  // phase tracing buffer (COPRIS_TRACE=1 at context creation)

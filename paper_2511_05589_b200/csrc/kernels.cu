@@ -179,11 +179,20 @@ __device__ __forceinline__ void warp_lse(Lse& st) {
 // Phase timer for COPRIS_TRACE (one thread per CTA accumulates cycle deltas).
 struct PhaseTimer {
   long long acc[kTraceSlots] = {};
-  long long last = 0;
+  long long last = 0, c0 = 0;
+  unsigned long long g0 = 0;
   bool on = false;
+  __device__ __forceinline__ static unsigned long long gtimer() {
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    return g;
+  }
   __device__ __forceinline__ void start(bool enable) {
     on = enable;
-    if (on) last = clock64();
+    if (on) {
+      last = c0 = clock64();
+      g0 = gtimer();
+    }
   }
   __device__ __forceinline__ void mark(int k) {
     if (on) {
@@ -192,9 +201,13 @@ struct PhaseTimer {
       last = now;
     }
   }
+  // slots 8/9: the traced thread's lifetime in ns and SM cycles
   __device__ __forceinline__ void flush(long long* trace) {
-    if (on)
+    if (on) {
+      acc[8] = static_cast<long long>(gtimer() - g0);
+      acc[9] = clock64() - c0;
       for (int k = 0; k < kTraceSlots; ++k) trace[blockIdx.x * kTraceSlots + k] += acc[k];
+    }
   }
 };
 
@@ -392,27 +405,47 @@ __global__ void __launch_bounds__(WARPS * 32, (WARPS == 8 && CL == 1) ? 3 : 1)
                       bytes, bar, pol);
   };
 
+  // Row schedule: the first two rows of each CTA are static (cid, cid + ncl);
+  // every later row is CLAIMED from a per-launch counter (CL == 1), so CTAs
+  // that run faster take more rows and all finish within about one row of
+  // each other (a static stride left the slowest CTA ~20% behind the mean).
+  // Thread 0 keeps the claim one row ahead: while row r runs, r1 (the next
+  // row) is known to every thread and the claim for the row after r1 is in
+  // flight. Cluster launches keep the static stride (all CTAs of a cluster
+  // must walk the same rows).
+  const bool dyn = CL == 1 && P.row_ctr != nullptr;
+  __shared__ int64_t claim_sh;
   int64_t r = cid;
+  int64_t r1 = cid + ncl;
   if (lane == 0 && r < P.n_rows)
     for (int p = 0; p < npieces; ++p) issue(r, p);
-  // per-row metadata, prefetched one row ahead
+  // per-row metadata, loaded one row ahead
   int32_t y_next = r < P.n_rows ? P.target[P.row_base + r] : 0;
-  MetaPipe mp;
-  if (threadIdx.x == 0) mp.init(P, r, ncl);
+  RowMeta meta_next{};
+  if (threadIdx.x == 0 && r < P.n_rows) meta_next = load_meta(P, P.row_base + r);
 
   PhaseTimer tm;
   tm.start(P.trace && threadIdx.x == 0 && blockIdx.x < kTraceCtas);
-  for (uint32_t it = 0; r < P.n_rows; r += ncl, ++it) {
+  for (uint32_t it = 0; r < P.n_rows; ++it) {
     const uint32_t par = it & 1u;
     const int64_t t = P.row_base + r;
     const int32_t y = y_next;
     RowMeta meta{};
-    if (threadIdx.x == 0) meta = mp.advance(P, r, ncl);
+    int64_t claim = 0;
+    if (threadIdx.x == 0) {
+      meta = meta_next;
+      if (r1 < P.n_rows) {
+        meta_next = load_meta(P, P.row_base + r1);
+        claim = dyn ? 2 * ncl + static_cast<int64_t>(atomicAdd(P.row_ctr, 1ull)) : r1 + ncl;
+      } else {
+        claim = P.n_rows;
+      }
+    }
     const int32_t ycol = y - col0;
     // Pull the NEXT row's slice toward L2 now, so the HBM pipe stays busy
     // through the scalar phase and pass C's refills hit L2.
-    if (kPrefetchL2 && lane == 0 && r + ncl < P.n_rows) {
-      const TIn* nrow = logits + (r + ncl) * P.ld + col0;
+    if (kPrefetchL2 && lane == 0 && r1 < P.n_rows) {
+      const TIn* nrow = logits + r1 * P.ld + col0;
       for (int p = 0; p < npieces; ++p) {
         const int32_t v0 = wv0 + p * pv;
         ptx::bulk_prefetch_l2(nrow + static_cast<int64_t>(v0) * VN,
@@ -486,13 +519,15 @@ __global__ void __launch_bounds__(WARPS * 32, (WARPS == 8 && CL == 1) ? 3 : 1)
     tm.mark(0);
     warp_lse<ENT>(st);
     if (lane == 0) red[warp] = st;
+    if (threadIdx.x == 0) claim_sh = claim;
     __syncthreads();
     tm.mark(1);
 
-    // prefetch the next row's metadata while the scalar phase runs
-    const int64_t nxt = r + ncl;
+    // the next row's target while the scalar phase runs
+    const int64_t nxt = r1;
     const bool has_next = nxt < P.n_rows;
     if (has_next) y_next = P.target[P.row_base + nxt];
+    const int64_t r2 = claim_sh;  // read before the barrier that ends the scalar phase
 
     // ---- scalar phase (warp 0): CTA total, cluster exchange, token math -----
     if (warp == 0) {
@@ -628,6 +663,8 @@ __global__ void __launch_bounds__(WARPS * 32, (WARPS == 8 && CL == 1) ? 3 : 1)
     }
     tm.mark(4);
     tm.acc[5] += 1;
+    r = r1;
+    r1 = r2 < P.n_rows ? r2 : P.n_rows;
   }
   tm.flush(P.trace);
   // no CTA may exit while a peer can still address its shared memory
@@ -1970,6 +2007,10 @@ cudaError_t launch_tma(const LossParams& p, int32_t E, int num_sms, cudaStream_t
     info->cluster = CL;
     info->grid = static_cast<int>(ncl * CL);
     info->kernel = "fused_tma_kernel";
+  }
+  if (CL == 1 && p.row_ctr) {
+    e = cudaMemsetAsync(p.row_ctr, 0, sizeof(unsigned long long), stream);
+    if (e != cudaSuccess) return e;
   }
   return cudaLaunchKernelEx(&cfg, kernel, p, E);
 }

@@ -57,11 +57,13 @@ struct LossParams {
   uint8_t* flags;
   uint32_t* err;
   long long* trace;  // optional per-CTA phase-cycle accumulators (COPRIS_TRACE)
+  unsigned long long* row_ctr;  // dynamic row claims; zeroed by the launcher before each launch
 };
 
 // Phase accumulators written by the fused kernels when LossParams::trace is
-// set: [cta * kTraceSlots + k], k = pass B, wait A, scalar, wait B, pass C, rows.
-constexpr int kTraceSlots = 8;
+// set: [cta * kTraceSlots + k], k = pass B, wait A, scalar, wait B, pass C, rows,
+// ring waits (2), lifetime ns, lifetime cycles.
+constexpr int kTraceSlots = 10;
 constexpr int kTraceCtas = 2048;
 
 enum class DType : int { BF16 = 0, F32 = 1 };

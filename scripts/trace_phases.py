@@ -21,14 +21,14 @@ dl = torch.empty_like(logits)
 for rep in range(3):
     ctx.loss_chunk_fused(logits, batch, ClipConfig(), outs, dlogits=dl, total_tokens=T)
 torch.cuda.synchronize()
-buf = (C.c_longlong * (2048 * 8))()
-ctx.lib.copris_ctx_trace_read(ctx.h, buf, 2048 * 8)  # reset after warmup
+buf = (C.c_longlong * (2048 * 10))()
+ctx.lib.copris_ctx_trace_read(ctx.h, buf, 2048 * 10)  # reset after warmup
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
 ctx.loss_chunk_fused(logits, batch, ClipConfig(), outs, dlogits=dl, total_tokens=T)
 e1.record(); torch.cuda.synchronize()
-ctx._call(ctx.lib.copris_ctx_trace_read(ctx.h, buf, 2048 * 8))
-a = np.frombuffer(buf, dtype=np.int64).reshape(2048, 8)
+ctx._call(ctx.lib.copris_ctx_trace_read(ctx.h, buf, 2048 * 10))
+a = np.frombuffer(buf, dtype=np.int64).reshape(2048, 10)
 a = a[a[:, 5] > 0]
 info = ctx.last_launch()
 per = a[:, :5].sum(0) / a[:, 5].sum()
@@ -38,4 +38,10 @@ print(f"V={V} rows={T} kernel={info} {ms:.3f} ms, {T * (4*V+16) / ms / 1e6:.0f} 
 for name, v in zip(["passB", "waitA", "scalar", "waitB", "passC"], per):
     print(f"  {name:8s} {v:9.0f} cycles/row ({100*v/per.sum():.1f}%)")
 print(f"  total    {per.sum():9.0f} cycles/row; CTAs traced {len(a)}")
-print(f"  of which waiting for ring data: passB {waits[0]:.0f}, passC {waits[1]:.0f} cycles/row")
+if not info["kernel"].startswith("fused_tma_kernel"):
+    print(f"  of which waiting for ring data: passB {waits[0]:.0f}, passC {waits[1]:.0f} cycles/row")
+life_ns, life_cyc = a[:, 8], a[:, 9]
+print(f"  CTA lifetime: {life_cyc.mean():.0f} cycles, {life_ns.mean() / 1e3:.1f} us "
+      f"(min {life_ns.min() / 1e3:.1f}, max {life_ns.max() / 1e3:.1f}) -> "
+      f"{(life_cyc / life_ns).mean():.3f} GHz; rows/CTA {a[:, 5].mean():.1f} "
+      f"(min {a[:, 5].min()}, max {a[:, 5].max()})")
