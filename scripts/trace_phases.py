@@ -18,7 +18,8 @@ blp = np.zeros(T, np.float32)
 batch = upload(ctx, hb.tok_off, hb.group_off, hb.target, blp, hb.cur_stage, stage=hb.stage, reward=hb.reward)
 outs = ctx.alloc_outputs(T, logits.device)
 dl = torch.empty_like(logits)
-for rep in range(3):
+# TRACE_WARMUP launches first (e.g. a few thousand to reach the power cap)
+for rep in range(int(os.environ.get("TRACE_WARMUP", "3"))):
     ctx.loss_chunk_fused(logits, batch, ClipConfig(), outs, dlogits=dl, total_tokens=T)
 torch.cuda.synchronize()
 buf = (C.c_longlong * (2048 * 10))()
