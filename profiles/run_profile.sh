@@ -12,6 +12,10 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
 ncu --set full --clock-control none --import-source on -k regex:fused_ -s 3 -c 1 \
     -o $OUT/prof_fused -f \
     python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --chunk-rows 8192 > $OUT/prof_fused.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:fused_tma -s 2 -c 1 \
+    -o $OUT/prof_tma -f \
+    python bench.py --config grpo_128x8_v32000_L1024 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline \
+    --chunk-rows 16384 > $OUT/prof_tma.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"bwd_kernel|logprob_gather" -s 2 -c 2 \
     -o $OUT/prof_unfused -f \
     python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --chunk-rows 8192 --unfused > $OUT/prof_unfused.log 2>&1

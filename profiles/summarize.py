@@ -110,6 +110,14 @@ def main():
             traffic["unfused:grpo_128x8_v151936"] = {"dram_bytes_per_row": sum(t.values()),
                                                      "kernel": "+".join(t),
                                                      "source": "sum of the unfused kernels"}
+    if os.path.exists(os.path.join(src, "prof_tma.ncu-rep")):
+        # V = 32,000 (configs[4]); run_profile.sh captures with --chunk-rows 16384
+        t = ncu_summary(os.path.join(src, "prof_tma.ncu-rep"), os.path.join(HERE, f"{tag}_ncu"), 16384)
+        for k, v in t.items():
+            for cfg in ("grpo_128x8_v32000_L256", "grpo_128x8_v32000_L512", "grpo_128x8_v32000_L1024",
+                        "grpo_128x8_v32000_L2048", "grpo_128x8_v32000_L4096"):
+                traffic[cfg] = {"dram_bytes_per_row": v, "kernel": k,
+                                "source": f"profiles/{tag}_ncu_{k}.txt (V = 32,000, 16384-row launch)"}
     if os.path.exists(os.path.join(src, "prof_lmhead.ncu-rep")):
         ncu_summary(os.path.join(src, "prof_lmhead.ncu-rep"), os.path.join(HERE, f"{tag}_ncu"), 4096)
     if traffic:

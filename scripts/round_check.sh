@@ -4,6 +4,8 @@ python __graft_entry__.py smoke > gpurun_out/smoke.log 2>&1
 timeout 600 python bench.py > gpurun_out/bench.log 2>&1
 timeout 300 python bench.py --config grpo_128x8_v32000_L1024 --no-e2e --no-cpu-baseline > gpurun_out/bench_v32000.log 2>&1
 timeout 300 python bench.py --config grpo_128x8_v151936_longtail_4stage --no-e2e --no-cpu-baseline > gpurun_out/bench_longtail.log 2>&1
+timeout 600 python bench.py --config grpo_512x16_v151936 --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/bench_512x16.log 2>&1
+timeout 300 python bench.py --config grpo_1x8_v32000_L256 --steps 300 --graph --no-e2e --no-cpu-baseline > gpurun_out/bench_1x8_graph.log 2>&1
 timeout 300 python bench.py --unfused --no-e2e --no-cpu-baseline --steps 5 > gpurun_out/bench_unfused.log 2>&1
 timeout 300 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.log 2>&1
 bash profiles/run_profile.sh
