@@ -163,10 +163,15 @@ __device__ __forceinline__ void lse_merge(Lse& x, const Lse& y) {
   x.m = M;
 }
 
-template <bool ENT>
+// Butterfly over the first WIDTH lanes (a power of two); when only lanes
+// [0, n) hold partials and the rest are empty, WIDTH = pow2ceil(n) gives lane 0
+// the same bits as the full 32-lane butterfly (merging an empty state is a no-op).
+constexpr int lse_width(int n) { return n <= 1 ? 1 : (n <= 2 ? 2 : (n <= 4 ? 4 : (n <= 8 ? 8 : (n <= 16 ? 16 : 32)))); }
+
+template <bool ENT, int WIDTH = 32>
 __device__ __forceinline__ void warp_lse(Lse& st) {
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
+  for (int off = WIDTH / 2; off > 0; off >>= 1) {
     Lse o;
     o.m = __shfl_xor_sync(0xffffffffu, st.m, off);
     o.s = __shfl_xor_sync(0xffffffffu, st.s, off);
@@ -532,7 +537,7 @@ __global__ void __launch_bounds__(WARPS * 32, (WARPS == 8 && CL == 1) ? 3 : 1)
     // ---- scalar phase (warp 0): CTA total, cluster exchange, token math -----
     if (warp == 0) {
       Lse tot = lane < WARPS ? red[lane] : lse_empty();
-      warp_lse<ENT>(tot);  // butterfly: every lane holds the CTA total
+      warp_lse<ENT, lse_width(WARPS)>(tot);  // lane 0 holds the CTA total
       if (lane == 0) {
         float zy = 0.f;
         if (static_cast<uint32_t>(ycol) < static_cast<uint32_t>(ncols)) {
@@ -1459,7 +1464,7 @@ __global__ void __launch_bounds__((CW + 2) * 32, CW <= 8 ? 2 : 1)
       const uint32_t bsel = i & 1u, par = (i >> 1) & 1u;
       ptx::mbar_wait_u32(p1b + bsel * 8, par);
       Lse tot = lane < CW ? red[bsel][lane] : lse_empty();
-      warp_lse<ENT>(tot);
+      warp_lse<ENT, lse_width(CW)>(tot);
       if (lane == 0) {
         const float zy = static_cast<uint32_t>(meta.y) < static_cast<uint32_t>(V) ? zy_sh[bsel] : 0.f;
         bc[bsel] = row_scalar_phase<ENT>(P, P.row_base + r, meta.y, meta.st, meta.blp, meta.rl,

@@ -170,9 +170,12 @@ __device__ __forceinline__ RowBroadcast row_scalar_phase(const LossParams& P, in
   b.y = y;
   b.eg = (ENT && !tr.err) ? static_cast<float>(P.inv_t * P.entropy_coeff) : 0.f;
   b.k0 = ENT ? H - ln_s : 0.f;
-  const double ac = fabs(static_cast<double>(b.coef));
-  b.c2 = ac > 0.0 ? static_cast<float>(static_cast<double>(M) * kLog2eD +
-                                       static_cast<double>(ln_s) * kLog2eD - log2(ac))
+  // log2|coef| in fp32 (MUFU lg2, ~1 ulp of |log2| <= ~40, i.e. <= 2^-18 in the
+  // exponent of a bf16 output) instead of a fp64 log2 on every row's critical path
+  const float ac = fabsf(b.coef);
+  b.c2 = ac > 0.f ? static_cast<float>(static_cast<double>(M) * kLog2eD +
+                                       static_cast<double>(ln_s) * kLog2eD -
+                                       static_cast<double>(log2f(ac)))
                   : 0.f;
   b.smask = b.coef > 0.f ? 0x80008000u : 0u;
   return b;
