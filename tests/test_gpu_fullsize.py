@@ -122,3 +122,48 @@ def test_full_size_determinism_and_chunking(ctx, big):
     ctx.check()
     assert torch.equal(dl, res.dlogits)
     assert torch.equal(outs["obj"], res.obj)
+
+
+def test_v32000_claimed_rows_against_oracle(ctx, oracle):
+    """V = 32,000 (config #5) with 8,192 rows: far more rows than the TMA
+    kernel's 444 CTAs, so almost every row is CLAIMED from the per-launch
+    counter at run time. Every per-token output and the loss against the CPU
+    oracle, dlogits on sampled rows; a rerun (a different row-to-CTA
+    assignment) is bitwise identical."""
+    from paper_2511_05589_b200 import ClipConfig
+    from paper_2511_05589_b200.packing import upload
+    from paper_2511_05589_b200.workload import make_host_batch, make_logits, stale_logprobs
+    from parity_util import assert_loss_close
+    V = 32000
+    hb = make_host_batch(3, 16, 8, V, fixed_len=64)
+    T = hb.n_tok
+    tgt = torch.from_numpy(hb.target).cuda()
+    logits = make_logits(T, V, tgt, 3, device="cuda")
+    z64 = logits.double().cpu().numpy()
+    cur = oracle.logprob_gather(z64, hb.target)
+    blp = stale_logprobs(cur, hb.stage, hb.cur_stage, 3)
+    adv = oracle.advantages(hb.reward, hb.group_off)
+    ref = oracle.is_loss(z64, hb.tok_off, hb.target, hb.stage, hb.cur_stage, blp.astype(np.float64),
+                         adv, want_dlogits=False)
+    batch = upload(ctx, hb.tok_off, hb.group_off, hb.target, blp, hb.cur_stage, stage=hb.stage,
+                   reward=hb.reward)
+    res = ctx.grpo_step_loss(logits, batch, ClipConfig(), coef=True)
+    assert ctx.last_launch()["kernel"] == "fused_tma_kernel"
+    assert_scalar_close(res.cur_lp.cpu().numpy(), ref.cur_lp, what="cur_lp")
+    assert_scalar_close(res.obj.cpu().numpy(), ref.obj, what="obj")
+    np.testing.assert_array_equal((res.flags.cpu().numpy() >> 1) & 1, ref.clipped)
+    assert res.stale_tokens == ref.stale_tokens and res.clipped_tokens == ref.clipped_tokens
+    assert_loss_close(res.loss, ref.loss, ref.obj, T)
+    rows = np.sort(np.random.default_rng(4).choice(T, 64, replace=False))
+    coef = res.coef.cpu().numpy()[rows]
+    z = z64[rows]
+    e = np.exp(z - z.max(axis=1, keepdims=True))
+    p = e / e.sum(axis=1, keepdims=True)
+    want = -coef[:, None] * p
+    want[np.arange(len(rows)), hb.target[rows]] = coef * (1.0 - p[np.arange(len(rows)), hb.target[rows]])
+    got = res.dlogits[torch.from_numpy(rows).cuda()].float().cpu().numpy()
+    assert_rows_close(got, want, bf16=True, what="sampled rows",
+                      row_atol=(V + 8) * 2.0 ** -52 * np.abs(coef))
+    again = ctx.grpo_step_loss(logits, batch, ClipConfig(), coef=True)
+    assert torch.equal(again.dlogits.view(torch.int16), res.dlogits.view(torch.int16))
+    assert torch.equal(again.obj, res.obj) and again.loss == res.loss
