@@ -413,8 +413,11 @@ def run_ours(args):
     # sample of this rank's batch: pinned host logits + metadata in, host
     # dlogits + loss out, host<->device copies inside the timed region.
     if not args.no_e2e:
-        # whole trajectories from the front of the batch, at least e2e_tokens
-        n_tr = int(np.searchsorted(tok_off, min(args.e2e_tokens, T), side="left"))
+        # whole trajectories from the front of the batch, at least e2e_tokens;
+        # the pinned host buffers (logits in, dlogits out: 4V bytes per token)
+        # of all ranks together stay under ~48 GB of host memory
+        e2e_tokens = min(args.e2e_tokens, max(2048, int(48e9 // (4 * V)) // world))
+        n_tr = int(np.searchsorted(tok_off, min(e2e_tokens, T), side="left"))
         n_tr = min(max(1, n_tr), len(tok_off) - 1)
         Ts = int(tok_off[n_tr])
         s_tok_off = torch.from_numpy(tok_off[: n_tr + 1].copy()).pin_memory()
