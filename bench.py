@@ -394,8 +394,10 @@ def run_ours(args):
                 "parallelism": f"dp{world} (whole prompt groups, LPT by tokens)",
                 "path": ("unfused K1->K2->K3" if args.unfused else "fused single pass")
                         + (" (CUDA graph replay)" if graph is not None else ""),
-                "kernel": info, "l2": "inputs larger than L2 (logits chunk "
-                f"{chunk * V * 2 / 1e9:.1f} GB >> 126 MB)", "loss": loss,
+                "kernel": info, "l2": (f"inputs larger than L2: each step streams {T * V * 2 / 1e6:.0f} MB "
+                                       f"of logits and writes as much dlogits (chunk buffer "
+                                       f"{chunk * V * 2 / 1e6:.0f} MB; L2 126 MB); no flush"),
+                "loss": loss,
                 "offpolicy_fraction": out4[2].item() / out4[1].item() if out4[1].item() else 0.0,
                 "clipped_tokens": int(out4[3].item()),
             },

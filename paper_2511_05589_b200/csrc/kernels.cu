@@ -1806,12 +1806,38 @@ __global__ void __launch_bounds__(256) bwd_kernel(const LossParams P) {
 // ---------------------------------------------------------------------------
 // small kernels
 // ---------------------------------------------------------------------------
+// VEC (every pointer 16-byte aligned, flags 4-byte): 4 tokens per thread with
+// 16-byte loads/stores and one 4-byte flag store; the remaining n % 4 tokens
+// scalar. Same per-token select either way (bit-exact).
+template <bool VEC>
 __global__ void behaviour_kernel(const uint32_t* __restrict__ stage, uint32_t cur_stage,
                                  const float* __restrict__ blp, const float* __restrict__ cur,
                                  int is_enabled, int behav_mode, int64_t n, float* __restrict__ out,
                                  uint8_t* __restrict__ flags) {
-  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n;
-       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t i0 = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  int64_t tail = 0;
+  if constexpr (VEC) {
+    const int64_t nq = n / 4;
+    for (int64_t q = i0; q < nq; q += stride) {
+      const uint4 s = reinterpret_cast<const uint4*>(stage)[q];
+      const float4 b = reinterpret_cast<const float4*>(blp)[q];
+      const float4 c = reinterpret_cast<const float4*>(cur)[q];
+      float4 r;
+      r.x = select_behaviour(s.x, cur_stage, b.x, c.x, is_enabled, behav_mode);
+      r.y = select_behaviour(s.y, cur_stage, b.y, c.y, is_enabled, behav_mode);
+      r.z = select_behaviour(s.z, cur_stage, b.z, c.z, is_enabled, behav_mode);
+      r.w = select_behaviour(s.w, cur_stage, b.w, c.w, is_enabled, behav_mode);
+      reinterpret_cast<float4*>(out)[q] = r;
+      if (flags) {
+        const uint32_t f = (s.x < cur_stage ? FLAG_STALE : 0u) | (s.y < cur_stage ? FLAG_STALE : 0u) << 8 |
+                           (s.z < cur_stage ? FLAG_STALE : 0u) << 16 | (s.w < cur_stage ? FLAG_STALE : 0u) << 24;
+        reinterpret_cast<uint32_t*>(flags)[q] = f;
+      }
+    }
+    tail = nq * 4;
+  }
+  for (int64_t t = tail + i0; t < n; t += stride) {
     const uint32_t st = stage[t];
     out[t] = select_behaviour(st, cur_stage, blp[t], cur[t], is_enabled, behav_mode);
     if (flags) flags[t] = st < cur_stage ? FLAG_STALE : 0;
@@ -1825,7 +1851,15 @@ __global__ void expand_u32_kernel(const int64_t* __restrict__ off, const uint32_
   const int lane = threadIdx.x & 31;
   if (w >= n) return;
   const uint32_t v = val ? val[w] : static_cast<uint32_t>(w);
-  for (int64_t t = off[w] + lane; t < off[w + 1]; t += 32) out[t] = v;
+  const int64_t a = off[w], b = off[w + 1];
+  // head up to a 16-byte boundary, 16-byte body, tail (out is 4-byte aligned)
+  int64_t a4 = a + ((4 - static_cast<int64_t>((reinterpret_cast<uintptr_t>(out) / 4 + a) & 3)) & 3);
+  if (a4 > b) a4 = b;
+  const int64_t b4 = a4 + ((b - a4) & ~int64_t{3});
+  for (int64_t t = a + lane; t < a4; t += 32) out[t] = v;
+  const uint4 vv{v, v, v, v};
+  for (int64_t t = a4 + 4 * lane; t < b4; t += 128) *reinterpret_cast<uint4*>(out + t) = vv;
+  for (int64_t t = b4 + lane; t < b; t += 32) out[t] = v;
 }
 
 __global__ void terminal_rewards_kernel(const int32_t* __restrict__ tokens,
@@ -1908,22 +1942,60 @@ struct ReduceScratch {
   unsigned int ticket;
 };
 
+// VEC (obj 16-byte and flags 4-byte aligned): each block's range starts at a
+// multiple of 4 tokens and a thread reads 4 tokens per step (two double2 and
+// one 4-byte flag word), two steps in flight — the scalar form kept too few
+// bytes in flight per SM (0.41 of HBM at 47M tokens). Fixed partition and
+// order either way, so a rerun is bitwise identical.
+template <bool VEC>
 __global__ void __launch_bounds__(kReduceThreads)
     reduce_kernel(const double* __restrict__ obj, const uint8_t* __restrict__ flags, int64_t n,
                   double* __restrict__ out4, ReduceScratch* sc) {
   __shared__ double so[kReduceThreads];
-  __shared__ unsigned long long ss[kReduceThreads], sk[kReduceThreads];
+  __shared__ unsigned long long ss[kReduceThreads], sk[kReduceThreads], smk[kReduceThreads];
   __shared__ bool last;
   const int64_t nb = gridDim.x;
-  const int64_t b0 = n * blockIdx.x / nb, b1 = n * (blockIdx.x + 1) / nb;
+  int64_t b0 = n * blockIdx.x / nb, b1 = n * (blockIdx.x + 1) / nb;
   double o = 0.0;
   unsigned long long st = 0, cl = 0, mk = 0;
-  for (int64_t t = b0 + threadIdx.x; t < b1; t += blockDim.x) {
-    o += obj[t];
-    const uint8_t f = flags[t];
+  auto tally = [&](uint32_t f) {
     st += f & FLAG_STALE;
     cl += (f >> 1) & 1u;
     mk += (f >> 2) & 1u;
+  };
+  if constexpr (VEC) {
+    b0 &= ~int64_t{3};
+    if (blockIdx.x + 1 < gridDim.x) b1 &= ~int64_t{3};
+    const int64_t q1 = b0 + ((b1 - b0) & ~int64_t{3});  // end of whole quads
+    const int64_t step = 4 * static_cast<int64_t>(blockDim.x);
+    int64_t t = b0 + 4 * static_cast<int64_t>(threadIdx.x);
+    for (; t + step < q1; t += 2 * step) {
+      const double2 a0 = *reinterpret_cast<const double2*>(obj + t);
+      const double2 a1 = *reinterpret_cast<const double2*>(obj + t + 2);
+      const double2 c0 = *reinterpret_cast<const double2*>(obj + t + step);
+      const double2 c1 = *reinterpret_cast<const double2*>(obj + t + step + 2);
+      const uint32_t fa = *reinterpret_cast<const uint32_t*>(flags + t);
+      const uint32_t fc = *reinterpret_cast<const uint32_t*>(flags + t + step);
+      o += ((a0.x + a0.y) + (a1.x + a1.y)) + ((c0.x + c0.y) + (c1.x + c1.y));
+      tally(fa & 0xFFu); tally((fa >> 8) & 0xFFu); tally((fa >> 16) & 0xFFu); tally(fa >> 24);
+      tally(fc & 0xFFu); tally((fc >> 8) & 0xFFu); tally((fc >> 16) & 0xFFu); tally(fc >> 24);
+    }
+    for (; t < q1; t += step) {
+      const double2 a0 = *reinterpret_cast<const double2*>(obj + t);
+      const double2 a1 = *reinterpret_cast<const double2*>(obj + t + 2);
+      const uint32_t fa = *reinterpret_cast<const uint32_t*>(flags + t);
+      o += (a0.x + a0.y) + (a1.x + a1.y);
+      tally(fa & 0xFFu); tally((fa >> 8) & 0xFFu); tally((fa >> 16) & 0xFFu); tally(fa >> 24);
+    }
+    for (int64_t u = q1 + threadIdx.x; u < b1; u += blockDim.x) {
+      o += obj[u];
+      tally(flags[u]);
+    }
+  } else {
+    for (int64_t t = b0 + threadIdx.x; t < b1; t += blockDim.x) {
+      o += obj[t];
+      tally(flags[t]);
+    }
   }
   // stale/clipped counts < 2^32 per block: pack them with the masked count
   so[threadIdx.x] = o;
@@ -1946,22 +2018,41 @@ __global__ void __launch_bounds__(kReduceThreads)
     last = atomicAdd(&sc->ticket, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (last && threadIdx.x == 0) {
+  if (last) {
+    // the last block sums the per-block partials with all its threads (a
+    // fixed thread-to-partial map and the same tree, so the order is fixed);
+    // one thread walking 512 partials cost ~40 us of dependent L2 loads
     __threadfence();
     double O = 0.0;
     unsigned long long Sx = 0, Cx = 0, Mx = 0;
-    for (int i = 0; i < gridDim.x; ++i) {
+    for (int i = threadIdx.x; i < gridDim.x; i += blockDim.x) {
       O += *reinterpret_cast<volatile double*>(&sc->obj[i]);
       const unsigned long long sm = *reinterpret_cast<volatile unsigned long long*>(&sc->stale[i]);
       Sx += sm & 0xFFFFFFFFull;
       Mx += sm >> 32;
       Cx += *reinterpret_cast<volatile unsigned long long*>(&sc->clipped[i]);
     }
-    out4[0] = O;
-    out4[1] = static_cast<double>(n - static_cast<int64_t>(Mx));
-    out4[2] = static_cast<double>(Sx);
-    out4[3] = static_cast<double>(Cx);
-    sc->ticket = 0;
+    so[threadIdx.x] = O;
+    ss[threadIdx.x] = Sx;
+    sk[threadIdx.x] = Cx;
+    smk[threadIdx.x] = Mx;
+    __syncthreads();
+    for (int h = blockDim.x / 2; h > 0; h >>= 1) {
+      if (threadIdx.x < h) {
+        so[threadIdx.x] += so[threadIdx.x + h];
+        ss[threadIdx.x] += ss[threadIdx.x + h];
+        sk[threadIdx.x] += sk[threadIdx.x + h];
+        smk[threadIdx.x] += smk[threadIdx.x + h];
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      out4[0] = so[0];
+      out4[1] = static_cast<double>(n - static_cast<int64_t>(smk[0]));
+      out4[2] = static_cast<double>(ss[0]);
+      out4[3] = static_cast<double>(sk[0]);
+      sc->ticket = 0;
+    }
   }
 }
 
@@ -2289,9 +2380,19 @@ cudaError_t launch_behaviour(const uint32_t* stage, uint32_t cur_stage, const fl
                              const float* cur_lp, int is_enabled, int behav_mode, int64_t n_tok,
                              float* out_behav, uint8_t* out_flags, cudaStream_t stream) {
   if (n_tok == 0) return cudaSuccess;
-  const int64_t blocks = (n_tok + 255) / 256;
-  behaviour_kernel<<<static_cast<unsigned>(blocks < 65535 ? blocks : 65535), 256, 0, stream>>>(
-      stage, cur_stage, blp, cur_lp, is_enabled, behav_mode, n_tok, out_behav, out_flags);
+  auto a16 = [](const void* p) { return reinterpret_cast<uintptr_t>(p) % 16 == 0; };
+  const bool vec = a16(stage) && a16(blp) && a16(cur_lp) && a16(out_behav) &&
+                   reinterpret_cast<uintptr_t>(out_flags) % 4 == 0;
+  const int64_t per = vec ? 4 : 1;
+  int64_t blocks = (n_tok / per + 255) / 256;
+  if (blocks < 1) blocks = 1;
+  if (blocks > 65535) blocks = 65535;
+  if (vec)
+    behaviour_kernel<true><<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
+        stage, cur_stage, blp, cur_lp, is_enabled, behav_mode, n_tok, out_behav, out_flags);
+  else
+    behaviour_kernel<false><<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
+        stage, cur_stage, blp, cur_lp, is_enabled, behav_mode, n_tok, out_behav, out_flags);
   return cudaGetLastError();
 }
 
@@ -2334,8 +2435,14 @@ cudaError_t launch_reduce(const double* obj, const uint8_t* flags, int64_t n_tok
   int64_t nb = (n_tok + 4 * kReduceThreads - 1) / (4 * kReduceThreads);
   if (nb > kReduceBlocks) nb = kReduceBlocks;
   if (nb < 1) nb = 1;
-  reduce_kernel<<<static_cast<unsigned>(nb), kReduceThreads, 0, stream>>>(
-      obj, flags, n_tok, out4, static_cast<ReduceScratch*>(scratch));
+  const bool vec = (reinterpret_cast<uintptr_t>(obj) % 16 == 0) &&
+                   (reinterpret_cast<uintptr_t>(flags) % 4 == 0);
+  if (vec)
+    reduce_kernel<true><<<static_cast<unsigned>(nb), kReduceThreads, 0, stream>>>(
+        obj, flags, n_tok, out4, static_cast<ReduceScratch*>(scratch));
+  else
+    reduce_kernel<false><<<static_cast<unsigned>(nb), kReduceThreads, 0, stream>>>(
+        obj, flags, n_tok, out4, static_cast<ReduceScratch*>(scratch));
   return cudaGetLastError();
 }
 
