@@ -201,7 +201,8 @@ int copris_logprob_gather(copris_ctx* ctx, const void* logits, int64_t ld, int32
   if (vocab < 1 || ld < vocab) return fail(COPRIS_E_INVALID, "bad vocab/ld");
   DeviceGuard g(ctx->device);
   cudaError_t e = launch_logprob_gather(logits, ld, dt(dtype), target, n_tok, vocab, out_lp,
-                                        out_lse, ctx->d_err, ctx->num_sms, as_stream(stream));
+                                        out_lse, ctx->d_err, ctx->d_rowctr, ctx->num_sms,
+                                        as_stream(stream));
   return e == cudaSuccess ? COPRIS_OK : cuda_fail(e, "logprob_gather launch");
 }
 

@@ -8,9 +8,12 @@
 //                         shared-memory copy. Persistent: each cluster walks
 //                         rows r, r + n_clusters, ... and prefetches row r+1
 //                         piece by piece while finishing row r.
+//   fused_stream_la_kernel  rows too large for shared memory: a TMA ring, pass 1
+//                         from HBM, pass 2 from L2, dedicated scalar warp with
+//                         a one-row lookahead (the default at V = 151,936).
 //   fused_generic_kernel  same arithmetic for rows that are not 16-byte
 //                         aligned (tiny/odd vocab); two passes through L2.
-//   logprob_gather_kernel K1: streaming log-softmax + gather (cur_lp, lse).
+//   K1 (sequence_logprobs) is the fused kernels in gather-only mode.
 //   bwd_kernel            unfused K3: second streaming pass from lse.
 //   + behaviour select (K2), segment expansion, rewards, advantages and a
 //     deterministic fixed-order reduction.
@@ -226,8 +229,10 @@ struct RowMeta {
 };
 
 __device__ __forceinline__ RowMeta load_meta(const LossParams& P, int64_t t) {
-  RowMeta m;
+  RowMeta m{};
   m.y = P.target[t];
+  m.keep = true;
+  if (P.gather_only) return m;
   m.st = P.stage[t];
   m.blp = P.buffered_lp[t];
   m.rl = P.ref_lp ? P.ref_lp[t] : 0.f;
@@ -245,13 +250,15 @@ struct MetaPipe {
   int32_t traj_ahead = 0;
   __device__ __forceinline__ void init(const LossParams& P, int64_t r, int64_t stride) {
     if (r < P.n_rows) next = load_meta(P, P.row_base + r);
-    if (r + stride < P.n_rows) traj_ahead = P.tok_traj[P.row_base + r + stride];
+    if (!P.gather_only && r + stride < P.n_rows) traj_ahead = P.tok_traj[P.row_base + r + stride];
   }
   // Returns row r's metadata and starts the loads for row r + stride.
   __device__ __forceinline__ RowMeta advance(const LossParams& P, int64_t r, int64_t stride) {
     const RowMeta cur = next;
     const int64_t r1 = r + stride;
-    if (r1 < P.n_rows) {
+    if (r1 < P.n_rows && P.gather_only) {
+      next.y = P.target[P.row_base + r1];
+    } else if (r1 < P.n_rows) {
       const int64_t t1 = P.row_base + r1;
       next.y = P.target[t1];
       next.st = P.stage[t1];
@@ -1632,69 +1639,7 @@ __global__ void __launch_bounds__(256) fused_generic_kernel(const LossParams P) 
 }
 
 // ---------------------------------------------------------------------------
-// K1: streaming log-softmax + gather
-// ---------------------------------------------------------------------------
-template <typename TIn, bool VECTOR>
-__global__ void __launch_bounds__(256)
-    logprob_gather_kernel(const TIn* __restrict__ logits, int64_t ld, const int32_t* __restrict__ target,
-                          int64_t n_tok, int32_t V, float* __restrict__ out_lp,
-                          float* __restrict__ out_lse, uint32_t* err) {
-  using VI = Vec<TIn>;
-  constexpr int VN = VI::N;
-  constexpr int UNROLL = 4;
-  __shared__ Lse red[8];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nw = blockDim.x >> 5;
-  for (int64_t r = blockIdx.x; r < n_tok; r += gridDim.x) {
-    const TIn* row = logits + r * ld;
-    const int32_t y = target[r];
-    Lse st = lse_empty();
-    if constexpr (VECTOR) {
-      const int32_t nvec = V / VN;
-      const uint4* rv = reinterpret_cast<const uint4*>(row);
-      for (int32_t v = threadIdx.x; v < nvec; v += UNROLL * blockDim.x) {
-        uint4 buf[UNROLL];
-#pragma unroll
-        for (int k = 0; k < UNROLL; ++k) {
-          const int32_t vi = v + k * blockDim.x;
-          if (vi < nvec) buf[k] = ptx::ld_global_nc_v4(rv + vi);
-        }
-#pragma unroll
-        for (int k = 0; k < UNROLL; ++k) {
-          const int32_t vi = v + k * static_cast<int32_t>(blockDim.x);
-          if (vi < nvec) {
-            float x[VN];
-            VI::unpack(buf[k], x);
-            const int jt = y - vi * VN;
-            online_update<VN, false>(x, st, static_cast<uint32_t>(jt) < VN ? jt : -1);
-          }
-        }
-      }
-    } else {
-      for (int32_t k = threadIdx.x; k < V; k += blockDim.x) {
-        float x = VI::load1(row + k);
-        online_update<1, false>(&x, st, k == y ? 0 : -1);
-      }
-    }
-    warp_lse<false>(st);
-    if (lane == 0) red[warp] = st;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      Lse tot = lse_empty();
-      for (int w = 0; w < nw; ++w) lse_merge<false>(tot, red[w]);
-      const bool ok = static_cast<uint32_t>(y) < static_cast<uint32_t>(V);
-      const float zy = ok ? VI::load1(row + y) : 0.f;
-      const LogProb lp = finish_logprob(tot.m, tot.s, zy, ok);
-      if (!ok) atomicOr(err, ERR_TOKEN_OOV);
-      out_lp[r] = lp.cur;
-      if (out_lse) out_lse[r] = static_cast<float>(lp.lse);
-    }
-    __syncthreads();
-  }
-}
-
-// ---------------------------------------------------------------------------
-// unfused K3: per-token objective from (cur_lp, lse, behav) + dlogits pass
+// K3 (unfused): dlogits from (cur_lp, lse, behav) in a second streaming pass
 // ---------------------------------------------------------------------------
 template <typename TIn, typename TOut, bool ENT, bool VECTOR>
 __global__ void __launch_bounds__(256) bwd_kernel(const LossParams P) {
@@ -2333,29 +2278,31 @@ cudaError_t launch_bwd(const LossParams& p, DType in, DType out, int num_sms,
                                 : by_types<false>(true, p, in, out, num_sms, stream, info);
 }
 
+// K1 = the fused kernels in gather-only mode: the same TMA/shared-memory
+// staged row stream and online LSE as the loss pass (and therefore bitwise the
+// same cur_lp/lse as the loss kernel recomputes, the GPU form of
+// test_policy.cpp:157-172), without metadata, objective or dlogits.
 cudaError_t launch_logprob_gather(const void* logits, int64_t ld, DType in, const int32_t* target,
                                   int64_t n_tok, int32_t vocab, float* out_lp, float* out_lse,
-                                  uint32_t* err, int num_sms, cudaStream_t stream) {
+                                  uint32_t* err, unsigned long long* row_ctr, int num_sms,
+                                  cudaStream_t stream) {
   if (n_tok == 0) return cudaSuccess;
-  const int grid = grid_rows(n_tok, num_sms, 8);
-  const size_t es = in == DType::BF16 ? 2 : 4;
-  const int vn = in == DType::BF16 ? 8 : 4;
-  const bool aligned = (vocab % vn == 0) && ((ld * es) % 16 == 0) &&
-                       (reinterpret_cast<uintptr_t>(logits) % 16 == 0);
-  if (in == DType::BF16) {
-    auto lg = static_cast<const __nv_bfloat16*>(logits);
-    if (aligned)
-      logprob_gather_kernel<__nv_bfloat16, true><<<grid, 256, 0, stream>>>(lg, ld, target, n_tok, vocab, out_lp, out_lse, err);
-    else
-      logprob_gather_kernel<__nv_bfloat16, false><<<grid, 256, 0, stream>>>(lg, ld, target, n_tok, vocab, out_lp, out_lse, err);
-  } else {
-    auto lg = static_cast<const float*>(logits);
-    if (aligned)
-      logprob_gather_kernel<float, true><<<grid, 256, 0, stream>>>(lg, ld, target, n_tok, vocab, out_lp, out_lse, err);
-    else
-      logprob_gather_kernel<float, false><<<grid, 256, 0, stream>>>(lg, ld, target, n_tok, vocab, out_lp, out_lse, err);
-  }
-  return cudaGetLastError();
+  LossParams p{};
+  p.logits = logits;
+  p.ld = ld;
+  p.vocab = vocab;
+  p.n_rows = n_tok;
+  p.row_base = 0;
+  p.target = target;
+  p.cur_lp = out_lp;
+  p.lse = out_lse;
+  p.err = err;
+  p.row_ctr = row_ctr;
+  p.gather_only = 1;
+  p.clamp_lo = 0.8;
+  p.clamp_hi = 1.28;
+  p.inv_t = 1.0;
+  return launch_fused(p, in, DType::BF16, num_sms, stream, nullptr);
 }
 
 cudaError_t launch_expand_segments(const int64_t* seg_off, const uint32_t* seg_ver, int64_t n_seg,

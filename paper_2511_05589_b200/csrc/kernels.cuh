@@ -58,6 +58,7 @@ struct LossParams {
   uint32_t* err;
   long long* trace;  // optional per-CTA phase-cycle accumulators (COPRIS_TRACE)
   unsigned long long* row_ctr;  // dynamic row claims; zeroed by the launcher before each launch
+  int32_t gather_only;  // K1 mode: only (cur_lp, lse) per row — no metadata, no objective
 };
 
 // Phase accumulators written by the fused kernels when LossParams::trace is
@@ -85,7 +86,8 @@ cudaError_t launch_bwd(const LossParams& p, DType in, DType out, int num_sms,
 // K1.
 cudaError_t launch_logprob_gather(const void* logits, int64_t ld, DType in, const int32_t* target,
                                   int64_t n_tok, int32_t vocab, float* out_lp, float* out_lse,
-                                  uint32_t* err, int num_sms, cudaStream_t stream);
+                                  uint32_t* err, unsigned long long* row_ctr, int num_sms,
+                                  cudaStream_t stream);
 // K2.
 cudaError_t launch_expand_segments(const int64_t* seg_off, const uint32_t* seg_ver, int64_t n_seg,
                                    uint32_t* out_stage, cudaStream_t stream);

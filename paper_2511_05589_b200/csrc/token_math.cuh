@@ -132,6 +132,15 @@ __device__ __forceinline__ RowBroadcast row_scalar_phase(const LossParams& P, in
   const bool oov = static_cast<uint32_t>(y) >= static_cast<uint32_t>(P.vocab);
   const float M = tot.m;
   const LogProb lp = finish_logprob(M, tot.s, zy, !oov);
+  if (P.gather_only) {  // K1 (sequence_logprobs): the log-prob and LSE only
+    if (oov) atomicOr(P.err, ERR_TOKEN_OOV);  // policy.hpp:169
+    if (write) {
+      P.cur_lp[t] = lp.cur;
+      if (P.lse) P.lse[t] = static_cast<float>(lp.lse);
+    }
+    RowBroadcast z{};
+    return z;
+  }
   const float ln_s = lp.ln_s;
   const double lse = lp.lse;
   const float cur = lp.cur;

@@ -16,7 +16,7 @@ ncu --set full --clock-control none --import-source on -k regex:fused_tma -s 2 -
     -o $OUT/prof_tma -f \
     python bench.py --config grpo_128x8_v32000_L1024 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline \
     --chunk-rows 16384 > $OUT/prof_tma.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"bwd_kernel|logprob_gather" -s 2 -c 2 \
+ncu --set full --clock-control none --import-source on -k regex:"bwd_kernel|fused_stream" -s 2 -c 2 \
     -o $OUT/prof_unfused -f \
     python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --chunk-rows 8192 --unfused > $OUT/prof_unfused.log 2>&1
 COPRIS_LMHEAD_GROUP=16 ncu --set full --clock-control none --import-source on -k regex:lmhead_fwd_pair -c 1 \

@@ -105,7 +105,8 @@ def main():
             traffic["grpo_128x8_v151936"] = {"dram_bytes_per_row": v, "kernel": k,
                                              "source": f"profiles/{tag}_ncu_{k}.txt"}
     if os.path.exists(os.path.join(src, "prof_unfused.ncu-rep")):
-        t = ncu_summary(os.path.join(src, "prof_unfused.ncu-rep"), os.path.join(HERE, f"{tag}_ncu"), rows)
+        # K1 (the fused kernel in gather-only mode) and K3 of one chunk
+        t = ncu_summary(os.path.join(src, "prof_unfused.ncu-rep"), os.path.join(HERE, f"{tag}_ncu_unfused"), rows)
         if t:
             traffic["unfused:grpo_128x8_v151936"] = {"dram_bytes_per_row": sum(t.values()),
                                                      "kernel": "+".join(t),

@@ -447,3 +447,19 @@ def test_cuda_graph_replay_bitwise(ctx, oracle, V):
     for k in ("cur_lp", "obj", "flags"):
         assert torch.equal(outs[k], eager[k]), k
     assert_loss_close(-o4[0].item() / T, case.ref.loss, case.ref.obj, T, what="graph loss")
+
+
+@pytest.mark.parametrize("V,dtype", [(151936, BF16), (32000, BF16), (4099, BF16), (151936, F32),
+                                     (32000, F32), (6, F32)])
+def test_k1_equals_loss_recompute_bitwise(ctx, oracle, V, dtype):
+    """test_policy.cpp:157-172 on the GPU: the log-probs K1 (sequence_logprobs,
+    what a sampler records) returns are bitwise the ones the loss kernel
+    recomputes, so a current-stage token's ratio is exactly 1 in either
+    behaviour mode; K1 is the fused kernels in gather-only mode."""
+    case = Case(oracle, seed=19, P=2, G=4, V=V, dtype=dtype, mu=math.log(10), lmax=24)
+    logits = case.logits_gpu()
+    lp, lse = ctx.sequence_logprobs(logits, torch.from_numpy(case.hb.target).cuda())
+    _, res = run(ctx, case, F32)
+    assert torch.equal(lp.view(torch.int32), res.cur_lp.view(torch.int32))
+    assert torch.equal(lse.view(torch.int32), res.lse.view(torch.int32))
+    assert_scalar_close(lp.cpu().numpy(), case.ref.cur_lp, what=f"K1 V={V}")
