@@ -69,9 +69,12 @@ typedef struct copris_ctx copris_ctx;
 COPRIS_API int copris_abi_version(void);
 COPRIS_API const char* copris_last_error(void);
 
-/* Context: device binding, SM count, device error word and reduction scratch.
- * Re-entrant: one context per (thread, device) or shared under the caller's
- * lock; no global mutable state (SURVEY.md §8(b) Threading). */
+/* Context: device binding, SM count, device error word, row-claim counter and
+ * reduction scratch. Re-entrant: one context per (thread, device) or shared
+ * under the caller's lock; no global mutable state (SURVEY.md §8(b) Threading).
+ * A context's launches must not overlap on different streams (the row-claim
+ * counter and the reduction scratch are per context): issue them on one
+ * stream, or use one context per stream. */
 COPRIS_API int copris_ctx_create(int device, copris_ctx** out);
 COPRIS_API int copris_ctx_destroy(copris_ctx* ctx);
 /* Synchronises `stream`, then reports and clears the device error word. */
