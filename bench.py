@@ -311,11 +311,13 @@ def run_ours(args):
     graph = None
 
     def step(evs=None):
+        torch.cuda.nvtx.range_push("copris step")
         if graph is not None:
             graph.replay()
         else:
             launches(evs)
         allreduce_scalars(out4)
+        torch.cuda.nvtx.range_pop()
 
     for _ in range(max(args.warmup, 1)):
         step()

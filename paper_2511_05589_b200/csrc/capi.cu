@@ -193,6 +193,7 @@ int copris_ctx_check(copris_ctx* ctx, void* stream) {
 int copris_logprob_gather(copris_ctx* ctx, const void* logits, int64_t ld, int32_t dtype,
                           const int32_t* target, int64_t n_tok, int32_t vocab, float* out_lp,
                           float* out_lse, void* stream) {
+  NvtxRange nv("copris_logprob_gather");
   if (!ctx) return fail(COPRIS_E_INVALID, "null ctx");
   if (n_tok < 0) return fail(COPRIS_E_INVALID, "negative n_tok");
   if (n_tok == 0) return COPRIS_OK;  // test_policy.cpp:151-155
@@ -322,6 +323,7 @@ int copris_token_traj(copris_ctx* ctx, const int64_t* tok_off, int64_t n_traj, i
 
 int copris_is_loss_fused(copris_ctx* ctx, const copris_loss_batch* batch,
                          const copris_loss_cfg* cfg, const copris_loss_out* out, void* stream) {
+  NvtxRange nv("copris_is_loss_fused");
   int rc = validate_loss(ctx, batch, cfg, out);
   if (rc) return rc;
   if (!out->cur_lp) return fail(COPRIS_E_INVALID, "null output pointer (cur_lp)");
@@ -336,6 +338,7 @@ int copris_is_loss_fused(copris_ctx* ctx, const copris_loss_batch* batch,
 int copris_is_loss_bwd(copris_ctx* ctx, const copris_loss_batch* batch,
                        const copris_loss_cfg* cfg, const float* cur_lp, const float* lse,
                        const float* behav, const copris_loss_out* out, void* stream) {
+  NvtxRange nv("copris_is_loss_bwd");
   int rc = validate_loss(ctx, batch, cfg, out);
   if (rc) return rc;
   if (!cur_lp || !lse || !behav) return fail(COPRIS_E_INVALID, "null cur_lp/lse/behav input");

@@ -169,6 +169,7 @@ int copris_workspace_destroy(copris_workspace* ws) {
 
 int copris_grpo_step_loss_host(copris_ctx* ctx, copris_workspace* w, const copris_host_batch* b,
                                const copris_loss_cfg* cfg_in, copris_host_result* out) {
+  NvtxRange nv("copris_grpo_step_loss_host");
   if (!ctx || !w || !b || !cfg_in || !out) return fail(COPRIS_E_INVALID, "null argument");
   if (w->ctx != ctx) return fail(COPRIS_E_INVALID, "workspace belongs to another context");
   // grpo.hpp:120-133 order: empty batch, then per-item checks, then no tokens
@@ -237,6 +238,7 @@ int copris_grpo_step_loss_host(copris_ctx* ctx, copris_workspace* w, const copri
 
   const int64_t nchunks = (T + w->chunk_rows - 1) / w->chunk_rows;
   for (int64_t c = 0; c < nchunks; ++c) {
+    NvtxRange nvc("chunk: h2d -> fused -> d2h");
     const int i = static_cast<int>(c & 1);
     const int64_t r0 = c * w->chunk_rows;
     const int64_t rows = std::min(w->chunk_rows, T - r0);

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: no-ops unless a profiler attaches
 
 #include <string>
 
@@ -23,6 +24,14 @@ namespace copris_b200 {
 // Records `msg` as this thread's last error and returns `code`.
 int fail(int code, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* where);
+
+// NVTX range over a host scope (visible in Nsight Systems timelines).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Makes `dev` current for the scope of a call and restores the caller's device.
 struct DeviceGuard {
