@@ -20,9 +20,7 @@ compiled from /root/reference's headers) on the host cores, rank 0 only.
 from __future__ import annotations
 
 import argparse
-import ctypes as C
 import json
-import math
 import os
 import statistics
 import subprocess

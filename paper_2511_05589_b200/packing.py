@@ -9,7 +9,7 @@ trajectory ids from tok_off, advantages from rewards (K3a).
 from __future__ import annotations
 
 from dataclasses import dataclass, field
-from typing import Optional, Sequence
+from typing import Sequence
 
 import numpy as np
 import torch

@@ -6,7 +6,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from paper_2511_05589_b200 import ClipConfig, Copris
 from paper_2511_05589_b200.packing import upload
-from paper_2511_05589_b200.workload import make_host_batch, make_logits, stale_logprobs
+from paper_2511_05589_b200.workload import make_host_batch, make_logits
 
 V = int(sys.argv[1]) if len(sys.argv) > 1 else 151936
 rows = int(sys.argv[2]) if len(sys.argv) > 2 else 16384

@@ -9,7 +9,6 @@ properties (the oracle cannot run 10^10-element rows in test time):
   * stale/clipped counts and the loss agree with the per-token outputs;
   * bit-identical reruns and chunk-size invariance at full size.
 """
-import math
 
 import numpy as np
 import pytest

@@ -13,7 +13,7 @@ import numpy as np
 import pytest
 import torch
 
-from parity_util import assert_loss_close, assert_rows_close, assert_scalar_close
+from parity_util import assert_loss_close, assert_scalar_close
 
 pytestmark = pytest.mark.gpu
 

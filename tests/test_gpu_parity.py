@@ -272,20 +272,47 @@ def test_logprob_gather_k1(ctx, oracle):
         assert_scalar_close(lp.cpu().numpy(), case.ref.cur_lp, what=f"K1 V={V}")
 
 
-def test_behaviour_concat_k2_bit_exact(ctx, oracle):
+@pytest.mark.parametrize("n,off", [(100_000, 0), (100_003, 0), (100_003, 1), (3, 0)])
+def test_behaviour_concat_k2_bit_exact(ctx, oracle, n, off):
+    """16-byte vector path (aligned), its scalar tail (n % 4) and the scalar
+    kernel (inputs offset by one element, so not 16-byte aligned)."""
     rng = np.random.default_rng(1)
-    n = 100_000
-    stage = rng.integers(0, 6, n).astype(np.uint32)
-    blp = rng.standard_normal(n).astype(np.float32)
-    cur = rng.standard_normal(n).astype(np.float32)
-    d = lambda a: torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else a).cuda()
+    stage = rng.integers(0, 6, n + off).astype(np.uint32)
+    blp = rng.standard_normal(n + off).astype(np.float32)
+    cur = rng.standard_normal(n + off).astype(np.float32)
+    d = lambda a: torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else a).cuda()[off:]
+    stage, blp, cur = stage[off:], blp[off:], cur[off:]
     for is_on in (True, False):
         for mode in (0, 1):
-            behav, flags = ctx.concat_segments(d(stage), 5, d(blp), d(cur), is_on, mode)
+            behav, flags = ctx.concat_segments(d(np.concatenate([np.zeros(off, np.uint32), stage])), 5,
+                                               d(np.concatenate([np.zeros(off, np.float32), blp])),
+                                               d(np.concatenate([np.zeros(off, np.float32), cur])),
+                                               is_on, mode)
             ref, n_stale = oracle.behaviour(stage, 5, blp, cur, is_on, mode)
             np.testing.assert_array_equal(behav.cpu().numpy(), ref.astype(np.float32))
             np.testing.assert_array_equal(flags.cpu().numpy(), (stage < 5).astype(np.uint8))
             assert int(flags.sum().item()) == n_stale
+
+
+@pytest.mark.parametrize("n,off", [(1_000_003, 0), (1_000_003, 1), (5, 0), (4099, 3)])
+def test_reduce_vector_and_scalar_paths(ctx, n, off):
+    """copris_loss_reduce: vectorized (aligned) and scalar (offset) kernels give
+    exact integer counts and the fp64 sum within rounding; reruns are bitwise."""
+    rng = np.random.default_rng(2)
+    obj = torch.from_numpy(rng.standard_normal(n + off)).cuda()
+    flags = torch.from_numpy(rng.integers(0, 8, n + off).astype(np.uint8)).cuda()
+    outs = {"obj": obj[off:], "flags": flags[off:]}
+    out4 = torch.empty(4, dtype=torch.float64, device="cuda")
+    ctx.reduce(outs, n, out4)
+    first = out4.clone()
+    ctx.reduce(outs, n, out4)
+    assert torch.equal(first, out4)
+    f = flags[off:].cpu().numpy()
+    o = obj[off:].cpu().numpy()
+    assert out4[1].item() == n - int(((f >> 2) & 1).sum())
+    assert out4[2].item() == int((f & 1).sum())
+    assert out4[3].item() == int(((f >> 1) & 1).sum())
+    assert abs(out4[0].item() - float(np.sum(o))) <= 1e-12 * max(1.0, float(np.abs(o).sum()))
 
 
 def test_expand_segments(ctx):
