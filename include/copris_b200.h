@@ -114,6 +114,20 @@ COPRIS_API int copris_lse_merge(copris_ctx* ctx, const float* partials, int32_t 
                                 int64_t n_rows, int32_t vocab, float* out_lp, float* out_lse,
                                 void* stream);
 
+/* LM-head backward, hidden gradient, on the same CTA-pair tcgen05 kernel:
+ *   dhidden[t][h] = bf16( sum_k dlogits[t][k] * weight_t[h][k] )   (fp32 accumulate)
+ * for t < n_rows, h < hidden_dim; weight_t = weight^T [hidden_dim x vocab]
+ * (K-major along the vocab, transposed once per optimizer step). The vocab
+ * reduction is split over copris_lmhead_dhidden_splits(...) ranges into
+ * `work` (splits * n_rows * hidden_dim fp32) and summed in a fixed order, so
+ * reruns are bitwise identical. hidden_dim % 4 == 0; bf16 operands with
+ * 16-byte aligned rows (ld_* in elements). */
+COPRIS_API int32_t copris_lmhead_dhidden_splits(copris_ctx* ctx, int64_t n_rows, int32_t hidden_dim);
+COPRIS_API int copris_lmhead_dhidden(copris_ctx* ctx, const void* dlogits, int64_t ld_dlogits,
+                                     const void* weight_t, int64_t ld_weight_t, int64_t n_rows,
+                                     int32_t hidden_dim, int32_t vocab, void* dhidden,
+                                     int64_t ld_dhidden, float* work, void* stream);
+
 /* ---- K2: segmented cross-stage behaviour concat -----------------------------
  * copris_expand_segments: per-token stage ids from segment tables
  *   (segments in packed order; seg_off[n_seg+1] token offsets, seg_ver[n_seg]).

@@ -250,6 +250,35 @@ int copris_lse_merge(copris_ctx* ctx, const float* partials, int32_t n_vt, const
   return e == cudaSuccess ? COPRIS_OK : cuda_fail(e, "lse_merge launch");
 }
 
+int32_t copris_lmhead_dhidden_splits(copris_ctx* ctx, int64_t n_rows, int32_t hidden_dim) {
+  if (!ctx || n_rows < 1 || hidden_dim < 1) return 0;
+  return gemm_nt_splits(n_rows, hidden_dim, ctx->num_sms);
+}
+
+int copris_lmhead_dhidden(copris_ctx* ctx, const void* dlogits, int64_t ld_dlogits,
+                          const void* weight_t, int64_t ld_weight_t, int64_t n_rows,
+                          int32_t hidden_dim, int32_t vocab, void* dhidden, int64_t ld_dhidden,
+                          float* work, void* stream) {
+  if (!ctx) return fail(COPRIS_E_INVALID, "null ctx");
+  if (n_rows < 0) return fail(COPRIS_E_INVALID, "negative n_rows");
+  if (n_rows == 0) return COPRIS_OK;
+  if (!dlogits || !weight_t || !dhidden || !work) return fail(COPRIS_E_INVALID, "null pointer");
+  if (vocab < 1 || hidden_dim < 4 || hidden_dim % 4) return fail(COPRIS_E_INVALID, "bad vocab/hidden_dim");
+  if (ld_dlogits < vocab || ld_weight_t < vocab || ld_dlogits % 8 || ld_weight_t % 8 ||
+      ld_dhidden < hidden_dim || ld_dhidden % 4)
+    return fail(COPRIS_E_INVALID, "bad row strides");
+  if ((reinterpret_cast<uintptr_t>(dlogits) | reinterpret_cast<uintptr_t>(weight_t)) & 15 ||
+      reinterpret_cast<uintptr_t>(dhidden) & 7 || reinterpret_cast<uintptr_t>(work) & 15)
+    return fail(COPRIS_E_INVALID, "misaligned operand");
+  if (n_rows > INT32_MAX) return fail(COPRIS_E_INVALID, "too many rows");
+  DeviceGuard g(ctx->device);
+  cudaError_t e = launch_gemm_nt_bf16(dlogits, ld_dlogits, weight_t, ld_weight_t, n_rows, hidden_dim,
+                                      vocab, dhidden, ld_dhidden, work,
+                                      gemm_nt_splits(n_rows, hidden_dim, ctx->num_sms), ctx->num_sms,
+                                      as_stream(stream), &ctx->last);
+  return e == cudaSuccess ? COPRIS_OK : cuda_fail(e, "lmhead_dhidden launch");
+}
+
 int copris_expand_segments(copris_ctx* ctx, const int64_t* seg_off, const uint32_t* seg_ver,
                            int64_t n_seg, uint32_t* out_stage, void* stream) {
   if (!ctx) return fail(COPRIS_E_INVALID, "null ctx");

@@ -63,6 +63,13 @@ struct LmParams {
   float2* partials;  // [n_rows][n_vt]
   const int32_t* target;
   int32_t group;     // token-pair blocks per raster group (pair kernel)
+  // plain GEMM mode (EPI == 1, the LM-head backward dhidden = dlogits W):
+  // C[split][M x N] fp32 partials over k-block ranges of k_per_split blocks
+  float* c_out;
+  int64_t ldc;
+  int64_t split_stride;  // elements between the partial matrices of two splits
+  int32_t n_split, k_per_split;
+  int32_t a_evict_first;
 };
 
 __device__ __forceinline__ float bf16_round(float x) {
@@ -271,6 +278,10 @@ constexpr int kPBBytes = 128 * kBK * 2;  // 16 KB: this CTA's half of the weight
 constexpr int kPStageBytes = kPABytes + kPBBytes;
 constexpr size_t kPSmemBytes = 1024 + kPStages * kPStageBytes + 256;
 
+// EPI 0: logits + LSE partials (the forward). EPI 1: C = A B^T as fp32 split-K
+// partials (A [M x K], B [N x K], both K-major; M = tokens, N = P.V columns,
+// K = P.H), e.g. dhidden = dlogits [T x V] * (W^T [H x V])^T.
+template <int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     lmhead_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_x,
                            const __grid_constant__ CUtensorMap tm_w, const LmParams P) {
@@ -311,12 +322,25 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int nk = (P.H + kBK - 1) / kBK;
   const int64_t n_mpair = (P.n_rows + 255) / 256;
-  const int64_t n_units = n_mpair * P.n_vt;
+  const int32_t n_split = EPI == 1 ? P.n_split : 1;
+  const int64_t n_units = n_mpair * P.n_vt * n_split;
+  // k-block range of a unit's split
+  auto k_range = [&](int64_t u, int& kb0, int& kb1) {
+    if (EPI == 1) {
+      const int64_t sp = u / (n_mpair * P.n_vt);
+      kb0 = static_cast<int>(sp * P.k_per_split);
+      kb1 = min(nk, kb0 + P.k_per_split);
+    } else {
+      kb0 = 0;
+      kb1 = nk;
+    }
+  };
   // Grouped raster: units sweep every vocab tile for a group of `grp` token
   // pairs before moving on, so the group's hidden rows stay L2-resident while
   // each weight tile is shared by the group's concurrently running clusters.
   const int64_t grp = P.group < n_mpair ? static_cast<int64_t>(P.group) : n_mpair;
   auto unit_coords = [&](int64_t u, int64_t& mp, int32_t& vt) {
+    if (EPI == 1) u %= n_mpair * P.n_vt;  // split-major: the same raster in every split
     const int64_t per = grp * P.n_vt;
     const int64_t g = u / per, w = u % per;
     const int64_t gsz = grp < n_mpair - g * grp ? grp : n_mpair - g * grp;  // last group may be short
@@ -328,7 +352,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       // ===== TMA producer (both CTAs) =====
       const uint64_t pol_w = ptx::policy_evict_normal();
-      const uint64_t pol_x = ptx::policy_evict_last();
+      // forward: the hidden block is small and reused by every vocab tile;
+      // GEMM mode: A (dlogits) is a large stream, no reason to pin it
+      const uint64_t pol_x = EPI == 1 ? (P.a_evict_first ? ptx::policy_evict_first()
+                                                         : ptx::policy_evict_normal())
+                                      : ptx::policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t u = cid; u < n_units; u += ncl) {
@@ -337,7 +365,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         unit_coords(u, mp, vt);
         const int32_t m0 = static_cast<int32_t>(mp) * 256 + 128 * rank;
         const int32_t n0 = vt * kBN + 128 * rank;
-        for (int kb = 0; kb < nk; ++kb) {
+        int kb0, kb1;
+        k_range(u, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait_u32(empty_bar(stage), phase ^ 1u);
           const uint32_t fb = ptx::mapa(full_bar(stage), 0);
           if (leader) ptx::mbar_arrive_expect_tx_u32(full_bar(stage), 2 * kPStageBytes);
@@ -362,14 +392,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::mbar_wait_u32(tempty_bar(acc), acc_phase ^ 1u);
         tc::fence_after_sync();
         const uint32_t d = tmem_base + static_cast<uint32_t>(acc * kBN);
-        for (int kb = 0; kb < nk; ++kb) {
+        int kb0, kb1;
+        k_range(u, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait_u32(full_bar(stage), phase);
           tc::fence_after_sync();
           const uint32_t a = sA + stage * kPABytes, b = sB + stage * kPBBytes;
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k)
             tc::mma_bf16_ss_pair(d, tc::smem_desc_sw128(a + 32 * k),
-                                 tc::smem_desc_sw128(b + 32 * k), idesc, (kb | k) != 0);
+                                 tc::smem_desc_sw128(b + 32 * k), idesc,
+                                 (kb != kb0 || k != 0) ? 1u : 0u);
           tc::commit_pair(empty_bar(stage), 0x3);
           if (++stage == kPStages) {
             stage = 0;
@@ -398,17 +431,44 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t row = mp * 256 + 128 * rank + r_in;
       const int32_t n0 = vt * kBN;
       const bool row_ok = row < P.n_rows;
-      const int32_t yrel = row_ok ? P.target[row] - n0 : -1;
       const int32_t ncols = min(kBN, P.V - n0);
       ptx::mbar_wait_u32(tfull_bar(acc), acc_phase);
       tc::fence_after_sync();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(sub * 32) << 16) +
                              static_cast<uint32_t>(acc * kBN);
+      if constexpr (EPI == 1) {
+        // fp32 tile row straight from TMEM to this split's partial matrix
+        const int64_t sp = u / (n_mpair * P.n_vt);
+        float* out = P.c_out + sp * P.split_stride + row * P.ldc + n0;
+#pragma unroll 1
+        for (int c = 0; c < kBN; c += 32) {
+          uint32_t r[32];
+          tc::tmem_ld_32x32b_x32(taddr + c, r);
+          tc::tmem_wait_ld();
+          if (c >= ncols) break;  // uniform across the warp
+          if (row_ok) {
+            if (c + 32 <= ncols) {
+#pragma unroll
+              for (int q = 0; q < 8; ++q)
+                ptx::st_global_v4_hint(out + c + 4 * q,
+                                       make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]),
+                                       st_pol);
+            } else {
+              for (int j = 0; j < 32 && c + j < ncols; ++j) out[c + j] = __uint_as_float(r[j]);
+            }
+          }
+        }
+        tc::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_remote(ptx::mapa(tempty_bar(acc), 0));
+      } else {
+      const int32_t yrel = row_ok ? P.target[row] - n0 : -1;
       const float2 part = epilogue_row(taddr, row, row_ok, n0, ncols, yrel, P, st_pol);
       tc::fence_before_sync();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive_remote(ptx::mapa(tempty_bar(acc), 0));
       if (row_ok) P.partials[row * P.n_vt + vt] = part;
+      }
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1u;
@@ -421,6 +481,31 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) {
     tc::fence_after_sync();
     tc::tmem_dealloc_pair<kTmemCols>(tmem_base);
+  }
+}
+
+// Split-K finish of the plain GEMM: out[m][n] = bf16(sum_s part[s][m][n]) in a
+// fixed split order (deterministic). 4 columns per thread.
+__global__ void __launch_bounds__(256)
+    splitk_sum_bf16_kernel(const float* __restrict__ part, int64_t split_stride, int32_t n_split,
+                           int64_t M, int32_t N, int64_t ldc, __nv_bfloat16* __restrict__ out,
+                           int64_t ldo) {
+  const int32_t nq = N / 4;
+  const int64_t total = M * nq;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t m = i / nq;
+    const int32_t n = static_cast<int32_t>(i % nq) * 4;
+    float4 a = *reinterpret_cast<const float4*>(part + m * ldc + n);
+    for (int s = 1; s < n_split; ++s) {
+      const float4 b = *reinterpret_cast<const float4*>(part + s * split_stride + m * ldc + n);
+      a.x += b.x;
+      a.y += b.y;
+      a.z += b.z;
+      a.w += b.w;
+    }
+    *reinterpret_cast<uint2*>(out + m * ldo + n) =
+        make_uint2(ptx::pack_bf16x2(a.x, a.y), ptx::pack_bf16x2(a.z, a.w));
   }
 }
 
@@ -542,7 +627,7 @@ cudaError_t launch_lmhead_fwd(const void* hidden, int64_t ld_h, const void* weig
   // the pair kernel stages half of the weight tile per CTA: 128-row boxes
   if (!make_map(&tw, weight, V, H, ld_w, 128)) return cudaErrorInvalidValue;
   // per call: the attribute is per device, and one process may drive several
-  cudaError_t ea = cudaFuncSetAttribute(lmhead_fwd_pair_kernel,
+  cudaError_t ea = cudaFuncSetAttribute(lmhead_fwd_pair_kernel<0>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(kPSmemBytes));
   if (ea != cudaSuccess) return ea;
@@ -560,9 +645,75 @@ cudaError_t launch_lmhead_fwd(const void* hidden, int64_t ld_h, const void* weig
   attr_cl[0].val.clusterDim.z = 1;
   cfg.attrs = attr_cl;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, lmhead_fwd_pair_kernel, tx, tw, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, lmhead_fwd_pair_kernel<0>, tx, tw, p);
   if (info) *info = LaunchInfo{num_sms, 2, grid, "lmhead_fwd_pair_kernel"};
   return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+int32_t gemm_nt_splits(int64_t M, int32_t N, int num_sms) {
+  if (const char* e = std::getenv("COPRIS_GEMM_SPLITS")) return std::max(1, std::atoi(e));
+  const int64_t units = (M + 255) / 256 * ((N + kBN - 1) / kBN);
+  const int64_t clusters = num_sms / 2;
+  int64_t s = (4 * clusters + units - 1) / units;  // >= ~4 waves of cluster tiles
+  if (s < 1) s = 1;
+  if (s > 8) s = 8;
+  return static_cast<int32_t>(s);
+}
+
+cudaError_t launch_gemm_nt_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M,
+                                int32_t N, int32_t K, void* out, int64_t ldo, float* work,
+                                int32_t n_split, int num_sms, cudaStream_t stream,
+                                LaunchInfo* info) {
+  if (M == 0 || N == 0) return cudaSuccess;
+  CUtensorMap ta, tb;
+  if (!make_map(&ta, A, M, K, lda, 128) || !make_map(&tb, B, N, K, ldb, 128))
+    return cudaErrorInvalidValue;
+  const int nk = (K + kBK - 1) / kBK;
+  if (n_split < 1) n_split = 1;
+  if (n_split > nk) n_split = nk;
+  LmParams p{};
+  p.n_rows = M;
+  p.H = K;
+  p.V = N;
+  p.n_vt = (N + kBN - 1) / kBN;
+  {
+    const char* g = std::getenv("COPRIS_LMHEAD_GROUP");
+    p.group = g ? std::max(1, std::atoi(g)) : 16;
+    const char* ef = std::getenv("COPRIS_GEMM_A_EVICT_FIRST");
+    p.a_evict_first = ef ? std::atoi(ef) : 0;
+  }
+  p.c_out = work;
+  p.ldc = N;
+  p.split_stride = M * static_cast<int64_t>(N);
+  p.n_split = n_split;
+  p.k_per_split = (nk + n_split - 1) / n_split;
+  p.n_split = (nk + p.k_per_split - 1) / p.k_per_split;  // no empty split
+  cudaError_t e = cudaFuncSetAttribute(lmhead_fwd_pair_kernel<1>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(kPSmemBytes));
+  if (e != cudaSuccess) return e;
+  const int64_t units = (M + 255) / 256 * p.n_vt * p.n_split;
+  const int grid = static_cast<int>(std::min<int64_t>(2 * units, num_sms & ~1));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kPSmemBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr_cl[1];
+  attr_cl[0].id = cudaLaunchAttributeClusterDimension;
+  attr_cl[0].val.clusterDim.x = 2;
+  attr_cl[0].val.clusterDim.y = 1;
+  attr_cl[0].val.clusterDim.z = 1;
+  cfg.attrs = attr_cl;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, lmhead_fwd_pair_kernel<1>, ta, tb, p);
+  if (e != cudaSuccess) return e;
+  const int64_t quads = M * (N / 4);
+  const int64_t blocks = std::min<int64_t>((quads + 255) / 256, static_cast<int64_t>(num_sms) * 8);
+  splitk_sum_bf16_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
+      work, p.split_stride, p.n_split, M, N, N, static_cast<__nv_bfloat16*>(out), ldo);
+  if (info) *info = LaunchInfo{num_sms, 2, grid, "lmhead_fwd_pair_kernel<gemm>"};
+  return cudaGetLastError();
 }
 
 cudaError_t launch_lse_merge(const float* partials, int32_t n_vt, const void* logits, int64_t ld,

@@ -21,6 +21,16 @@ cudaError_t launch_lmhead_fwd(const void* hidden, int64_t ld_h, const void* weig
                               void* logits, int64_t ld, float* partials, int num_sms,
                               cudaStream_t stream, LaunchInfo* info);
 
+// C[M x N] (bf16, row stride ldo) = A[M x K] * B[N x K]^T, both bf16 K-major
+// (the LM-head backward dhidden = dlogits * W with B = W^T [H x V]) on the
+// CTA-pair tcgen05 kernel, split-K over `n_split` ranges into `work`
+// (n_split * M * N fp32) and a deterministic fixed-order sum. N % 4 == 0.
+int32_t gemm_nt_splits(int64_t M, int32_t N, int num_sms);
+cudaError_t launch_gemm_nt_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M,
+                                int32_t N, int32_t K, void* out, int64_t ldo, float* work,
+                                int32_t n_split, int num_sms, cudaStream_t stream,
+                                LaunchInfo* info);
+
 cudaError_t launch_lse_merge(const float* partials, int32_t n_vt, const void* logits, int64_t ld,
                              const int32_t* target, int64_t n_rows, int32_t V, float* out_lp,
                              float* out_lse, uint32_t* err, int num_sms, cudaStream_t stream);

@@ -201,6 +201,21 @@ class Copris:
             _p(target), _p(logits), logits.stride(0), _p(partials), self._stream(stream)))
         return logits, partials
 
+    def lmhead_dhidden(self, dlogits: torch.Tensor, weight_t: torch.Tensor,
+                       out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        """dhidden = dlogits @ weight (bf16) on the tcgen05 pair kernel; weight_t
+        is weight^T [H x V] contiguous (transpose once per optimizer step)."""
+        n, V = dlogits.shape
+        H = weight_t.shape[0]
+        if out is None:
+            out = torch.empty((n, H), dtype=torch.bfloat16, device=dlogits.device)
+        splits = int(self.lib.copris_lmhead_dhidden_splits(self.h, n, H))
+        work = torch.empty((max(1, splits), n, H), dtype=torch.float32, device=dlogits.device)
+        self._call(self.lib.copris_lmhead_dhidden(
+            self.h, _p(dlogits), dlogits.stride(0), _p(weight_t), weight_t.stride(0), n, H, V,
+            _p(out), out.stride(0), _p(work), self._stream(stream)))
+        return out
+
     def lse_merge(self, partials: torch.Tensor, logits: torch.Tensor, target: torch.Tensor,
                   out_lp=None, out_lse=None, stream=None):
         """(cur_lp, lse) from lmhead partials — what sequence_logprobs gives on the logits."""

@@ -51,10 +51,15 @@ def lmhead_grpo_step_loss(ctx: Copris, hidden: torch.Tensor, weight: torch.Tenso
                           is_enabled: bool = True, behav_mode: int = L.COPRIS_BEHAV_RECOMPUTED,
                           total_tokens: Optional[int] = None, want_grad: bool = True,
                           dweight: Optional[torch.Tensor] = None, coef: bool = False,
+                          dhidden_impl: str = "cublas", weight_t: Optional[torch.Tensor] = None,
                           stream=None) -> LmHeadStepResult:
     """grpo.hpp:117-185 with logits = hidden @ weight^T (bf16 in, fp32 accumulate).
 
     ``dweight`` (fp32 [V x H]) is accumulated into when given (zeros otherwise).
+    ``dhidden_impl="tcgen05"`` computes dhidden = dlogits @ weight on the
+    CTA-pair tcgen05 kernel (copris_lmhead_dhidden; needs weight^T, passed as
+    ``weight_t`` or transposed here once); the default is cuBLAS, measured
+    5-15% faster for this shape. dweight is always cuBLAS.
     """
     cfg = cfg or ClipConfig()
     cfg.validate()
@@ -80,6 +85,10 @@ def lmhead_grpo_step_loss(ctx: Copris, hidden: torch.Tensor, weight: torch.Tenso
     if want_grad and dweight is None:
         dweight = torch.zeros((V, H), dtype=torch.float32, device=dev)
     s = ctx._stream(stream)
+    if want_grad and dhidden_impl == "tcgen05" and weight_t is None:
+        weight_t = weight.t().contiguous()
+    elif dhidden_impl not in ("cublas", "tcgen05"):
+        raise ValueError("dhidden_impl must be 'cublas' or 'tcgen05'")
     for a in range(0, T, chunk):
         n = min(chunk, T - a)
         sl = slice(a, a + n)
@@ -97,8 +106,11 @@ def lmhead_grpo_step_loss(ctx: Copris, hidden: torch.Tensor, weight: torch.Tenso
                                              _p(outs["lse"]), _p(outs["behav"]), C.byref(o), s))
         if want_grad:
             # dlogits now sits in `lg`: the LM-head backward (plain GEMMs)
+            if dhidden_impl == "tcgen05":
+                ctx.lmhead_dhidden(lg, weight_t, out=dhidden[sl], stream=stream)
             with torch.cuda.stream(stream) if stream is not None else _null():
-                torch.mm(lg, weight, out=dhidden[sl])
+                if dhidden_impl == "cublas":
+                    torch.mm(lg, weight, out=dhidden[sl])
                 torch.addmm(dweight, lg.t(), hidden[sl], out_dtype=torch.float32, out=dweight)
     out4 = torch.empty(4, dtype=torch.float64, device=dev)
     ctx.reduce(outs, T, out4, stream=stream)

@@ -78,7 +78,8 @@ def test_lmhead_saturated_rows(ctx):
 
 
 @pytest.mark.parametrize("chunk", [4096, 100])
-def test_lmhead_loss_path_against_oracle(ctx, oracle, chunk):
+@pytest.mark.parametrize("dhidden_impl", ["cublas", "tcgen05"])
+def test_lmhead_loss_path_against_oracle(ctx, oracle, chunk, dhidden_impl):
     from paper_2511_05589_b200 import ClipConfig
     from paper_2511_05589_b200.lmhead import lmhead_grpo_step_loss
     from paper_2511_05589_b200.packing import upload
@@ -102,7 +103,8 @@ def test_lmhead_loss_path_against_oracle(ctx, oracle, chunk):
     reward = (rng.random(n_traj) < 0.5).astype(np.float64)
     group_off = np.arange(0, n_traj + 1, G, dtype=np.int64)
     batch = upload(ctx, tok_off, group_off, target, blp, 2, stage=stage, reward=reward)
-    res = lmhead_grpo_step_loss(ctx, x, w, batch, ClipConfig(), chunk_rows=chunk, coef=True)
+    res = lmhead_grpo_step_loss(ctx, x, w, batch, ClipConfig(), chunk_rows=chunk, coef=True,
+                                dhidden_impl=dhidden_impl)
     z = lg_full.double().cpu().numpy()
     adv = batch.adv.cpu().numpy()
     ref = oracle.is_loss(z, tok_off, target, stage, 2, blp.astype(np.float64), adv)
@@ -184,3 +186,25 @@ def test_lmhead_token_out_of_vocabulary(ctx):
     ctx.lse_merge(part, lg, tgt)
     with pytest.raises(ContractViolation, match="token out of vocabulary"):
         ctx.check()
+
+
+@pytest.mark.parametrize("T,H,V", [(300, 512, 4096), (256, 256, 1000), (1024, 4096, 151936)])
+def test_lmhead_dhidden_tcgen05(ctx, T, H, V):
+    """LM-head backward dhidden = dlogits @ W on the CTA-pair tcgen05 kernel
+    (B = W^T, split-K with a fixed-order sum): vs the fp32 product within bf16
+    rounding of the output, and bitwise on a rerun."""
+    g = torch.Generator(device="cuda").manual_seed(T + H)
+    ldv = (V + 7) // 8 * 8
+    dl = (torch.randn((T, ldv), device="cuda", generator=g) * 1e-3).to(torch.bfloat16)[:, :V]
+    w = (torch.randn((V, H), device="cuda", generator=g) * 0.02).to(torch.bfloat16)
+    wt = w.t().contiguous()
+    if ldv != V:
+        wt = torch.nn.functional.pad(wt, (0, ldv - V))[:, :V]
+    out = ctx.lmhead_dhidden(dl, wt)
+    torch.cuda.synchronize()
+    ref = dl.float() @ w.float()
+    err = (out.float() - ref).abs()
+    tol = 2.0 ** -8 * ref.abs() + 1e-3 * ref.abs().max()
+    assert bool((err <= tol).all()), float((err - tol).max())
+    again = ctx.lmhead_dhidden(dl, wt)
+    assert torch.equal(again.view(torch.int16), out.view(torch.int16))
