@@ -128,6 +128,19 @@ COPRIS_API int copris_lmhead_dhidden(copris_ctx* ctx, const void* dlogits, int64
                                      int32_t hidden_dim, int32_t vocab, void* dhidden,
                                      int64_t ld_dhidden, float* work, void* stream);
 
+/* LM-head backward, weight gradient, on the same CTA-pair tcgen05 kernel with
+ * both operands MN-major (the token dimension is the reduction):
+ *   dweight[k][h] += sum_t dlogits[t][k] * hidden[t][h]   (fp32 accumulate)
+ * for k < vocab, h < hidden_dim, t < n_rows; dweight is fp32 [vocab x
+ * hidden_dim] (ld_dweight % 4 == 0, 16-byte aligned). Each 256 x 256 tile of
+ * dweight is accumulated by one CTA pair in token order, so reruns are bitwise
+ * identical. Replaces the cuBLAS addmm of the reference-facing trainer step
+ * (the table-gradient scatter of trainer.hpp:176 in the LLM setting). */
+COPRIS_API int copris_lmhead_dweight(copris_ctx* ctx, const void* dlogits, int64_t ld_dlogits,
+                                     const void* hidden, int64_t ld_hidden, int64_t n_rows,
+                                     int32_t hidden_dim, int32_t vocab, float* dweight,
+                                     int64_t ld_dweight, void* stream);
+
 /* ---- K2: segmented cross-stage behaviour concat -----------------------------
  * copris_expand_segments: per-token stage ids from segment tables
  *   (segments in packed order; seg_off[n_seg+1] token offsets, seg_ver[n_seg]).

@@ -85,6 +85,7 @@ _SIGS = {
     "copris_lse_merge": ([P, P, I32, P, I64, P, I64, I32, P, P, P], C.c_int),
     "copris_lmhead_dhidden_splits": ([P, I64, I32], I32),
     "copris_lmhead_dhidden": ([P, P, I64, P, I64, I64, I32, I32, P, I64, P, P], C.c_int),
+    "copris_lmhead_dweight": ([P, P, I64, P, I64, I64, I32, I32, P, I64, P], C.c_int),
     "copris_expand_segments": ([P, P, P, I64, P, P], C.c_int),
     "copris_behaviour_concat": ([P, P, U32, P, P, I32, I32, I64, P, P, P], C.c_int),
     "copris_terminal_rewards": ([P, P, P, I64, P, P, I32, P, P], C.c_int),

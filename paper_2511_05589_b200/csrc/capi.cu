@@ -279,6 +279,30 @@ int copris_lmhead_dhidden(copris_ctx* ctx, const void* dlogits, int64_t ld_dlogi
   return e == cudaSuccess ? COPRIS_OK : cuda_fail(e, "lmhead_dhidden launch");
 }
 
+int copris_lmhead_dweight(copris_ctx* ctx, const void* dlogits, int64_t ld_dlogits,
+                          const void* hidden, int64_t ld_hidden, int64_t n_rows,
+                          int32_t hidden_dim, int32_t vocab, float* dweight, int64_t ld_dweight,
+                          void* stream) {
+  if (!ctx) return fail(COPRIS_E_INVALID, "null ctx");
+  if (n_rows < 0) return fail(COPRIS_E_INVALID, "negative n_rows");
+  if (n_rows == 0) return COPRIS_OK;
+  if (!dlogits || !hidden || !dweight) return fail(COPRIS_E_INVALID, "null pointer");
+  if (vocab < 1 || hidden_dim < 1 || vocab > INT32_MAX - 256 || hidden_dim > INT32_MAX - 256)
+    return fail(COPRIS_E_INVALID, "bad vocab/hidden_dim");
+  if (ld_dlogits < vocab || ld_hidden < hidden_dim || ld_dlogits % 8 || ld_hidden % 8 ||
+      ld_dweight < hidden_dim || ld_dweight % 4)
+    return fail(COPRIS_E_INVALID, "bad row strides");
+  if ((reinterpret_cast<uintptr_t>(dlogits) | reinterpret_cast<uintptr_t>(hidden) |
+       reinterpret_cast<uintptr_t>(dweight)) & 15)
+    return fail(COPRIS_E_INVALID, "misaligned operand");
+  if (n_rows > INT32_MAX) return fail(COPRIS_E_INVALID, "too many rows");
+  DeviceGuard g(ctx->device);
+  cudaError_t e = launch_gemm_tn_acc_f32(dlogits, ld_dlogits, hidden, ld_hidden, n_rows, vocab,
+                                         hidden_dim, dweight, ld_dweight, ctx->num_sms,
+                                         as_stream(stream), &ctx->last);
+  return e == cudaSuccess ? COPRIS_OK : cuda_fail(e, "lmhead_dweight launch");
+}
+
 int copris_expand_segments(copris_ctx* ctx, const int64_t* seg_off, const uint32_t* seg_ver,
                            int64_t n_seg, uint32_t* out_stage, void* stream) {
   if (!ctx) return fail(COPRIS_E_INVALID, "null ctx");

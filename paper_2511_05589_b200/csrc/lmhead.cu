@@ -277,10 +277,16 @@ constexpr int kPABytes = 128 * kBK * 2;  // 16 KB: this CTA's 128 token rows
 constexpr int kPBBytes = 128 * kBK * 2;  // 16 KB: this CTA's half of the weight tile
 constexpr int kPStageBytes = kPABytes + kPBBytes;
 constexpr size_t kPSmemBytes = 1024 + kPStages * kPStageBytes + 256;
+constexpr uint32_t kMnBoxBytes = kBK * 128;  // MN-major box: kBK K-rows x 64 elements
 
 // EPI 0: logits + LSE partials (the forward). EPI 1: C = A B^T as fp32 split-K
 // partials (A [M x K], B [N x K], both K-major; M = tokens, N = P.V columns,
 // K = P.H), e.g. dhidden = dlogits [T x V] * (W^T [H x V])^T.
+// EPI 2: C += A^T B with both operands MN-major (A [K x M], B [K x N] row-major,
+// the reduction over their rows; M = P.n_rows, N = P.V, K = P.H), i.e. the
+// weight gradient dW [V x H] += dlogits [T x V]^T * hidden [T x H]. Each stage
+// holds two 64-wide MN boxes per operand (LBO = one box); the fp32 epilogue
+// adds the tile into C (each tile is owned by exactly one unit: no split).
 template <int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     lmhead_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_x,
@@ -371,8 +377,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::mbar_wait_u32(empty_bar(stage), phase ^ 1u);
           const uint32_t fb = ptx::mapa(full_bar(stage), 0);
           if (leader) ptx::mbar_arrive_expect_tx_u32(full_bar(stage), 2 * kPStageBytes);
-          tc::tma_load_2d_pair(sA + stage * kPABytes, &tm_x, fb, kb * kBK, m0, pol_x);
-          tc::tma_load_2d_pair(sB + stage * kPBBytes, &tm_w, fb, kb * kBK, n0, pol_w);
+          if constexpr (EPI == 2) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              tc::tma_load_2d_pair(sA + stage * kPABytes + j * kMnBoxBytes, &tm_x, fb, m0 + 64 * j,
+                                   kb * kBK, pol_x);
+              tc::tma_load_2d_pair(sB + stage * kPBBytes + j * kMnBoxBytes, &tm_w, fb, n0 + 64 * j,
+                                   kb * kBK, pol_w);
+            }
+          } else {
+            tc::tma_load_2d_pair(sA + stage * kPABytes, &tm_x, fb, kb * kBK, m0, pol_x);
+            tc::tma_load_2d_pair(sB + stage * kPBBytes, &tm_w, fb, kb * kBK, n0, pol_w);
+          }
           if (++stage == kPStages) {
             stage = 0;
             phase ^= 1u;
@@ -383,7 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     if (lane == 0 && leader) {
       // ===== MMA issuer (leader CTA) =====
-      constexpr uint32_t idesc = tc::idesc_bf16_f32<256, kBN>();
+      constexpr uint32_t idesc = tc::idesc_bf16_f32<256, kBN, EPI == 2, EPI == 2>();
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -399,10 +415,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc::fence_after_sync();
           const uint32_t a = sA + stage * kPABytes, b = sB + stage * kPBBytes;
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k)
-            tc::mma_bf16_ss_pair(d, tc::smem_desc_sw128(a + 32 * k),
-                                 tc::smem_desc_sw128(b + 32 * k), idesc,
-                                 (kb != kb0 || k != 0) ? 1u : 0u);
+          for (int k = 0; k < kBK / 16; ++k) {
+            // K-major: 16 elements = 32 bytes along the swizzled row;
+            // MN-major: 16 K-rows = two 1024-byte atoms
+            const uint64_t da = EPI == 2 ? tc::smem_desc_sw128_mn(a + 2048 * k, kMnBoxBytes)
+                                         : tc::smem_desc_sw128(a + 32 * k);
+            const uint64_t db = EPI == 2 ? tc::smem_desc_sw128_mn(b + 2048 * k, kMnBoxBytes)
+                                         : tc::smem_desc_sw128(b + 32 * k);
+            tc::mma_bf16_ss_pair(d, da, db, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+          }
           tc::commit_pair(empty_bar(stage), 0x3);
           if (++stage == kPStages) {
             stage = 0;
@@ -436,7 +457,40 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::fence_after_sync();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(sub * 32) << 16) +
                              static_cast<uint32_t>(acc * kBN);
-      if constexpr (EPI == 1) {
+      if constexpr (EPI == 2) {
+        // C row (vocab index) += the tile row; fp32 read-modify-write
+        float* out = P.c_out + row * P.ldc + n0;
+#pragma unroll 1
+        for (int c = 0; c < kBN; c += 32) {
+          uint32_t r[32];
+          tc::tmem_ld_32x32b_x32(taddr + c, r);
+          tc::tmem_wait_ld();
+          if (c >= ncols) break;  // uniform across the warp
+          if (row_ok) {
+            if (c + 32 <= ncols && P.ldc % 4 == 0) {
+              float4 o[8];
+#pragma unroll
+              for (int q = 0; q < 8; ++q) o[q] = *reinterpret_cast<const float4*>(out + c + 4 * q);
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                o[q].x += __uint_as_float(r[4 * q]);
+                o[q].y += __uint_as_float(r[4 * q + 1]);
+                o[q].z += __uint_as_float(r[4 * q + 2]);
+                o[q].w += __uint_as_float(r[4 * q + 3]);
+                ptx::st_global_v4_hint(out + c + 4 * q,
+                                       make_uint4(__float_as_uint(o[q].x), __float_as_uint(o[q].y),
+                                                  __float_as_uint(o[q].z), __float_as_uint(o[q].w)),
+                                       st_pol);
+              }
+            } else {
+              for (int j = 0; j < 32 && c + j < ncols; ++j) out[c + j] += __uint_as_float(r[j]);
+            }
+          }
+        }
+        tc::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_remote(ptx::mapa(tempty_bar(acc), 0));
+      } else if constexpr (EPI == 1) {
         // fp32 tile row straight from TMEM to this split's partial matrix
         const int64_t sp = u / (n_mpair * P.n_vt);
         float* out = P.c_out + sp * P.split_stride + row * P.ldc + n0;
@@ -714,6 +768,49 @@ cudaError_t launch_gemm_nt_bf16(const void* A, int64_t lda, const void* B, int64
       work, p.split_stride, p.n_split, M, N, N, static_cast<__nv_bfloat16*>(out), ldo);
   if (info) *info = LaunchInfo{num_sms, 2, grid, "lmhead_fwd_pair_kernel<gemm>"};
   return cudaGetLastError();
+}
+
+cudaError_t launch_gemm_tn_acc_f32(const void* A, int64_t lda, const void* B, int64_t ldb,
+                                   int64_t K, int32_t M, int32_t N, float* c, int64_t ldc,
+                                   int num_sms, cudaStream_t stream, LaunchInfo* info) {
+  if (K == 0 || M == 0 || N == 0) return cudaSuccess;
+  // MN-major boxes: 64 columns (the contiguous dimension) x kBK rows
+  CUtensorMap ta, tb;
+  if (!make_map(&ta, A, K, M, lda, kBK) || !make_map(&tb, B, K, N, ldb, kBK))
+    return cudaErrorInvalidValue;
+  LmParams p{};
+  p.n_rows = M;
+  p.H = static_cast<int32_t>(K);
+  p.V = N;
+  p.n_vt = (N + kBN - 1) / kBN;
+  {
+    const char* g = std::getenv("COPRIS_LMHEAD_GROUP");
+    p.group = g ? std::max(1, std::atoi(g)) : 16;
+  }
+  p.c_out = c;
+  p.ldc = ldc;
+  p.n_split = 1;
+  cudaError_t e = cudaFuncSetAttribute(lmhead_fwd_pair_kernel<2>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(kPSmemBytes));
+  if (e != cudaSuccess) return e;
+  const int64_t units = (static_cast<int64_t>(M) + 255) / 256 * p.n_vt;
+  const int grid = static_cast<int>(std::min<int64_t>(2 * units, num_sms & ~1));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kPSmemBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr_cl[1];
+  attr_cl[0].id = cudaLaunchAttributeClusterDimension;
+  attr_cl[0].val.clusterDim.x = 2;
+  attr_cl[0].val.clusterDim.y = 1;
+  attr_cl[0].val.clusterDim.z = 1;
+  cfg.attrs = attr_cl;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, lmhead_fwd_pair_kernel<2>, ta, tb, p);
+  if (info) *info = LaunchInfo{num_sms, 2, grid, "lmhead_fwd_pair_kernel<dW>"};
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_lse_merge(const float* partials, int32_t n_vt, const void* logits, int64_t ld,

@@ -31,6 +31,14 @@ cudaError_t launch_gemm_nt_bf16(const void* A, int64_t lda, const void* B, int64
                                 int32_t n_split, int num_sms, cudaStream_t stream,
                                 LaunchInfo* info);
 
+// C[M x N] (fp32, row stride ldc) += A[K x M]^T * B[K x N], both bf16 row-major
+// (MN-major operands; the LM-head backward dW [V x H] += dlogits^T * hidden)
+// on the CTA-pair tcgen05 kernel. Every C tile is accumulated by one CTA pair
+// in a fixed k order: deterministic. lda / ldb % 8 == 0, 16-byte aligned.
+cudaError_t launch_gemm_tn_acc_f32(const void* A, int64_t lda, const void* B, int64_t ldb,
+                                   int64_t K, int32_t M, int32_t N, float* c, int64_t ldc,
+                                   int num_sms, cudaStream_t stream, LaunchInfo* info);
+
 cudaError_t launch_lse_merge(const float* partials, int32_t n_vt, const void* logits, int64_t ld,
                              const int32_t* target, int64_t n_rows, int32_t V, float* out_lp,
                              float* out_lse, uint32_t* err, int num_sms, cudaStream_t stream);

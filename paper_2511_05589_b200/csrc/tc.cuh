@@ -60,14 +60,26 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t smem_addr) {
          (1ull << 46) | (2ull << 61);
 }
 
+// MN-major operand tile written by TMA with SWIZZLE_128B as boxes of
+// [rows along K] x [64 MN elements = 128 bytes]: in 16-byte units the canonical
+// layout is ((8, n), (8, k)) : ((1, LBO), (8, SBO)) — 64 MN elements contiguous
+// (swizzled), 8 K-rows per 1024-byte atom, K atoms SBO = 1024 bytes apart and
+// 64-element MN atoms LBO = `mn_atom_bytes` apart (one TMA box each).
+__device__ __forceinline__ uint64_t smem_desc_sw128_mn(uint32_t smem_addr, uint32_t mn_atom_bytes) {
+  return static_cast<uint64_t>((smem_addr & 0x3FFFFu) >> 4) |
+         (static_cast<uint64_t>((mn_atom_bytes >> 4) & 0x3FFFu) << 16) | (64ull << 32) |
+         (1ull << 46) | (2ull << 61);
+}
+
 // kind::f16 instruction descriptor: D f32 [4,6)=1, A bf16 [7,10)=1, B bf16
-// [10,13)=1, both K-major (bits 15/16 = 0), N >> 3 at [17,23), M >> 4 at [24,29).
-template <int M, int N>
+// [10,13)=1, A / B major at bits 15 / 16 (0 = K-major, 1 = MN-major), N >> 3 at
+// [17,23), M >> 4 at [24,29).
+template <int M, int N, bool kAMn = false, bool kBMn = false>
 __host__ __device__ constexpr uint32_t idesc_bf16_f32() {
   static_assert(M == 64 || M == 128 || M == 256, "M");
   static_assert(N % 16 == 0 && N >= 16 && N <= 256, "N");
-  return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
-         (static_cast<uint32_t>(M >> 4) << 24);
+  return (1u << 4) | (1u << 7) | (1u << 10) | (kAMn ? 1u << 15 : 0u) | (kBMn ? 1u << 16 : 0u) |
+         (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(M >> 4) << 24);
 }
 
 // ---- MMA ------------------------------------------------------------------------

@@ -216,6 +216,21 @@ class Copris:
             _p(out), out.stride(0), _p(work), self._stream(stream)))
         return out
 
+    def lmhead_dweight(self, dlogits: torch.Tensor, hidden: torch.Tensor,
+                       out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        """dweight (fp32 [V x H]) += dlogits^T @ hidden on the tcgen05 pair kernel
+        (MN-major operands; zeros first when ``out`` is None)."""
+        n, V = dlogits.shape
+        H = hidden.shape[1]
+        if hidden.shape[0] != n:
+            raise ValueError("dlogits and hidden must have the same number of rows")
+        if out is None:
+            out = torch.zeros((V, H), dtype=torch.float32, device=dlogits.device)
+        self._call(self.lib.copris_lmhead_dweight(
+            self.h, _p(dlogits), dlogits.stride(0), _p(hidden), hidden.stride(0), n, H, V,
+            _p(out), out.stride(0), self._stream(stream)))
+        return out
+
     def lse_merge(self, partials: torch.Tensor, logits: torch.Tensor, target: torch.Tensor,
                   out_lp=None, out_lse=None, stream=None):
         """(cur_lp, lse) from lmhead partials — what sequence_logprobs gives on the logits."""

@@ -52,14 +52,16 @@ def lmhead_grpo_step_loss(ctx: Copris, hidden: torch.Tensor, weight: torch.Tenso
                           total_tokens: Optional[int] = None, want_grad: bool = True,
                           dweight: Optional[torch.Tensor] = None, coef: bool = False,
                           dhidden_impl: str = "cublas", weight_t: Optional[torch.Tensor] = None,
-                          stream=None) -> LmHeadStepResult:
+                          dweight_impl: str = "cublas", stream=None) -> LmHeadStepResult:
     """grpo.hpp:117-185 with logits = hidden @ weight^T (bf16 in, fp32 accumulate).
 
     ``dweight`` (fp32 [V x H]) is accumulated into when given (zeros otherwise).
     ``dhidden_impl="tcgen05"`` computes dhidden = dlogits @ weight on the
     CTA-pair tcgen05 kernel (copris_lmhead_dhidden; needs weight^T, passed as
     ``weight_t`` or transposed here once); the default is cuBLAS, measured
-    5-15% faster for this shape. dweight is always cuBLAS.
+    5-15% faster for this shape. ``dweight_impl="tcgen05"``
+    accumulates dweight += dlogits^T @ hidden on the same kernel with MN-major
+    operands (copris_lmhead_dweight); the default is cuBLAS addmm.
     """
     cfg = cfg or ClipConfig()
     cfg.validate()
@@ -89,6 +91,8 @@ def lmhead_grpo_step_loss(ctx: Copris, hidden: torch.Tensor, weight: torch.Tenso
         weight_t = weight.t().contiguous()
     elif dhidden_impl not in ("cublas", "tcgen05"):
         raise ValueError("dhidden_impl must be 'cublas' or 'tcgen05'")
+    if dweight_impl not in ("cublas", "tcgen05"):
+        raise ValueError("dweight_impl must be 'cublas' or 'tcgen05'")
     for a in range(0, T, chunk):
         n = min(chunk, T - a)
         sl = slice(a, a + n)
@@ -108,10 +112,13 @@ def lmhead_grpo_step_loss(ctx: Copris, hidden: torch.Tensor, weight: torch.Tenso
             # dlogits now sits in `lg`: the LM-head backward (plain GEMMs)
             if dhidden_impl == "tcgen05":
                 ctx.lmhead_dhidden(lg, weight_t, out=dhidden[sl], stream=stream)
+            if dweight_impl == "tcgen05":
+                ctx.lmhead_dweight(lg, hidden[sl], out=dweight, stream=stream)
             with torch.cuda.stream(stream) if stream is not None else _null():
                 if dhidden_impl == "cublas":
                     torch.mm(lg, weight, out=dhidden[sl])
-                torch.addmm(dweight, lg.t(), hidden[sl], out_dtype=torch.float32, out=dweight)
+                if dweight_impl == "cublas":
+                    torch.addmm(dweight, lg.t(), hidden[sl], out_dtype=torch.float32, out=dweight)
     out4 = torch.empty(4, dtype=torch.float64, device=dev)
     ctx.reduce(outs, T, out4, stream=stream)
     ctx.check(stream)

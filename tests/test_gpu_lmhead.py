@@ -78,8 +78,8 @@ def test_lmhead_saturated_rows(ctx):
 
 
 @pytest.mark.parametrize("chunk", [4096, 100])
-@pytest.mark.parametrize("dhidden_impl", ["cublas", "tcgen05"])
-def test_lmhead_loss_path_against_oracle(ctx, oracle, chunk, dhidden_impl):
+@pytest.mark.parametrize("dhidden_impl,dweight_impl", [("cublas", "cublas"), ("tcgen05", "tcgen05")])
+def test_lmhead_loss_path_against_oracle(ctx, oracle, chunk, dhidden_impl, dweight_impl):
     from paper_2511_05589_b200 import ClipConfig
     from paper_2511_05589_b200.lmhead import lmhead_grpo_step_loss
     from paper_2511_05589_b200.packing import upload
@@ -104,7 +104,7 @@ def test_lmhead_loss_path_against_oracle(ctx, oracle, chunk, dhidden_impl):
     group_off = np.arange(0, n_traj + 1, G, dtype=np.int64)
     batch = upload(ctx, tok_off, group_off, target, blp, 2, stage=stage, reward=reward)
     res = lmhead_grpo_step_loss(ctx, x, w, batch, ClipConfig(), chunk_rows=chunk, coef=True,
-                                dhidden_impl=dhidden_impl)
+                                dhidden_impl=dhidden_impl, dweight_impl=dweight_impl)
     z = lg_full.double().cpu().numpy()
     adv = batch.adv.cpu().numpy()
     ref = oracle.is_loss(z, tok_off, target, stage, 2, blp.astype(np.float64), adv)
@@ -208,3 +208,39 @@ def test_lmhead_dhidden_tcgen05(ctx, T, H, V):
     assert bool((err <= tol).all()), float((err - tol).max())
     again = ctx.lmhead_dhidden(dl, wt)
     assert torch.equal(again.view(torch.int16), out.view(torch.int16))
+
+
+@pytest.mark.parametrize("T,H,V", [(300, 512, 4096), (257, 192, 1000), (64, 520, 300), (1, 64, 256),
+                                   (4100, 1024, 32000), (1024, 4096, 151936)])
+def test_lmhead_dweight_tcgen05(ctx, T, H, V):
+    """LM-head backward dW += dlogits^T @ hidden on the CTA-pair tcgen05 kernel
+    with both operands MN-major (the token dimension is the reduction): vs the
+    fp64 product within fp32-accumulation error, accumulation into an existing
+    dW, ragged T/H/V (TMA zero fill), and bitwise on a rerun."""
+    g = torch.Generator(device="cuda").manual_seed(T + H + V)
+    ldv = (V + 7) // 8 * 8
+    dl = (torch.randn((T, ldv), device="cuda", generator=g) * 1e-3).to(torch.bfloat16)[:, :V]
+    x = torch.randn((T, H), device="cuda", generator=g).to(torch.bfloat16)
+    dw0 = torch.randn((V, H), device="cuda", generator=g)
+    out = ctx.lmhead_dweight(dl, x, out=dw0.clone())
+    torch.cuda.synchronize()
+    if V * H <= 1 << 24:
+        ref = dw0.double() + dl.double().t() @ x.double()
+        bound = (dl.double().abs().t() @ x.double().abs())
+    else:  # fp32 on the GPU for the big case (its own error is inside the bound)
+        ref = (dw0 + dl.float().t() @ x.float()).double()
+        bound = (dl.float().abs().t() @ x.float().abs()).double()
+    tol = (T + 2) * 2.0 ** -23 * bound + 2.0 ** -23 * dw0.double().abs() + 1e-30
+    err = (out.double() - ref).abs()
+    assert bool((err <= tol).all()), float((err - tol).max())
+    again = ctx.lmhead_dweight(dl, x, out=dw0.clone())
+    assert torch.equal(again.view(torch.int32), out.view(torch.int32))
+
+
+def test_lmhead_dweight_errors(ctx):
+    dl = torch.zeros((8, 64), dtype=torch.bfloat16, device="cuda")
+    x = torch.zeros((8, 64), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(ValueError):
+        ctx.lmhead_dweight(dl, x[:4])
+    with pytest.raises(ValueError, match="bad row strides"):
+        ctx.lmhead_dweight(dl, x, out=torch.zeros((64, 66), device="cuda")[:, :64])
