@@ -277,6 +277,12 @@ constexpr int kPABytes = 128 * kBK * 2;  // 16 KB: this CTA's 128 token rows
 constexpr int kPBBytes = 128 * kBK * 2;  // 16 KB: this CTA's half of the weight tile
 constexpr int kPStageBytes = kPABytes + kPBBytes;
 constexpr size_t kPSmemBytes = 1024 + kPStages * kPStageBytes + 256;
+// dW (EPI 2): one stage fewer, and per epilogue warp two 32 x 32 fp32 staging
+// boxes (SWIZZLE_128B, 4 KB each) for the TMA reduce-add into dW
+constexpr int kPStagesDw = 6;
+constexpr uint32_t kDwBoxBytes = 32 * 32 * 4;
+constexpr size_t kPSmemBytesDw = 1024 + kPStagesDw * kPStageBytes + 1024 + 8 * kDwBoxBytes;
+static_assert(kPSmemBytesDw <= 232448, "dW smem");
 constexpr uint32_t kMnBoxBytes = kBK * 128;  // MN-major box: kBK K-rows x 64 elements
 
 // EPI 0: logits + LSE partials (the forward). EPI 1: C = A B^T as fp32 split-K
@@ -290,7 +296,9 @@ constexpr uint32_t kMnBoxBytes = kBK * 128;  // MN-major box: kBK K-rows x 64 el
 template <int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     lmhead_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_x,
-                           const __grid_constant__ CUtensorMap tm_w, const LmParams P) {
+                           const __grid_constant__ CUtensorMap tm_w,
+                           const __grid_constant__ CUtensorMap tm_c, const LmParams P) {
+  constexpr int kPStages = EPI == 2 ? kPStagesDw : ::copris_b200::kPStages;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
   const uint32_t sA = base;
@@ -301,6 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto tfull_bar = [&](int b) { return bars + 8u * (2 * kPStages + b); };
   auto tempty_bar = [&](int b) { return bars + 8u * (2 * kPStages + 2 + b); };
   const uint32_t tmem_slot = bars + 8u * (2 * kPStages + 4);
+  const uint32_t stg = bars + 1024;  // EPI 2 staging (1024-aligned)
   volatile uint32_t* tmem_slot_ptr = reinterpret_cast<volatile uint32_t*>(
       smem_raw + (tmem_slot - ptx::smem_u32(smem_raw)));
 
@@ -319,6 +328,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::fence_mbarrier_init();
     tc::prefetch_tensormap(&tm_x);
     tc::prefetch_tensormap(&tm_w);
+    if (EPI == 2) tc::prefetch_tensormap(&tm_c);
   }
   if (warp == 1) tc::tmem_alloc_pair<kTmemCols>(tmem_slot);
   tc::fence_before_sync();
@@ -357,12 +367,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ===== TMA producer (both CTAs) =====
-      const uint64_t pol_w = ptx::policy_evict_normal();
+      // dW (EPI 2): COPRIS_DW_POLICY bit 0 keeps A (dlogits slices) and bit 1
+      // keeps B (hidden) at evict_last against the dW read-modify-write stream
+      const uint64_t pol_w = EPI == 2 && (P.a_evict_first & 2) ? ptx::policy_evict_last()
+                                                               : ptx::policy_evict_normal();
       // forward: the hidden block is small and reused by every vocab tile;
       // GEMM mode: A (dlogits) is a large stream, no reason to pin it
-      const uint64_t pol_x = EPI == 1 ? (P.a_evict_first ? ptx::policy_evict_first()
-                                                         : ptx::policy_evict_normal())
-                                      : ptx::policy_evict_last();
+      const uint64_t pol_x = EPI == 1   ? (P.a_evict_first ? ptx::policy_evict_first()
+                                                           : ptx::policy_evict_normal())
+                             : EPI == 2 ? ((P.a_evict_first & 1) ? ptx::policy_evict_last()
+                                                                 : ptx::policy_evict_normal())
+                                        : ptx::policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t u = cid; u < n_units; u += ncl) {
@@ -443,6 +458,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int r_in = sub * 32 + lane;
     // logits are streamed out: keep L2 for the operand tiles
     const uint64_t st_pol = ptx::policy_evict_first();
+    int dw_buf = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int64_t u = cid; u < n_units; u += ncl) {
@@ -458,34 +474,31 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(sub * 32) << 16) +
                              static_cast<uint32_t>(acc * kBN);
       if constexpr (EPI == 2) {
-        // C row (vocab index) += the tile row; fp32 read-modify-write
-        float* out = P.c_out + row * P.ldc + n0;
+        // C tile += the accumulator through TMA reduce-add: each warp stages
+        // its 32 rows x 32 columns in a swizzled box (16-byte chunk j of row
+        // r at j ^ (r & 7): conflict-free) and one lane issues the bulk add;
+        // two boxes per warp alternate so staging overlaps the adds in flight
+        const int32_t row0 = static_cast<int32_t>(mp * 256 + 128 * rank + sub * 32);
 #pragma unroll 1
         for (int c = 0; c < kBN; c += 32) {
           uint32_t r[32];
           tc::tmem_ld_32x32b_x32(taddr + c, r);
           tc::tmem_wait_ld();
           if (c >= ncols) break;  // uniform across the warp
-          if (row_ok) {
-            if (c + 32 <= ncols && P.ldc % 4 == 0) {
-              float4 o[8];
+          const uint32_t box = stg + static_cast<uint32_t>(sub * 2 + dw_buf) * kDwBoxBytes;
+          if (lane == 0) tc::bulk_wait_group_read<1>();  // the add issued 2 boxes ago read `box`
+          __syncwarp();
 #pragma unroll
-              for (int q = 0; q < 8; ++q) o[q] = *reinterpret_cast<const float4*>(out + c + 4 * q);
-#pragma unroll
-              for (int q = 0; q < 8; ++q) {
-                o[q].x += __uint_as_float(r[4 * q]);
-                o[q].y += __uint_as_float(r[4 * q + 1]);
-                o[q].z += __uint_as_float(r[4 * q + 2]);
-                o[q].w += __uint_as_float(r[4 * q + 3]);
-                ptx::st_global_v4_hint(out + c + 4 * q,
-                                       make_uint4(__float_as_uint(o[q].x), __float_as_uint(o[q].y),
-                                                  __float_as_uint(o[q].z), __float_as_uint(o[q].w)),
-                                       st_pol);
-              }
-            } else {
-              for (int j = 0; j < 32 && c + j < ncols; ++j) out[c + j] += __uint_as_float(r[j]);
-            }
+          for (int q = 0; q < 8; ++q)
+            ptx::sts_v4(box + lane * 128 + ((q ^ (lane & 7)) << 4),
+                        make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]));
+          ptx::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tc::tma_reduce_add_2d(&tm_c, box, n0 + c, row0);
+            tc::bulk_commit_group();
           }
+          dw_buf ^= 1;
         }
         tc::fence_before_sync();
         __syncwarp();
@@ -529,6 +542,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
+  if (EPI == 2 && warp >= 2 && lane == 0) tc::bulk_wait_group<0>();
   tc::fence_before_sync();
   __syncthreads();
   ptx::cluster_sync_all();
@@ -641,6 +655,20 @@ bool make_map(CUtensorMap* map, const void* ptr, int64_t rows, int32_t k, int64_
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// fp32 matrix [rows x cols] with row stride ld elements, 32 x 32 boxes
+// (128-byte rows, SWIZZLE_128B): the TMA reduce-add target of the dW epilogue.
+bool make_map_f32_box32(CUtensorMap* map, const void* ptr, int64_t rows, int32_t cols, int64_t ld) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 4};
+  const cuuint32_t box[2] = {32, 32};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace
 
 int32_t lmhead_num_vtiles(int32_t vocab) { return (vocab + kBN - 1) / kBN; }
@@ -699,7 +727,7 @@ cudaError_t launch_lmhead_fwd(const void* hidden, int64_t ld_h, const void* weig
   attr_cl[0].val.clusterDim.z = 1;
   cfg.attrs = attr_cl;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, lmhead_fwd_pair_kernel<0>, tx, tw, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, lmhead_fwd_pair_kernel<0>, tx, tw, tw, p);
   if (info) *info = LaunchInfo{num_sms, 2, grid, "lmhead_fwd_pair_kernel"};
   return e != cudaSuccess ? e : cudaGetLastError();
 }
@@ -760,7 +788,7 @@ cudaError_t launch_gemm_nt_bf16(const void* A, int64_t lda, const void* B, int64
   attr_cl[0].val.clusterDim.z = 1;
   cfg.attrs = attr_cl;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, lmhead_fwd_pair_kernel<1>, ta, tb, p);
+  e = cudaLaunchKernelEx(&cfg, lmhead_fwd_pair_kernel<1>, ta, tb, tb, p);
   if (e != cudaSuccess) return e;
   const int64_t quads = M * (N / 4);
   const int64_t blocks = std::min<int64_t>((quads + 255) / 256, static_cast<int64_t>(num_sms) * 8);
@@ -774,32 +802,36 @@ cudaError_t launch_gemm_tn_acc_f32(const void* A, int64_t lda, const void* B, in
                                    int64_t K, int32_t M, int32_t N, float* c, int64_t ldc,
                                    int num_sms, cudaStream_t stream, LaunchInfo* info) {
   if (K == 0 || M == 0 || N == 0) return cudaSuccess;
-  // MN-major boxes: 64 columns (the contiguous dimension) x kBK rows
-  CUtensorMap ta, tb;
-  if (!make_map(&ta, A, K, M, lda, kBK) || !make_map(&tb, B, K, N, ldb, kBK))
-    return cudaErrorInvalidValue;
+  CUtensorMap tc_map;
+  if (!make_map_f32_box32(&tc_map, c, M, N, ldc)) return cudaErrorInvalidValue;
   LmParams p{};
   p.n_rows = M;
-  p.H = static_cast<int32_t>(K);
   p.V = N;
   p.n_vt = (N + kBN - 1) / kBN;
-  {
-    const char* g = std::getenv("COPRIS_LMHEAD_GROUP");
-    p.group = g ? std::max(1, std::atoi(g)) : 16;
-  }
+  // raster: every H tile of one vocab pair before the next (group 1), so the
+  // 16 concurrent users of a dlogits slice share one DRAM read; the hidden
+  // block is kept at evict_last (policy bit 1) and re-read from L2
+  const char* g = std::getenv("COPRIS_DW_GROUP");
+  p.group = g ? std::max(1, std::atoi(g)) : 1;
+  const char* pol = std::getenv("COPRIS_DW_POLICY");
+  p.a_evict_first = pol ? std::atoi(pol) : 2;
   p.c_out = c;
   p.ldc = ldc;
   p.n_split = 1;
+  // the token reduction runs in launches of <= kchunk rows, in order, so the
+  // hidden block of one launch (kchunk x H bf16) stays L2-resident
+  const char* kc = std::getenv("COPRIS_DW_KCHUNK");
+  const int64_t kchunk = kc ? std::max<int64_t>(kBK, std::atoll(kc) / kBK * kBK) : 8192;
   cudaError_t e = cudaFuncSetAttribute(lmhead_fwd_pair_kernel<2>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(kPSmemBytes));
+                                       static_cast<int>(kPSmemBytesDw));
   if (e != cudaSuccess) return e;
   const int64_t units = (static_cast<int64_t>(M) + 255) / 256 * p.n_vt;
   const int grid = static_cast<int>(std::min<int64_t>(2 * units, num_sms & ~1));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = kPSmemBytes;
+  cfg.dynamicSmemBytes = kPSmemBytesDw;
   cfg.stream = stream;
   cudaLaunchAttribute attr_cl[1];
   attr_cl[0].id = cudaLaunchAttributeClusterDimension;
@@ -808,9 +840,19 @@ cudaError_t launch_gemm_tn_acc_f32(const void* A, int64_t lda, const void* B, in
   attr_cl[0].val.clusterDim.z = 1;
   cfg.attrs = attr_cl;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, lmhead_fwd_pair_kernel<2>, ta, tb, p);
+  for (int64_t k0 = 0; k0 < K; k0 += kchunk) {
+    const int64_t kn = std::min(kchunk, K - k0);
+    // MN-major boxes: 64 columns (the contiguous dimension) x kBK rows
+    CUtensorMap ta, tb;
+    if (!make_map(&ta, static_cast<const __nv_bfloat16*>(A) + k0 * lda, kn, M, lda, kBK) ||
+        !make_map(&tb, static_cast<const __nv_bfloat16*>(B) + k0 * ldb, kn, N, ldb, kBK))
+      return cudaErrorInvalidValue;
+    p.H = static_cast<int32_t>(kn);
+    e = cudaLaunchKernelEx(&cfg, lmhead_fwd_pair_kernel<2>, ta, tb, tc_map, p);
+    if (e != cudaSuccess) return e;
+  }
   if (info) *info = LaunchInfo{num_sms, 2, grid, "lmhead_fwd_pair_kernel<dW>"};
-  return e != cudaSuccess ? e : cudaGetLastError();
+  return cudaGetLastError();
 }
 
 cudaError_t launch_lse_merge(const float* partials, int32_t n_vt, const void* logits, int64_t ld,

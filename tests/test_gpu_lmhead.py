@@ -237,6 +237,26 @@ def test_lmhead_dweight_tcgen05(ctx, T, H, V):
     assert torch.equal(again.view(torch.int32), out.view(torch.int32))
 
 
+def test_lmhead_dweight_token_chunks(ctx, monkeypatch):
+    """The token reduction in several ordered launches (COPRIS_DW_KCHUNK): the
+    same bound plus one fp32 rounding of dW per launch, bitwise on a rerun."""
+    monkeypatch.setenv("COPRIS_DW_KCHUNK", "128")
+    T, H, V = 300, 256, 1000
+    g = torch.Generator(device="cuda").manual_seed(5)
+    dl = (torch.randn((T, V), device="cuda", generator=g) * 1e-3).to(torch.bfloat16)
+    x = torch.randn((T, H), device="cuda", generator=g).to(torch.bfloat16)
+    dw0 = torch.randn((V, H), device="cuda", generator=g)
+    out = ctx.lmhead_dweight(dl, x, out=dw0.clone())
+    torch.cuda.synchronize()
+    ref = dw0.double() + dl.double().t() @ x.double()
+    bound = dl.double().abs().t() @ x.double().abs()
+    tol = (T + 2) * 2.0 ** -23 * bound + 3 * 2.0 ** -23 * (dw0.double().abs() + bound) + 1e-30
+    err = (out.double() - ref).abs()
+    assert bool((err <= tol).all()), float((err - tol).max())
+    again = ctx.lmhead_dweight(dl, x, out=dw0.clone())
+    assert torch.equal(again.view(torch.int32), out.view(torch.int32))
+
+
 def test_lmhead_dweight_errors(ctx):
     dl = torch.zeros((8, 64), dtype=torch.bfloat16, device="cuda")
     x = torch.zeros((8, 64), dtype=torch.bfloat16, device="cuda")
