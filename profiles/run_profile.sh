@@ -21,3 +21,5 @@ ncu --set full --clock-control none --import-source on -k regex:"bwd_kernel|fuse
     python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --chunk-rows 8192 --unfused > $OUT/prof_unfused.log 2>&1
 COPRIS_LMHEAD_GROUP=16 ncu --set full --clock-control none --import-source on -k regex:lmhead_fwd_pair -c 1 \
     -o $OUT/prof_lmhead -f python scripts/bench_lmhead.py 4096 > $OUT/prof_lmhead.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:lmhead_fwd_pair -c 1 \
+    -o $OUT/prof_lmhead_dw -f python scripts/bench_lmhead_dw.py 4096 > $OUT/prof_lmhead_dw.log 2>&1

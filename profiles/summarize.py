@@ -121,6 +121,9 @@ def main():
                                 "source": f"profiles/{tag}_ncu_{k}.txt (V = 32,000, 16384-row launch)"}
     if os.path.exists(os.path.join(src, "prof_lmhead.ncu-rep")):
         ncu_summary(os.path.join(src, "prof_lmhead.ncu-rep"), os.path.join(HERE, f"{tag}_ncu"), 4096)
+    if os.path.exists(os.path.join(src, "prof_lmhead_dw.ncu-rep")):
+        # LM-head backward dW (MN-major operands), T = 4096 tokens
+        ncu_summary(os.path.join(src, "prof_lmhead_dw.ncu-rep"), os.path.join(HERE, f"{tag}_ncu_dw"), 4096)
     if traffic:
         with open(os.path.join(HERE, "ncu_traffic.json"), "w") as f:
             json.dump(traffic, f, indent=1)

@@ -1,6 +1,7 @@
 """LM-head backward weight gradient dW [V x H] += dlogits^T @ hidden:
 copris_lmhead_dweight (tcgen05 CTA pair, MN-major operands) vs cuBLAS addmm
-(fp32 out). Usage: python scripts/bench_lmhead_dw.py [T ...] (H=4096, V=151,936)."""
+(fp32 out); --dhidden also times dhidden = dlogits @ W (copris_lmhead_dhidden vs
+torch.mm). Usage: python scripts/bench_lmhead_dw.py [--dhidden] [T ...] (H=4096, V=151,936)."""
 import sys
 
 import torch
@@ -23,7 +24,8 @@ def timeit(fn, iters=10, warm=3):
 
 
 def main():
-    Ts = [int(a) for a in sys.argv[1:]] or [4096, 8192]
+    flags = [a for a in sys.argv[1:] if a.startswith("--")]
+    Ts = [int(a) for a in sys.argv[1:] if not a.startswith("--")] or [4096, 8192]
     H, V = 4096, 151936
     ctx = Copris(0)
     g = torch.Generator(device="cuda").manual_seed(0)
@@ -49,6 +51,15 @@ def main():
               f"max |ref| {float(dW2.abs().max()):.3e}")
         dW.zero_()
         dW2.zero_()
+        if "--dhidden" in flags:
+            w = (torch.randn((V, H), device="cuda", generator=g) * 0.02).to(torch.bfloat16)
+            wt = torch.nn.functional.pad(w.t().contiguous(), (0, w_ld - V))[:, :V]
+            dh = torch.empty((T, H), dtype=torch.bfloat16, device="cuda")
+            t_dh = timeit(lambda: ctx.lmhead_dhidden(dl, wt, out=dh))
+            t_dhc = timeit(lambda: torch.mm(dl, w, out=dh))
+            print(f"T={T} dhidden tcgen05 pair    {t_dh:.3f} ms  {flops / t_dh / 1e9:.0f} TFLOP/s")
+            print(f"T={T} dhidden cuBLAS mm       {t_dhc:.3f} ms  {flops / t_dhc / 1e9:.0f} TFLOP/s")
+            del w, wt, dh
 
 
 if __name__ == "__main__":
