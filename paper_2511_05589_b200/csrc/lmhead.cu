@@ -293,7 +293,7 @@ constexpr uint32_t kMnBoxBytes = kBK * 128;  // MN-major box: kBK K-rows x 64 el
 // weight gradient dW [V x H] += dlogits [T x V]^T * hidden [T x H]. Each stage
 // holds two 64-wide MN boxes per operand (LBO = one box); the fp32 epilogue
 // adds the tile into C (each tile is owned by exactly one unit: no split).
-template <int EPI>
+template <int EPI, bool MC = false>
 __global__ void __launch_bounds__(kThreads, 1)
     lmhead_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_x,
                            const __grid_constant__ CUtensorMap tm_w,
@@ -315,11 +315,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = ptx::cluster_ctarank();
-  const bool leader = rank == 0;
+  // MC: a 4-CTA cluster of two pairs on vertically adjacent tiles (same vocab /
+  // N tile, consecutive token pairs); each B half is loaded once by pair 0 and
+  // multicast to both pairs. prank = rank in the pair, lrank = pair leader.
+  const uint32_t prank = rank & 1u, pair = MC ? rank >> 1 : 0u, lrank = rank & ~1u;
+  const bool leader = prank == 0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kPStages; ++s) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full_bar(s)));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(empty_bar(s)));
+      // MC: both pair leaders release a slot (B was multicast into both pairs)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(empty_bar(s)), "n"(MC ? 2 : 1));
     }
     for (int b = 0; b < 2; ++b) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tfull_bar(b)));
@@ -339,11 +344,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nk = (P.H + kBK - 1) / kBK;
   const int64_t n_mpair = (P.n_rows + 255) / 256;
   const int32_t n_split = EPI == 1 ? P.n_split : 1;
-  const int64_t n_units = n_mpair * P.n_vt * n_split;
+  const int64_t n_mu = MC ? (n_mpair + 1) / 2 : n_mpair;  // token pairs (MC: pairs of pairs)
+  const int64_t n_units = n_mu * P.n_vt * n_split;
   // k-block range of a unit's split
   auto k_range = [&](int64_t u, int& kb0, int& kb1) {
     if (EPI == 1) {
-      const int64_t sp = u / (n_mpair * P.n_vt);
+      const int64_t sp = u / (n_mu * P.n_vt);
       kb0 = static_cast<int>(sp * P.k_per_split);
       kb1 = min(nk, kb0 + P.k_per_split);
     } else {
@@ -354,16 +360,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   // Grouped raster: units sweep every vocab tile for a group of `grp` token
   // pairs before moving on, so the group's hidden rows stay L2-resident while
   // each weight tile is shared by the group's concurrently running clusters.
-  const int64_t grp = P.group < n_mpair ? static_cast<int64_t>(P.group) : n_mpair;
+  const int64_t grp = P.group < n_mu ? static_cast<int64_t>(P.group) : n_mu;
   auto unit_coords = [&](int64_t u, int64_t& mp, int32_t& vt) {
-    if (EPI == 1) u %= n_mpair * P.n_vt;  // split-major: the same raster in every split
+    if (EPI == 1) u %= n_mu * P.n_vt;  // split-major: the same raster in every split
     const int64_t per = grp * P.n_vt;
     const int64_t g = u / per, w = u % per;
-    const int64_t gsz = grp < n_mpair - g * grp ? grp : n_mpair - g * grp;  // last group may be short
+    const int64_t gsz = grp < n_mu - g * grp ? grp : n_mu - g * grp;  // last group may be short
     vt = static_cast<int32_t>(w / gsz);
     mp = g * grp + w % gsz;
+    if (MC) mp = 2 * mp + pair;  // may be one past the last pair: rows masked, TMA zero-fills
   };
-  const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int64_t cid = blockIdx.x >> (MC ? 2 : 1), ncl = gridDim.x >> (MC ? 2 : 1);
   if (warp == 0) {
     if (lane == 0) {
       // ===== TMA producer (both CTAs) =====
@@ -384,13 +391,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         int64_t mp;
         int32_t vt;
         unit_coords(u, mp, vt);
-        const int32_t m0 = static_cast<int32_t>(mp) * 256 + 128 * rank;
-        const int32_t n0 = vt * kBN + 128 * rank;
+        const int32_t m0 = static_cast<int32_t>(mp) * 256 + 128 * prank;
+        const int32_t n0 = vt * kBN + 128 * prank;
         int kb0, kb1;
         k_range(u, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait_u32(empty_bar(stage), phase ^ 1u);
-          const uint32_t fb = ptx::mapa(full_bar(stage), 0);
+          const uint32_t fb = ptx::mapa(full_bar(stage), lrank);
           if (leader) ptx::mbar_arrive_expect_tx_u32(full_bar(stage), 2 * kPStageBytes);
           if constexpr (EPI == 2) {
 #pragma unroll
@@ -400,6 +407,11 @@ __global__ void __launch_bounds__(kThreads, 1)
               tc::tma_load_2d_pair(sB + stage * kPBBytes + j * kMnBoxBytes, &tm_w, fb, n0 + 64 * j,
                                    kb * kBK, pol_w);
             }
+          } else if constexpr (MC) {
+            tc::tma_load_2d_pair(sA + stage * kPABytes, &tm_x, fb, kb * kBK, m0, pol_x);
+            if (pair == 0)
+              tc::tma_load_2d_pair_mc(sB + stage * kPBBytes, &tm_w, fb, kb * kBK, n0,
+                                      static_cast<uint16_t>(0x5u << prank), pol_w);
           } else {
             tc::tma_load_2d_pair(sA + stage * kPABytes, &tm_x, fb, kb * kBK, m0, pol_x);
             tc::tma_load_2d_pair(sB + stage * kPBBytes, &tm_w, fb, kb * kBK, n0, pol_w);
@@ -439,13 +451,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                                          : tc::smem_desc_sw128(b + 32 * k);
             tc::mma_bf16_ss_pair(d, da, db, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
           }
-          tc::commit_pair(empty_bar(stage), 0x3);
+          tc::commit_pair(empty_bar(stage), MC ? 0xF : 0x3);
           if (++stage == kPStages) {
             stage = 0;
             phase ^= 1u;
           }
         }
-        tc::commit_pair(tfull_bar(acc), 0x3);
+        tc::commit_pair(tfull_bar(acc), static_cast<uint16_t>(0x3u << (2 * pair)));
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1u;
@@ -465,7 +477,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int64_t mp;
       int32_t vt;
       unit_coords(u, mp, vt);
-      const int64_t row = mp * 256 + 128 * rank + r_in;
+      const int64_t row = mp * 256 + 128 * prank + r_in;
       const int32_t n0 = vt * kBN;
       const bool row_ok = row < P.n_rows;
       const int32_t ncols = min(kBN, P.V - n0);
@@ -478,7 +490,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // its 32 rows x 32 columns in a swizzled box (16-byte chunk j of row
         // r at j ^ (r & 7): conflict-free) and one lane issues the bulk add;
         // two boxes per warp alternate so staging overlaps the adds in flight
-        const int32_t row0 = static_cast<int32_t>(mp * 256 + 128 * rank + sub * 32);
+        const int32_t row0 = static_cast<int32_t>(mp * 256 + 128 * prank + sub * 32);
 #pragma unroll 1
         for (int c = 0; c < kBN; c += 32) {
           uint32_t r[32];
@@ -502,10 +514,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tc::fence_before_sync();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive_remote(ptx::mapa(tempty_bar(acc), 0));
+        if (lane == 0) ptx::mbar_arrive_remote(ptx::mapa(tempty_bar(acc), lrank));
       } else if constexpr (EPI == 1) {
         // fp32 tile row straight from TMEM to this split's partial matrix
-        const int64_t sp = u / (n_mpair * P.n_vt);
+        const int64_t sp = u / (n_mu * P.n_vt);
         float* out = P.c_out + sp * P.split_stride + row * P.ldc + n0;
 #pragma unroll 1
         for (int c = 0; c < kBN; c += 32) {
@@ -527,13 +539,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tc::fence_before_sync();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive_remote(ptx::mapa(tempty_bar(acc), 0));
+        if (lane == 0) ptx::mbar_arrive_remote(ptx::mapa(tempty_bar(acc), lrank));
       } else {
       const int32_t yrel = row_ok ? P.target[row] - n0 : -1;
       const float2 part = epilogue_row(taddr, row, row_ok, n0, ncols, yrel, P, st_pol);
       tc::fence_before_sync();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive_remote(ptx::mapa(tempty_bar(acc), 0));
+      if (lane == 0) ptx::mbar_arrive_remote(ptx::mapa(tempty_bar(acc), lrank));
       if (row_ok) P.partials[row * P.n_vt + vt] = part;
       }
       if (++acc == 2) {
@@ -770,12 +782,17 @@ cudaError_t launch_gemm_nt_bf16(const void* A, int64_t lda, const void* B, int64
   p.n_split = n_split;
   p.k_per_split = (nk + n_split - 1) / n_split;
   p.n_split = (nk + p.k_per_split - 1) / p.k_per_split;  // no empty split
-  cudaError_t e = cudaFuncSetAttribute(lmhead_fwd_pair_kernel<1>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+  // COPRIS_GEMM_MC=1: 4-CTA clusters, W^T halves multicast to two token pairs
+  const char* mc_env = std::getenv("COPRIS_GEMM_MC");
+  const bool mc = mc_env && std::atoi(mc_env) != 0;
+  auto kern = mc ? lmhead_fwd_pair_kernel<1, true> : lmhead_fwd_pair_kernel<1, false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(kPSmemBytes));
   if (e != cudaSuccess) return e;
-  const int64_t units = (M + 255) / 256 * p.n_vt * p.n_split;
-  const int grid = static_cast<int>(std::min<int64_t>(2 * units, num_sms & ~1));
+  const int cl = mc ? 4 : 2;
+  const int64_t n_mu = mc ? ((M + 255) / 256 + 1) / 2 : (M + 255) / 256;
+  const int64_t units = n_mu * p.n_vt * p.n_split;
+  const int grid = static_cast<int>(std::min<int64_t>(cl * units, num_sms & ~(cl - 1)));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
@@ -783,18 +800,27 @@ cudaError_t launch_gemm_nt_bf16(const void* A, int64_t lda, const void* B, int64
   cfg.stream = stream;
   cudaLaunchAttribute attr_cl[1];
   attr_cl[0].id = cudaLaunchAttributeClusterDimension;
-  attr_cl[0].val.clusterDim.x = 2;
+  attr_cl[0].val.clusterDim.x = cl;
   attr_cl[0].val.clusterDim.y = 1;
   attr_cl[0].val.clusterDim.z = 1;
   cfg.attrs = attr_cl;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, lmhead_fwd_pair_kernel<1>, ta, tb, tb, p);
+  if (mc) {
+    // 4-CTA clusters do not tile every GPC: size the persistent grid to the
+    // clusters that are co-resident
+    int max_cl = 0;
+    if (cudaOccupancyMaxActiveClusters(&max_cl, kern, &cfg) == cudaSuccess && max_cl > 0)
+      cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(cl * units, cl * max_cl)));
+  }
+  e = cudaLaunchKernelEx(&cfg, kern, ta, tb, tb, p);
   if (e != cudaSuccess) return e;
   const int64_t quads = M * (N / 4);
   const int64_t blocks = std::min<int64_t>((quads + 255) / 256, static_cast<int64_t>(num_sms) * 8);
   splitk_sum_bf16_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(
       work, p.split_stride, p.n_split, M, N, N, static_cast<__nv_bfloat16*>(out), ldo);
-  if (info) *info = LaunchInfo{num_sms, 2, grid, "lmhead_fwd_pair_kernel<gemm>"};
+  if (info)
+    *info = LaunchInfo{num_sms, cl, static_cast<int>(cfg.gridDim.x),
+                       mc ? "lmhead_fwd_pair_kernel<gemm,mc>" : "lmhead_fwd_pair_kernel<gemm>"};
   return cudaGetLastError();
 }
 

@@ -138,6 +138,19 @@ __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap
       : "memory");
 }
 
+// The same, multicast to the CTAs in `mask` (same shared offset in each);
+// with the peer bit of `bar` clear, every destination's bytes complete on the
+// mbarrier of that destination's pair leader.
+__device__ __forceinline__ void tma_load_2d_pair_mc(uint32_t dst, const CUtensorMap* map,
+                                                    uint32_t bar, int32_t c0, int32_t c1,
+                                                    uint16_t mask, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster.L2::cache_hint [%0], [%1, {%4, %5}], [%2], %3, %6;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "h"(mask), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
+}
+
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc_pair(uint32_t slot_smem) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(slot_smem),

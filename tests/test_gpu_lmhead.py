@@ -189,7 +189,8 @@ def test_lmhead_token_out_of_vocabulary(ctx):
 
 
 @pytest.mark.parametrize("T,H,V", [(300, 512, 4096), (256, 256, 1000), (1024, 4096, 151936)])
-def test_lmhead_dhidden_tcgen05(ctx, T, H, V):
+@pytest.mark.parametrize("mc", [False, True])
+def test_lmhead_dhidden_tcgen05(ctx, T, H, V, mc, monkeypatch):
     """LM-head backward dhidden = dlogits @ W on the CTA-pair tcgen05 kernel
     (B = W^T, split-K with a fixed-order sum): vs the fp32 product within bf16
     rounding of the output, and bitwise on a rerun."""
@@ -208,6 +209,16 @@ def test_lmhead_dhidden_tcgen05(ctx, T, H, V):
     assert bool((err <= tol).all()), float((err - tol).max())
     again = ctx.lmhead_dhidden(dl, wt)
     assert torch.equal(again.view(torch.int16), out.view(torch.int16))
+    if mc:
+        small_ref = ctx.lmhead_dhidden(dl[:1], wt)
+        # 4-CTA clusters with W^T multicast to two token pairs: same tiles, same
+        # k order -> bitwise the 2-CTA result (odd pair counts: a masked tail pair)
+        monkeypatch.setenv("COPRIS_GEMM_MC", "1")
+        multi = ctx.lmhead_dhidden(dl, wt)
+        assert ctx.last_launch()["cluster"] == 4
+        assert torch.equal(multi.view(torch.int16), out.view(torch.int16))
+        small = ctx.lmhead_dhidden(dl[:1], wt)
+        assert torch.equal(small.view(torch.int16), small_ref.view(torch.int16))
 
 
 @pytest.mark.parametrize("T,H,V", [(300, 512, 4096), (257, 192, 1000), (64, 520, 300), (1, 64, 256),
