@@ -252,6 +252,23 @@ COPRIS_API int copris_is_loss_bwd(copris_ctx* ctx, const copris_loss_batch* batc
 COPRIS_API int copris_loss_reduce(copris_ctx* ctx, const double* obj, const uint8_t* flags, int64_t n_tok,
                        double* out4, void* stream);
 
+/* ---- Sharded batches: the one collective --------------------
+ * Each rank runs the kernels on its whole prompt groups with the GLOBAL token
+ * count, reduces its own out4, then SUM-allreduces the four fp64 scalars:
+ *   copris_allreduce_scalars(comm, d_out4, stream); loss = -out4[0] / T_global.
+ * `comm` is an ncclComm_t (the caller's own, or one made by the helpers below:
+ * one process driving several GPUs -> copris_nccl_comm_init_all, one process
+ * per GPU -> copris_nccl_unique_id on rank 0, broadcast the 128 bytes, then
+ * copris_nccl_comm_init_rank on every rank). NCCL is loaded at run time
+ * (libnccl.so.2, the copy already in the process if any); COPRIS_E_CUDA
+ * carries NCCL's message. dlogits never leave the rank. */
+COPRIS_API int copris_allreduce_scalars(void* comm, double* d_buf4, void* stream);
+COPRIS_API int copris_nccl_comm_init_all(int32_t n_dev, const int32_t* devices, void** out_comms);
+COPRIS_API int copris_nccl_unique_id(uint8_t out_id[128]);
+COPRIS_API int copris_nccl_comm_init_rank(int32_t device, int32_t n_ranks, const uint8_t id[128],
+                                          int32_t rank, void** out_comm);
+COPRIS_API int copris_nccl_comm_destroy(void* comm);
+
 /* ---- Host-buffer drop-in for grpo_step_loss (grpo.hpp:117-185) -------------
  * The reference call takes host data and returns a host gradient. This entry
  * takes HOST arrays (page-locked memory lets the copies overlap compute),

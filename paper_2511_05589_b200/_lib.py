@@ -85,6 +85,11 @@ _SIGS = {
     "copris_lse_merge": ([P, P, I32, P, I64, P, I64, I32, P, P, P], C.c_int),
     "copris_lmhead_dhidden_splits": ([P, I64, I32], I32),
     "copris_lmhead_dhidden": ([P, P, I64, P, I64, I64, I32, I32, P, I64, P, P], C.c_int),
+    "copris_allreduce_scalars": ([P, P, P], C.c_int),
+    "copris_nccl_comm_init_all": ([I32, P, P], C.c_int),
+    "copris_nccl_unique_id": ([P], C.c_int),
+    "copris_nccl_comm_init_rank": ([I32, I32, P, I32, P], C.c_int),
+    "copris_nccl_comm_destroy": ([P], C.c_int),
     "copris_lmhead_dweight": ([P, P, I64, P, I64, I64, I32, I32, P, I64, P], C.c_int),
     "copris_expand_segments": ([P, P, P, I64, P, P], C.c_int),
     "copris_behaviour_concat": ([P, P, U32, P, P, I32, I32, I64, P, P, P], C.c_int),

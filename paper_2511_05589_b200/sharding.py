@@ -69,3 +69,72 @@ def allreduce_scalars(out4, group=None):
 def loss_from_scalars(out4, total_tokens: int) -> float:
     """grpo.hpp:183: loss = -objective * (1 / T)."""
     return -float(out4[0]) * (1.0 / float(total_tokens))
+
+
+class NcclScalars:
+    """The C-ABI form of the collective (copris_allreduce_scalars), for callers
+    that drive NCCL themselves instead of through torch.distributed — the C++
+    trainer's path. ``NcclScalars.init_all([0, 1, ...])`` builds one
+    communicator per GPU in this process (ncclCommInitAll);
+    ``NcclScalars(device, n_ranks, uid, rank)`` joins a multi-process group
+    whose 128-byte id came from ``NcclScalars.unique_id()`` on rank 0."""
+
+    def __init__(self, device: int = None, n_ranks: int = None, uid: bytes = None,
+                 rank: int = None, *, _comm=None):
+        import ctypes as C
+        from . import _lib as L
+        from .grpo import _raise
+        self._lib, self._raise = L.load(), _raise
+        if _comm is not None:
+            self.comm = _comm
+            return
+        h = C.c_void_p()
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        rc = self._lib.copris_nccl_comm_init_rank(device, n_ranks, buf, rank, C.byref(h))
+        if rc:
+            self._raise(rc, self._lib)
+        self.comm = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        import ctypes as C
+        from . import _lib as L
+        from .grpo import _raise
+        lib = L.load()
+        buf = (C.c_uint8 * 128)()
+        rc = lib.copris_nccl_unique_id(buf)
+        if rc:
+            _raise(rc, lib)
+        return bytes(buf)
+
+    @classmethod
+    def init_all(cls, devices) -> list["NcclScalars"]:
+        import ctypes as C
+        from . import _lib as L
+        from .grpo import _raise
+        lib = L.load()
+        n = len(devices)
+        devs = (C.c_int32 * n)(*devices)
+        comms = (C.c_void_p * n)()
+        rc = lib.copris_nccl_comm_init_all(n, devs, comms)
+        if rc:
+            _raise(rc, lib)
+        return [cls(_comm=C.c_void_p(comms[i])) for i in range(n)]
+
+    def allreduce(self, out4, stream=None):
+        """SUM-allreduce of a device f64[4] (in place) on `stream` (default: current)."""
+        import ctypes as C
+        import torch
+        s = stream if stream is not None else torch.cuda.current_stream(out4.device)
+        rc = self._lib.copris_allreduce_scalars(self.comm, C.c_void_p(out4.data_ptr()),
+                                                C.c_void_p(s.cuda_stream))
+        if rc:
+            self._raise(rc, self._lib)
+        return out4
+
+    def close(self):
+        if self.comm:
+            rc = self._lib.copris_nccl_comm_destroy(self.comm)
+            self.comm = None
+            if rc:
+                self._raise(rc, self._lib)
