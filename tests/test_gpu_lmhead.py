@@ -268,6 +268,26 @@ def test_lmhead_dweight_token_chunks(ctx, monkeypatch):
     assert torch.equal(again.view(torch.int32), out.view(torch.int32))
 
 
+def test_lmhead_dweight_strided(ctx):
+    """Row strides larger than the logical widths on every operand: dlogits and
+    hidden as column slices of wider buffers, dW rows padded; the padding is
+    neither read into the product nor written."""
+    T, H, V = 200, 264, 1000
+    g = torch.Generator(device="cuda").manual_seed(9)
+    dl_full = (torch.randn((T, V + 24), device="cuda", generator=g) * 1e-3).to(torch.bfloat16)
+    x_full = torch.randn((T, H + 8), device="cuda", generator=g).to(torch.bfloat16)
+    dl, x = dl_full[:, :V], x_full[:, :H]
+    dw_full = torch.full((V, H + 12), 7.0, device="cuda")
+    dw = dw_full[:, :H]
+    dw.zero_()
+    ctx.lmhead_dweight(dl, x, out=dw)
+    torch.cuda.synchronize()
+    ref = dl.double().t() @ x.double()
+    bound = dl.double().abs().t() @ x.double().abs()
+    assert bool(((dw.double() - ref).abs() <= (T + 2) * 2.0 ** -23 * bound + 1e-30).all())
+    assert bool((dw_full[:, H:] == 7.0).all())
+
+
 def test_lmhead_dweight_errors(ctx):
     dl = torch.zeros((8, 64), dtype=torch.bfloat16, device="cuda")
     x = torch.zeros((8, 64), dtype=torch.bfloat16, device="cuda")
