@@ -283,6 +283,8 @@ constexpr int kPStagesDw = 6;
 constexpr uint32_t kDwBoxBytes = 32 * 32 * 4;
 constexpr size_t kPSmemBytesDw = 1024 + kPStagesDw * kPStageBytes + 1024 + 8 * kDwBoxBytes;
 static_assert(kPSmemBytesDw <= 232448, "dW smem");
+constexpr int kPStagesWide = 4;  // 48 KB stages (A 16 KB + two B halves)
+constexpr size_t kPSmemBytesWide = 1024 + kPStagesWide * (kPABytes + 2 * kPBBytes) + 256;
 constexpr uint32_t kMnBoxBytes = kBK * 128;  // MN-major box: kBK K-rows x 64 elements
 
 // EPI 0: logits + LSE partials (the forward). EPI 1: C = A B^T as fp32 split-K
@@ -293,17 +295,25 @@ constexpr uint32_t kMnBoxBytes = kBK * 128;  // MN-major box: kBK K-rows x 64 el
 // weight gradient dW [V x H] += dlogits [T x V]^T * hidden [T x H]. Each stage
 // holds two 64-wide MN boxes per operand (LBO = one box); the fp32 epilogue
 // adds the tile into C (each tile is owned by exactly one unit: no split).
-template <int EPI, bool MC = false>
+template <int EPI, bool MC = false, bool WIDE = false>
 __global__ void __launch_bounds__(kThreads, 1)
     lmhead_fwd_pair_kernel(const __grid_constant__ CUtensorMap tm_x,
                            const __grid_constant__ CUtensorMap tm_w,
                            const __grid_constant__ CUtensorMap tm_c, const LmParams P) {
-  constexpr int kPStages = EPI == 2 ? kPStagesDw : ::copris_b200::kPStages;
+  // WIDE (EPI 1 only): a 256 x 512 tile per pair, two N = 256 MMAs per k-step
+  // into all 512 TMEM columns (no accumulator double buffer: with a 151,936-long
+  // reduction the epilogue is ~0.3% of a unit); each A tile feeds twice the MMA
+  // work, so the operand traffic per flop drops by a quarter
+  static_assert(!WIDE || (EPI == 1 && !MC), "WIDE is the plain-GEMM mode only");
+  constexpr int kNT = WIDE ? 2 * kBN : kBN;           // N columns per unit
+  constexpr int kBStage = (kNT / kBN) * kPBBytes;     // this CTA's B bytes per stage
+  constexpr int kStageB = kPABytes + kBStage;
+  constexpr int kPStages = EPI == 2 ? kPStagesDw : WIDE ? kPStagesWide : ::copris_b200::kPStages;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
   const uint32_t sA = base;
   const uint32_t sB = base + kPStages * kPABytes;
-  const uint32_t bars = base + kPStages * kPStageBytes;
+  const uint32_t bars = base + kPStages * kStageB;
   auto full_bar = [&](int s) { return bars + 8u * s; };
   auto empty_bar = [&](int s) { return bars + 8u * (kPStages + s); };
   auto tfull_bar = [&](int b) { return bars + 8u * (2 * kPStages + b); };
@@ -392,29 +402,32 @@ __global__ void __launch_bounds__(kThreads, 1)
         int32_t vt;
         unit_coords(u, mp, vt);
         const int32_t m0 = static_cast<int32_t>(mp) * 256 + 128 * prank;
-        const int32_t n0 = vt * kBN + 128 * prank;
+        const int32_t n0 = vt * kNT + 128 * prank;
         int kb0, kb1;
         k_range(u, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait_u32(empty_bar(stage), phase ^ 1u);
           const uint32_t fb = ptx::mapa(full_bar(stage), lrank);
-          if (leader) ptx::mbar_arrive_expect_tx_u32(full_bar(stage), 2 * kPStageBytes);
+          if (leader) ptx::mbar_arrive_expect_tx_u32(full_bar(stage), 2 * kStageB);
           if constexpr (EPI == 2) {
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
               tc::tma_load_2d_pair(sA + stage * kPABytes + j * kMnBoxBytes, &tm_x, fb, m0 + 64 * j,
                                    kb * kBK, pol_x);
-              tc::tma_load_2d_pair(sB + stage * kPBBytes + j * kMnBoxBytes, &tm_w, fb, n0 + 64 * j,
+              tc::tma_load_2d_pair(sB + stage * kBStage + j * kMnBoxBytes, &tm_w, fb, n0 + 64 * j,
                                    kb * kBK, pol_w);
             }
           } else if constexpr (MC) {
             tc::tma_load_2d_pair(sA + stage * kPABytes, &tm_x, fb, kb * kBK, m0, pol_x);
             if (pair == 0)
-              tc::tma_load_2d_pair_mc(sB + stage * kPBBytes, &tm_w, fb, kb * kBK, n0,
+              tc::tma_load_2d_pair_mc(sB + stage * kBStage, &tm_w, fb, kb * kBK, n0,
                                       static_cast<uint16_t>(0x5u << prank), pol_w);
           } else {
             tc::tma_load_2d_pair(sA + stage * kPABytes, &tm_x, fb, kb * kBK, m0, pol_x);
-            tc::tma_load_2d_pair(sB + stage * kPBBytes, &tm_w, fb, kb * kBK, n0, pol_w);
+            tc::tma_load_2d_pair(sB + stage * kBStage, &tm_w, fb, kb * kBK, n0, pol_w);
+            if constexpr (WIDE)
+              tc::tma_load_2d_pair(sB + stage * kBStage + kPBBytes, &tm_w, fb, kb * kBK, n0 + kBN,
+                                   pol_w);
           }
           if (++stage == kPStages) {
             stage = 0;
@@ -434,13 +447,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int64_t u = cid; u < n_units; u += ncl) {
         ptx::mbar_wait_u32(tempty_bar(acc), acc_phase ^ 1u);
         tc::fence_after_sync();
-        const uint32_t d = tmem_base + static_cast<uint32_t>(acc * kBN);
+        const uint32_t d = tmem_base + static_cast<uint32_t>(WIDE ? 0 : acc * kBN);
         int kb0, kb1;
         k_range(u, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait_u32(full_bar(stage), phase);
           tc::fence_after_sync();
-          const uint32_t a = sA + stage * kPABytes, b = sB + stage * kPBBytes;
+          const uint32_t a = sA + stage * kPABytes, b = sB + stage * kBStage;
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k) {
             // K-major: 16 elements = 32 bytes along the swizzled row;
@@ -450,6 +463,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t db = EPI == 2 ? tc::smem_desc_sw128_mn(b + 2048 * k, kMnBoxBytes)
                                          : tc::smem_desc_sw128(b + 32 * k);
             tc::mma_bf16_ss_pair(d, da, db, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+            if constexpr (WIDE)
+              tc::mma_bf16_ss_pair(d + kBN, da, tc::smem_desc_sw128(b + kPBBytes + 32 * k), idesc,
+                                   (kb != kb0 || k != 0) ? 1u : 0u);
           }
           tc::commit_pair(empty_bar(stage), MC ? 0xF : 0x3);
           if (++stage == kPStages) {
@@ -458,7 +474,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         tc::commit_pair(tfull_bar(acc), static_cast<uint16_t>(0x3u << (2 * pair)));
-        if (++acc == 2) {
+        if (WIDE) {
+          acc_phase ^= 1u;
+        } else if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1u;
         }
@@ -478,13 +496,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       int32_t vt;
       unit_coords(u, mp, vt);
       const int64_t row = mp * 256 + 128 * prank + r_in;
-      const int32_t n0 = vt * kBN;
+      const int32_t n0 = vt * kNT;
       const bool row_ok = row < P.n_rows;
-      const int32_t ncols = min(kBN, P.V - n0);
+      const int32_t ncols = min(kNT, P.V - n0);
       ptx::mbar_wait_u32(tfull_bar(acc), acc_phase);
       tc::fence_after_sync();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(sub * 32) << 16) +
-                             static_cast<uint32_t>(acc * kBN);
+                             static_cast<uint32_t>(WIDE ? 0 : acc * kBN);
       if constexpr (EPI == 2) {
         // C tile += the accumulator through TMA reduce-add: each warp stages
         // its 32 rows x 32 columns in a swizzled box (16-byte chunk j of row
@@ -520,7 +538,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int64_t sp = u / (n_mu * P.n_vt);
         float* out = P.c_out + sp * P.split_stride + row * P.ldc + n0;
 #pragma unroll 1
-        for (int c = 0; c < kBN; c += 32) {
+        for (int c = 0; c < kNT; c += 32) {
           uint32_t r[32];
           tc::tmem_ld_32x32b_x32(taddr + c, r);
           tc::tmem_wait_ld();
@@ -548,7 +566,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) ptx::mbar_arrive_remote(ptx::mapa(tempty_bar(acc), lrank));
       if (row_ok) P.partials[row * P.n_vt + vt] = part;
       }
-      if (++acc == 2) {
+      if (WIDE) {
+        acc_phase ^= 1u;
+      } else if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1u;
       }
@@ -744,10 +764,34 @@ cudaError_t launch_lmhead_fwd(const void* hidden, int64_t ld_h, const void* weig
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
+static bool gemm_wide() {
+  const char* w = std::getenv("COPRIS_GEMM_WIDE");
+  const char* mc = std::getenv("COPRIS_GEMM_MC");
+  // default on; COPRIS_GEMM_WIDE=0 selects the 256 x 256 tile
+  return !(w && std::atoi(w) == 0) && !(mc && std::atoi(mc) != 0);
+}
+
 int32_t gemm_nt_splits(int64_t M, int32_t N, int num_sms) {
   if (const char* e = std::getenv("COPRIS_GEMM_SPLITS")) return std::max(1, std::atoi(e));
-  const int64_t units = (M + 255) / 256 * ((N + kBN - 1) / kBN);
   const int64_t clusters = num_sms / 2;
+  if (gemm_wide()) {
+    // 256 x 512 tiles are few: pick the split count whose units fill the last
+    // wave of clusters best (ties: fewer splits, less partial traffic)
+    const int64_t base = (M + 255) / 256 * ((N + 2 * kBN - 1) / (2 * kBN));
+    int32_t best = 1;
+    double best_eff = -1.0;
+    for (int32_t s = 1; s <= 8; ++s) {
+      const int64_t u = base * s;
+      const int64_t rounds = (u + clusters - 1) / clusters;
+      const double eff = static_cast<double>(u) / static_cast<double>(rounds * clusters);
+      if (eff > best_eff + 1e-9) {
+        best_eff = eff;
+        best = s;
+      }
+    }
+    return best;
+  }
+  const int64_t units = (M + 255) / 256 * ((N + kBN - 1) / kBN);
   int64_t s = (4 * clusters + units - 1) / units;  // >= ~4 waves of cluster tiles
   if (s < 1) s = 1;
   if (s > 8) s = 8;
@@ -782,12 +826,19 @@ cudaError_t launch_gemm_nt_bf16(const void* A, int64_t lda, const void* B, int64
   p.n_split = n_split;
   p.k_per_split = (nk + n_split - 1) / n_split;
   p.n_split = (nk + p.k_per_split - 1) / p.k_per_split;  // no empty split
-  // COPRIS_GEMM_MC=1: 4-CTA clusters, W^T halves multicast to two token pairs
+  // default: 256 x 512 tiles per pair (two MMAs per k-step); COPRIS_GEMM_WIDE=0:
+  // 256 x 256 tiles; COPRIS_GEMM_MC=1: 256 x 256 tiles on 4-CTA clusters with the
+  // W^T halves multicast to two token pairs
   const char* mc_env = std::getenv("COPRIS_GEMM_MC");
   const bool mc = mc_env && std::atoi(mc_env) != 0;
-  auto kern = mc ? lmhead_fwd_pair_kernel<1, true> : lmhead_fwd_pair_kernel<1, false>;
+  const bool wide = gemm_wide();
+  auto kern = mc     ? lmhead_fwd_pair_kernel<1, true>
+              : wide ? lmhead_fwd_pair_kernel<1, false, true>
+                     : lmhead_fwd_pair_kernel<1, false>;
+  const size_t smem = wide ? kPSmemBytesWide : kPSmemBytes;
+  if (wide) p.n_vt = (N + 2 * kBN - 1) / (2 * kBN);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(kPSmemBytes));
+                                       static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   const int cl = mc ? 4 : 2;
   const int64_t n_mu = mc ? ((M + 255) / 256 + 1) / 2 : (M + 255) / 256;
@@ -796,7 +847,7 @@ cudaError_t launch_gemm_nt_bf16(const void* A, int64_t lda, const void* B, int64
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = kPSmemBytes;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr_cl[1];
   attr_cl[0].id = cudaLaunchAttributeClusterDimension;
@@ -820,7 +871,9 @@ cudaError_t launch_gemm_nt_bf16(const void* A, int64_t lda, const void* B, int64
       work, p.split_stride, p.n_split, M, N, N, static_cast<__nv_bfloat16*>(out), ldo);
   if (info)
     *info = LaunchInfo{num_sms, cl, static_cast<int>(cfg.gridDim.x),
-                       mc ? "lmhead_fwd_pair_kernel<gemm,mc>" : "lmhead_fwd_pair_kernel<gemm>"};
+                       mc     ? "lmhead_fwd_pair_kernel<gemm,mc>"
+                       : wide ? "lmhead_fwd_pair_kernel<gemm,wide>"
+                              : "lmhead_fwd_pair_kernel<gemm>"};
   return cudaGetLastError();
 }
 

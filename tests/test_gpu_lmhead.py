@@ -189,11 +189,13 @@ def test_lmhead_token_out_of_vocabulary(ctx):
 
 
 @pytest.mark.parametrize("T,H,V", [(300, 512, 4096), (256, 256, 1000), (1024, 4096, 151936)])
-@pytest.mark.parametrize("mc", [False, True])
-def test_lmhead_dhidden_tcgen05(ctx, T, H, V, mc, monkeypatch):
+@pytest.mark.parametrize("variant", ["wide", "pair", "mc"])
+def test_lmhead_dhidden_tcgen05(ctx, T, H, V, variant, monkeypatch):
     """LM-head backward dhidden = dlogits @ W on the CTA-pair tcgen05 kernel
-    (B = W^T, split-K with a fixed-order sum): vs the fp32 product within bf16
-    rounding of the output, and bitwise on a rerun."""
+    (B = W^T, split-K with a fixed-order sum): the default 256 x 512 tiles vs the
+    fp32 product within bf16 rounding of the output, bitwise on a rerun; the
+    256 x 256 tile (pair) and the multicast 4-CTA variant (mc) at the same split
+    count are bitwise the default (same k order for every output element)."""
     g = torch.Generator(device="cuda").manual_seed(T + H)
     ldv = (V + 7) // 8 * 8
     dl = (torch.randn((T, ldv), device="cuda", generator=g) * 1e-3).to(torch.bfloat16)[:, :V]
@@ -201,7 +203,11 @@ def test_lmhead_dhidden_tcgen05(ctx, T, H, V, mc, monkeypatch):
     wt = w.t().contiguous()
     if ldv != V:
         wt = torch.nn.functional.pad(wt, (0, ldv - V))[:, :V]
+    monkeypatch.delenv("COPRIS_GEMM_WIDE", raising=False)
+    monkeypatch.delenv("COPRIS_GEMM_MC", raising=False)
+    monkeypatch.delenv("COPRIS_GEMM_SPLITS", raising=False)
     out = ctx.lmhead_dhidden(dl, wt)
+    assert ctx.last_launch()["kernel"].endswith(",wide>")
     torch.cuda.synchronize()
     ref = dl.float() @ w.float()
     err = (out.float() - ref).abs()
@@ -209,14 +215,15 @@ def test_lmhead_dhidden_tcgen05(ctx, T, H, V, mc, monkeypatch):
     assert bool((err <= tol).all()), float((err - tol).max())
     again = ctx.lmhead_dhidden(dl, wt)
     assert torch.equal(again.view(torch.int16), out.view(torch.int16))
-    if mc:
+    if variant != "wide":
+        monkeypatch.setenv("COPRIS_GEMM_SPLITS", "2")
+        base = ctx.lmhead_dhidden(dl, wt)
         small_ref = ctx.lmhead_dhidden(dl[:1], wt)
-        # 4-CTA clusters with W^T multicast to two token pairs: same tiles, same
-        # k order -> bitwise the 2-CTA result (odd pair counts: a masked tail pair)
-        monkeypatch.setenv("COPRIS_GEMM_MC", "1")
+        monkeypatch.setenv("COPRIS_GEMM_MC" if variant == "mc" else "COPRIS_GEMM_WIDE",
+                           "1" if variant == "mc" else "0")
         multi = ctx.lmhead_dhidden(dl, wt)
-        assert ctx.last_launch()["cluster"] == 4
-        assert torch.equal(multi.view(torch.int16), out.view(torch.int16))
+        assert ctx.last_launch()["kernel"].endswith(f",{variant}>" if variant == "mc" else "<gemm>")
+        assert torch.equal(multi.view(torch.int16), base.view(torch.int16))
         small = ctx.lmhead_dhidden(dl[:1], wt)
         assert torch.equal(small.view(torch.int16), small_ref.view(torch.int16))
 
