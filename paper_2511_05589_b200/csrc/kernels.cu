@@ -25,7 +25,10 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <set>
 #include <type_traits>
+#include <utility>
 
 #include "kernels.cuh"
 #include "ptx.cuh"
@@ -2006,7 +2009,7 @@ __global__ void __launch_bounds__(kReduceThreads)
 // ---------------------------------------------------------------------------
 template <typename K>
 cudaError_t set_smem(K kernel, int bytes) {
-  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  return allow_dyn_smem(reinterpret_cast<const void*>(kernel), bytes);
 }
 
 int grid_rows(int64_t n_rows, int num_sms, int per_sm) {
@@ -2391,6 +2394,27 @@ cudaError_t launch_reduce(const double* obj, const uint8_t* flags, int64_t n_tok
     reduce_kernel<false><<<static_cast<unsigned>(nb), kReduceThreads, 0, stream>>>(
         obj, flags, n_tok, out4, static_cast<ReduceScratch*>(scratch));
   return cudaGetLastError();
+}
+
+cudaError_t allow_dyn_smem(const void* func, int bytes) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> raised;
+  std::lock_guard<std::mutex> lock(mu);
+  if (raised.count({func, dev})) return cudaSuccess;
+  cudaFuncAttributes fa{};
+  e = cudaFuncGetAttributes(&fa, func);
+  if (e != cudaSuccess) return e;
+  int optin = 0;
+  e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e != cudaSuccess) return e;
+  const int max_dyn = optin - static_cast<int>(fa.sharedSizeBytes);
+  if (bytes > max_dyn) return cudaErrorInvalidValue;
+  e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn);
+  if (e == cudaSuccess) raised.insert({func, dev});
+  return e;
 }
 
 }  // namespace copris_b200

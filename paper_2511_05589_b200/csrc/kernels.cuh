@@ -9,6 +9,13 @@
 
 namespace copris_b200 {
 
+// Allow `bytes` of dynamic shared memory for `func` on the current device. The
+// attribute is per function and device — shared by every context and thread of
+// the process — so it is raised once, to the device's opt-in maximum, and never
+// lowered: concurrent launches of the same kernel with different sizes on other
+// threads cannot see a smaller limit (re-entrancy).
+cudaError_t allow_dyn_smem(const void* func, int bytes);
+
 // Bits of the device error word (copris_ctx_check maps them to the
 // reference's exception messages).
 enum : uint32_t {

@@ -730,8 +730,7 @@ cudaError_t launch_lmhead_fwd(const void* hidden, int64_t ld_h, const void* weig
   }
   const char* impl = std::getenv("COPRIS_LMHEAD_IMPL");
   if (impl && std::strcmp(impl, "1sm") == 0) {
-    cudaError_t ea = cudaFuncSetAttribute(lmhead_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(kSmemBytes));
+    cudaError_t ea = allow_dyn_smem(reinterpret_cast<const void*>(lmhead_fwd_kernel), static_cast<int>(kSmemBytes));
     if (ea != cudaSuccess) return ea;
     const int grid = static_cast<int>(std::min<int64_t>(p.n_tiles, num_sms));
     lmhead_fwd_kernel<<<grid, kThreads, kSmemBytes, stream>>>(tx, tw, p);
@@ -741,9 +740,7 @@ cudaError_t launch_lmhead_fwd(const void* hidden, int64_t ld_h, const void* weig
   // the pair kernel stages half of the weight tile per CTA: 128-row boxes
   if (!make_map(&tw, weight, V, H, ld_w, 128)) return cudaErrorInvalidValue;
   // per call: the attribute is per device, and one process may drive several
-  cudaError_t ea = cudaFuncSetAttribute(lmhead_fwd_pair_kernel<0>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(kPSmemBytes));
+  cudaError_t ea = allow_dyn_smem(reinterpret_cast<const void*>(lmhead_fwd_pair_kernel<0>), static_cast<int>(kPSmemBytes));
   if (ea != cudaSuccess) return ea;
   const int64_t units = (n_rows + 255) / 256 * p.n_vt;
   const int grid = static_cast<int>(std::min<int64_t>(2 * units, num_sms & ~1));
@@ -837,8 +834,7 @@ cudaError_t launch_gemm_nt_bf16(const void* A, int64_t lda, const void* B, int64
                      : lmhead_fwd_pair_kernel<1, false>;
   const size_t smem = wide ? kPSmemBytesWide : kPSmemBytes;
   if (wide) p.n_vt = (N + 2 * kBN - 1) / (2 * kBN);
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
+  cudaError_t e = allow_dyn_smem(reinterpret_cast<const void*>(kern), static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   const int cl = mc ? 4 : 2;
   const int64_t n_mu = mc ? ((M + 255) / 256 + 1) / 2 : (M + 255) / 256;
@@ -901,9 +897,7 @@ cudaError_t launch_gemm_tn_acc_f32(const void* A, int64_t lda, const void* B, in
   // hidden block of one launch (kchunk x H bf16) stays L2-resident
   const char* kc = std::getenv("COPRIS_DW_KCHUNK");
   const int64_t kchunk = kc ? std::max<int64_t>(kBK, std::atoll(kc) / kBK * kBK) : 8192;
-  cudaError_t e = cudaFuncSetAttribute(lmhead_fwd_pair_kernel<2>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(kPSmemBytesDw));
+  cudaError_t e = allow_dyn_smem(reinterpret_cast<const void*>(lmhead_fwd_pair_kernel<2>), static_cast<int>(kPSmemBytesDw));
   if (e != cudaSuccess) return e;
   const int64_t units = (static_cast<int64_t>(M) + 255) / 256 * p.n_vt;
   const int grid = static_cast<int>(std::min<int64_t>(2 * units, num_sms & ~1));
