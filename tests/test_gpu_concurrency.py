@@ -109,3 +109,54 @@ def test_error_state_is_per_thread_and_per_context(oracle):
         _same(o, ref)
     # the failed context is usable again after the error was reported
     _same(_run(ctx_bad, good, s_bad)[0], ref)
+
+
+def test_host_dropin_on_threads_bitwise(oracle):
+    """The host-buffer drop-in (copris_grpo_step_loss_host: pinned host arrays in,
+    3-stream chunked pipeline, host loss and dlogits out) from several threads,
+    each with its own context and workspace: bitwise the single-threaded result."""
+    import math
+    import numpy as np
+    from paper_2511_05589_b200 import Copris
+    from paper_2511_05589_b200.grpo import HostWorkspace
+    specs = [(31, 32000), (32, 151936), (33, 8000), (34, 32000)]
+    cases = [Case(oracle, seed=s, P=4, G=4, V=v, mu=math.log(20), lmax=64) for s, v in specs]
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    ctxs = [Copris(0) for _ in cases]
+    wss = [HostWorkspace(ctx, chunk_rows=37, vocab=c.V, max_tokens=c.hb.n_tok, max_traj=c.hb.n_traj,
+                         dlogits_dtype=torch.bfloat16) for ctx, c in zip(ctxs, cases)]
+
+    def call(i):
+        c, hb = cases[i], cases[i].hb
+        dl = torch.empty((hb.n_tok, c.V), dtype=torch.bfloat16).pin_memory()
+        out = wss[i].grpo_step_loss(c.logits_cpu.pin_memory(), pin(hb.tok_off), pin(hb.target),
+                                    pin(hb.stage.view(np.int32)), pin(c.blp), hb.cur_stage,
+                                    rewards=pin(hb.reward), group_off=pin(hb.group_off),
+                                    cfg=c.clip(), dlogits=dl)
+        return out, dl
+
+    alone = [call(i) for i in range(len(cases))]
+    errors = []
+    start = threading.Barrier(len(cases))
+
+    def worker(i):
+        try:
+            start.wait()
+            for _ in range(3):
+                out, dl = call(i)
+                assert out == alone[i][0]
+                assert torch.equal(dl.view(torch.int16), alone[i][1].view(torch.int16))
+        except BaseException as e:  # surfaced below
+            errors.append((i, e))
+
+    threads = [threading.Thread(target=worker, args=(i,)) for i in range(len(cases))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for i, c in enumerate(cases):
+        assert alone[i][0]["token_count"] == c.hb.n_tok
+        assert alone[i][0]["stale_tokens"] == c.ref.stale_tokens
+    for ws in wss:
+        ws.close()
