@@ -9,7 +9,10 @@
 // nonzero if the loss or the table gradient differ beyond 1e-5 (relative).
 #include <cmath>
 #include <cstdio>
+#include <cstring>
+#include <mutex>
 #include <span>
+#include <thread>
 #include <vector>
 
 #include "copris/trainer.hpp"
@@ -31,15 +34,58 @@ RunConfig desk_config() {  // io.hpp:445-457
   return cfg;
 }
 
+struct Case {
+  const char* name;
+  RunConfig cfg;
+  int steps;
+};
+
+struct StepOut {
+  double loss_gpu;
+  bool ok;
+};
+
+// One case: the reference Trainer with its own DropIn context; prints one JSON
+// line per captured step (under `io`) and returns the GPU losses in step order.
+std::vector<StepOut> run_case(const Case& cs, const char* mode, std::mutex& io) {
+  copris_b200::DropIn gpu(0);
+  std::vector<StepOut> outs;
+  Trainer trainer(cs.cfg);
+  int step = 0;
+  trainer.set_inspector([&](const TrainBatch& batch, const std::vector<GrpoItem>& items) {
+    const PolicyParams& params = trainer.params();
+    GrpoStepResult ref = grpo_step_loss(params, items, cs.cfg.clip);
+    GrpoStepResult got = gpu.grpo_step_loss<GrpoStepResult, ContractViolation, ConfigError>(
+        params, std::span<const GrpoItem>(items), cs.cfg.clip);
+    double gmax = 0.0, gerr = 0.0;
+    for (size_t i = 0; i < ref.grad.size(); ++i) {
+      gmax = std::max(gmax, std::abs(ref.grad[i]));
+      gerr = std::max(gerr, std::abs(ref.grad[i] - got.grad[i]));
+    }
+    const double lerr = std::abs(ref.loss - got.loss);
+    const bool ok = got.token_count == ref.token_count && lerr <= 1e-5 * std::max(1e-3, std::abs(ref.loss)) &&
+                    gerr <= 1e-5 * gmax;
+    outs.push_back({got.loss, ok});
+    std::lock_guard<std::mutex> lock(io);
+    std::printf(
+        "{\"mode\":\"%s\",\"case\":\"%s\",\"step\":%d,\"tokens\":%zu,\"rollout_version\":%llu,"
+        "\"loss_ref\":%.17g,\"loss_gpu\":%.17g,\"loss_abs_err\":%.3g,\"grad_max\":%.6g,"
+        "\"grad_abs_err\":%.3g,\"ok\":%s}\n",
+        mode, cs.name, step, ref.token_count, (unsigned long long)batch.rollout_version, ref.loss,
+        got.loss, lerr, gmax, gerr, ok ? "true" : "false");
+  });
+  for (step = 0; step < cs.steps; ++step) trainer.train_step();
+  return outs;
+}
+
 }  // namespace
 
-int main() {
-  copris_b200::DropIn gpu(0);
-  struct Case {
-    const char* name;
-    RunConfig cfg;
-    int steps;
-  };
+// usage: dropin_check [--threads]   (--threads: after the sequential pass, every
+// case again on its own std::thread with its own context, as the reference CLI
+// runs one Trainer per thread (copris_cli.cpp:98-115); the GPU losses must be
+// bitwise the sequential ones)
+int main(int argc, char** argv) {
+  const bool threaded = argc > 1 && std::strcmp(argv[1], "--threads") == 0;
   std::vector<Case> cases;
   cases.push_back({"desk", desk_config(), 6});
   {
@@ -63,31 +109,28 @@ int main() {
     c.cluster.memory_capacity = 4096;
     cases.push_back({"v64_h16_c128", c, 8});
   }
+  std::mutex io;
   int bad = 0;
+  std::vector<std::vector<StepOut>> seq;
   for (auto& cs : cases) {
-    Trainer trainer(cs.cfg);
-    int step = 0;
-    trainer.set_inspector([&](const TrainBatch& batch, const std::vector<GrpoItem>& items) {
-      const PolicyParams& params = trainer.params();
-      GrpoStepResult ref = grpo_step_loss(params, items, cs.cfg.clip);
-      GrpoStepResult got = gpu.grpo_step_loss<GrpoStepResult, ContractViolation, ConfigError>(
-          params, std::span<const GrpoItem>(items), cs.cfg.clip);
-      double gmax = 0.0, gerr = 0.0;
-      for (size_t i = 0; i < ref.grad.size(); ++i) {
-        gmax = std::max(gmax, std::abs(ref.grad[i]));
-        gerr = std::max(gerr, std::abs(ref.grad[i] - got.grad[i]));
-      }
-      const double lerr = std::abs(ref.loss - got.loss);
-      const bool ok = got.token_count == ref.token_count && lerr <= 1e-5 * std::max(1e-3, std::abs(ref.loss)) &&
-                      gerr <= 1e-5 * gmax;
-      bad += !ok;
-      std::printf(
-          "{\"case\":\"%s\",\"step\":%d,\"tokens\":%zu,\"rollout_version\":%llu,\"loss_ref\":%.17g,"
-          "\"loss_gpu\":%.17g,\"loss_abs_err\":%.3g,\"grad_max\":%.6g,\"grad_abs_err\":%.3g,\"ok\":%s}\n",
-          cs.name, step, ref.token_count, (unsigned long long)batch.rollout_version, ref.loss, got.loss,
-          lerr, gmax, gerr, ok ? "true" : "false");
-    });
-    for (step = 0; step < cs.steps; ++step) trainer.train_step();
+    seq.push_back(run_case(cs, "sequential", io));
+    for (auto& o : seq.back()) bad += !o.ok;
+  }
+  if (threaded) {
+    std::vector<std::vector<StepOut>> par(cases.size());
+    std::vector<std::thread> ts;
+    for (size_t i = 0; i < cases.size(); ++i)
+      ts.emplace_back([&, i] { par[i] = run_case(cases[i], "threaded", io); });
+    for (auto& t : ts) t.join();
+    for (size_t i = 0; i < cases.size(); ++i) {
+      bool same = par[i].size() == seq[i].size();
+      for (size_t k = 0; same && k < par[i].size(); ++k)
+        same = std::memcmp(&par[i][k].loss_gpu, &seq[i][k].loss_gpu, sizeof(double)) == 0 &&
+               par[i][k].ok;
+      bad += !same;
+      std::printf("{\"mode\":\"threaded_vs_sequential\",\"case\":\"%s\",\"steps\":%zu,\"ok\":%s}\n",
+                  cases[i].name, par[i].size(), same ? "true" : "false");
+    }
   }
   return bad ? 1 : 0;
 }
