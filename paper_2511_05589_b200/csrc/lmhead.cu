@@ -128,6 +128,67 @@ __device__ __forceinline__ float2 epilogue_row(uint32_t taddr, int64_t row, bool
   return make_float2(m, s);
 }
 
+// epilogue_row with the logits leaving through TMA stores: the warp stages its
+// 32 rows x 64 columns of rounded bf16 in a swizzled 4 KB box (16-byte chunk j
+// of row r at j ^ (r & 7)) and one lane stores it (full 128-byte lines instead
+// of 16-byte pieces of 32 different rows per instruction). The {max, sum}
+// arithmetic is exactly epilogue_row's. `box0` = this warp's two staging boxes.
+__device__ __forceinline__ float2 epilogue_row_tma(uint32_t taddr, int32_t row0, int32_t n0,
+                                                   int32_t ncols, int32_t yrel,
+                                                   const CUtensorMap* tm_l, uint32_t box0,
+                                                   int& buf, uint64_t st_pol) {
+  const int lane = threadIdx.x & 31;
+  float m = -INFINITY, s = 0.f;
+#pragma unroll 1
+  for (int c = 0; c < kBN; c += 64) {
+    if (c >= ncols) break;  // uniform across the warp (tile-level)
+    const uint32_t box = box0 + static_cast<uint32_t>(buf) * 4096u;
+    if (lane == 0) tc::bulk_wait_group_read<1>();  // the store issued 2 boxes ago read `box`
+    __syncwarp();
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+      const int cc = c + 32 * h;
+      uint32_t r[32];
+      tc::tmem_ld_32x32b_x32(taddr + cc, r);
+      tc::tmem_wait_ld();
+      float z[32];
+      float cm = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        z[j] = bf16_round(__uint_as_float(r[j]));
+        if (cc + j < ncols) cm = fmaxf(cm, z[j]);
+      }
+      if (cc < ncols) {
+        if (cm > m) {
+          s *= ptx::ex2((m - cm) * kLog2e);
+          m = cm;
+        }
+        const float mb = m * kLog2e;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float e = ptx::ex2(fmaf(z[j], kLog2e, -mb));
+          if (cc + j < ncols && cc + j != yrel) s += e;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        ptx::sts_v4(box + lane * 128 + (((4 * h + q) ^ (lane & 7)) << 4),
+                    make_uint4(ptx::pack_bf16x2(z[8 * q + 0], z[8 * q + 1]),
+                               ptx::pack_bf16x2(z[8 * q + 2], z[8 * q + 3]),
+                               ptx::pack_bf16x2(z[8 * q + 4], z[8 * q + 5]),
+                               ptx::pack_bf16x2(z[8 * q + 6], z[8 * q + 7])));
+    }
+    ptx::fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tc::tma_store_2d(tm_l, box, n0 + c, row0, st_pol);
+      tc::bulk_commit_group();
+    }
+    buf ^= 1;
+  }
+  return make_float2(m, s);
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
     lmhead_fwd_kernel(const __grid_constant__ CUtensorMap tm_x,
                       const __grid_constant__ CUtensorMap tm_w, const LmParams P) {
@@ -287,7 +348,8 @@ constexpr int kPStagesWide = 4;  // 48 KB stages (A 16 KB + two B halves)
 constexpr size_t kPSmemBytesWide = 1024 + kPStagesWide * (kPABytes + 2 * kPBBytes) + 256;
 constexpr uint32_t kMnBoxBytes = kBK * 128;  // MN-major box: kBK K-rows x 64 elements
 
-// EPI 0: logits + LSE partials (the forward). EPI 1: C = A B^T as fp32 split-K
+// EPI 0: logits + LSE partials (the forward). EPI 3: the same with the logits
+// leaving through swizzled staging boxes and TMA stores (epilogue_row_tma). EPI 1: C = A B^T as fp32 split-K
 // partials (A [M x K], B [N x K], both K-major; M = tokens, N = P.V columns,
 // K = P.H), e.g. dhidden = dlogits [T x V] * (W^T [H x V])^T.
 // EPI 2: C += A^T B with both operands MN-major (A [K x M], B [K x N] row-major,
@@ -308,7 +370,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int kNT = WIDE ? 2 * kBN : kBN;           // N columns per unit
   constexpr int kBStage = (kNT / kBN) * kPBBytes;     // this CTA's B bytes per stage
   constexpr int kStageB = kPABytes + kBStage;
-  constexpr int kPStages = EPI == 2 ? kPStagesDw : WIDE ? kPStagesWide : ::copris_b200::kPStages;
+  // EPI 2 / 3: one stage fewer, for the epilogue's staging boxes
+  constexpr int kPStages = EPI >= 2 ? kPStagesDw : WIDE ? kPStagesWide : ::copris_b200::kPStages;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t base = (ptx::smem_u32(smem_raw) + 1023u) & ~1023u;
   const uint32_t sA = base;
@@ -343,7 +406,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::fence_mbarrier_init();
     tc::prefetch_tensormap(&tm_x);
     tc::prefetch_tensormap(&tm_w);
-    if (EPI == 2) tc::prefetch_tensormap(&tm_c);
+    if (EPI >= 2) tc::prefetch_tensormap(&tm_c);
   }
   if (warp == 1) tc::tmem_alloc_pair<kTmemCols>(tmem_slot);
   tc::fence_before_sync();
@@ -558,6 +621,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::fence_before_sync();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive_remote(ptx::mapa(tempty_bar(acc), lrank));
+      } else if constexpr (EPI == 3) {
+        const int32_t yrel = row_ok ? P.target[row] - n0 : -1;
+        const int32_t row0 = static_cast<int32_t>(mp * 256 + 128 * prank + sub * 32);
+        const float2 part = epilogue_row_tma(taddr, row0, n0, ncols, yrel, &tm_c,
+                                             stg + static_cast<uint32_t>(sub) * 8192u, dw_buf,
+                                             st_pol);
+        tc::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_remote(ptx::mapa(tempty_bar(acc), lrank));
+        if (row_ok) P.partials[row * P.n_vt + vt] = part;
       } else {
       const int32_t yrel = row_ok ? P.target[row] - n0 : -1;
       const float2 part = epilogue_row(taddr, row, row_ok, n0, ncols, yrel, P, st_pol);
@@ -574,7 +647,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
-  if (EPI == 2 && warp >= 2 && lane == 0) tc::bulk_wait_group<0>();
+  if (EPI >= 2 && warp >= 2 && lane == 0) tc::bulk_wait_group<0>();
   tc::fence_before_sync();
   __syncthreads();
   ptx::cluster_sync_all();
@@ -740,14 +813,23 @@ cudaError_t launch_lmhead_fwd(const void* hidden, int64_t ld_h, const void* weig
   // the pair kernel stages half of the weight tile per CTA: 128-row boxes
   if (!make_map(&tw, weight, V, H, ld_w, 128)) return cudaErrorInvalidValue;
   // per call: the attribute is per device, and one process may drive several
-  cudaError_t ea = allow_dyn_smem(reinterpret_cast<const void*>(lmhead_fwd_pair_kernel<0>), static_cast<int>(kPSmemBytes));
+  // logits through staging boxes + TMA stores (EPI 3) unless COPRIS_LMHEAD_TMA_STORE=0;
+  // only when a row is a whole number of 16-byte pieces (V % 8 == 0): TMA clips
+  // a store box at 16-byte granularity, so it would write the row padding
+  const char* ts = std::getenv("COPRIS_LMHEAD_TMA_STORE");
+  const bool tma_store = !(ts && std::atoi(ts) == 0) && V % 8 == 0;
+  CUtensorMap tl = tw;
+  if (tma_store && !make_map(&tl, logits, n_rows, V, ld, 32)) return cudaErrorInvalidValue;
+  auto kern = tma_store ? lmhead_fwd_pair_kernel<3> : lmhead_fwd_pair_kernel<0>;
+  const size_t smem = tma_store ? kPSmemBytesDw : kPSmemBytes;
+  cudaError_t ea = allow_dyn_smem(reinterpret_cast<const void*>(kern), static_cast<int>(smem));
   if (ea != cudaSuccess) return ea;
   const int64_t units = (n_rows + 255) / 256 * p.n_vt;
   const int grid = static_cast<int>(std::min<int64_t>(2 * units, num_sms & ~1));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = kPSmemBytes;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr_cl[1];
   attr_cl[0].id = cudaLaunchAttributeClusterDimension;
@@ -756,8 +838,10 @@ cudaError_t launch_lmhead_fwd(const void* hidden, int64_t ld_h, const void* weig
   attr_cl[0].val.clusterDim.z = 1;
   cfg.attrs = attr_cl;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, lmhead_fwd_pair_kernel<0>, tx, tw, tw, p);
-  if (info) *info = LaunchInfo{num_sms, 2, grid, "lmhead_fwd_pair_kernel"};
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tx, tw, tl, p);
+  if (info)
+    *info = LaunchInfo{num_sms, 2, grid,
+                       tma_store ? "lmhead_fwd_pair_kernel<tma_store>" : "lmhead_fwd_pair_kernel"};
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 

@@ -48,7 +48,8 @@ def _check_logits(lg, x, w):
 def test_lmhead_logits_and_partials(ctx, impl, T, H, V):
     x, w, tgt = _inputs(T, H, V, T + H + V)
     lg, part = ctx.lmhead_logits(x, w, tgt)
-    assert ctx.last_launch()["kernel"] == ("lmhead_fwd_pair_kernel" if impl == "pair" else "lmhead_fwd_kernel")
+    pair = "lmhead_fwd_pair_kernel<tma_store>" if V % 8 == 0 else "lmhead_fwd_pair_kernel"
+    assert ctx.last_launch()["kernel"] == (pair if impl == "pair" else "lmhead_fwd_kernel")
     torch.cuda.synchronize()
     rows = torch.arange(T, device="cuda") if T * V <= 2 ** 26 else torch.randperm(T, device="cuda")[:32]
     _check_logits(lg[rows], x[rows], w)
@@ -302,3 +303,32 @@ def test_lmhead_dweight_errors(ctx):
         ctx.lmhead_dweight(dl, x[:4])
     with pytest.raises(ValueError, match="bad row strides"):
         ctx.lmhead_dweight(dl, x, out=torch.zeros((64, 66), device="cuda")[:, :64])
+
+
+@pytest.mark.parametrize("T,H,V", [(1, 64, 256), (130, 64, 300), (257, 192, 1000), (300, 520, 4099),
+                                   (129, 64, 1064), (1024, 4096, 151936)])
+def test_lmhead_tma_store_epilogue_bitwise(ctx, T, H, V, impl, monkeypatch):
+    """The forward with the logits leaving through swizzled staging boxes and TMA
+    stores (the default when V % 8 == 0): logits and LSE partials bitwise the
+    register-store epilogue's (COPRIS_LMHEAD_TMA_STORE=0), ragged T included; at
+    V % 8 != 0 the register-store epilogue runs (TMA would clip at 16-byte
+    granularity and write the row padding)."""
+    if impl == "1sm":
+        pytest.skip("pair kernel only")
+    x, w, tgt = _inputs(T, H, V, 23)
+    ldv = (V + 7) // 8 * 8
+    lg0 = torch.full((T, ldv), 3.0, dtype=torch.bfloat16, device="cuda")
+    lg1 = lg0.clone()
+    nvt = int(ctx.lib.copris_lmhead_num_vtiles(V))
+    p0 = torch.empty((T, nvt, 2), dtype=torch.float32, device="cuda")
+    p1 = torch.empty_like(p0)
+    monkeypatch.setenv("COPRIS_LMHEAD_TMA_STORE", "0")
+    ctx.lmhead_logits(x, w, tgt, logits=lg0[:, :V], partials=p0)
+    assert ctx.last_launch()["kernel"] == "lmhead_fwd_pair_kernel"
+    monkeypatch.delenv("COPRIS_LMHEAD_TMA_STORE")
+    ctx.lmhead_logits(x, w, tgt, logits=lg1[:, :V], partials=p1)
+    assert ctx.last_launch()["kernel"] == ("lmhead_fwd_pair_kernel<tma_store>" if V % 8 == 0
+                                           else "lmhead_fwd_pair_kernel")
+    torch.cuda.synchronize()
+    assert torch.equal(lg1.view(torch.int16), lg0.view(torch.int16))  # padding untouched too
+    assert torch.equal(p1.view(torch.int32), p0.view(torch.int32))
