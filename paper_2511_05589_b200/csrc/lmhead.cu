@@ -345,7 +345,9 @@ constexpr uint32_t kDwBoxBytes = 32 * 32 * 4;
 constexpr size_t kPSmemBytesDw = 1024 + kPStagesDw * kPStageBytes + 1024 + 8 * kDwBoxBytes;
 static_assert(kPSmemBytesDw <= 232448, "dW smem");
 constexpr int kPStagesWide = 4;  // 48 KB stages (A 16 KB + two B halves)
-constexpr size_t kPSmemBytesWide = 1024 + kPStagesWide * (kPABytes + 2 * kPBBytes) + 256;
+// + 1024 barrier block + 8 x 4 KB fp32 staging boxes for the TMA-store epilogue
+constexpr size_t kPSmemBytesWide = 1024 + kPStagesWide * (kPABytes + 2 * kPBBytes) + 1024 + 8 * 4096;
+static_assert(kPSmemBytesWide <= 232448, "wide smem");
 constexpr uint32_t kMnBoxBytes = kBK * 128;  // MN-major box: kBK K-rows x 64 elements
 
 // EPI 0: logits + LSE partials (the forward). EPI 3: the same with the logits
@@ -406,7 +408,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::fence_mbarrier_init();
     tc::prefetch_tensormap(&tm_x);
     tc::prefetch_tensormap(&tm_w);
-    if (EPI >= 2) tc::prefetch_tensormap(&tm_c);
+    if (EPI >= 2 || WIDE) tc::prefetch_tensormap(&tm_c);
   }
   if (warp == 1) tc::tmem_alloc_pair<kTmemCols>(tmem_slot);
   tc::fence_before_sync();
@@ -596,6 +598,36 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::fence_before_sync();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive_remote(ptx::mapa(tempty_bar(acc), lrank));
+      } else if constexpr (EPI == 1 && WIDE) {
+        // fp32 partial tile through swizzled 32 x 32 staging boxes and 3-D TMA
+        // stores (columns, rows, split: the box is clipped per split)
+        const int32_t sp = static_cast<int32_t>(u / (n_mu * P.n_vt));
+        const int32_t row0 = static_cast<int32_t>(mp * 256 + 128 * prank + sub * 32);
+        const uint32_t box0 = stg + static_cast<uint32_t>(sub) * 8192u;
+#pragma unroll 1
+        for (int c = 0; c < kNT; c += 32) {
+          uint32_t r[32];
+          tc::tmem_ld_32x32b_x32(taddr + c, r);
+          tc::tmem_wait_ld();
+          if (c >= ncols) break;  // uniform across the warp
+          const uint32_t box = box0 + static_cast<uint32_t>(dw_buf) * kDwBoxBytes;
+          if (lane == 0) tc::bulk_wait_group_read<1>();
+          __syncwarp();
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            ptx::sts_v4(box + lane * 128 + ((q ^ (lane & 7)) << 4),
+                        make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]));
+          ptx::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tc::tma_store_3d(&tm_c, box, n0 + c, row0, sp, st_pol);
+            tc::bulk_commit_group();
+          }
+          dw_buf ^= 1;
+        }
+        tc::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_remote(ptx::mapa(tempty_bar(acc), lrank));
       } else if constexpr (EPI == 1) {
         // fp32 tile row straight from TMEM to this split's partial matrix
         const int64_t sp = u / (n_mu * P.n_vt);
@@ -647,7 +679,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   }
-  if (EPI >= 2 && warp >= 2 && lane == 0) tc::bulk_wait_group<0>();
+  if ((EPI >= 2 || WIDE) && warp >= 2 && lane == 0) tc::bulk_wait_group<0>();
   tc::fence_before_sync();
   __syncthreads();
   ptx::cluster_sync_all();
@@ -770,6 +802,23 @@ bool make_map_f32_box32(CUtensorMap* map, const void* ptr, int64_t rows, int32_t
   const cuuint32_t box[2] = {32, 32};
   const cuuint32_t estr[2] = {1, 1};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// fp32 partial matrices [splits][rows][cols] (contiguous), 32 x 32 x 1 boxes,
+// SWIZZLE_128B: the TMA-store target of the 256 x 512 plain-GEMM epilogue.
+bool make_map_f32_3d_box32(CUtensorMap* map, const void* ptr, int64_t splits, int64_t rows,
+                           int32_t cols) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows),
+                              static_cast<cuuint64_t>(splits)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(cols) * 4,
+                                 static_cast<cuuint64_t>(cols) * 4 * static_cast<cuuint64_t>(rows)};
+  const cuuint32_t box[3] = {32, 32, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(ptr), dims, strides, box,
             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -943,7 +992,9 @@ cudaError_t launch_gemm_nt_bf16(const void* A, int64_t lda, const void* B, int64
     if (cudaOccupancyMaxActiveClusters(&max_cl, kern, &cfg) == cudaSuccess && max_cl > 0)
       cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(cl * units, cl * max_cl)));
   }
-  e = cudaLaunchKernelEx(&cfg, kern, ta, tb, tb, p);
+  CUtensorMap tp = tb;
+  if (wide && !make_map_f32_3d_box32(&tp, work, p.n_split, M, N)) return cudaErrorInvalidValue;
+  e = cudaLaunchKernelEx(&cfg, kern, ta, tb, tp, p);
   if (e != cudaSuccess) return e;
   const int64_t quads = M * (N / 4);
   const int64_t blocks = std::min<int64_t>((quads + 255) / 256, static_cast<int64_t>(num_sms) * 8);
