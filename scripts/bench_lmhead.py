@@ -59,6 +59,9 @@ def main():
     t_step_tc = timeit(lambda: lmhead_grpo_step_loss(ctx, x, w, batch, ClipConfig(), chunk_rows=chunk,
                                                      dweight=dW, dhidden_impl="tcgen05", weight_t=wt,
                                                      dweight_impl="tcgen05"), iters=3, warm=1)
+    t_step_dh = timeit(lambda: lmhead_grpo_step_loss(ctx, x, w, batch, ClipConfig(), chunk_rows=chunk,
+                                                     dweight=dW, dhidden_impl="tcgen05", weight_t=wt),
+                       iters=3, warm=1)
     dh = torch.empty_like(x)
     outs = ctx.alloc_outputs(T, x.device)
     out4 = torch.empty(4, dtype=torch.float64, device="cuda")
@@ -76,7 +79,7 @@ def main():
         return out4.cpu()
 
     t_comp = timeit(composed, iters=3, warm=1)
-    out.update({"step_ms": t_step, "step_tcgen05_bwd_ms": t_step_tc, "composed_step_ms": t_comp, "chunk": chunk,
+    out.update({"step_ms": t_step, "step_tcgen05_bwd_ms": t_step_tc, "step_tcgen05_dhidden_ms": t_step_dh, "composed_step_ms": t_comp, "chunk": chunk,
                 "step_tflops": 6 * T * H * V / t_step / 1e9})
     print(json.dumps(out))
 
