@@ -77,6 +77,16 @@ COPRIS_API const char* copris_last_error(void);
  * stream, or use one context per stream. */
 COPRIS_API int copris_ctx_create(int device, copris_ctx** out);
 COPRIS_API int copris_ctx_destroy(copris_ctx* ctx);
+/* Kernel selection and tunables of this context (not a reference entry point).
+ * copris_ctx_create reads the COPRIS_* environment ONCE into the context;
+ * launches never read the environment again. Change an option between
+ * launches (not concurrently with a launch on the same context). Names:
+ * fused_impl (0 auto, 1 stream, 2 tma, 3 pair), lookahead, slots, resident,
+ * one_exp, lmhead_impl (0 pair, 1 single SM), lmhead_group, lmhead_tma_store,
+ * gemm_wide, gemm_mc, gemm_splits, gemm_a_evict_first, dw_group, dw_policy,
+ * dw_kchunk, trace. COPRIS_E_INVALID for an unknown name or out-of-range value. */
+COPRIS_API int copris_ctx_set_option(copris_ctx* ctx, const char* name, int64_t value);
+COPRIS_API int copris_ctx_get_option(const copris_ctx* ctx, const char* name, int64_t* value);
 /* Synchronises `stream`, then reports and clears the device error word. */
 COPRIS_API int copris_ctx_check(copris_ctx* ctx, void* stream);
 
@@ -405,8 +415,8 @@ COPRIS_API int copris_ctx_last_launch(const copris_ctx* ctx, int* cluster, int* 
                            const char** kernel_name);
 
 /* Diagnostics (not a reference entry point): per-CTA phase-cycle counters of
- * the fused kernels, recorded when COPRIS_TRACE is set in the environment at
- * context creation; 8 int64 per CTA (pass B, barrier A, scalar phase,
+ * the fused kernels, recorded when the context's `trace` option is on
+ * (COPRIS_TRACE in the environment at creation); 10 int64 per CTA (pass B, barrier A, scalar phase,
  * barrier B, pass C, rows). Reading resets them. */
 COPRIS_API int copris_ctx_trace_read(copris_ctx* ctx, long long* host, int n);
 

@@ -106,6 +106,8 @@ _SIGS = {
     "copris_grpo_step_loss_host": ([P, P, C.POINTER(HostBatch), C.POINTER(LossCfg),
                                     C.POINTER(HostResult)], C.c_int),
     "copris_ctx_trace_read": ([P, P, C.c_int], C.c_int),
+    "copris_ctx_set_option": ([P, C.c_char_p, I64], C.c_int),
+    "copris_ctx_get_option": ([P, C.c_char_p, C.POINTER(I64)], C.c_int),
     "copris_adam_update": ([P, P, P, P, P, I64, I64, C.POINTER(AdamCfg), P], C.c_int),
     "copris_checkpoint_write": ([C.c_char_p, P, P, C.c_uint64, C.c_uint64], C.c_int),
     "copris_checkpoint_read": ([C.c_char_p, P, P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)], C.c_int),

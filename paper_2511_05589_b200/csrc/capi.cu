@@ -140,12 +140,13 @@ int copris_ctx_create(int device, copris_ctx** out) {
   auto* ctx = new copris_ctx{};
   ctx->device = device;
   ctx->num_sms = prop.multiProcessorCount;
+  ctx->tuning = tuning_from_env();  // the only environment read: launches use this copy
   e = cudaMalloc(&ctx->d_err, sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMemset(ctx->d_err, 0, sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMalloc(&ctx->d_rowctr, sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMalloc(&ctx->d_scratch, reduce_scratch_bytes());
   if (e == cudaSuccess) e = cudaMemset(ctx->d_scratch, 0, reduce_scratch_bytes());
-  if (e == cudaSuccess && getenv("COPRIS_TRACE")) {
+  if (e == cudaSuccess && ctx->tuning.trace) {
     e = cudaMalloc(&ctx->d_trace, sizeof(long long) * kTraceCtas * kTraceSlots);
     if (e == cudaSuccess) e = cudaMemset(ctx->d_trace, 0, sizeof(long long) * kTraceCtas * kTraceSlots);
   }
@@ -187,6 +188,8 @@ int copris_ctx_check(copris_ctx* ctx, void* stream) {
   if (err & ERR_NONFINITE_LP) return fail(COPRIS_E_CONTRACT, "token_ratio requires finite log-probs");
   if (err & ERR_NOT_TERMINATED)
     return fail(COPRIS_E_CONTRACT, "terminal_reward requires a terminated trajectory");
+  if (err & ERR_EMPTY_TERMINATED)
+    return fail(COPRIS_E_CONTRACT, "terminated trajectory cannot be empty");
   return fail(COPRIS_E_CUDA, "unknown device error");
 }
 
@@ -203,7 +206,7 @@ int copris_logprob_gather(copris_ctx* ctx, const void* logits, int64_t ld, int32
   DeviceGuard g(ctx->device);
   cudaError_t e = launch_logprob_gather(logits, ld, dt(dtype), target, n_tok, vocab, out_lp,
                                         out_lse, ctx->d_err, ctx->d_rowctr, ctx->num_sms,
-                                        as_stream(stream));
+                                        ctx->tuning, as_stream(stream));
   return e == cudaSuccess ? COPRIS_OK : cuda_fail(e, "logprob_gather launch");
 }
 
@@ -231,7 +234,7 @@ int copris_lmhead_logits(copris_ctx* ctx, const void* hidden, int64_t ld_hidden,
   DeviceGuard g(ctx->device);
   cudaError_t e = launch_lmhead_fwd(hidden, ld_hidden, weight, ld_weight, n_rows, hidden_dim, vocab,
                                     target, logits, ld_logits, partials, ctx->num_sms,
-                                    as_stream(stream), &ctx->last);
+                                    ctx->tuning, as_stream(stream), &ctx->last);
   return e == cudaSuccess ? COPRIS_OK : cuda_fail(e, "lmhead_logits launch");
 }
 
@@ -252,7 +255,7 @@ int copris_lse_merge(copris_ctx* ctx, const float* partials, int32_t n_vt, const
 
 int32_t copris_lmhead_dhidden_splits(copris_ctx* ctx, int64_t n_rows, int32_t hidden_dim) {
   if (!ctx || n_rows < 1 || hidden_dim < 1) return 0;
-  return gemm_nt_splits(n_rows, hidden_dim, ctx->num_sms);
+  return gemm_nt_splits(n_rows, hidden_dim, ctx->num_sms, ctx->tuning);
 }
 
 int copris_lmhead_dhidden(copris_ctx* ctx, const void* dlogits, int64_t ld_dlogits,
@@ -274,8 +277,8 @@ int copris_lmhead_dhidden(copris_ctx* ctx, const void* dlogits, int64_t ld_dlogi
   DeviceGuard g(ctx->device);
   cudaError_t e = launch_gemm_nt_bf16(dlogits, ld_dlogits, weight_t, ld_weight_t, n_rows, hidden_dim,
                                       vocab, dhidden, ld_dhidden, work,
-                                      gemm_nt_splits(n_rows, hidden_dim, ctx->num_sms), ctx->num_sms,
-                                      as_stream(stream), &ctx->last);
+                                      gemm_nt_splits(n_rows, hidden_dim, ctx->num_sms, ctx->tuning),
+                                      ctx->num_sms, ctx->tuning, as_stream(stream), &ctx->last);
   return e == cudaSuccess ? COPRIS_OK : cuda_fail(e, "lmhead_dhidden launch");
 }
 
@@ -299,7 +302,7 @@ int copris_lmhead_dweight(copris_ctx* ctx, const void* dlogits, int64_t ld_dlogi
   DeviceGuard g(ctx->device);
   cudaError_t e = launch_gemm_tn_acc_f32(dlogits, ld_dlogits, hidden, ld_hidden, n_rows, vocab,
                                          hidden_dim, dweight, ld_dweight, ctx->num_sms,
-                                         as_stream(stream), &ctx->last);
+                                         ctx->tuning, as_stream(stream), &ctx->last);
   return e == cudaSuccess ? COPRIS_OK : cuda_fail(e, "lmhead_dweight launch");
 }
 
@@ -384,7 +387,7 @@ int copris_is_loss_fused(copris_ctx* ctx, const copris_loss_batch* batch,
   DeviceGuard g(ctx->device);
   LossParams p = make_params(ctx, batch, cfg, out);
   cudaError_t e = launch_fused(p, dt(batch->logits_dtype), dt(out->dlogits_dtype), ctx->num_sms,
-                               as_stream(stream), &ctx->last);
+                               ctx->tuning, as_stream(stream), &ctx->last);
   return e == cudaSuccess ? COPRIS_OK : cuda_fail(e, "is_loss_fused launch");
 }
 
@@ -429,6 +432,25 @@ int copris_ctx_last_launch(const copris_ctx* ctx, int* cluster, int* grid, int* 
   if (grid) *grid = ctx->last.grid;
   if (num_sms) *num_sms = ctx->num_sms;
   if (kernel_name) *kernel_name = ctx->last.kernel ? ctx->last.kernel : "";
+  return COPRIS_OK;
+}
+
+int copris_ctx_set_option(copris_ctx* ctx, const char* name, int64_t value) {
+  if (!ctx || !name) return fail(COPRIS_E_INVALID, "null argument");
+  if (!tuning_set(ctx->tuning, name, value))
+    return fail(COPRIS_E_INVALID, std::string("unknown option or value out of range: ") + name);
+  if (ctx->tuning.trace && !ctx->d_trace) {
+    DeviceGuard g(ctx->device);
+    cudaError_t e = cudaMalloc(&ctx->d_trace, sizeof(long long) * kTraceCtas * kTraceSlots);
+    if (e == cudaSuccess) e = cudaMemset(ctx->d_trace, 0, sizeof(long long) * kTraceCtas * kTraceSlots);
+    if (e != cudaSuccess) return cuda_fail(e, "trace buffer");
+  }
+  return COPRIS_OK;
+}
+
+int copris_ctx_get_option(const copris_ctx* ctx, const char* name, int64_t* value) {
+  if (!ctx || !name || !value) return fail(COPRIS_E_INVALID, "null argument");
+  if (!tuning_get(ctx->tuning, name, value)) return fail(COPRIS_E_INVALID, std::string("unknown option: ") + name);
   return COPRIS_OK;
 }
 

@@ -1,5 +1,6 @@
 // engine_capi.cpp — C-ABI over the host rollout scheduler
 // (include/copris_b200/rollout.hpp). Host-only bookkeeping: no device work.
+#include <algorithm>
 #include <cstring>
 #include <exception>
 #include <string>
@@ -15,6 +16,7 @@ struct copris_engine {
   RolloutEngine engine;
   PackedBatch last;
   bool have_batch = false;
+  int64_t admit_bound = 0;  // max ids one begin_stage / refill_active can admit
 };
 
 namespace {
@@ -52,9 +54,13 @@ int copris_engine_create(const copris_engine_cfg* c, copris_engine** out) {
     EngineConfig ec{c->concurrency, c->batch_prompts, c->rollouts_per_prompt, c->max_response_len,
                     c->max_staleness};
     PolicyShape ps{c->num_classes, c->horizon, c->vocab, c->answer_vocab};
+    // fill_to(target) admits at most `target` trajectories, target being the
+    // concurrency (copris / naive) or B*N (synchronous), rollout.hpp:181-191
+    const int64_t bound = std::max<int64_t>(c->concurrency,
+                                            static_cast<int64_t>(c->batch_prompts) * c->rollouts_per_prompt);
     *out = new copris_engine{RolloutEngine(ec, static_cast<SchedulingMode>(c->mode), ps,
                                            NamedStream(c->seed, "prompt")),
-                             {}, false};
+                             {}, false, bound};
     return COPRIS_OK;
   });
 }
@@ -64,14 +70,24 @@ int copris_engine_destroy(copris_engine* e) {
   return COPRIS_OK;
 }
 
+// The id buffer is checked against the admission bound BEFORE the engine
+// admits anything: a too-small buffer leaves the engine state untouched.
+static int check_cap(const copris_engine* e, const uint64_t* ids, int64_t cap) {
+  if (!ids || cap < e->admit_bound)
+    return fail(COPRIS_E_INVALID, "id buffer capacity too small (need max(concurrency, B*N))");
+  return COPRIS_OK;
+}
+
 int copris_engine_begin_stage(copris_engine* e, uint64_t version, uint64_t* ids, int64_t cap,
                               int64_t* n) {
   if (!e) return fail(COPRIS_E_INVALID, "null engine");
+  if (int rc = check_cap(e, ids, cap)) return rc;
   return guarded([&] { return put_ids(e->engine.begin_stage(version), ids, cap, n); });
 }
 
 int copris_engine_refill_active(copris_engine* e, uint64_t* ids, int64_t cap, int64_t* n) {
   if (!e) return fail(COPRIS_E_INVALID, "null engine");
+  if (int rc = check_cap(e, ids, cap)) return rc;
   return guarded([&] { return put_ids(e->engine.refill_active(), ids, cap, n); });
 }
 

@@ -198,8 +198,31 @@ int copris_grpo_step_loss_host(copris_ctx* ctx, copris_workspace* w, const copri
   }
   copris_loss_cfg cfg = *cfg_in;
   if (cfg.total_tokens == 0) cfg.total_tokens = b->n_tok;
+  // every argument check runs BEFORE the first copy is enqueued: an error
+  // return must not leave DMA reading the caller's (pinned) host buffers
+  if (!b->adv && !(b->adv_epsilon > 0.0)) return fail(COPRIS_E_CONFIG, "grpo.adv_epsilon must be > 0");
+  if (cfg.clip_low <= 0.0 || cfg.clip_high <= 0.0)  // grpo.hpp:21-22
+    return fail(COPRIS_E_CONFIG, "grpo.clip_low and grpo.clip_high must be > 0");
+  if (cfg.kl_coeff < 0.0) return fail(COPRIS_E_CONFIG, "grpo.kl_coeff must be >= 0");
+  if (cfg.kl_coeff > 0.0 && !b->ref_lp)  // grpo.hpp:126-127
+    return fail(COPRIS_E_CONTRACT, "reference log-probs required when kl_coeff > 0");
+  if (cfg.behav_mode != COPRIS_BEHAV_RECOMPUTED && cfg.behav_mode != COPRIS_BEHAV_RECORDED)
+    return fail(COPRIS_E_INVALID, "behav_mode must be COPRIS_BEHAV_RECOMPUTED or _RECORDED");
+  if (cfg.total_tokens < b->n_tok) return fail(COPRIS_E_CONTRACT, "log-prob vectors must align with token count");
 
   DeviceGuard g(ctx->device);
+  // past this point work is in flight: a failing call drains all three
+  // streams before it returns (the caller may free its buffers right after)
+  struct Drain {
+    copris_workspace* w;
+    bool armed = true;
+    ~Drain() {
+      if (!armed) return;
+      cudaStreamSynchronize(w->s_h2d);
+      cudaStreamSynchronize(w->s_comp);
+      cudaStreamSynchronize(w->s_d2h);
+    }
+  } drain{w};
   const int64_t T = b->n_tok, n = b->n_traj;
   cudaStream_t sc = w->s_comp;
   // per-token / per-trajectory metadata
@@ -214,7 +237,6 @@ int copris_grpo_step_loss_host(copris_ctx* ctx, copris_workspace* w, const copri
   } else {
     CK(cudaMemcpyAsync(w->rewards, b->rewards, n * 8, cudaMemcpyHostToDevice, sc));
     CK(cudaMemcpyAsync(w->group_off, b->group_off, (b->n_groups + 1) * 8, cudaMemcpyHostToDevice, sc));
-    if (!(b->adv_epsilon > 0.0)) return fail(COPRIS_E_CONFIG, "grpo.adv_epsilon must be > 0");
     CK(launch_group_advantages(w->rewards, w->group_off, b->n_groups, b->adv_epsilon, w->adv, sc));
   }
 
@@ -267,6 +289,7 @@ int copris_grpo_step_loss_host(copris_ctx* ctx, copris_workspace* w, const copri
   if (out->cur_lp) CK(cudaMemcpyAsync(out->cur_lp, w->cur_lp, T * 4, cudaMemcpyDeviceToHost, sc));
   CK(cudaStreamSynchronize(w->s_h2d));
   CK(cudaStreamSynchronize(w->s_d2h));
+  drain.armed = false;  // every stream is idle from here on
   int rc = copris_ctx_check(ctx, sc);  // syncs sc, maps device-detected violations
   if (rc) return rc;
   const double* o4 = w->h_out4;

@@ -16,6 +16,7 @@ struct copris_ctx {
   void* d_scratch;   // reduction scratch
   copris_b200::LaunchInfo last;  // what the last loss launch did (introspection)
   long long* d_trace;  // phase tracing buffer (COPRIS_TRACE=1 at context creation)
+  copris_b200::Tuning tuning;  // kernel selection, read from COPRIS_* once at creation
 };
 
 

@@ -338,15 +338,6 @@ struct PassB<float> {
   static constexpr uint32_t kNegInfWord = 0xFF800000u;
 };
 
-// Forces column j of a packed vector to -inf (rare path: the target column).
-__device__ __forceinline__ void kill_col(uint64_t* x, int j) {
-  const int k = j >> 1;
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-    if (i == k)
-      x[i] = (j & 1) ? ptx::f2(ptx::f2lo(x[i]), -INFINITY) : ptx::f2(-INFINITY, ptx::f2hi(x[i]));
-}
-
 // Stores NP packed fp32 pairs (2*NP columns) as TOut at a 16-byte aligned address.
 template <typename TOut, int NP>
 __device__ __forceinline__ void store_pairs(TOut* p, const uint64_t* g, uint64_t pol) {
@@ -689,205 +680,9 @@ __global__ void __launch_bounds__(WARPS * 32, (WARPS == 8 && CL == 1) ? 3 : 1)
 }
 
 // ---------------------------------------------------------------------------
-// fused two-pass streaming kernel: no shared-memory row copy. Pass 1 reads the
-// row from HBM and leaves it in L2 (evict_last); after the row's scalar phase
-// pass 2 re-reads it from L2 (evict_first) and streams dlogits out. Several
-// CTAs per SM work on independent rows, so one CTA's reduction/scalar phase
-// overlaps the others' streaming — no cluster coupling between SMs.
-// ---------------------------------------------------------------------------
-template <typename TIn, typename TOut, int WARPS, int U, bool ENT>
-__global__ void __launch_bounds__(WARPS * 32)
-    fused_l2_kernel(const LossParams P, const int keep_policy) {
-  using VI = Vec<TIn>;
-  using PB = PassB<TIn>;
-  constexpr int VN = VI::N;
-  constexpr int NP = VN / 2;
-  constexpr int NT = WARPS * 32;
-  __shared__ Lse red[WARPS];
-  __shared__ RowBroadcast bc;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int32_t V = P.vocab;
-  const int32_t nvec = V / VN;
-  const uint64_t pol_first = ptx::policy_evict_first();
-  const uint64_t pol_keep = keep_policy == 2 ? ptx::policy_evict_last()
-                            : keep_policy == 1 ? ptx::policy_evict_normal() : pol_first;
-  const uint64_t L2 = ptx::f2(kLog2e, kLog2e);
-
-  int64_t r = blockIdx.x;
-  int32_t y_next = r < P.n_rows ? P.target[P.row_base + r] : 0;
-  MetaPipe mp;
-  if (threadIdx.x == 0) mp.init(P, r, gridDim.x);
-
-  for (; r < P.n_rows; r += gridDim.x) {
-    const int64_t t = P.row_base + r;
-    const int32_t y = y_next;
-    RowMeta meta{};
-    if (threadIdx.x == 0) meta = mp.advance(P, r, gridDim.x);
-    const uint4* row = reinterpret_cast<const uint4*>(static_cast<const TIn*>(P.logits) + r * P.ld);
-
-    // ---- pass 1 (HBM -> registers, line kept in L2) ------------------------
-    Lse st = lse_empty();
-    if constexpr (ENT) {
-      for (int32_t v = threadIdx.x; v < nvec; v += NT) {
-        float x[VN];
-        VI::unpack(ptx::ld_global_v4_hint(row + v, pol_keep), x);
-        const int jt = y - v * VN;
-        online_update<VN, true>(x, st, static_cast<uint32_t>(jt) < VN ? jt : -1);
-      }
-    } else {
-      float m = -INFINITY;
-      uint64_t negm = ptx::f2(INFINITY, INFINITY);
-      uint64_t acc0 = ptx::f2(0.f, 0.f), acc1 = acc0;
-      const uint4 ninf{PB::kNegInfWord, PB::kNegInfWord, PB::kNegInfWord, PB::kNegInfWord};
-      for (int32_t v = threadIdx.x; v < nvec; v += U * NT) {
-        uint4 buf[U];
-#pragma unroll
-        for (int k = 0; k < U; ++k) {
-          const int32_t vi = v + k * NT;
-          buf[k] = vi < nvec ? ptx::ld_global_v4_hint(row + vi, pol_keep) : ninf;
-        }
-#pragma unroll
-        for (int k = 0; k < U; k += 2) {
-          const float vm = PB::vmax(buf[k], buf[k + 1]);
-          if (vm > m) {
-            const float rs = ptx::ex2((m - vm) * kLog2e);
-            const uint64_t rs2 = ptx::f2(rs, rs);
-            acc0 = ptx::fmul2(acc0, rs2);
-            acc1 = ptx::fmul2(acc1, rs2);
-            m = vm;
-            negm = ptx::f2(-m, -m);
-          }
-          uint64_t xa[4], xb[4];
-          PB::unpack2(buf[k], xa);
-          PB::unpack2(buf[k + 1], xb);
-          const int ja = y - (v + k * NT) * VN, jb = ja - NT * VN;
-          if (static_cast<uint32_t>(ja) < VN) kill_col(xa, ja);
-          if (static_cast<uint32_t>(jb) < VN) kill_col(xb, jb);
-#pragma unroll
-          for (int i = 0; i < NP; ++i) {
-            acc0 = ptx::fadd2(acc0, ptx::ex2x2(ptx::fmul2(ptx::fadd2(xa[i], negm), L2)));
-            acc1 = ptx::fadd2(acc1, ptx::ex2x2(ptx::fmul2(ptx::fadd2(xb[i], negm), L2)));
-          }
-        }
-      }
-      const uint64_t acc = ptx::fadd2(acc0, acc1);
-      st.m = m;
-      st.s = ptx::f2lo(acc) + ptx::f2hi(acc);
-    }
-    warp_lse<ENT>(st);
-    if (lane == 0) red[warp] = st;
-    __syncthreads();
-
-    const int64_t nxt = r + gridDim.x;
-    if (nxt < P.n_rows) y_next = P.target[P.row_base + nxt];
-    if (warp == 0) {
-      Lse tot = lane < WARPS ? red[lane] : lse_empty();
-      warp_lse<ENT>(tot);
-      if (lane == 0) {
-        const float zy = static_cast<uint32_t>(meta.y) < static_cast<uint32_t>(V)
-                             ? VI::load1(static_cast<const TIn*>(P.logits) + r * P.ld + meta.y) : 0.f;
-        bc = row_scalar_phase<ENT>(P, t, meta.y, meta.st, meta.blp, meta.rl, meta.adv, tot, zy, true, meta.keep);
-      }
-    }
-    __syncthreads();
-
-    // ---- pass 2 (L2 -> registers -> dlogits) ----------------------------------
-    const RowBroadcast b = bc;
-    if (P.dlogits) {
-      TOut* drow = static_cast<TOut*>(P.dlogits) + r * P.ld_d;
-      const bool zero_row = (b.coef == 0.f) && (!ENT || b.eg == 0.f);
-      const uint64_t negM = ptx::f2(-b.m, -b.m);
-      const uint64_t nl2s = ptx::f2(-b.log2s, -b.log2s);
-      const uint64_t ncoef = ptx::f2(-b.coef, -b.coef);
-      if (zero_row) {
-        float d[VN];
-#pragma unroll
-        for (int j = 0; j < VN; ++j) d[j] = 0.f;
-        for (int32_t v = threadIdx.x; v < nvec; v += NT)
-          store_vec<TOut, VN>(drow + static_cast<int64_t>(v) * VN, d, pol_first);
-      } else if constexpr (ENT) {
-        for (int32_t v = threadIdx.x; v < nvec; v += NT) {
-          float x[VN], d[VN];
-          VI::unpack(ptx::ld_global_v4_hint(row + v, pol_first), x);
-          row_grad<VN, ENT>(x, d, v * VN, b);
-          store_vec<TOut, VN>(drow + static_cast<int64_t>(v) * VN, d, pol_first);
-        }
-      } else {
-        for (int32_t v = threadIdx.x; v < nvec; v += U * NT) {
-          uint4 buf[U];
-#pragma unroll
-          for (int k = 0; k < U; ++k) {
-            const int32_t vi = v + k * NT;
-            if (vi < nvec) buf[k] = ptx::ld_global_v4_hint(row + vi, pol_first);
-          }
-#pragma unroll
-          for (int k = 0; k < U; ++k) {
-            const int32_t vi = v + k * NT;
-            if (vi < nvec) {
-              uint64_t x[4];
-              PB::unpack2(buf[k], x);
-              float d[VN];
-#pragma unroll
-              for (int i = 0; i < NP; ++i) {
-                const uint64_t g =
-                    ptx::fmul2(ptx::ex2x2(ptx::ffma2(ptx::fadd2(x[i], negM), L2, nl2s)), ncoef);
-                d[2 * i] = ptx::f2lo(g);
-                d[2 * i + 1] = ptx::f2hi(g);
-              }
-              const int jt = b.y - vi * VN;
-              if (static_cast<uint32_t>(jt) < VN) {
-#pragma unroll
-                for (int j = 0; j < VN; ++j)
-                  if (j == jt) d[j] = b.dy;
-              }
-              store_vec<TOut, VN>(drow + static_cast<int64_t>(vi) * VN, d, pol_first);
-            }
-          }
-        }
-      }
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// fused TMA-streaming kernel (warp-specialised). One producer warp streams
-// every row twice through a ring of shared-memory slots with TMA bulk copies:
-// pass 1 from HBM (lines kept in L2: evict_last), pass 2 from L2 (evict_first).
-// CW consumer warps reduce pass 1 (online log-sum-exp), run the row's scalar
-// phase, and turn pass 2 into dlogits. The producer never waits on the scalar
-// phase — it runs ahead into the next row as far as the ring allows — so HBM
-// stays busy while the consumers synchronise, and no cluster couples SMs.
+// fused TMA-streaming kernel (warp-specialised): constants and ring position
 // ---------------------------------------------------------------------------
 constexpr int kStreamK = 4;  // 16-byte vectors per consumer thread per ring slot
-constexpr int kStreamLookahead = 2;  // ring segments of row r+1 consumed before pass 2 of row r
-#ifndef COPRIS_STREAM_PREFETCH
-#define COPRIS_STREAM_PREFETCH 0  // 1|2 = L2-prefetch next row before pass 1|2; measured slower (L2 thrash)
-#endif
-__device__ __forceinline__ int tune_prefetch() { return COPRIS_STREAM_PREFETCH; }
-
-// Which fp32 pairs of a 16-byte vector take 2^x on the FMA pipe instead of
-// MUFU (bit i = pair i). MUFU.EX2 issues 16 results/clk/SM and two of them per
-// element would otherwise bound the consumers below the HBM rate; moving a
-// quarter of the exponentials to FFMA2 polynomials balances the two pipes.
-#ifndef COPRIS_EMU_MASK
-#define COPRIS_EMU_MASK 0x0
-#endif
-template <int i>
-__device__ __forceinline__ uint64_t exp2_pair(uint64_t x) {
-  if constexpr (((COPRIS_EMU_MASK >> i) & 1) != 0) return ptx::ex2x2_fma(x);
-  return ptx::ex2x2(x);
-}
-
-// Element j of a 16-byte vector: 2^x on MUFU, or on the FMA pipe for the
-// columns selected by COPRIS_EMU_COLS (bit j) — balances the two pipes.
-#ifndef COPRIS_EMU_COLS
-#define COPRIS_EMU_COLS 0x00
-#endif
-template <int j>
-__device__ __forceinline__ float exp2_col(float x) {
-  if constexpr (((COPRIS_EMU_COLS >> j) & 1) != 0) return ptx::ex2_fma(x);
-  return ptx::ex2(x);
-}
 
 // Position in the slot ring (slot index + phase parity), advanced without
 // integer division.
@@ -901,295 +696,6 @@ struct Ring {
     }
   }
 };
-
-template <typename TIn, typename TOut, int CW, int KV, bool ENT>
-__global__ void __launch_bounds__((CW + 1) * 32, CW <= 8 ? 2 : 1)
-    fused_stream_kernel(const LossParams P, const int nslots) {
-  constexpr int kStreamSlotVec = CW * 32 * KV;  // vectors per ring slot
-  using VI = Vec<TIn>;
-  using PB = PassB<TIn>;
-  constexpr int VN = VI::N;
-  constexpr int NC = CW * 32;                  // consumer threads
-  constexpr int K = KV;                        // vectors per consumer thread per slot
-  extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t full[32], empty[32];
-  __shared__ Lse red[CW];
-  __shared__ RowBroadcast bc;
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int32_t V = P.vocab;
-  const int32_t nvec = V / VN;
-  const int32_t nseg = (nvec + kStreamSlotVec - 1) / kStreamSlotVec;
-  const uint32_t sbase = ptx::smem_u32(smem);
-  const uint32_t fbase = ptx::smem_u32(full), ebase = ptx::smem_u32(empty);
-
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < nslots; ++i) {
-      ptx::mbar_init(&full[i], 1);
-      ptx::mbar_init(&empty[i], CW);
-    }
-    ptx::fence_mbarrier_init();
-  }
-  __syncthreads();
-
-  if (warp == CW) {
-    // ---------------- producer ----------------
-    if (lane == 0) {
-      const uint64_t keep = ptx::policy_evict_last(), drop = ptx::policy_evict_first();
-      Ring ring(nslots);
-      const int pf = tune_prefetch();
-      for (int64_t r = blockIdx.x; r < P.n_rows; r += gridDim.x) {
-        const TIn* row = static_cast<const TIn*>(P.logits) + r * P.ld;
-        for (int pass = 0; pass < 2; ++pass) {
-          if (pass == 1 && !P.dlogits) break;
-          // Before the (L2-resident) second pass of row r, pull the next row
-          // toward L2 so its HBM reads overlap this row's dlogits writes.
-          if (pass == pf - 1 && r + gridDim.x < P.n_rows) {
-            const TIn* nrow = static_cast<const TIn*>(P.logits) + (r + gridDim.x) * P.ld;
-            for (int32_t v0 = 0; v0 < nvec; v0 += kStreamSlotVec)
-              ptx::bulk_prefetch_l2(nrow + static_cast<int64_t>(v0) * VN,
-                                    static_cast<uint32_t>(min(kStreamSlotVec, nvec - v0)) * 16u, keep);
-          }
-          for (int32_t sg = 0; sg < nseg; ++sg, ring.next()) {
-            const uint32_t slot = ring.slot, par = ring.ph;
-            ptx::mbar_wait_u32(ebase + slot * 8, par ^ 1u);
-            const int32_t v0 = sg * kStreamSlotVec;
-            const uint32_t bytes = static_cast<uint32_t>(min(kStreamSlotVec, nvec - v0)) * 16u;
-            ptx::mbar_arrive_expect_tx_u32(fbase + slot * 8, bytes);
-            ptx::bulk_g2s_u32(sbase + slot * (kStreamSlotVec * 16), row + static_cast<int64_t>(v0) * VN,
-                              bytes, fbase + slot * 8, pass == 0 ? keep : drop);
-          }
-        }
-      }
-    }
-    return;
-  }
-
-  // ---------------- consumers ----------------
-  const int tid = threadIdx.x;  // 0 .. NC-1
-  const uint64_t pol = ptx::policy_evict_first();
-  const uint64_t L2 = ptx::f2(kLog2e, kLog2e);
-  Ring ring(nslots);
-  int64_t r = blockIdx.x;
-  int32_t y_next = r < P.n_rows ? P.target[P.row_base + r] : 0;
-  MetaPipe mp;
-  if (tid == 0) mp.init(P, r, gridDim.x);
-
-  PhaseTimer tm;
-  tm.start(P.trace && tid == 0 && blockIdx.x < kTraceCtas);
-  for (; r < P.n_rows; r += gridDim.x) {
-    const int64_t t = P.row_base + r;
-    const int32_t y = y_next;
-    RowMeta meta{};
-    if (tid == 0) meta = mp.advance(P, r, gridDim.x);
-
-    // ---- pass 1 ----
-    Lse st = lse_empty();
-    float m = -INFINITY, nml = INFINITY;
-    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-    float zy_local = 0.f;
-    bool have_zy = false;
-    for (int32_t sg = 0; sg < nseg; ++sg, ring.next()) {
-      const uint32_t slot = ring.slot, par = ring.ph;
-      const uint32_t sb = sbase + slot * (kStreamSlotVec * 16);
-      const int32_t v0 = sg * kStreamSlotVec;
-      const int32_t cnt = min(kStreamSlotVec, nvec - v0);
-      const long long w0 = tm.on ? clock64() : 0;
-      ptx::mbar_wait_u32(fbase + slot * 8, par);
-      if (tm.on) tm.acc[6] += clock64() - w0;
-      if constexpr (ENT) {
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          const int32_t j = tid + k * NC;
-          if (j < cnt) {
-            float x[VN];
-            VI::unpack(ptx::lds_v4(sb + j * 16), x);
-            const int jt = y - (v0 + j) * VN;
-            if (static_cast<uint32_t>(jt) < VN) {
-#pragma unroll
-              for (int q = 0; q < VN; ++q)
-                if (q == jt) zy_local = x[q];
-              have_zy = true;
-            }
-            online_update<VN, true>(x, st, static_cast<uint32_t>(jt) < VN ? jt : -1);
-          }
-        }
-      } else {
-        // does this segment hold the target column? (warp-uniform)
-        const bool tseg = static_cast<uint32_t>(y - v0 * VN) < static_cast<uint32_t>(cnt * VN);
-        const bool full_seg = cnt == kStreamSlotVec;  // warp-uniform: no bounds checks
-#pragma unroll
-        for (int k = 0; k < K; k += 2) {
-          const int32_t ja_i = tid + k * NC, jb_i = ja_i + NC;
-          uint4 a, b;
-          if (full_seg) {
-            a = ptx::lds_v4(sb + ja_i * 16);
-            b = ptx::lds_v4(sb + jb_i * 16);
-          } else {
-            const uint4 ninf{PB::kNegInfWord, PB::kNegInfWord, PB::kNegInfWord, PB::kNegInfWord};
-            a = ja_i < cnt ? ptx::lds_v4(sb + ja_i * 16) : ninf;
-            b = jb_i < cnt ? ptx::lds_v4(sb + jb_i * 16) : ninf;
-          }
-          const float vm = PB::vmax(a, b);
-          if (vm > m) {
-            const float rs = ptx::ex2((m - vm) * kLog2e);
-            s0 *= rs;
-            s1 *= rs;
-            s2 *= rs;
-            s3 *= rs;
-            m = vm;
-            nml = -(m * kLog2e);
-          }
-          float xa[VN], xb[VN];
-          VI::unpack(a, xa);
-          VI::unpack(b, xb);
-          if (tseg) {
-            const int ja = y - (v0 + ja_i) * VN, jb = y - (v0 + jb_i) * VN;
-#pragma unroll
-            for (int q = 0; q < VN; ++q) {
-              if (q == ja) {
-                zy_local = xa[q];
-                have_zy = true;
-                xa[q] = -INFINITY;
-              }
-              if (q == jb) {
-                zy_local = xb[q];
-                have_zy = true;
-                xb[q] = -INFINITY;
-              }
-            }
-          }
-          // e = 2^(x log2e - m log2e); four independent accumulators
-          s0 += exp2_col<0>(fmaf(xa[0], kLog2e, nml));
-          s1 += exp2_col<1>(fmaf(xa[1], kLog2e, nml));
-          s2 += exp2_col<0>(fmaf(xb[0], kLog2e, nml));
-          s3 += exp2_col<1>(fmaf(xb[1], kLog2e, nml));
-          s0 += exp2_col<2>(fmaf(xa[2], kLog2e, nml));
-          s1 += exp2_col<3>(fmaf(xa[3], kLog2e, nml));
-          s2 += exp2_col<2>(fmaf(xb[2], kLog2e, nml));
-          s3 += exp2_col<3>(fmaf(xb[3], kLog2e, nml));
-          if constexpr (VN == 8) {
-            s0 += exp2_col<4>(fmaf(xa[4], kLog2e, nml));
-            s1 += exp2_col<5>(fmaf(xa[5], kLog2e, nml));
-            s2 += exp2_col<4>(fmaf(xb[4], kLog2e, nml));
-            s3 += exp2_col<5>(fmaf(xb[5], kLog2e, nml));
-            s0 += exp2_col<6>(fmaf(xa[6], kLog2e, nml));
-            s1 += exp2_col<7>(fmaf(xa[7], kLog2e, nml));
-            s2 += exp2_col<6>(fmaf(xb[6], kLog2e, nml));
-            s3 += exp2_col<7>(fmaf(xb[7], kLog2e, nml));
-          }
-        }
-      }
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive_u32(ebase + slot * 8);
-    }
-    if constexpr (!ENT) {
-      st.m = m;
-      st.s = (s0 + s1) + (s2 + s3);
-    }
-    tm.mark(0);
-    warp_lse<ENT>(st);
-    if (lane == 0) red[warp] = st;
-    __shared__ float zy_sh;
-    if (have_zy) zy_sh = zy_local;  // exactly one consumer thread owns the target
-    ptx::named_bar_sync(1, NC);
-    tm.mark(1);
-
-    const int64_t nxt = r + gridDim.x;
-    if (nxt < P.n_rows) y_next = P.target[P.row_base + nxt];
-    if (warp == 0) {
-      Lse tot = lane < CW ? red[lane] : lse_empty();
-      warp_lse<ENT>(tot);
-      if (lane == 0) {
-        const float zy = static_cast<uint32_t>(meta.y) < static_cast<uint32_t>(V) ? zy_sh : 0.f;
-        bc = row_scalar_phase<ENT>(P, t, meta.y, meta.st, meta.blp, meta.rl, meta.adv, tot, zy, true, meta.keep);
-      }
-    }
-    tm.mark(2);
-    ptx::named_bar_sync(1, NC);
-    tm.mark(3);
-
-    // ---- pass 2 ----
-    if (!P.dlogits) continue;
-    const RowBroadcast b = bc;
-    TOut* drow = static_cast<TOut*>(P.dlogits) + r * P.ld_d;
-    const bool zero_row = (b.coef == 0.f) && (!ENT || b.eg == 0.f);
-    const uint64_t nc1 = ptx::f2(-b.c1, -b.c1);
-    const uint64_t ncoef = ptx::f2(-b.coef, -b.coef);
-    for (int32_t sg = 0; sg < nseg; ++sg, ring.next()) {
-      const uint32_t slot = ring.slot, par = ring.ph;
-      const uint32_t sb = sbase + slot * (kStreamSlotVec * 16);
-      const int32_t v0 = sg * kStreamSlotVec;
-      const int32_t cnt = min(kStreamSlotVec, nvec - v0);
-      const bool tseg = static_cast<uint32_t>(b.y - v0 * VN) < static_cast<uint32_t>(cnt * VN);
-      const long long w0 = tm.on ? clock64() : 0;
-      ptx::mbar_wait_u32(fbase + slot * 8, par);
-      if (tm.on) tm.acc[7] += clock64() - w0;
-      TOut* dseg = drow + static_cast<int64_t>(v0) * VN;
-      if (!ENT && !zero_row && cnt == kStreamSlotVec) {
-        // full segment: all K shared-memory loads first, then the math, then the stores
-        uint4 raw[K];
-#pragma unroll
-        for (int q = 0; q < K; ++q) raw[q] = ptx::lds_v4(sb + (tid + q * NC) * 16);
-#pragma unroll
-        for (int q = 0; q < K; ++q) {
-          float x[VN], d[VN];
-          VI::unpack(raw[q], x);
-          d[0] = exp2_col<0>(fmaf(x[0], kLog2e, -b.c1)) * -b.coef;
-          d[1] = exp2_col<1>(fmaf(x[1], kLog2e, -b.c1)) * -b.coef;
-          d[2] = exp2_col<2>(fmaf(x[2], kLog2e, -b.c1)) * -b.coef;
-          d[3] = exp2_col<3>(fmaf(x[3], kLog2e, -b.c1)) * -b.coef;
-          if constexpr (VN == 8) {
-            d[4] = exp2_col<4>(fmaf(x[4], kLog2e, -b.c1)) * -b.coef;
-            d[5] = exp2_col<5>(fmaf(x[5], kLog2e, -b.c1)) * -b.coef;
-            d[6] = exp2_col<6>(fmaf(x[6], kLog2e, -b.c1)) * -b.coef;
-            d[7] = exp2_col<7>(fmaf(x[7], kLog2e, -b.c1)) * -b.coef;
-          }
-          if (tseg) {
-            const int jt = b.y - (v0 + tid + q * NC) * VN;
-#pragma unroll
-            for (int e = 0; e < VN; ++e)
-              if (e == jt) d[e] = b.dy;
-          }
-          store_vec<TOut, VN>(dseg + static_cast<int64_t>(tid + q * NC) * VN, d, pol);
-        }
-      } else {
-#pragma unroll
-        for (int q = 0; q < K; ++q) {
-          const int32_t j = tid + q * NC;
-          if (j < cnt) {
-            float d[VN];
-            if (zero_row) {
-#pragma unroll
-              for (int e = 0; e < VN; ++e) d[e] = 0.f;
-            } else {
-              float x[VN];
-              VI::unpack(ptx::lds_v4(sb + j * 16), x);
-              if constexpr (ENT) {
-                row_grad<VN, ENT>(x, d, (v0 + j) * VN, b);
-              } else {
-#pragma unroll
-                for (int e = 0; e < VN; ++e) d[e] = ptx::ex2(fmaf(x[e], kLog2e, -b.c1)) * -b.coef;
-                if (tseg) {
-                  const int jt = b.y - (v0 + j) * VN;
-#pragma unroll
-                  for (int e = 0; e < VN; ++e)
-                    if (e == jt) d[e] = b.dy;
-                }
-              }
-            }
-            store_vec<TOut, VN>(dseg + static_cast<int64_t>(j) * VN, d, pol);
-          }
-        }
-      }
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive_u32(ebase + slot * 8);
-    }
-    tm.mark(4);
-    tm.acc[5] += 1;
-  }
-  tm.flush(P.trace);
-}
 
 // ---------------------------------------------------------------------------
 // fused_stream_la_kernel: the streaming kernel with a one-row lookahead that
@@ -1818,8 +1324,8 @@ __global__ void terminal_rewards_kernel(const int32_t* __restrict__ tokens,
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n_traj;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t b = tok_off[i], n = tok_off[i + 1] - b;
-    if (!terminated[i] || n == 0) {  // grpo.hpp:36,38
-      atomicOr(err, ERR_NOT_TERMINATED);
+    if (!terminated[i] || n == 0) {  // grpo.hpp:36,38 (two different messages)
+      atomicOr(err, terminated[i] ? ERR_EMPTY_TERMINATED : ERR_NOT_TERMINATED);
       out[i] = 0.0;
       continue;
     }
@@ -2018,165 +1524,73 @@ int grid_rows(int64_t n_rows, int num_sms, int per_sm) {
   return static_cast<int>(g < 1 ? 1 : g);
 }
 
-template <typename TIn, typename TOut, int CL, int WARPS, bool ENT>
+template <typename TIn, typename TOut, int WARPS, bool ENT>
 cudaError_t launch_tma(const LossParams& p, int32_t E, int num_sms, cudaStream_t stream,
                        LaunchInfo* info) {
   constexpr int VN = Vec<TIn>::N;
+  constexpr int CL = 1;
   auto kernel = fused_tma_kernel<TIn, TOut, CL, WARPS, ENT>;
   const int smem = ((E / VN) * 16 + 127) / 128 * 128;
   cudaError_t e = set_smem(kernel, smem);
   if (e != cudaSuccess) return e;
-  cudaLaunchConfig_t cfg{};
-  cudaLaunchAttribute attr[1];
-  cfg.blockDim = dim3(WARPS * 32);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = stream;
-  int resident = 0;
-  if (CL > 1) {
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CL;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cfg.gridDim = dim3(CL * num_sms);
-    int ncl = 0;
-    e = cudaOccupancyMaxActiveClusters(&ncl, kernel, &cfg);
-    if (e != cudaSuccess) return e;
-    resident = ncl;
-  } else {
-    int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, WARPS * 32, smem);
-    if (e != cudaSuccess) return e;
-    resident = per_sm * num_sms;
-  }
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, WARPS * 32, smem);
+  if (e != cudaSuccess) return e;
+  const int64_t resident = static_cast<int64_t>(per_sm) * num_sms;
   if (resident < 1) return cudaErrorInvalidConfiguration;
-  int64_t ncl = resident;
-  if (p.n_rows < ncl) ncl = p.n_rows;
-  cfg.gridDim = dim3(static_cast<unsigned>(ncl * CL));
+  const int64_t grid = p.n_rows < resident ? p.n_rows : resident;
   if (info) {
     info->cluster = CL;
-    info->grid = static_cast<int>(ncl * CL);
+    info->grid = static_cast<int>(grid);
     info->kernel = "fused_tma_kernel";
   }
-  if (CL == 1 && p.row_ctr) {
+  if (p.row_ctr) {
     e = cudaMemsetAsync(p.row_ctr, 0, sizeof(unsigned long long), stream);
     if (e != cudaSuccess) return e;
   }
-  return cudaLaunchKernelEx(&cfg, kernel, p, E);
-}
-
-// Tuning overrides for experiments (bf16 -> bf16, no entropy only):
-// COPRIS_TUNE_CL in {2, 4} and COPRIS_TUNE_WARPS in {8, 16, 32}.
-int tune_env(const char* name, int dflt) {
-  const char* e = getenv(name);
-  return e ? atoi(e) : dflt;
-}
-
-template <typename TIn, typename TOut, bool ENT>
-bool launch_tuned(const LossParams& p, int num_sms, cudaStream_t stream, LaunchInfo* info,
-                  cudaError_t* err) {
-  if constexpr (std::is_same<TIn, __nv_bfloat16>::value && std::is_same<TOut, __nv_bfloat16>::value && !ENT) {
-    static const int cl = tune_env("COPRIS_TUNE_CL", 0), w = tune_env("COPRIS_TUNE_WARPS", 0);
-    if (cl == 0 && w == 0) return false;
-    const int c = cl ? cl : 2, ww = w ? w : 16;
-    const int64_t per = (p.vocab + c - 1) / c;
-    const int32_t E = static_cast<int32_t>((per + 7) / 8 * 8);
-    if (c == 2 && ww == 8) *err = launch_tma<TIn, TOut, 2, 8, ENT>(p, E, num_sms, stream, info);
-    else if (c == 2 && ww == 16) *err = launch_tma<TIn, TOut, 2, 16, ENT>(p, E, num_sms, stream, info);
-    else if (c == 2 && ww == 32) *err = launch_tma<TIn, TOut, 2, 32, ENT>(p, E, num_sms, stream, info);
-    else if (c == 4 && ww == 8) *err = launch_tma<TIn, TOut, 4, 8, ENT>(p, E, num_sms, stream, info);
-    else if (c == 4 && ww == 16) *err = launch_tma<TIn, TOut, 4, 16, ENT>(p, E, num_sms, stream, info);
-    else return false;
-    return true;
-  }
-  return false;
-}
-
-template <typename TIn, typename TOut, int WARPS, int U, bool ENT>
-cudaError_t launch_l2(const LossParams& p, int num_sms, cudaStream_t stream, LaunchInfo* info) {
-  auto kernel = fused_l2_kernel<TIn, TOut, WARPS, U, ENT>;
-  int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, WARPS * 32, 0);
-  if (e != cudaSuccess) return e;
-  const int cap = tune_env("COPRIS_TUNE_CTAS", 0);
-  if (cap > 0 && cap < per_sm) per_sm = cap;
-  const int grid = grid_rows(p.n_rows, num_sms, per_sm < 1 ? 1 : per_sm);
-  if (info) {
-    info->cluster = 1;
-    info->grid = grid;
-    info->kernel = "fused_l2_kernel";
-  }
-  kernel<<<grid, WARPS * 32, 0, stream>>>(p, tune_env("COPRIS_TUNE_KEEP", 2));
+  kernel<<<static_cast<unsigned>(grid), WARPS * 32, smem, stream>>>(p, E);
   return cudaGetLastError();
 }
 
-template <typename TIn, typename TOut, int CW, bool ENT, int KV = kStreamK>
-cudaError_t launch_stream(const LossParams& p, int num_sms, cudaStream_t stream, LaunchInfo* info) {
-  const int look = tune_env("COPRIS_TUNE_LOOKAHEAD", kStreamLookahead);
-  if (look > 0) {
-    auto kernel = fused_stream_la_kernel<TIn, TOut, CW, KV, ENT>;
-    constexpr int slot_bytes = CW * 32 * KV * 16;
-    const int nslots = tune_env("COPRIS_TUNE_SLOTS", (CW >= 16 ? 196608 : 98304) / slot_bytes);
-    const int smem = nslots * slot_bytes;
-    cudaError_t e = set_smem(kernel, smem);
-    if (e != cudaSuccess) return e;
-    int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, (CW + 2) * 32, smem);
-    if (e != cudaSuccess) return e;
-    const int grid = grid_rows(p.n_rows, num_sms, per_sm < 1 ? 1 : per_sm);
-    if (info) {
-      info->cluster = 1;
-      info->grid = grid;
-      info->kernel = "fused_stream_la_kernel";
-    }
-    // resident rows: three whole rows fit in the ring (pass 2 reuses pass 1's
-    // segments instead of re-reading the row from L2)
-    const int64_t nseg = (p.vocab / Vec<TIn>::N + CW * 32 * KV - 1) / (CW * 32 * KV);
-    const int resident = tune_env("COPRIS_TUNE_RESIDENT", 1) && p.dlogits != nullptr &&
-                         3 * nseg <= nslots;
-    if (info) info->kernel = resident ? "fused_stream_la_kernel[resident]" : "fused_stream_la_kernel";
-    kernel<<<grid, (CW + 2) * 32, smem, stream>>>(p, nslots, look, resident);
-    return cudaGetLastError();
-  }
-  auto kernel = fused_stream_kernel<TIn, TOut, CW, KV, ENT>;
+template <typename TIn, typename TOut, bool ENT>
+cudaError_t launch_stream(const LossParams& p, int num_sms, const Tuning& tu, cudaStream_t stream,
+                          LaunchInfo* info) {
+  constexpr int CW = 16, KV = kStreamK;
+  auto kernel = fused_stream_la_kernel<TIn, TOut, CW, KV, ENT>;
   constexpr int slot_bytes = CW * 32 * KV * 16;
-  const int nslots = tune_env("COPRIS_TUNE_SLOTS", (CW >= 16 ? 196608 : 98304) / slot_bytes);
+  const int nslots = tu.slots > 0 ? tu.slots : 196608 / slot_bytes;
+  if (nslots > 32 || nslots < 2) return cudaErrorInvalidValue;
   const int smem = nslots * slot_bytes;
   cudaError_t e = set_smem(kernel, smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, (CW + 1) * 32, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, (CW + 2) * 32, smem);
   if (e != cudaSuccess) return e;
   const int grid = grid_rows(p.n_rows, num_sms, per_sm < 1 ? 1 : per_sm);
+  // resident rows: three whole rows fit in the ring (pass 2 reuses pass 1's
+  // segments instead of re-reading the row from L2)
+  const int64_t nseg = (p.vocab / Vec<TIn>::N + CW * 32 * KV - 1) / (CW * 32 * KV);
+  const int resident = tu.resident && p.dlogits != nullptr && 3 * nseg <= nslots;
   if (info) {
     info->cluster = 1;
     info->grid = grid;
-    info->kernel = "fused_stream_kernel";
+    info->kernel = resident ? "fused_stream_la_kernel[resident]" : "fused_stream_la_kernel";
   }
-  kernel<<<grid, (CW + 1) * 32, smem, stream>>>(p, nslots);
+  kernel<<<grid, (CW + 2) * 32, smem, stream>>>(p, nslots, tu.lookahead < 0 ? 0 : tu.lookahead,
+                                                 resident);
   return cudaGetLastError();
 }
 
-// Fused-kernel selection. COPRIS_FUSED_IMPL (read per call) forces one of
-// "stream", "tma", "l2" for experiments and tests; "auto" (default) picks:
+// Fused-kernel selection (ctx tuning `fused_impl`: 0 auto, 1 stream, 2 tma):
 //   rows <= 72 KB : fused_tma_kernel, whole row in shared memory, several
 //                   CTAs per SM (independent rows overlap their sync phases);
-//   larger rows   : fused_stream_kernel (TMA ring + L2 re-read, 1 CTA/SM);
+//   larger rows   : fused_stream_la_kernel (TMA ring + L2 re-read, 1 CTA/SM);
 //   unaligned     : fused_generic_kernel.
-int fused_impl() {
-  const char* e = getenv("COPRIS_FUSED_IMPL");
-  if (!e || !*e || !strcmp(e, "auto")) return 0;
-  if (!strcmp(e, "stream")) return 1;
-  if (!strcmp(e, "tma")) return 2;
-  if (!strcmp(e, "l2")) return 3;
-  return 0;
-}
-
 template <typename TIn, typename TOut, bool ENT>
-cudaError_t dispatch_fused(const LossParams& p, int num_sms, cudaStream_t stream, LaunchInfo* info) {
+cudaError_t dispatch_fused(const LossParams& p, int num_sms, const Tuning& tu, cudaStream_t stream,
+                           LaunchInfo* info) {
   constexpr int VN = Vec<TIn>::N;
-  constexpr int64_t kMaxChunkBytes = 200 * 1024;
+  constexpr int64_t kMaxTmaRowBytes = 200 * 1024;
   const int64_t row_bytes = static_cast<int64_t>(p.vocab) * sizeof(TIn);
   const bool aligned = (p.vocab % VN == 0) && ((p.ld * sizeof(TIn)) % 16 == 0) &&
                        (reinterpret_cast<uintptr_t>(p.logits) % 16 == 0) &&
@@ -2184,37 +1598,16 @@ cudaError_t dispatch_fused(const LossParams& p, int num_sms, cudaStream_t stream
                         (((p.ld_d * sizeof(TOut)) % 16 == 0) &&
                          (reinterpret_cast<uintptr_t>(p.dlogits) % 16 == 0))) &&
                        p.vocab >= 32 * VN;
-  auto chunk = [&](int cl) {
-    const int64_t per = (p.vocab + cl - 1) / cl;
-    return static_cast<int32_t>((per + VN - 1) / VN * VN);
-  };
   if (aligned) {
-    int impl = fused_impl();
+    int impl = tu.fused_impl;
+    if (impl == 2 && row_bytes > kMaxTmaRowBytes) impl = 1;
     if (impl == 0) impl = row_bytes <= 72 * 1024 ? 2 : 1;
-    if (impl == 1) {
-      const int w = tune_env("COPRIS_TUNE_WARPS", 16);
-      if (w == 8) return launch_stream<TIn, TOut, 8, ENT>(p, num_sms, stream, info);
-      if (w == 24) return launch_stream<TIn, TOut, 24, ENT>(p, num_sms, stream, info);
-      if (tune_env("COPRIS_TUNE_K", 4) == 8) return launch_stream<TIn, TOut, 16, ENT, 8>(p, num_sms, stream, info);
-      if (tune_env("COPRIS_TUNE_K", 4) == 2) return launch_stream<TIn, TOut, 16, ENT, 2>(p, num_sms, stream, info);
-      return launch_stream<TIn, TOut, 16, ENT>(p, num_sms, stream, info);
+    if (impl == 2) {
+      const int32_t E = static_cast<int32_t>((p.vocab + VN - 1) / VN * VN);
+      if (row_bytes <= 72 * 1024) return launch_tma<TIn, TOut, 8, ENT>(p, E, num_sms, stream, info);
+      return launch_tma<TIn, TOut, 16, ENT>(p, E, num_sms, stream, info);
     }
-    if (impl == 3) {
-      const int w = tune_env("COPRIS_TUNE_WARPS", 32);
-      if (w == 8) return launch_l2<TIn, TOut, 8, 4, ENT>(p, num_sms, stream, info);
-      if (w == 16) return launch_l2<TIn, TOut, 16, 4, ENT>(p, num_sms, stream, info);
-      return launch_l2<TIn, TOut, 32, 4, ENT>(p, num_sms, stream, info);
-    }
-    // impl == 2: whole row resident in shared memory (split over a cluster)
-    if (row_bytes <= 72 * 1024) return launch_tma<TIn, TOut, 1, 8, ENT>(p, chunk(1), num_sms, stream, info);
-    if (row_bytes <= kMaxChunkBytes) return launch_tma<TIn, TOut, 1, 16, ENT>(p, chunk(1), num_sms, stream, info);
-    if (row_bytes <= 2 * kMaxChunkBytes) {
-      cudaError_t e;
-      if (launch_tuned<TIn, TOut, ENT>(p, num_sms, stream, info, &e)) return e;
-      return launch_tma<TIn, TOut, 2, 16, ENT>(p, chunk(2), num_sms, stream, info);
-    }
-    if (row_bytes <= 4 * kMaxChunkBytes) return launch_tma<TIn, TOut, 4, 16, ENT>(p, chunk(4), num_sms, stream, info);
-    return launch_stream<TIn, TOut, 16, ENT>(p, num_sms, stream, info);
+    return launch_stream<TIn, TOut, ENT>(p, num_sms, tu, stream, info);
   }
   if (info) {
     info->cluster = 1;
@@ -2248,37 +1641,38 @@ cudaError_t dispatch_bwd(const LossParams& p, int num_sms, cudaStream_t stream, 
 
 template <bool ENT>
 cudaError_t by_types(bool bwd, const LossParams& p, DType in, DType out, int num_sms,
-                     cudaStream_t stream, LaunchInfo* info) {
+                     const Tuning& tu, cudaStream_t stream, LaunchInfo* info) {
   using bf16 = __nv_bfloat16;
   if (in == DType::BF16 && out == DType::BF16)
     return bwd ? dispatch_bwd<bf16, bf16, ENT>(p, num_sms, stream, info)
-               : dispatch_fused<bf16, bf16, ENT>(p, num_sms, stream, info);
+               : dispatch_fused<bf16, bf16, ENT>(p, num_sms, tu, stream, info);
   if (in == DType::BF16 && out == DType::F32)
     return bwd ? dispatch_bwd<bf16, float, ENT>(p, num_sms, stream, info)
-               : dispatch_fused<bf16, float, ENT>(p, num_sms, stream, info);
+               : dispatch_fused<bf16, float, ENT>(p, num_sms, tu, stream, info);
   if (in == DType::F32 && out == DType::BF16)
     return bwd ? dispatch_bwd<float, bf16, ENT>(p, num_sms, stream, info)
-               : dispatch_fused<float, bf16, ENT>(p, num_sms, stream, info);
+               : dispatch_fused<float, bf16, ENT>(p, num_sms, tu, stream, info);
   return bwd ? dispatch_bwd<float, float, ENT>(p, num_sms, stream, info)
-             : dispatch_fused<float, float, ENT>(p, num_sms, stream, info);
+             : dispatch_fused<float, float, ENT>(p, num_sms, tu, stream, info);
 }
 
 }  // namespace
 
-cudaError_t launch_fused(const LossParams& p, DType in, DType out, int num_sms,
+cudaError_t launch_fused(const LossParams& p, DType in, DType out, int num_sms, const Tuning& tu,
                          cudaStream_t stream, LaunchInfo* info) {
   if (info) info->num_sms = num_sms;
   if (p.n_rows == 0) return cudaSuccess;
-  return p.entropy_coeff != 0.0 ? by_types<true>(false, p, in, out, num_sms, stream, info)
-                                : by_types<false>(false, p, in, out, num_sms, stream, info);
+  return p.entropy_coeff != 0.0 ? by_types<true>(false, p, in, out, num_sms, tu, stream, info)
+                                : by_types<false>(false, p, in, out, num_sms, tu, stream, info);
 }
 
 cudaError_t launch_bwd(const LossParams& p, DType in, DType out, int num_sms,
                        cudaStream_t stream, LaunchInfo* info) {
   if (info) info->num_sms = num_sms;
   if (p.n_rows == 0) return cudaSuccess;
-  return p.entropy_coeff != 0.0 ? by_types<true>(true, p, in, out, num_sms, stream, info)
-                                : by_types<false>(true, p, in, out, num_sms, stream, info);
+  const Tuning tu{};
+  return p.entropy_coeff != 0.0 ? by_types<true>(true, p, in, out, num_sms, tu, stream, info)
+                                : by_types<false>(true, p, in, out, num_sms, tu, stream, info);
 }
 
 // K1 = the fused kernels in gather-only mode: the same TMA/shared-memory
@@ -2288,7 +1682,7 @@ cudaError_t launch_bwd(const LossParams& p, DType in, DType out, int num_sms,
 cudaError_t launch_logprob_gather(const void* logits, int64_t ld, DType in, const int32_t* target,
                                   int64_t n_tok, int32_t vocab, float* out_lp, float* out_lse,
                                   uint32_t* err, unsigned long long* row_ctr, int num_sms,
-                                  cudaStream_t stream) {
+                                  const Tuning& tu, cudaStream_t stream) {
   if (n_tok == 0) return cudaSuccess;
   LossParams p{};
   p.logits = logits;
@@ -2305,8 +1699,89 @@ cudaError_t launch_logprob_gather(const void* logits, int64_t ld, DType in, cons
   p.clamp_lo = 0.8;
   p.clamp_hi = 1.28;
   p.inv_t = 1.0;
-  return launch_fused(p, in, DType::BF16, num_sms, stream, nullptr);
+  return launch_fused(p, in, DType::BF16, num_sms, tu, stream, nullptr);
 }
+
+// ---------------------------------------------------------------------------
+// per-context tuning (read from the environment once, at context creation)
+// ---------------------------------------------------------------------------
+namespace {
+using I32Field = int Tuning::*;
+using I64Field = int64_t Tuning::*;
+struct TuneField {
+  const char* name;  // option name (copris_ctx_set_option)
+  const char* env;   // COPRIS_* variable read by tuning_from_env
+  int64_t lo, hi;
+  I32Field i32;
+  I64Field i64;
+};
+const TuneField kFields[] = {
+    {"fused_impl", "COPRIS_FUSED_IMPL", 0, 3, &Tuning::fused_impl, nullptr},
+    {"lookahead", "COPRIS_TUNE_LOOKAHEAD", 0, 16, &Tuning::lookahead, nullptr},
+    {"slots", "COPRIS_TUNE_SLOTS", 0, 32, &Tuning::slots, nullptr},
+    {"resident", "COPRIS_TUNE_RESIDENT", 0, 1, &Tuning::resident, nullptr},
+    {"one_exp", "COPRIS_ONE_EXP", 0, 1, &Tuning::one_exp, nullptr},
+    {"lmhead_impl", "COPRIS_LMHEAD_IMPL", 0, 1, &Tuning::lmhead_impl, nullptr},
+    {"lmhead_group", "COPRIS_LMHEAD_GROUP", 1, 1 << 20, &Tuning::lmhead_group, nullptr},
+    {"lmhead_tma_store", "COPRIS_LMHEAD_TMA_STORE", 0, 1, &Tuning::lmhead_tma_store, nullptr},
+    {"gemm_wide", "COPRIS_GEMM_WIDE", 0, 1, &Tuning::gemm_wide, nullptr},
+    {"gemm_mc", "COPRIS_GEMM_MC", 0, 1, &Tuning::gemm_mc, nullptr},
+    {"gemm_splits", "COPRIS_GEMM_SPLITS", 0, 64, &Tuning::gemm_splits, nullptr},
+    {"gemm_a_evict_first", "COPRIS_GEMM_A_EVICT_FIRST", 0, 3, &Tuning::gemm_a_evict_first, nullptr},
+    {"dw_group", "COPRIS_DW_GROUP", 1, 1 << 20, &Tuning::dw_group, nullptr},
+    {"dw_policy", "COPRIS_DW_POLICY", 0, 3, &Tuning::dw_policy, nullptr},
+    {"dw_kchunk", "COPRIS_DW_KCHUNK", 64, int64_t(1) << 40, nullptr, &Tuning::dw_kchunk},
+    {"trace", "COPRIS_TRACE", 0, 1, &Tuning::trace, nullptr},
+};
+
+// fused_impl and lmhead_impl also accept their names in the environment
+int64_t parse_env(const TuneField& f, const char* v) {
+  if (!strcmp(f.name, "fused_impl")) {
+    if (!strcmp(v, "auto") || !*v) return 0;
+    if (!strcmp(v, "stream")) return 1;
+    if (!strcmp(v, "tma")) return 2;
+    if (!strcmp(v, "pair")) return 3;
+  }
+  if (!strcmp(f.name, "lmhead_impl")) {
+    if (!strcmp(v, "1sm")) return 1;
+    if (!strcmp(v, "pair")) return 0;
+  }
+  if (!strcmp(f.name, "trace")) return 1;  // any value turns tracing on
+  return atoll(v);
+}
+}  // namespace
+
+bool tuning_set(Tuning& t, const char* name, int64_t value) {
+  if (!name) return false;
+  for (const TuneField& f : kFields) {
+    if (strcmp(f.name, name) != 0) continue;
+    if (value < f.lo || value > f.hi) return false;
+    if (f.i32) t.*(f.i32) = static_cast<int>(value);
+    else t.*(f.i64) = value;
+    return true;
+  }
+  return false;
+}
+
+bool tuning_get(const Tuning& t, const char* name, int64_t* value) {
+  if (!name || !value) return false;
+  for (const TuneField& f : kFields) {
+    if (strcmp(f.name, name) != 0) continue;
+    *value = f.i32 ? static_cast<int64_t>(t.*(f.i32)) : t.*(f.i64);
+    return true;
+  }
+  return false;
+}
+
+Tuning tuning_from_env() {
+  Tuning t;
+  for (const TuneField& f : kFields) {
+    const char* v = getenv(f.env);
+    if (v) tuning_set(t, f.name, parse_env(f, v));  // out-of-range values keep the default
+  }
+  return t;
+}
+
 
 cudaError_t launch_expand_segments(const int64_t* seg_off, const uint32_t* seg_ver, int64_t n_seg,
                                    uint32_t* out_stage, cudaStream_t stream) {

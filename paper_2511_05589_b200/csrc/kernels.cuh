@@ -23,6 +23,7 @@ enum : uint32_t {
   ERR_NONFINITE_LP = 2u,     // grpo.hpp:69-70 "token_ratio requires finite log-probs"
   ERR_NONFINITE_ADV = 4u,    // grpo.hpp:128 "advantage must be finite"
   ERR_NOT_TERMINATED = 8u,   // grpo.hpp:36 "terminal_reward requires a terminated trajectory"
+  ERR_EMPTY_TERMINATED = 16u,  // grpo.hpp:38 "terminated trajectory cannot be empty"
 };
 
 // Everything one loss launch needs, by value (kernel parameter space).
@@ -76,6 +77,35 @@ constexpr int kTraceCtas = 2048;
 
 enum class DType : int { BF16 = 0, F32 = 1 };
 
+// Kernel selection and tunables of one context. Filled once from the COPRIS_*
+// environment at copris_ctx_create (tuning_from_env) and changed only through
+// copris_ctx_set_option; launchers read this copy and never the environment,
+// so a setenv on one thread cannot change another context's kernels mid-run
+// (re-entrancy).
+struct Tuning {
+  int fused_impl = 0;     // 0 auto, 1 stream (TMA ring + L2 re-read), 2 tma (row in smem), 3 pair
+  int lookahead = 2;      // stream kernel: ring segments of row r+1 before pass 2 of row r
+  int slots = 0;          // stream kernel ring slots (0 = as many 32 KB slots as fit 192 KB)
+  int resident = 1;       // stream kernel: pass 2 from resident segments when 3 rows fit
+  int one_exp = 1;        // pair kernel, bf16 dlogits: TMEM-staged exponentials (1 ex2/element)
+  int lmhead_impl = 0;    // 0 CTA pair (cta_group::2), 1 single SM
+  int lmhead_group = 16;  // LM-head raster group (token pairs per vocab sweep)
+  int lmhead_tma_store = 1;
+  int gemm_wide = 1;      // dhidden GEMM: 256 x 512 tiles per pair
+  int gemm_mc = 0;        // dhidden GEMM: 4-CTA clusters with W^T multicast
+  int gemm_splits = 0;    // 0 = automatic split-K count
+  int gemm_a_evict_first = 0;
+  int dw_group = 1;
+  int dw_policy = 2;
+  int64_t dw_kchunk = 8192;
+  int trace = 0;          // per-CTA phase tracing (COPRIS_TRACE)
+};
+
+Tuning tuning_from_env();
+// Sets one option by name; returns false for an unknown name or bad value.
+bool tuning_set(Tuning& t, const char* name, int64_t value);
+bool tuning_get(const Tuning& t, const char* name, int64_t* value);
+
 struct LaunchInfo {
   int num_sms;
   int cluster;       // CTAs per row chosen by the dispatcher (fused TMA path)
@@ -86,7 +116,7 @@ struct LaunchInfo {
 // Fused single-pass loss. Chooses the TMA/cluster kernel when rows are 16-byte
 // aligned, otherwise the generic kernel.
 cudaError_t launch_fused(const LossParams& p, DType in, DType out, int num_sms,
-                         cudaStream_t stream, LaunchInfo* info);
+                         const Tuning& tu, cudaStream_t stream, LaunchInfo* info);
 // Unfused K3 (second logits pass from lse).
 cudaError_t launch_bwd(const LossParams& p, DType in, DType out, int num_sms,
                        cudaStream_t stream, LaunchInfo* info);
@@ -94,7 +124,7 @@ cudaError_t launch_bwd(const LossParams& p, DType in, DType out, int num_sms,
 cudaError_t launch_logprob_gather(const void* logits, int64_t ld, DType in, const int32_t* target,
                                   int64_t n_tok, int32_t vocab, float* out_lp, float* out_lse,
                                   uint32_t* err, unsigned long long* row_ctr, int num_sms,
-                                  cudaStream_t stream);
+                                  const Tuning& tu, cudaStream_t stream);
 // K2.
 cudaError_t launch_expand_segments(const int64_t* seg_off, const uint32_t* seg_ver, int64_t n_seg,
                                    uint32_t* out_stage, cudaStream_t stream);

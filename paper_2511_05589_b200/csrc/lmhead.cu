@@ -830,7 +830,7 @@ int32_t lmhead_num_vtiles(int32_t vocab) { return (vocab + kBN - 1) / kBN; }
 cudaError_t launch_lmhead_fwd(const void* hidden, int64_t ld_h, const void* weight, int64_t ld_w,
                               int64_t n_rows, int32_t H, int32_t V, const int32_t* target,
                               void* logits, int64_t ld, float* partials, int num_sms,
-                              cudaStream_t stream, LaunchInfo* info) {
+                              const Tuning& tu, cudaStream_t stream, LaunchInfo* info) {
   CUtensorMap tx, tw;
   if (!make_map(&tx, hidden, n_rows, H, ld_h, kBM) || !make_map(&tw, weight, V, H, ld_w, kBN))
     return cudaErrorInvalidValue;
@@ -846,12 +846,8 @@ cudaError_t launch_lmhead_fwd(const void* hidden, int64_t ld_h, const void* weig
   p.ld = ld;
   p.partials = reinterpret_cast<float2*>(partials);
   p.target = target;
-  {
-    const char* g = std::getenv("COPRIS_LMHEAD_GROUP");
-    p.group = g ? std::max(1, std::atoi(g)) : 16;
-  }
-  const char* impl = std::getenv("COPRIS_LMHEAD_IMPL");
-  if (impl && std::strcmp(impl, "1sm") == 0) {
+  p.group = std::max(1, tu.lmhead_group);
+  if (tu.lmhead_impl == 1) {
     cudaError_t ea = allow_dyn_smem(reinterpret_cast<const void*>(lmhead_fwd_kernel), static_cast<int>(kSmemBytes));
     if (ea != cudaSuccess) return ea;
     const int grid = static_cast<int>(std::min<int64_t>(p.n_tiles, num_sms));
@@ -862,11 +858,10 @@ cudaError_t launch_lmhead_fwd(const void* hidden, int64_t ld_h, const void* weig
   // the pair kernel stages half of the weight tile per CTA: 128-row boxes
   if (!make_map(&tw, weight, V, H, ld_w, 128)) return cudaErrorInvalidValue;
   // per call: the attribute is per device, and one process may drive several
-  // logits through staging boxes + TMA stores (EPI 3) unless COPRIS_LMHEAD_TMA_STORE=0;
+  // logits through staging boxes + TMA stores (EPI 3) unless lmhead_tma_store = 0;
   // only when a row is a whole number of 16-byte pieces (V % 8 == 0): TMA clips
   // a store box at 16-byte granularity, so it would write the row padding
-  const char* ts = std::getenv("COPRIS_LMHEAD_TMA_STORE");
-  const bool tma_store = !(ts && std::atoi(ts) == 0) && V % 8 == 0;
+  const bool tma_store = tu.lmhead_tma_store != 0 && V % 8 == 0;
   CUtensorMap tl = tw;
   if (tma_store && !make_map(&tl, logits, n_rows, V, ld, 32)) return cudaErrorInvalidValue;
   auto kern = tma_store ? lmhead_fwd_pair_kernel<3> : lmhead_fwd_pair_kernel<0>;
@@ -894,17 +889,15 @@ cudaError_t launch_lmhead_fwd(const void* hidden, int64_t ld_h, const void* weig
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
-static bool gemm_wide() {
-  const char* w = std::getenv("COPRIS_GEMM_WIDE");
-  const char* mc = std::getenv("COPRIS_GEMM_MC");
-  // default on; COPRIS_GEMM_WIDE=0 selects the 256 x 256 tile
-  return !(w && std::atoi(w) == 0) && !(mc && std::atoi(mc) != 0);
+static bool gemm_wide(const Tuning& tu) {
+  // default on; gemm_wide = 0 selects the 256 x 256 tile
+  return tu.gemm_wide != 0 && tu.gemm_mc == 0;
 }
 
-int32_t gemm_nt_splits(int64_t M, int32_t N, int num_sms) {
-  if (const char* e = std::getenv("COPRIS_GEMM_SPLITS")) return std::max(1, std::atoi(e));
+int32_t gemm_nt_splits(int64_t M, int32_t N, int num_sms, const Tuning& tu) {
+  if (tu.gemm_splits > 0) return tu.gemm_splits;
   const int64_t clusters = num_sms / 2;
-  if (gemm_wide()) {
+  if (gemm_wide(tu)) {
     // 256 x 512 tiles are few: pick the split count whose units fill the last
     // wave of clusters best (ties: fewer splits, less partial traffic)
     const int64_t base = (M + 255) / 256 * ((N + 2 * kBN - 1) / (2 * kBN));
@@ -930,8 +923,8 @@ int32_t gemm_nt_splits(int64_t M, int32_t N, int num_sms) {
 
 cudaError_t launch_gemm_nt_bf16(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t M,
                                 int32_t N, int32_t K, void* out, int64_t ldo, float* work,
-                                int32_t n_split, int num_sms, cudaStream_t stream,
-                                LaunchInfo* info) {
+                                int32_t n_split, int num_sms, const Tuning& tu,
+                                cudaStream_t stream, LaunchInfo* info) {
   if (M == 0 || N == 0) return cudaSuccess;
   CUtensorMap ta, tb;
   if (!make_map(&ta, A, M, K, lda, 128) || !make_map(&tb, B, N, K, ldb, 128))
@@ -944,24 +937,19 @@ cudaError_t launch_gemm_nt_bf16(const void* A, int64_t lda, const void* B, int64
   p.H = K;
   p.V = N;
   p.n_vt = (N + kBN - 1) / kBN;
-  {
-    const char* g = std::getenv("COPRIS_LMHEAD_GROUP");
-    p.group = g ? std::max(1, std::atoi(g)) : 16;
-    const char* ef = std::getenv("COPRIS_GEMM_A_EVICT_FIRST");
-    p.a_evict_first = ef ? std::atoi(ef) : 0;
-  }
+  p.group = std::max(1, tu.lmhead_group);
+  p.a_evict_first = tu.gemm_a_evict_first;
   p.c_out = work;
   p.ldc = N;
   p.split_stride = M * static_cast<int64_t>(N);
   p.n_split = n_split;
   p.k_per_split = (nk + n_split - 1) / n_split;
   p.n_split = (nk + p.k_per_split - 1) / p.k_per_split;  // no empty split
-  // default: 256 x 512 tiles per pair (two MMAs per k-step); COPRIS_GEMM_WIDE=0:
-  // 256 x 256 tiles; COPRIS_GEMM_MC=1: 256 x 256 tiles on 4-CTA clusters with the
+  // default: 256 x 512 tiles per pair (two MMAs per k-step); gemm_wide = 0:
+  // 256 x 256 tiles; gemm_mc = 1: 256 x 256 tiles on 4-CTA clusters with the
   // W^T halves multicast to two token pairs
-  const char* mc_env = std::getenv("COPRIS_GEMM_MC");
-  const bool mc = mc_env && std::atoi(mc_env) != 0;
-  const bool wide = gemm_wide();
+  const bool mc = tu.gemm_mc != 0;
+  const bool wide = gemm_wide(tu);
   auto kern = mc     ? lmhead_fwd_pair_kernel<1, true>
               : wide ? lmhead_fwd_pair_kernel<1, false, true>
                      : lmhead_fwd_pair_kernel<1, false>;
@@ -1010,7 +998,8 @@ cudaError_t launch_gemm_nt_bf16(const void* A, int64_t lda, const void* B, int64
 
 cudaError_t launch_gemm_tn_acc_f32(const void* A, int64_t lda, const void* B, int64_t ldb,
                                    int64_t K, int32_t M, int32_t N, float* c, int64_t ldc,
-                                   int num_sms, cudaStream_t stream, LaunchInfo* info) {
+                                   int num_sms, const Tuning& tu, cudaStream_t stream,
+                                   LaunchInfo* info) {
   if (K == 0 || M == 0 || N == 0) return cudaSuccess;
   CUtensorMap tc_map;
   if (!make_map_f32_box32(&tc_map, c, M, N, ldc)) return cudaErrorInvalidValue;
@@ -1021,17 +1010,14 @@ cudaError_t launch_gemm_tn_acc_f32(const void* A, int64_t lda, const void* B, in
   // raster: every H tile of one vocab pair before the next (group 1), so the
   // 16 concurrent users of a dlogits slice share one DRAM read; the hidden
   // block is kept at evict_last (policy bit 1) and re-read from L2
-  const char* g = std::getenv("COPRIS_DW_GROUP");
-  p.group = g ? std::max(1, std::atoi(g)) : 1;
-  const char* pol = std::getenv("COPRIS_DW_POLICY");
-  p.a_evict_first = pol ? std::atoi(pol) : 2;
+  p.group = std::max(1, tu.dw_group);
+  p.a_evict_first = tu.dw_policy;
   p.c_out = c;
   p.ldc = ldc;
   p.n_split = 1;
   // the token reduction runs in launches of <= kchunk rows, in order, so the
   // hidden block of one launch (kchunk x H bf16) stays L2-resident
-  const char* kc = std::getenv("COPRIS_DW_KCHUNK");
-  const int64_t kchunk = kc ? std::max<int64_t>(kBK, std::atoll(kc) / kBK * kBK) : 8192;
+  const int64_t kchunk = std::max<int64_t>(kBK, tu.dw_kchunk / kBK * kBK);
   cudaError_t e = allow_dyn_smem(reinterpret_cast<const void*>(lmhead_fwd_pair_kernel<2>), static_cast<int>(kPSmemBytesDw));
   if (e != cudaSuccess) return e;
   const int64_t units = (static_cast<int64_t>(M) + 255) / 256 * p.n_vt;

@@ -77,11 +77,9 @@ class RolloutEngine:
     def _ids(self, fn, *args):
         buf = (C.c_uint64 * self.cap)()
         n = C.c_int64()
-        rc = fn(self.h, *args, buf, self.cap, C.byref(n))
-        if rc == L.COPRIS_E_INVALID and n.value > self.cap:
-            self.cap = n.value
-            return self._ids(fn, *args)
-        self._call(rc)
+        # cap >= max(concurrency, B*N), the admission bound the C-ABI checks
+        # before the engine admits anything
+        self._call(fn(self.h, *args, buf, self.cap, C.byref(n)))
         return list(buf[: n.value])
 
     def begin_stage(self, version: int) -> list[int]:

@@ -42,6 +42,23 @@ def _p(t: Optional[torch.Tensor]):
     return None if t is None else C.c_void_p(t.data_ptr())
 
 
+def _on_stream(fn):
+    """Run the method with `stream` as torch's current stream, so the buffers it
+    allocates (outputs, split-K work, zero-filled dweight) are allocated and
+    initialised on the stream the kernels run on: the caching allocator then
+    cannot hand a dropped work buffer to another stream while the kernel still
+    writes it (grpo.py:213)."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapped(self, *args, stream=None, **kw):
+        if stream is None:
+            return fn(self, *args, stream=None, **kw)
+        with torch.cuda.stream(stream):
+            return fn(self, *args, stream=stream, **kw)
+    return wrapped
+
+
 def _dtype_code(dt: torch.dtype) -> int:
     if dt == torch.bfloat16:
         return L.COPRIS_BF16
@@ -160,6 +177,37 @@ class Copris:
         """Synchronise and raise any device-detected contract violation."""
         self._call(self.lib.copris_ctx_check(self.h, self._stream(stream)))
 
+    # kernel selection / tunables of THIS context (copris_ctx_set_option); the
+    # COPRIS_* environment is read once, when the context is created
+    _NAMED = {"fused_impl": {"auto": 0, "stream": 1, "tma": 2, "pair": 3},
+              "lmhead_impl": {"pair": 0, "1sm": 1}}
+
+    def set_option(self, name: str, value) -> None:
+        if isinstance(value, str):
+            value = self._NAMED[name][value]
+        self._call(self.lib.copris_ctx_set_option(self.h, name.encode(), int(value)))
+
+    def get_option(self, name: str) -> int:
+        v = C.c_int64()
+        self._call(self.lib.copris_ctx_get_option(self.h, name.encode(), C.byref(v)))
+        return v.value
+
+    def options(self, **kw):
+        """Context manager: set options, restore the previous values on exit."""
+        import contextlib
+
+        @contextlib.contextmanager
+        def cm():
+            old = {k: self.get_option(k) for k in kw}
+            try:
+                for k, v in kw.items():
+                    self.set_option(k, v)
+                yield self
+            finally:
+                for k, v in old.items():
+                    self.set_option(k, v)
+        return cm()
+
     def last_launch(self) -> dict:
         cl, grid, sms = C.c_int(), C.c_int(), C.c_int()
         name = C.c_char_p()
@@ -169,6 +217,7 @@ class Copris:
                 "kernel": name.value.decode() if name.value else ""}
 
     # -- K1 -----------------------------------------------------------------------
+    @_on_stream
     def sequence_logprobs(self, logits: torch.Tensor, target: torch.Tensor, stream=None,
                           out_lp=None, out_lse=None):
         """policy.hpp:160-173 over packed rows -> (cur_lp f32 [T], lse f32 [T])."""
@@ -181,6 +230,7 @@ class Copris:
         return lp, lse
 
     # -- LM-head forward + log-softmax partials (tcgen05) ---------------------------
+    @_on_stream
     def lmhead_logits(self, hidden: torch.Tensor, weight: torch.Tensor, target: torch.Tensor,
                       logits: Optional[torch.Tensor] = None,
                       partials: Optional[torch.Tensor] = None, stream=None):
@@ -201,6 +251,7 @@ class Copris:
             _p(target), _p(logits), logits.stride(0), _p(partials), self._stream(stream)))
         return logits, partials
 
+    @_on_stream
     def lmhead_dhidden(self, dlogits: torch.Tensor, weight_t: torch.Tensor,
                        out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
         """dhidden = dlogits @ weight (bf16) on the tcgen05 pair kernel; weight_t
@@ -216,6 +267,7 @@ class Copris:
             _p(out), out.stride(0), _p(work), self._stream(stream)))
         return out
 
+    @_on_stream
     def lmhead_dweight(self, dlogits: torch.Tensor, hidden: torch.Tensor,
                        out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
         """dweight (fp32 [V x H]) += dlogits^T @ hidden on the tcgen05 pair kernel
@@ -231,6 +283,7 @@ class Copris:
             _p(out), out.stride(0), self._stream(stream)))
         return out
 
+    @_on_stream
     def lse_merge(self, partials: torch.Tensor, logits: torch.Tensor, target: torch.Tensor,
                   out_lp=None, out_lse=None, stream=None):
         """(cur_lp, lse) from lmhead partials — what sequence_logprobs gives on the logits."""
@@ -243,6 +296,7 @@ class Copris:
         return lp, lse
 
     # -- K2 -----------------------------------------------------------------------
+    @_on_stream
     def expand_segments(self, seg_off: torch.Tensor, seg_ver: torch.Tensor, n_tok: int,
                         stream=None) -> torch.Tensor:
         out = torch.empty(n_tok, dtype=torch.int32, device=seg_off.device)
@@ -250,6 +304,7 @@ class Copris:
                                                    seg_ver.numel(), _p(out), self._stream(stream)))
         return out
 
+    @_on_stream
     def concat_segments(self, stage, cur_stage: int, buffered_lp, cur_lp, is_enabled=True,
                         behav_mode=L.COPRIS_BEHAV_RECOMPUTED, stream=None):
         """trajectory.hpp:69-75 + trainer.hpp:149 -> (behav f32 [T], flags u8 [T])."""
@@ -262,6 +317,7 @@ class Copris:
         return behav, flags
 
     # -- K3a ----------------------------------------------------------------------
+    @_on_stream
     def terminal_rewards(self, tokens, tok_off, terminated, answer_target, eos_token: int,
                          stream=None) -> torch.Tensor:
         n = tok_off.numel() - 1
@@ -271,6 +327,7 @@ class Copris:
             _p(out), self._stream(stream)))
         return out
 
+    @_on_stream
     def compute_advantages(self, rewards: torch.Tensor, group_off: torch.Tensor,
                            adv_epsilon: float = 1e-6, group_off_host=None,
                            stream=None) -> torch.Tensor:
@@ -283,6 +340,7 @@ class Copris:
             adv_epsilon, _p(out), self._stream(stream)))
         return out
 
+    @_on_stream
     def token_traj(self, tok_off: torch.Tensor, n_tok: int, stream=None) -> torch.Tensor:
         out = torch.empty(n_tok, dtype=torch.int32, device=tok_off.device)
         self._call(self.lib.copris_token_traj(self.h, _p(tok_off), tok_off.numel() - 1, n_tok,
@@ -352,6 +410,7 @@ class Copris:
         self._call(self.lib.copris_loss_reduce(self.h, _p(obj), _p(flags), n_tok, _p(out4),
                                                self._stream(stream)))
 
+    @_on_stream
     def grpo_step_loss(self, logits: torch.Tensor, batch: PackedBatch, cfg: ClipConfig = None,
                        *, is_enabled: bool = True, behav_mode: int = L.COPRIS_BEHAV_RECOMPUTED,
                        fused: bool = True, dlogits: Optional[torch.Tensor] = None,

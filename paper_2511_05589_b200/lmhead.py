@@ -46,7 +46,15 @@ class LmHeadStepResult:
     coef: Optional[torch.Tensor] = None
 
 
-def lmhead_grpo_step_loss(ctx: Copris, hidden: torch.Tensor, weight: torch.Tensor,
+def lmhead_grpo_step_loss(ctx: Copris, *args, stream=None, **kw) -> "LmHeadStepResult":
+    """See _lmhead_grpo_step_loss; with ``stream`` every buffer is allocated on it."""
+    if stream is None:
+        return _lmhead_grpo_step_loss(ctx, *args, stream=None, **kw)
+    with torch.cuda.stream(stream):
+        return _lmhead_grpo_step_loss(ctx, *args, stream=stream, **kw)
+
+
+def _lmhead_grpo_step_loss(ctx: Copris, hidden: torch.Tensor, weight: torch.Tensor,
                           batch: PackedBatch, cfg: ClipConfig = None, *, chunk_rows: int = 8192,
                           is_enabled: bool = True, behav_mode: int = L.COPRIS_BEHAV_RECOMPUTED,
                           total_tokens: Optional[int] = None, want_grad: bool = True,
@@ -77,7 +85,10 @@ def lmhead_grpo_step_loss(ctx: Copris, hidden: torch.Tensor, weight: torch.Tenso
         raise ContractViolation("log-prob vectors must align with token count")
     if weight.shape[1] != H:
         raise ContractViolation("hidden and weight disagree on the hidden size")
-    T_glob = total_tokens if total_tokens is not None else T
+    # the masked token mean divides by the UNMASKED count, as grpo_step_loss does
+    T_glob = total_tokens if total_tokens is not None else batch.loss_tokens()
+    if T_glob <= 0:
+        raise ConfigError("grpo_step_loss batch has no tokens")
     dev = hidden.device
     chunk = max(1, min(chunk_rows, T))
     ldv = (V + 7) // 8 * 8

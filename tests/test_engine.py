@@ -134,3 +134,24 @@ def test_side_by_side_with_the_reference_engine():
     res = json.loads(p.stdout.strip().splitlines()[-1])
     assert p.returncode == 0 and res["mismatches"] == 0, p.stderr[-2000:]
     assert res["checks"] > 1_000_000
+
+
+def test_small_id_buffer_leaves_engine_untouched():
+    """copris_engine_begin_stage / _refill_active check the caller's id buffer
+    against the admission bound max(concurrency, B*N) BEFORE admitting: a
+    too-small buffer fails with COPRIS_E_INVALID and the engine state is
+    unchanged, so the same call then succeeds (engine_capi.cpp:70)."""
+    import ctypes as C
+    from paper_2511_05589_b200 import _lib as L
+    eng = RolloutEngine(concurrency=12, batch_prompts=2, rollouts_per_prompt=4,
+                        max_response_len=8, vocab=6, seed=3)
+    ref = RolloutEngine(concurrency=12, batch_prompts=2, rollouts_per_prompt=4,
+                        max_response_len=8, vocab=6, seed=3)
+    small = (C.c_uint64 * 4)()
+    n = C.c_int64()
+    rc = eng.lib.copris_engine_begin_stage(eng.h, C.c_uint64(1), small, 4, C.byref(n))
+    assert rc == L.COPRIS_E_INVALID
+    assert eng.begin_stage(1) == ref.begin_stage(1)
+    rc = eng.lib.copris_engine_refill_active(eng.h, small, 4, C.byref(n))
+    assert rc == L.COPRIS_E_INVALID
+    assert eng.refill_active() == ref.refill_active()

@@ -18,14 +18,18 @@ from parity_util import assert_loss_close, assert_scalar_close
 pytestmark = pytest.mark.gpu
 
 
+LM_DEFAULTS = dict(lmhead_impl=0, lmhead_tma_store=1, gemm_wide=1, gemm_mc=0, gemm_splits=0,
+                   dw_kchunk=8192)
+
+
 @pytest.fixture(params=["pair", "1sm"], autouse=True)
-def impl(request, monkeypatch):
-    """Both kernels: the CTA-pair (cta_group::2) default and the 1-SM variant."""
-    if request.param == "1sm":
-        monkeypatch.setenv("COPRIS_LMHEAD_IMPL", "1sm")
-    else:
-        monkeypatch.delenv("COPRIS_LMHEAD_IMPL", raising=False)
-    return request.param
+def impl(request, ctx):
+    """Both kernels: the CTA-pair (cta_group::2) default and the 1-SM variant
+    (the context's lmhead_impl option); every option is reset afterwards."""
+    ctx.set_option("lmhead_impl", request.param)
+    yield request.param
+    for k, v in LM_DEFAULTS.items():
+        ctx.set_option(k, v)
 
 
 def _inputs(T, H, V, seed, scale=1.0):
@@ -150,6 +154,41 @@ def test_lmhead_matches_logits_path(ctx):
     assert torch.allclose(a.dhidden.float(), dh, rtol=2e-2, atol=1e-3 * float(dh.abs().max()))
 
 
+def test_lmhead_loss_mask_equals_deletion(ctx, oracle):
+    """A token mask on the LM-head path divides by the UNMASKED count (the
+    masked token mean, as grpo_step_loss does): the result equals the oracle
+    run on the batch with the masked tokens deleted (lmhead.py:80)."""
+    from paper_2511_05589_b200 import ClipConfig
+    from paper_2511_05589_b200.lmhead import lmhead_grpo_step_loss
+    from paper_2511_05589_b200.packing import upload
+    from paper_2511_05589_b200.workload import stale_logprobs
+    from parity_util import assert_loss_close
+    T, H, V = 600, 256, 4096
+    x, w, tgt = _inputs(T, H, V, 31)
+    tok_off = np.linspace(0, T, 9).astype(np.int64)
+    group_off = np.arange(0, 9, 4, dtype=np.int64)
+    stage = (np.arange(T) % 3 == 0).astype(np.uint32) + 1
+    lg, _ = ctx.lmhead_logits(x, w, tgt)
+    z64 = lg.double().cpu().numpy()
+    cur = oracle.logprob_gather(z64, tgt.cpu().numpy())
+    blp = stale_logprobs(cur, stage, 2, 7)
+    reward = (np.arange(8) % 3 == 0).astype(np.float64)
+    batch = upload(ctx, tok_off, group_off, tgt.cpu().numpy(), blp, 2, stage=stage, reward=reward)
+    keep = np.random.default_rng(3).random(T) > 0.35
+    batch.loss_mask = torch.from_numpy(keep.astype(np.uint8)).cuda()
+    res = lmhead_grpo_step_loss(ctx, x, w, batch, ClipConfig(), chunk_rows=250)
+    csum = np.concatenate([[0], np.cumsum(keep)])
+    adv = oracle.advantages(reward, group_off)
+    ref = oracle.is_loss(z64[keep], csum[tok_off].astype(np.int64), tgt.cpu().numpy()[keep],
+                         stage[keep], 2, blp[keep].astype(np.float64), adv, want_dlogits=False)
+    assert res.token_count == int(keep.sum())
+    assert res.clipped_tokens == ref.clipped_tokens and res.stale_tokens == ref.stale_tokens
+    assert_loss_close(res.loss, ref.loss, ref.obj, int(keep.sum()), what="lmhead masked loss")
+    # and the same batch through the logits path gives the same masked mean
+    b = ctx.grpo_step_loss(lg.contiguous(), batch, ClipConfig())
+    assert abs(res.loss - b.loss) <= 1e-6 * max(1e-12, float(b.obj.abs().sum()) / keep.sum())
+
+
 def test_lmhead_argument_errors(ctx):
     """C-ABI validation: misaligned strides/pointers, short ld, partial-width mismatch."""
     from paper_2511_05589_b200.grpo import _p
@@ -204,9 +243,8 @@ def test_lmhead_dhidden_tcgen05(ctx, T, H, V, variant, monkeypatch):
     wt = w.t().contiguous()
     if ldv != V:
         wt = torch.nn.functional.pad(wt, (0, ldv - V))[:, :V]
-    monkeypatch.delenv("COPRIS_GEMM_WIDE", raising=False)
-    monkeypatch.delenv("COPRIS_GEMM_MC", raising=False)
-    monkeypatch.delenv("COPRIS_GEMM_SPLITS", raising=False)
+    for k in ("gemm_wide", "gemm_mc", "gemm_splits"):
+        ctx.set_option(k, LM_DEFAULTS[k])
     out = ctx.lmhead_dhidden(dl, wt)
     assert ctx.last_launch()["kernel"].endswith(",wide>")
     torch.cuda.synchronize()
@@ -217,11 +255,10 @@ def test_lmhead_dhidden_tcgen05(ctx, T, H, V, variant, monkeypatch):
     again = ctx.lmhead_dhidden(dl, wt)
     assert torch.equal(again.view(torch.int16), out.view(torch.int16))
     if variant != "wide":
-        monkeypatch.setenv("COPRIS_GEMM_SPLITS", "2")
+        ctx.set_option("gemm_splits", 2)
         base = ctx.lmhead_dhidden(dl, wt)
         small_ref = ctx.lmhead_dhidden(dl[:1], wt)
-        monkeypatch.setenv("COPRIS_GEMM_MC" if variant == "mc" else "COPRIS_GEMM_WIDE",
-                           "1" if variant == "mc" else "0")
+        ctx.set_option("gemm_mc" if variant == "mc" else "gemm_wide", 1 if variant == "mc" else 0)
         multi = ctx.lmhead_dhidden(dl, wt)
         assert ctx.last_launch()["kernel"].endswith(f",{variant}>" if variant == "mc" else "<gemm>")
         assert torch.equal(multi.view(torch.int16), base.view(torch.int16))
@@ -257,9 +294,9 @@ def test_lmhead_dweight_tcgen05(ctx, T, H, V):
 
 
 def test_lmhead_dweight_token_chunks(ctx, monkeypatch):
-    """The token reduction in several ordered launches (COPRIS_DW_KCHUNK): the
+    """The token reduction in several ordered launches (dw_kchunk option): the
     same bound plus one fp32 rounding of dW per launch, bitwise on a rerun."""
-    monkeypatch.setenv("COPRIS_DW_KCHUNK", "128")
+    ctx.set_option("dw_kchunk", 128)
     T, H, V = 300, 256, 1000
     g = torch.Generator(device="cuda").manual_seed(5)
     dl = (torch.randn((T, V), device="cuda", generator=g) * 1e-3).to(torch.bfloat16)
@@ -310,7 +347,7 @@ def test_lmhead_dweight_errors(ctx):
 def test_lmhead_tma_store_epilogue_bitwise(ctx, T, H, V, impl, monkeypatch):
     """The forward with the logits leaving through swizzled staging boxes and TMA
     stores (the default when V % 8 == 0): logits and LSE partials bitwise the
-    register-store epilogue's (COPRIS_LMHEAD_TMA_STORE=0), ragged T included; at
+    register-store epilogue's (lmhead_tma_store = 0), ragged T included; at
     V % 8 != 0 the register-store epilogue runs (TMA would clip at 16-byte
     granularity and write the row padding)."""
     if impl == "1sm":
@@ -322,10 +359,10 @@ def test_lmhead_tma_store_epilogue_bitwise(ctx, T, H, V, impl, monkeypatch):
     nvt = int(ctx.lib.copris_lmhead_num_vtiles(V))
     p0 = torch.empty((T, nvt, 2), dtype=torch.float32, device="cuda")
     p1 = torch.empty_like(p0)
-    monkeypatch.setenv("COPRIS_LMHEAD_TMA_STORE", "0")
+    ctx.set_option("lmhead_tma_store", 0)
     ctx.lmhead_logits(x, w, tgt, logits=lg0[:, :V], partials=p0)
     assert ctx.last_launch()["kernel"] == "lmhead_fwd_pair_kernel"
-    monkeypatch.delenv("COPRIS_LMHEAD_TMA_STORE")
+    ctx.set_option("lmhead_tma_store", 1)
     ctx.lmhead_logits(x, w, tgt, logits=lg1[:, :V], partials=p1)
     assert ctx.last_launch()["kernel"] == ("lmhead_fwd_pair_kernel<tma_store>" if V % 8 == 0
                                            else "lmhead_fwd_pair_kernel")

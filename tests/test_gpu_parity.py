@@ -24,21 +24,17 @@ def run(ctx, case, dl_dtype=BF16, fused=True, **kw):
 # (V, logits dtype, forced implementation or None, expected kernel, expected cluster)
 SHAPES = [
     (151936, BF16, None, "fused_stream_la_kernel", 1),  # Qwen2.5 vocab: TMA ring + L2 re-read, lookahead
-    (151936, BF16, "stream+la0", "fused_stream_kernel", 1),  # same without the lookahead
+    (151936, BF16, "stream+la0", "fused_stream_la_kernel", 1),  # same without the lookahead
     (151936, BF16, "stream+la5", "fused_stream_la_kernel", 1),
-    (151936, BF16, "tma", "fused_tma_kernel", 2),     # row split over a CTA pair (DSMEM)
-    (151936, BF16, "l2", "fused_l2_kernel", 1),       # register-streamed two-pass variant
     (32000, BF16, None, "fused_tma_kernel", 1),       # 64 KB rows resident, several CTAs/SM
     (32000, BF16, "stream", "fused_stream_la_kernel[resident]", 1),  # 3 rows fit the ring: no L2 re-read
     (32000, BF16, "stream+res0", "fused_stream_la_kernel", 1),  # 2 segments/row: lookahead = whole row
     (32000, BF16, "stream+la1+res0", "fused_stream_la_kernel", 1),
     (20000, BF16, "stream", "fused_stream_la_kernel[resident]", 1),  # partial last segment
-
-    (32000, BF16, "stream+la0", "fused_stream_kernel", 1),
+    (32000, BF16, "stream+la0+res0", "fused_stream_la_kernel", 1),
     (80000, BF16, "tma", "fused_tma_kernel", 1),      # 160 KB rows: one 16-warp CTA per row
     (151936, F32, None, "fused_stream_la_kernel", 1),
-    (151936, F32, "stream+la0", "fused_stream_kernel", 1),
-    (151936, F32, "tma", "fused_tma_kernel", 4),      # 608 KB f32 rows: 4-CTA cluster
+    (151936, F32, "stream+la0", "fused_stream_la_kernel", 1),
     (32000, F32, None, "fused_stream_la_kernel", 1),
     (256, BF16, None, "fused_tma_kernel", 1),
     (4099, BF16, None, "fused_generic_kernel", 1),    # odd vocab: unaligned rows
@@ -46,26 +42,32 @@ SHAPES = [
     (6, F32, None, "fused_generic_kernel", 1),        # desk vocab
 ]
 
+# the context options every test starts from (copris_ctx_set_option)
+DEFAULT_OPTS = dict(fused_impl=0, lookahead=2, resident=1, slots=0, one_exp=1)
+
 
 @pytest.fixture
-def impl(monkeypatch):
+def impl(ctx):
     def set_impl(name):
-        """name = implementation[+laN]: COPRIS_FUSED_IMPL and the stream
-        kernel's lookahead (COPRIS_TUNE_LOOKAHEAD, 0 = the kernel without it)."""
-        monkeypatch.delenv("COPRIS_TUNE_LOOKAHEAD", raising=False)
-        monkeypatch.delenv("COPRIS_TUNE_RESIDENT", raising=False)
+        """name = implementation[+laN][+resN]: the context's fused_impl and the
+        stream kernel's lookahead (0 = pass 2 right after pass 1) / resident mode."""
+        opts = dict(DEFAULT_OPTS)
         if name and "+" in name:
-            name, *opts = name.split("+")
-            for o in opts:
+            name, *rest = name.split("+")
+            for o in rest:
                 if o.startswith("la"):
-                    monkeypatch.setenv("COPRIS_TUNE_LOOKAHEAD", o[2:])
+                    opts["lookahead"] = int(o[2:])
                 elif o.startswith("res"):
-                    monkeypatch.setenv("COPRIS_TUNE_RESIDENT", o[3:])
+                    opts["resident"] = int(o[3:])
+                elif o.startswith("exp"):
+                    opts["one_exp"] = int(o[3:])
         if name:
-            monkeypatch.setenv("COPRIS_FUSED_IMPL", name)
-        else:
-            monkeypatch.delenv("COPRIS_FUSED_IMPL", raising=False)
-    return set_impl
+            opts["fused_impl"] = name
+        for k, v in opts.items():
+            ctx.set_option(k, v)
+    yield set_impl
+    for k, v in DEFAULT_OPTS.items():
+        ctx.set_option(k, v)
 
 
 @pytest.mark.parametrize("V,dtype,force,kernel,cluster", SHAPES)
@@ -88,9 +90,8 @@ def test_unfused_matches_oracle(ctx, oracle, V, dtype):
     case.check(res, F32, what=f"unfused V={V}")
 
 
-@pytest.mark.parametrize("V,force", [(151936, None), (151936, "stream+la0"), (151936, "tma"),
-                                     (151936, "l2"), (32000, None), (32000, "stream"),
-                                     (4099, None)])
+@pytest.mark.parametrize("V,force", [(151936, None), (151936, "stream+la0"), (80000, "tma"),
+                                     (32000, None), (32000, "stream"), (4099, None)])
 def test_kl_and_entropy(ctx, oracle, impl, V, force):
     impl(force)
     case = Case(oracle, seed=5, P=2, G=4, V=V, mu=math.log(10), lmax=24, kl_coeff=0.1,
@@ -387,7 +388,7 @@ def test_stream_rows_around_the_grid(ctx, oracle, impl, half):
     case.check(res, F32, what=f"rows={case.hb.n_tok}")
 
 
-@pytest.mark.parametrize("V,force", [(151936, None), (151936, "tma"), (32000, None),
+@pytest.mark.parametrize("V,force", [(151936, None), (80000, "tma"), (32000, None),
                                      (32000, "stream"), (4099, None)])
 @pytest.mark.parametrize("fused", [True, False])
 def test_loss_mask_equals_deletion(ctx, oracle, impl, V, force, fused):
