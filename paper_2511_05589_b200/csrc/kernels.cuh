@@ -87,7 +87,7 @@ struct Tuning {
   int lookahead = 2;      // stream kernel: ring segments of row r+1 before pass 2 of row r
   int slots = 0;          // stream kernel ring slots (0 = as many 32 KB slots as fit 192 KB)
   int resident = 1;       // stream kernel: pass 2 from resident segments when 3 rows fit
-  int one_exp = 1;        // pair kernel, bf16 dlogits: TMEM-staged exponentials (1 ex2/element)
+  int pair_lookahead = 3; // pair kernel: slots of row r+1 through pass 1 before pass 2 of row r
   int lmhead_impl = 0;    // 0 CTA pair (cta_group::2), 1 single SM
   int lmhead_group = 16;  // LM-head raster group (token pairs per vocab sweep)
   int lmhead_tma_store = 1;

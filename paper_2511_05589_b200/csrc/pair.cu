@@ -1,0 +1,503 @@
+// pair.cu — fused_pair_kernel: the IS-corrected loss pass for bf16 logits rows
+// too large for one SM's shared memory (V = 151,936: 297 KB per row), with ONE
+// exponential per element.
+//
+// A 2-CTA cluster owns a row; CTA h of the pair owns half of its columns.
+// Per CTA: 1 producer warp streams the half-row HBM -> shared memory through a
+// ring of 32 KB slots (cp.async.bulk + mbarrier complete_tx, read once,
+// evict_first); 16 consumer warps run pass 1 on each slot as it lands and
+// release it at once; 1 scalar warp merges the row's partials and runs the
+// token math. Nothing is re-read from L2: the slot ring is pure streaming.
+//
+// Pass 1, per thread and slot (32 columns): m = max of the thread's columns
+// (packed bf16 max, target column excluded), then for each column
+// e = 2^((z - m) log2(e) + 15) on MUFU — summed in fp32 for the log-sum-exp
+// (the sum never sees the rounding below) and stored as f16 in TENSOR MEMORY
+// (tcgen05.st, 16 columns of 32-bit per thread and slot; 2^15 keeps e in
+// f16's normal range down to 2^-29 of the thread's slot maximum), with
+// nml = 15 - m log2(e) kept in shared memory. Pass 2, after the scalar phase:
+// d = e * sign(-coef) 2^(-nml - c2) (one MUFU per thread and slot, none per
+// element): tcgen05.ld, f16 -> f32, packed multiply, bf16 store. The f16
+// staging adds <= 2^-12 relative before the final bf16 rounding, so dlogits
+// stay within one bf16 ulp of the exact value.
+//
+// The pair exchanges its per-warp partials (m, s, z_y) through DSMEM: every
+// consumer warp writes its entry into its own CTA's table (st.shared + local
+// mbarrier arrive) and into the peer's with st.async, whose bytes complete
+// on the peer's mbarrier (complete_tx: no cluster-scope fence on the
+// consumers' path). Both scalar warps merge the same 32 entries in the same
+// order — bitwise the same row statistics in both halves, no second
+// exchange. Rank 0 writes the per-token outputs.
+//
+// Reference semantics: policy.hpp:110-121,160-173 (log-softmax, gather),
+// grpo.hpp:117-185 + policy.hpp:180-196 (objective and dlogits) via
+// token_math.cuh, exactly as the other fused kernels.
+#include <cuda_bf16.h>
+
+#include <cstdint>
+
+#include "fused_common.cuh"
+#include "kernels.cuh"
+#include "pair.cuh"
+#include "ptx.cuh"
+#include "tc.cuh"
+#include "token_math.cuh"
+
+namespace copris_b200 {
+namespace {
+
+constexpr int kPW = 16;                     // consumer warps per CTA
+constexpr int kPK = 4;                      // 16-byte vectors per consumer thread per slot
+constexpr int kPThreads = kPW * 32;         // 512 consumer threads
+constexpr int kPSlotVec = kPThreads * kPK;  // 2048 vectors = 16,384 bf16 columns per slot
+constexpr int kPSlotBytes = kPSlotVec * 16; // 32 KB
+constexpr int kPTSlots = 8;                 // TMEM slots per thread (16 columns each)
+constexpr int kPTmemCols = 512;             // the whole tensor memory of the SM
+constexpr uint32_t kNegInf2 = 0xFF80FF80u;  // bf16x2 (-inf, -inf)
+
+__device__ __forceinline__ uint32_t f2_to_f16x2(uint64_t a) {
+  uint32_t r;
+  asm("{\n.reg .f32 lo, hi;\nmov.b64 {lo, hi}, %1;\ncvt.rn.f16x2.f32 %0, hi, lo;\n}" : "=r"(r) : "l"(a));
+  return r;
+}
+
+__device__ __forceinline__ uint64_t f16x2_to_f2(uint32_t w) {
+  uint64_t r;
+  asm("{\n.reg .f16 lo, hi;\n.reg .f32 a, b;\nmov.b32 {lo, hi}, %1;\n"
+      "cvt.f32.f16 a, lo;\ncvt.f32.f16 b, hi;\nmov.b64 %0, {a, b};\n}"
+      : "=l"(r)
+      : "r"(w));
+  return r;
+}
+
+__device__ __forceinline__ void tmem_st_x16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld_x16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+}
+
+// 16 bytes into the peer CTA's shared memory; the bytes complete on the
+// peer's mbarrier `rbar` (both shared::cluster addresses from mapa).
+__device__ __forceinline__ void st_async_v4(uint32_t raddr, float a, float b, float c, float d,
+                                            uint32_t rbar) {
+  asm volatile(
+      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+          raddr),
+      "f"(a), "f"(b), "f"(c), "f"(d), "r"(rbar)
+      : "memory");
+}
+
+__device__ __forceinline__ void st_global_b16(void* p, uint16_t v) {
+  asm volatile("st.global.b16 [%0], %1;" ::"l"(p), "h"(v) : "memory");
+}
+
+__device__ __forceinline__ void tmem_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+// Per-warp partial of one half-row, exchanged through DSMEM: (m, s) relative
+// to m over the non-target columns, the target logit and whether this warp
+// holds it.
+struct __align__(16) PairPart {
+  float m, s, zy, have;
+};
+
+// Lane state of pass 1: running max and the lane's sum of 2^15-scaled
+// exponentials relative to it.
+struct LaneAcc {
+  float m = -INFINITY, s = 0.f;
+  float zy = 0.f;
+  bool have = false;
+};
+
+// If column jt of a 16-byte vector lies in word k: record it as z_y and set it
+// to -inf (keeps the target out of the max and the sum).
+__device__ __forceinline__ void kill_col(uint32_t& w, int jt, int k, float& zy) {
+  if ((jt >> 1) != k) return;
+  if (jt & 1) {
+    zy = ptx::bf16_hi(w);
+    w = (w & 0x0000FFFFu) | 0xFF800000u;
+  } else {
+    zy = ptx::bf16_lo(w);
+    w = (w & 0xFFFF0000u) | 0xFF80u;
+  }
+}
+
+// Pass 1 of one consumer thread on one ring slot: `cnt` valid vectors starting
+// at vector v0 of this CTA's half; ycol = target column relative to the half.
+// STORE: stage the f16 exponentials in TMEM at taddr (16 columns). Returns
+// nml = 15 - m log2(e) of this thread's columns (+inf when it saw no finite
+// column) for pass 2.
+template <bool STORE>
+__device__ __forceinline__ float p1_slot(LaneAcc& a, uint32_t sb, int32_t v0, int32_t cnt,
+                                         int32_t ycol, int tid, uint32_t taddr) {
+  uint4 raw[kPK];
+  if (cnt == kPSlotVec) {
+#pragma unroll
+    for (int q = 0; q < kPK; ++q) raw[q] = ptx::lds_v4(sb + (tid + q * kPThreads) * 16);
+  } else {
+#pragma unroll
+    for (int q = 0; q < kPK; ++q) {
+      const int32_t j = tid + q * kPThreads;
+      raw[q] = j < cnt ? ptx::lds_v4(sb + j * 16) : uint4{kNegInf2, kNegInf2, kNegInf2, kNegInf2};
+    }
+  }
+  // the target column: record z_y, then keep it out of the max and the sum
+  if (static_cast<uint32_t>(ycol - v0 * 8) < static_cast<uint32_t>(cnt * 8)) {
+#pragma unroll
+    for (int q = 0; q < kPK; ++q) {
+      const int jt = ycol - (v0 + tid + q * kPThreads) * 8;
+      if (static_cast<uint32_t>(jt) < 8u) {
+        a.have = true;
+        kill_col(raw[q].x, jt, 0, a.zy);
+        kill_col(raw[q].y, jt, 1, a.zy);
+        kill_col(raw[q].z, jt, 2, a.zy);
+        kill_col(raw[q].w, jt, 3, a.zy);
+      }
+    }
+  }
+  uint32_t mx = ptx::bmax2(ptx::bmax2(raw[0].x, raw[0].y), ptx::bmax2(raw[0].z, raw[0].w));
+#pragma unroll
+  for (int q = 1; q < kPK; ++q)
+    mx = ptx::bmax2(mx, ptx::bmax2(ptx::bmax2(raw[q].x, raw[q].y), ptx::bmax2(raw[q].z, raw[q].w)));
+  const float ml = fmaxf(ptx::bf16_lo(mx), ptx::bf16_hi(mx));
+  const bool fin = ml != -INFINITY;
+  // all columns -inf: exponentials of -inf (0) with a finite offset
+  const float nml = fmaf(-(fin ? ml : 0.f), kLog2e, 15.f);
+  const uint64_t l2e = ptx::f2(kLog2e, kLog2e), nml2 = ptx::f2(nml, nml);
+  uint64_t acc0 = 0, acc1 = 0;  // two packed fp32 partial sums (0.0f bits)
+  uint32_t h[16];
+#pragma unroll
+  for (int q = 0; q < kPK; ++q) {
+    const uint32_t w[4] = {raw[q].x, raw[q].y, raw[q].z, raw[q].w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint64_t e = ptx::ex2x2(ptx::ffma2(ptx::bf16x2_to_f2(w[k]), l2e, nml2));
+      if (k & 1) acc1 = ptx::fadd2(acc1, e);
+      else acc0 = ptx::fadd2(acc0, e);
+      if (STORE) h[q * 4 + k] = f2_to_f16x2(e);
+    }
+  }
+  if (STORE) tmem_st_x16(taddr, h);
+  const uint64_t acc = ptx::fadd2(acc0, acc1);
+  const float sl = ptx::f2lo(acc) + ptx::f2hi(acc);
+  // online merge into the lane state (branch-free; both parts relative to mn)
+  const float mn = fmaxf(a.m, ml);
+  if (mn != -INFINITY) {
+    const float ra = a.m == -INFINITY ? 0.f : ptx::ex2((a.m - mn) * kLog2e);
+    const float rl = fin ? ptx::ex2((ml - mn) * kLog2e) : 0.f;
+    a.s = fmaf(a.s, ra, sl * rl);
+    a.m = mn;
+  }
+  return fin ? nml : INFINITY;
+}
+
+// Pass 2 of one consumer thread on one slot: dlogits from the staged
+// exponentials (or zeros), bf16 out. The target column is written by its
+// owner afterwards (a later store of the same thread to the same address).
+__device__ __forceinline__ void p2_slot(const RowBroadcast& b, bool zero_row, float nml,
+                                        uint32_t taddr, int32_t v0, int32_t cnt, int32_t ycol,
+                                        __nv_bfloat16* dseg, int tid) {
+  __nv_bfloat16* base = dseg + static_cast<int64_t>(tid) * 8;
+  if (zero_row) {
+    const uint4 z{0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int q = 0; q < kPK; ++q)
+      if (tid + q * kPThreads < cnt) ptx::st_global_cs_v4(base + q * kPThreads * 8, z);
+    return;
+  }
+  // |coef| p_k = e_k 2^(m log2(e) - 15 - c2) = e_k 2^(-nml - c2); 0 for a lane
+  // without finite columns (its staged e are 0 too)
+  float sc = nml == INFINITY ? 0.f : ptx::ex2(-(nml + b.c2));
+  if (b.coef > 0.f) sc = -sc;  // d = -coef p
+  const uint64_t sc2 = ptx::f2(sc, sc);
+  uint32_t h[16];
+  tmem_ld_x16(taddr, h);
+  tc::tmem_wait_ld();
+  uint4 v[kPK];
+#pragma unroll
+  for (int q = 0; q < kPK; ++q) {
+    uint32_t o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) o[k] = ptx::f2_to_bf16x2(ptx::fmul2(f16x2_to_f2(h[q * 4 + k]), sc2));
+    v[q] = uint4{o[0], o[1], o[2], o[3]};
+  }
+  if (cnt == kPSlotVec) {
+#pragma unroll
+    for (int q = 0; q < kPK; ++q) ptx::st_global_cs_v4(base + q * kPThreads * 8, v[q]);
+  } else {
+#pragma unroll
+    for (int q = 0; q < kPK; ++q)
+      if (tid + q * kPThreads < cnt) ptx::st_global_cs_v4(base + q * kPThreads * 8, v[q]);
+  }
+  // one-hot term coef (1 - p_y) (policy.hpp:193-194), by the thread that owns it
+  const int32_t rel = ycol - v0 * 8;
+  if (static_cast<uint32_t>(rel) < static_cast<uint32_t>(cnt * 8) && ((rel >> 3) & (kPThreads - 1)) == tid)
+    st_global_b16(dseg + rel, __bfloat16_as_ushort(__float2bfloat16_rn(b.dy)));
+}
+
+// grid = 2 x clusters, cluster (2, 1, 1); block = (kPW + 2) warps. Dynamic
+// shared memory: nslots ring slots of 32 KB, then nml[kPTSlots][512] floats.
+// nvec0 = vectors of CTA rank 0 (rank 1 takes the rest); look = slots of row
+// r+1 run through pass 1 before pass 2 of row r.
+__global__ void __launch_bounds__((kPW + 2) * 32, 1)
+    fused_pair_kernel(const LossParams P, const int nslots, const int look, const int32_t nvec0) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full[16], empty[16], p1done[2], sdone[2];
+  __shared__ PairPart red[2][2 * kPW];
+  __shared__ RowBroadcast bc[2];
+  __shared__ uint32_t tmem_slot;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = ptx::cluster_ctarank(), peer = rank ^ 1u;
+  const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int32_t nvec_all = P.vocab / 8;
+  const int32_t vbase = rank ? nvec0 : 0;                  // first vector of this half
+  const int32_t nvec = rank ? nvec_all - nvec0 : nvec0;     // vectors of this half
+  const int32_t col0 = vbase * 8;
+  const int32_t nseg = (nvec + kPSlotVec - 1) / kPSlotVec;
+  const int32_t L = min(look, nseg);
+  const bool grad = P.dlogits != nullptr && !P.gather_only;
+  const uint32_t sbase = ptx::smem_u32(smem);
+  float* nml_sh = reinterpret_cast<float*>(smem + nslots * kPSlotBytes);
+  const uint32_t fbase = ptx::smem_u32(full), ebase = ptx::smem_u32(empty);
+  const uint32_t p1b = ptx::smem_u32(p1done), sdb = ptx::smem_u32(sdone);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < nslots; ++i) {
+      ptx::mbar_init(&full[i], 1);
+      ptx::mbar_init(&empty[i], kPW);
+    }
+    for (int i = 0; i < 2; ++i) {
+      // 16 local warps + the scalar warp's arrive that expects the peer's 16 st.async entries
+      ptx::mbar_init(&p1done[i], kPW + 1);
+      ptx::mbar_init(&sdone[i], 1);
+    }
+    ptx::fence_mbarrier_init();
+  }
+  if (warp == 0 && grad) tc::tmem_alloc<kPTmemCols>(ptx::smem_u32(&tmem_slot));
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  ptx::cluster_sync_all();  // the peer's barriers exist before any remote write
+  const uint32_t tmem_base = grad ? tmem_slot : 0u;
+
+  if (warp == kPW) {
+    // ---------------- producer: this half of every row, slot by slot ------------
+    if (lane == 0) {
+      const uint64_t pol = ptx::policy_evict_first();  // read once
+      Ring ring(nslots);
+      for (int64_t r = cid; r < P.n_rows; r += ncl) {
+        const __nv_bfloat16* row = static_cast<const __nv_bfloat16*>(P.logits) + r * P.ld + col0;
+        for (int32_t sg = 0; sg < nseg; ++sg, ring.next()) {
+          const uint32_t slot = ring.slot;
+          ptx::mbar_wait_sleep(ebase + slot * 8, ring.ph ^ 1u);
+          const int32_t v0 = sg * kPSlotVec;
+          const uint32_t bytes = static_cast<uint32_t>(min(kPSlotVec, nvec - v0)) * 16u;
+          ptx::mbar_arrive_expect_tx_u32(fbase + slot * 8, bytes);
+          ptx::bulk_g2s_u32(sbase + slot * kPSlotBytes, row + static_cast<int64_t>(v0) * 8, bytes,
+                            fbase + slot * 8, pol);
+        }
+      }
+    }
+  } else if (warp == kPW + 1) {
+    // ---------------- scalar warp: merge the pair's 32 partials, token math ------
+    MetaPipe mp;
+    if (lane == 0) mp.init(P, cid, ncl);
+    uint32_t i = 0;
+    for (int64_t r = cid; r < P.n_rows; r += ncl, ++i) {
+      RowMeta meta{};
+      if (lane == 0) meta = mp.advance(P, r, ncl);
+      const uint32_t bsel = i & 1u, par = (i >> 1) & 1u;
+      if (lane == 0) ptx::mbar_arrive_expect_tx_u32(p1b + bsel * 8, kPW * sizeof(PairPart));
+      ptx::mbar_wait_sleep(p1b + bsel * 8, par);
+      const PairPart e = red[bsel][lane];  // entry lane = rank * 16 + warp: same order in both CTAs
+      Lse tot{e.m, e.s, 0.f, 0.f};
+      warp_lse<false>(tot);
+      const uint32_t hv = __ballot_sync(0xffffffffu, e.have != 0.f);
+      float zy = __shfl_sync(0xffffffffu, e.zy, hv ? __ffs(hv) - 1 : 0);
+      if (lane == 0) {
+        const bool ok = static_cast<uint32_t>(meta.y) < static_cast<uint32_t>(P.vocab);
+        if (!ok) zy = 0.f;
+        // the target column stayed out of every thread's max: fold it into M
+        // so that M >= z_y as finish_logprob assumes
+        if (ok && hv && zy > tot.m) {
+          tot.s = tot.m == -INFINITY ? 0.f : tot.s * ptx::ex2((tot.m - zy) * kLog2e);
+          tot.m = zy;
+        }
+        bc[bsel] = row_scalar_phase<false>(P, P.row_base + r, meta.y, meta.st, meta.blp, meta.rl,
+                                           meta.adv, tot, zy, rank == 0, meta.keep);
+        ptx::mbar_arrive_u32(sdb + bsel * 8);
+      }
+      __syncwarp();
+    }
+  } else {
+    // ---------------- consumers ------------------------------------------------------
+    const int tid = threadIdx.x;
+    const uint32_t taddr0 = tmem_base + (static_cast<uint32_t>((warp & 3) * 32) << 16) +
+                            static_cast<uint32_t>((warp >> 2) * (kPTSlots * 16));
+    Ring ring(nslots);
+    uint32_t ts = 0;  // TMEM slot of the next pass-1 slot (mod kPTSlots)
+    const uint32_t red_peer = ptx::mapa(ptx::smem_u32(&red[0][0]), peer);
+    const uint32_t p1_peer = ptx::mapa(p1b, peer);
+    PhaseTimer tm;    // trace slots: 0 pass 1, 2 broadcast wait, 4 pass 2
+    tm.start(P.trace && tid == 0 && blockIdx.x < kTraceCtas);
+
+    auto run_p1 = [&](LaneAcc& a, int32_t ycol, int32_t sg0, int32_t sg1) {
+      for (int32_t sg = sg0; sg < sg1; ++sg, ring.next()) {
+        const uint32_t slot = ring.slot;
+        const int32_t v0 = sg * kPSlotVec;
+        const int32_t cnt = min(kPSlotVec, nvec - v0);
+        ptx::mbar_wait_sleep(fbase + slot * 8, ring.ph);
+        const uint32_t tsl = (ts + static_cast<uint32_t>(sg)) % kPTSlots;
+        const float nml = grad ? p1_slot<true>(a, sbase + slot * kPSlotBytes, v0, cnt, ycol, tid,
+                                               taddr0 + tsl * 16)
+                               : p1_slot<false>(a, sbase + slot * kPSlotBytes, v0, cnt, ycol, tid, 0u);
+        nml_sh[tsl * kPThreads + tid] = nml;
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_u32(ebase + slot * 8);
+      }
+    };
+    // publish row i's warp partial: own table + arrive, peer table by st.async
+    auto finish_p1 = [&](LaneAcc& a, uint32_t i) {
+      // warp merge: common max, rescale, sum (lanes without columns hold -inf, 0)
+      float M = a.m;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+      float sv = a.m == -INFINITY ? 0.f : a.s * ptx::ex2((a.m - M) * kLog2e);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sv += __shfl_xor_sync(0xffffffffu, sv, o);
+      const Lse st{M, sv * (1.f / 32768.f), 0.f, 0.f};
+      const uint32_t hv = __ballot_sync(0xffffffffu, a.have);
+      const float zy = __shfl_sync(0xffffffffu, a.zy, hv ? __ffs(hv) - 1 : 0);
+      if (lane == 0) {
+        const uint32_t bsel = i & 1u;
+        const uint32_t off = (bsel * 2 * kPW + rank * kPW + warp) * sizeof(PairPart);
+        const float hvf = hv ? 1.f : 0.f;
+        red[bsel][rank * kPW + warp] = PairPart{st.m, st.s, zy, hvf};
+        ptx::mbar_arrive_u32(p1b + bsel * 8);
+        st_async_v4(red_peer + off, st.m, st.s, zy, hvf, p1_peer + bsel * 8);
+      }
+    };
+
+    int64_t r = cid;
+    uint32_t i = 0;
+    if (r < P.n_rows) {
+      LaneAcc a0;
+      run_p1(a0, P.target[P.row_base + r] - col0, 0, nseg);
+      finish_p1(a0, 0);
+    }
+    for (; r < P.n_rows; r += ncl, ++i) {
+      const int64_t rn = r + ncl;
+      const bool nx = rn < P.n_rows;
+      const uint32_t ts_row = ts;  // TMEM slots of row i: ts_row .. ts_row + nseg - 1
+      LaneAcc an;
+      const int32_t ycn = nx ? P.target[P.row_base + rn] - col0 : -1;
+      ts = (ts + static_cast<uint32_t>(nseg)) % kPTSlots;
+      tm.mark(0);
+      if (nx) run_p1(an, ycn, 0, L);
+      tm.mark(0);
+      const uint32_t bsel = i & 1u, par = (i >> 1) & 1u;
+      ptx::mbar_wait_backoff(sdb + bsel * 8, par);  // row i's broadcast
+      tm.mark(2);
+      if (grad) {
+        const RowBroadcast b = bc[bsel];
+        const bool zero_row = b.coef == 0.f;
+        const int32_t ycol = b.y - col0;
+        __nv_bfloat16* drow = static_cast<__nv_bfloat16*>(P.dlogits) + r * P.ld_d + col0;
+        tmem_wait_st();  // this thread's pass-1 stores of row i have landed
+        for (int32_t sg = 0; sg < nseg; ++sg) {
+          const uint32_t tsl = (ts_row + static_cast<uint32_t>(sg)) % kPTSlots;
+          const int32_t v0 = sg * kPSlotVec;
+          p2_slot(b, zero_row, nml_sh[tsl * kPThreads + tid], taddr0 + tsl * 16, v0,
+                  min(kPSlotVec, nvec - v0), ycol, drow + static_cast<int64_t>(v0) * 8, tid);
+        }
+      }
+      tm.mark(4);
+      if (nx) {
+        run_p1(an, ycn, L, nseg);
+        finish_p1(an, i + 1);
+      }
+      tm.mark(0);
+      tm.acc[5] += 1;
+    }
+    tm.flush(P.trace);
+  }
+  // no CTA may exit (or free TMEM) while its peer can still address its shared
+  // memory or a thread of its own still reads TMEM
+  tc::fence_before_sync();
+  __syncthreads();
+  ptx::cluster_sync_all();
+  if (warp == 0 && grad) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc<kPTmemCols>(tmem_base);
+  }
+}
+
+}  // namespace
+
+bool pair_supported(const LossParams& p, DType in, DType out, bool ent) {
+  if (in != DType::BF16 || ent) return false;
+  if (p.dlogits != nullptr && !p.gather_only && out != DType::BF16) return false;
+  if (p.vocab % 16 != 0 || (p.ld * 2) % 16 != 0 || reinterpret_cast<uintptr_t>(p.logits) % 16 != 0)
+    return false;
+  if (p.dlogits && ((p.ld_d * 2) % 16 != 0 || reinterpret_cast<uintptr_t>(p.dlogits) % 16 != 0))
+    return false;
+  const int32_t nvec0 = (p.vocab / 8 + 1) / 2;
+  const int32_t nseg = (nvec0 + kPSlotVec - 1) / kPSlotVec;
+  return nseg <= kPTSlots - 1;  // room for at least one lookahead slot in TMEM
+}
+
+cudaError_t launch_pair(const LossParams& p, int num_sms, const Tuning& tu, cudaStream_t stream,
+                        LaunchInfo* info) {
+  // 6 x 32 KB ring + 16 KB of per-thread nml fill the 227 KB a CTA may use
+  const int nslots = tu.slots > 0 ? (tu.slots > 6 ? 6 : tu.slots) : 6;
+  const int smem = nslots * kPSlotBytes + kPTSlots * kPThreads * static_cast<int>(sizeof(float));
+  cudaError_t e = allow_dyn_smem(reinterpret_cast<const void*>(fused_pair_kernel), smem);
+  if (e != cudaSuccess) return e;
+  const int32_t nvec0 = (p.vocab / 8 + 1) / 2;
+  const int32_t nseg = (nvec0 + kPSlotVec - 1) / kPSlotVec;
+  int look = tu.pair_lookahead;
+  if (look > kPTSlots - nseg) look = kPTSlots - nseg;
+  if (look < 0) look = 0;
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.blockDim = dim3((kPW + 2) * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cfg.gridDim = dim3(static_cast<unsigned>(num_sms & ~1));
+  int ncl = 0;
+  e = cudaOccupancyMaxActiveClusters(&ncl, fused_pair_kernel, &cfg);
+  if (e != cudaSuccess) return e;
+  if (ncl < 1) return cudaErrorInvalidConfiguration;
+  const int64_t nc = p.n_rows < ncl ? p.n_rows : ncl;
+  cfg.gridDim = dim3(static_cast<unsigned>(2 * nc));
+  if (info) {
+    info->cluster = 2;
+    info->grid = static_cast<int>(2 * nc);
+    info->kernel = "fused_pair_kernel";
+  }
+  return cudaLaunchKernelEx(&cfg, fused_pair_kernel, p, nslots, look, nvec0);
+}
+
+}  // namespace copris_b200

@@ -133,6 +133,41 @@ __device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
       : "memory");
 }
 
+// The same wait with a suspend-time hint: the warp sleeps in the barrier
+// unit until the phase completes (or ~1 ms passes) instead of spinning, so a
+// waiting warp takes no issue slots from the warps that do the work.
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+// Wait with exponential nanosleep backoff between polls (64 .. 512 ns): for
+// waits that are usually long and not latency-critical to a few hundred ns,
+// so the waiting warps neither spin through issue slots nor burn power.
+__device__ __forceinline__ bool mbar_test_u32(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_backoff(uint32_t bar, uint32_t parity) {
+  uint32_t ns = 64;
+  while (!mbar_test_u32(bar, parity)) {
+    __nanosleep(ns);
+    ns = ns < 512 ? 2 * ns : ns;
+  }
+}
+
 __device__ __forceinline__ void mbar_arrive_u32(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
@@ -191,6 +226,13 @@ __device__ __forceinline__ void st_global_v4_hint(void* p, uint4 v, uint64_t pol
       "st.global.L1::no_allocate.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p),
       "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "l"(policy)
       : "memory");
+}
+
+// Streaming 16-byte store (.cs: evict-first in L2, no policy register).
+__device__ __forceinline__ void st_global_cs_v4(void* p, uint4 v) {
+  asm volatile("st.global.cs.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
 }
 
 __device__ __forceinline__ uint4 ld_shared_v4(const void* p) {

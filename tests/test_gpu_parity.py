@@ -22,8 +22,18 @@ def run(ctx, case, dl_dtype=BF16, fused=True, **kw):
 
 
 # (V, logits dtype, forced implementation or None, expected kernel, expected cluster)
+PAIR, LA = ("fused_pair_kernel", 2), ("fused_stream_la_kernel", 1)
 SHAPES = [
-    (151936, BF16, None, "fused_stream_la_kernel", 1),  # Qwen2.5 vocab: TMA ring + L2 re-read, lookahead
+    # Qwen2.5 vocab: the CTA-pair kernel (exponentials staged in TMEM) for bf16
+    # dlogits, the TMA ring + L2 re-read kernel for fp32 dlogits
+    (151936, BF16, None, (PAIR, LA), None),
+    (151936, BF16, "pair+pl0", (PAIR, LA), None),   # no lookahead: pass 2 right after the row
+    (151936, BF16, "pair+pl1", (PAIR, LA), None),
+    (151936, BF16, "pair+pl3+slots3", (PAIR, LA), None),  # short ring: producer waits on slots
+    (200000, BF16, None, (PAIR, LA), None),         # 7 slots per half-row: the TMEM ring wraps every row
+    (80000, BF16, None, (PAIR, LA), None),          # 3 slots per half, partial last slot
+    (40000, BF16, None, (PAIR, LA), None),          # 80 KB rows: smallest pair vocab
+    (151936, BF16, "stream", "fused_stream_la_kernel", 1),  # the ring kernel forced for bf16 too
     (151936, BF16, "stream+la0", "fused_stream_la_kernel", 1),  # same without the lookahead
     (151936, BF16, "stream+la5", "fused_stream_la_kernel", 1),
     (32000, BF16, None, "fused_tma_kernel", 1),       # 64 KB rows resident, several CTAs/SM
@@ -43,7 +53,7 @@ SHAPES = [
 ]
 
 # the context options every test starts from (copris_ctx_set_option)
-DEFAULT_OPTS = dict(fused_impl=0, lookahead=2, resident=1, slots=0, one_exp=1)
+DEFAULT_OPTS = dict(fused_impl=0, lookahead=2, resident=1, slots=0, pair_lookahead=3)
 
 
 @pytest.fixture
@@ -59,8 +69,10 @@ def impl(ctx):
                     opts["lookahead"] = int(o[2:])
                 elif o.startswith("res"):
                     opts["resident"] = int(o[3:])
-                elif o.startswith("exp"):
-                    opts["one_exp"] = int(o[3:])
+                elif o.startswith("pl"):
+                    opts["pair_lookahead"] = int(o[2:])
+                elif o.startswith("slots"):
+                    opts["slots"] = int(o[5:])
         if name:
             opts["fused_impl"] = name
         for k, v in opts.items():
@@ -73,6 +85,8 @@ def impl(ctx):
 @pytest.mark.parametrize("V,dtype,force,kernel,cluster", SHAPES)
 @pytest.mark.parametrize("dl_dtype", [BF16, F32])
 def test_fused_matches_oracle(ctx, oracle, impl, V, dtype, force, kernel, cluster, dl_dtype):
+    if cluster is None:  # (bf16-dlogits kernel, fp32-dlogits kernel)
+        kernel, cluster = kernel[0] if dl_dtype == BF16 else kernel[1]
     impl(force)
     P, G = (2, 4) if V > 50000 else (4, 4)
     case = Case(oracle, seed=V % 97 + 3, P=P, G=G, V=V, dtype=dtype, mu=math.log(10), lmax=24)
@@ -250,17 +264,20 @@ def test_padded_rows(ctx, oracle):
         case.check(res, F32, what=f"ld={ld}")
 
 
-def test_saturated_rows_one_minus_p(ctx, oracle):
+@pytest.mark.parametrize("dl_dtype", [F32, BF16])
+def test_saturated_rows_one_minus_p(ctx, oracle, dl_dtype):
     """Rows whose target saturates (p_y -> 1) keep 1-p_y accurate (the target
-    is excluded from the running sum): checked on every 64th row."""
+    is excluded from the running sum): checked on every 64th row; bf16
+    dlogits run the CTA-pair kernel, where the saturated target also stays out
+    of every warp's staging maximum."""
     case = Case(oracle, seed=17, P=4, G=4, V=151936, fixed_len=32)
-    _, res = run(ctx, case, F32)
+    _, res = run(ctx, case, dl_dtype)
     sat = np.arange(case.hb.n_tok) % 64 == 0
     assert sat.any()
-    dl = res.dlogits.cpu().numpy()[sat]
+    dl = res.dlogits.float().cpu().numpy()[sat]
     coef = -case.ref.weight / case.hb.n_tok
     exact = exact_dlogits(case.z64[sat], case.hb.target[sat], coef[sat])
-    assert_rows_close(dl, exact, what="saturated rows vs cancellation-free fp64")
+    assert_rows_close(dl, exact, bf16=dl_dtype == BF16, what="saturated rows vs cancellation-free fp64")
     assert_scalar_close(res.cur_lp.cpu().numpy()[sat], case.ref.cur_lp[sat], rtol=1e-6,
                         what="saturated cur_lp")
 
@@ -377,6 +394,18 @@ def test_forward_only_matches_forward_backward(ctx, oracle, impl, V, force):
     assert torch.equal(fwd.cur_lp, full.cur_lp) and torch.equal(fwd.coef, full.coef)
 
 
+@pytest.mark.parametrize("rows", [1, 37, 73, 74, 75, 148, 149, 300])
+def test_pair_rows_around_the_grid(ctx, oracle, impl, rows):
+    """Row counts around the pair kernel's persistent grid (74 CTA pairs): a
+    single row, clusters with one row next to clusters with several; all
+    against the oracle."""
+    impl(None)
+    case = Case(oracle, seed=rows, P=1, G=2, V=151936, fixed_len=(rows + 1) // 2)
+    _, res = run(ctx, case, BF16)
+    assert ctx.last_launch()["kernel"] == "fused_pair_kernel"
+    case.check(res, BF16, what=f"rows={case.hb.n_tok}")
+
+
 @pytest.mark.parametrize("half", [37, 74, 75, 148, 150])
 def test_stream_rows_around_the_grid(ctx, oracle, impl, half):
     """Row counts around the persistent grid (148 SMs): 74 .. 300 rows, i.e. CTAs
@@ -487,7 +516,26 @@ def test_k1_equals_loss_recompute_bitwise(ctx, oracle, V, dtype):
     case = Case(oracle, seed=19, P=2, G=4, V=V, dtype=dtype, mu=math.log(10), lmax=24)
     logits = case.logits_gpu()
     lp, lse = ctx.sequence_logprobs(logits, torch.from_numpy(case.hb.target).cuda())
-    _, res = run(ctx, case, F32)
+    # bf16 dlogits: the kernel K1 shares its pass 1 with (the pair kernel at
+    # V = 151,936 with bf16 logits; fp32 dlogits run the ring kernel there)
+    _, res = run(ctx, case, BF16 if dtype == BF16 else F32)
     assert torch.equal(lp.view(torch.int32), res.cur_lp.view(torch.int32))
     assert torch.equal(lse.view(torch.int32), res.lse.view(torch.int32))
     assert_scalar_close(lp.cpu().numpy(), case.ref.cur_lp, what=f"K1 V={V}")
+
+
+def test_pair_and_ring_kernels_agree(ctx, oracle, impl):
+    """At V = 151,936 the CTA-pair kernel (bf16 dlogits, TMEM-staged f16
+    exponentials) and the ring kernel (fp32 dlogits, exponentials recomputed)
+    split the log-sum-exp differently: per-token outputs agree to fp32
+    rounding, the pair kernel's bf16 dlogits are within one bf16 ulp of the
+    ring kernel's fp32 dlogits, and branch decisions are identical."""
+    case = Case(oracle, seed=29, P=2, G=8, V=151936, mu=math.log(24), lmax=64)
+    _, a = run(ctx, case, BF16)
+    assert ctx.last_launch()["kernel"] == "fused_pair_kernel"
+    _, b = run(ctx, case, F32)
+    assert ctx.last_launch()["kernel"] == "fused_stream_la_kernel"
+    assert_scalar_close(a.cur_lp.cpu().numpy(), b.cur_lp.cpu().numpy(), rtol=2e-6, what="cur_lp")
+    assert torch.equal(a.flags, b.flags)
+    ref = b.dlogits.double().cpu().numpy()
+    assert_rows_close(a.dlogits.float().cpu().numpy(), ref, bf16=True, what="pair vs ring dlogits")
