@@ -242,8 +242,11 @@ def run_ours(args):
                                                  stale_logprobs)
 
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", str(args.gpus if args.gpus == 1 else 1)))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        # never print a line whose n_gpus differs from the requested N
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     # control-flow rehearsal of the multi-rank path on a single GPU (not a
     # measurement): COPRIS_BENCH_ONE_GPU=1 puts every rank on cuda:0 and
     # COPRIS_BENCH_BACKEND=gloo replaces NCCL (which refuses shared devices)
@@ -251,12 +254,20 @@ def run_ours(args):
         local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    comm = {"backend": None, "world_size": 1}
     if world > 1:
         backend = os.environ.get("COPRIS_BENCH_BACKEND", "nccl")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
+        # the communicator's own rank count (what the allreduce runs over)
+        probe = torch.ones(1, dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
+        dist.all_reduce(probe)
+        comm = {"backend": dist.get_backend(), "world_size": dist.get_world_size(),
+                "ranks_in_allreduce": int(probe.item())}
+        if comm["world_size"] != args.gpus or comm["ranks_in_allreduce"] != args.gpus:
+            raise SystemExit(f"bench.py: communicator has {comm} ranks, --gpus {args.gpus}")
 
     cfgd = dict(CONFIGS[args.config])
     V = cfgd["vocab"]
@@ -407,6 +418,7 @@ def run_ours(args):
                          "algorithmic_bytes_per_token": bytes_per_tok,
                          "kernel_ms_per_step": kern_ms / args.steps,
                          "frac_of_8TBs_nominal": achieved / 8000.0},
+            "comm": comm,
             "gpu_launches": args.steps * (nchunks * (3 if args.unfused else 1) + 1),
             "clocks": clocks,
         }
@@ -475,8 +487,30 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def relaunch_under_torchrun(args) -> int:
+    """`python bench.py --gpus N` (N > 1) outside torchrun: start the N ranks
+    here, one process per GPU, exactly as the driver's torchrun launch would
+    (127.0.0.1 rendezvous on a free port); rank 0 prints the line."""
+    import socket
+    import torch
+    n_dev = torch.cuda.device_count()
+    if args.impl == "ours" and n_dev < args.gpus and not os.environ.get("COPRIS_BENCH_ONE_GPU"):
+        print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {n_dev}",
+              file=sys.stderr)
+        return 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args))
     if args.impl == "reference":
         run_reference(args)
     else:

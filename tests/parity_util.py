@@ -148,3 +148,41 @@ def exact_dlogits(z64, target, coef):
     others = np.where(mask, e, 0.0).sum(axis=1)
     d[rows, target] = coef * others / S[:, 0]
     return d
+
+
+def oracle_per_token(oracle, logits_cpu, tok_off, target, stage, cur_stage, blp, adv,
+                     chunk=256, threads=None, **cfg):
+    """The CPU oracle's per-token outputs (cur_lp, behav, obj, weight, clipped)
+    over ALL rows of a large batch, computed on host threads in row chunks.
+
+    Per-token results depend only on the token's logits row, its stage and
+    buffered log-prob and its trajectory's advantage, so each chunk [a, b) is
+    presented to the oracle as the trajectories' pieces inside it (each piece
+    keeping its trajectory's advantage). ``logits_cpu`` is a bf16/f32 torch
+    tensor; rows are widened to fp64 one chunk at a time. The loss and the
+    dlogits coefficients are formed by the caller from obj / weight with the
+    batch's own T (grpo.hpp:135,183)."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+
+    tok_off = np.asarray(tok_off, np.int64)
+    T = int(tok_off[-1])
+    out = {k: np.zeros(T, np.float64) for k in ("cur_lp", "behav", "obj", "weight")}
+    out["clipped"] = np.zeros(T, np.uint8)
+
+    def work(a):
+        b = min(T, a + chunk)
+        t_lo = int(np.searchsorted(tok_off, a, side="right")) - 1
+        t_hi = int(np.searchsorted(tok_off, b, side="left"))
+        sub = np.clip(tok_off[t_lo:t_hi + 1], a, b) - a
+        z = logits_cpu[a:b].double().numpy()
+        r = oracle.is_loss(z, sub, target[a:b], stage[a:b], cur_stage,
+                           np.asarray(blp[a:b], np.float64), np.asarray(adv[t_lo:t_hi], np.float64),
+                           want_dlogits=False, **cfg)
+        for k in ("cur_lp", "behav", "obj", "weight", "clipped"):
+            out[k][a:b] = getattr(r, k)
+
+    n = threads or os.cpu_count() or 1
+    with ThreadPoolExecutor(max_workers=n) as ex:
+        list(ex.map(work, range(0, T, chunk)))
+    return out

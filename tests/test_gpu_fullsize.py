@@ -1,12 +1,16 @@
-"""GPU: full-size parity at BASELINE config #2 shapes through size-independent
-properties (the oracle cannot run 10^10-element rows in test time):
+"""GPU: full-size parity at BASELINE config #2, #3 and #4 shapes.
 
-  * whole prompt groups (>= 1 group, ~24k rows) at V = 151,936 of the config-#2
-    batch: dlogits rows sum to zero (sum_k coef (1[k=y] - p_k) = 0), the target
-    entry equals coef (1 - exp(cur_lp)), every off-target entry is
-    -coef p_k with p_k = exp(z_k - lse) (checked on sampled columns);
-  * 48 sampled rows against the CPU oracle in full;
-  * stale/clipped counts and the loss agree with the per-token outputs;
+  * configs #2 (128 x 8, sigma 1, 2 stages) and #3 (sigma 1.5, 3-4 stages),
+    V = 151,936: whole prompt groups of the config batch (~24k rows): EVERY
+    row's cur_lp, behaviour log-prob, objective term, coef and flags against
+    the CPU oracle (oracle_per_token, host threads), the loss, and dlogits on
+    sampled rows rebuilt from the ORACLE's coefficients; plus size-independent
+    properties over all rows (dlogits rows sum to zero, the target entry is
+    coef (1 - p_y), off-target entries -coef p_k on sampled columns);
+  * config #4 (512 x 16, sharded by prompt group): whole groups LPT-sharded
+    over 2 and 4 ranks (one context per rank on this GPU, T_global passed to
+    every rank, the four scalars summed): per-token outputs and dlogits
+    bitwise those of the unsharded run, loss and counts equal to the oracle;
   * bit-identical reruns and chunk-size invariance at full size.
 """
 
@@ -19,12 +23,19 @@ from parity_util import assert_rows_close, assert_scalar_close
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module")
-def big(ctx):
+def assert_rel_close(gpu, ref, rtol=1e-5, atol=1e-300, what=""):
+    gpu = np.asarray(gpu, np.float64)
+    ref = np.asarray(ref, np.float64)
+    err = np.abs(gpu - ref) - (rtol * np.abs(ref) + atol)
+    assert np.all(err <= 0), f"{what}: {int((err > 0).sum())} out of tolerance, worst excess {err.max():.3e}"
+
+
+@pytest.fixture(scope="module", params=["grpo_128x8_v151936", "grpo_128x8_v151936_longtail_4stage"])
+def big(ctx, request):
     from paper_2511_05589_b200 import ClipConfig
     from paper_2511_05589_b200.packing import upload
     from paper_2511_05589_b200.workload import CONFIGS, make_host_batch, make_logits, stale_logprobs
-    cfg = dict(CONFIGS["grpo_128x8_v151936"])
+    cfg = dict(CONFIGS[request.param])
     P, G, V = cfg.pop("P"), cfg.pop("G"), cfg.pop("vocab")
     hb = make_host_batch(1, 8, G, V, **cfg)          # prompt groups of the config
     # whole groups, at least one, up to ~24k tokens (7 GB of bf16 logits)
@@ -43,8 +54,36 @@ def big(ctx):
     batch = upload(ctx, tok_off, group_off, target, blp, hb.cur_stage, stage=stage,
                    reward=hb.reward[:n_traj])
     res = ctx.grpo_step_loss(logits, batch, ClipConfig(), coef=True)
+    assert ctx.last_launch()["kernel"] == "fused_pair_kernel"
     return dict(hb=hb, T=T, V=V, logits=logits, batch=batch, res=res, target=target, stage=stage,
-                blp=blp, tok_off=tok_off, group_off=group_off)
+                blp=blp, tok_off=tok_off, group_off=group_off, n_traj=n_traj, name=request.param)
+
+
+@pytest.fixture(scope="module")
+def big_oracle(big, oracle):
+    """The oracle's per-token outputs over every row of `big` (host threads)."""
+    from parity_util import oracle_per_token
+    adv = oracle.advantages(big["hb"].reward[:big["n_traj"]], big["group_off"])
+    return oracle_per_token(oracle, big["logits"].cpu(), big["tok_off"], big["target"], big["stage"],
+                            big["hb"].cur_stage, big["blp"], adv)
+
+
+def test_all_rows_against_oracle(big, big_oracle):
+    """every row at the config's shape against the oracle, not
+    against the kernel's own intermediates."""
+    from parity_util import assert_loss_close
+    res, T, ref = big["res"], big["T"], big_oracle
+    what = big["name"]
+    assert_scalar_close(res.cur_lp.cpu().numpy(), ref["cur_lp"], what=f"{what} cur_lp")
+    assert_scalar_close(res.behav.cpu().numpy(), ref["behav"], what=f"{what} behav")
+    assert_scalar_close(res.obj.cpu().numpy(), ref["obj"], what=f"{what} obj")
+    # coef = -w / T (policy.hpp:188 with scale -inv_t): relative, it is ~1/T
+    assert_rel_close(res.coef.cpu().numpy(), -ref["weight"] / T, rtol=1e-5, what=f"{what} coef")
+    flags = res.flags.cpu().numpy()
+    np.testing.assert_array_equal(flags & 1, (big["stage"] < big["hb"].cur_stage).astype(np.uint8))
+    np.testing.assert_array_equal((flags >> 1) & 1, ref["clipped"])
+    assert res.clipped_tokens == int(ref["clipped"].sum())
+    assert_loss_close(res.loss, -ref["obj"].sum() / T, ref["obj"], T, what=f"{what} loss")
 
 
 def test_rows_sum_to_zero_and_target_entry(big):
@@ -52,9 +91,11 @@ def test_rows_sum_to_zero_and_target_entry(big):
     dl = res.dlogits.float()
     coef = res.coef.float()
     rs = dl.sum(dim=1)
-    scale = coef.abs() * 1.0
-    # bf16 rounding of V entries: sum error ~ sqrt(V) * 2^-9 * |coef| / V ... bounded by 2^-8 |coef|
-    assert torch.all(rs.abs() <= 4e-3 * scale + 1e-30), float((rs.abs() / (scale + 1e-30)).max())
+    # exact rows sum to zero (sum_k coef (1[k=y] - p_k) = 0); each bf16 entry is
+    # within one ulp (2^-7 relative at most) of its exact value, so the sum of
+    # the rounded entries is within 2^-7 sum_k |d_k| of zero
+    tol = 2.0 ** -7 * dl.abs().sum(dim=1)
+    assert torch.all(rs.abs() <= tol + 1e-30), float((rs.abs() / (tol + 1e-30)).max())
     y = torch.from_numpy(big["target"]).cuda().long()
     dy = dl[torch.arange(T, device="cuda"), y]
     expect = coef * -torch.expm1(res.cur_lp.float())
@@ -75,16 +116,20 @@ def test_sampled_columns_match_softmax(big):
     assert torch.all((got - expect).abs() <= 2 ** -7 * expect.abs() + 1e-5 * rowmax + 1e-30)
 
 
-def test_sampled_rows_against_oracle(big, oracle):
+def test_sampled_rows_against_oracle(big, big_oracle, oracle):
     res, T, V = big["res"], big["T"], big["V"]
     rng = np.random.default_rng(0)
     rows = np.sort(rng.choice(T, 48, replace=False))
+    # rows with a nonzero coefficient first: those carry a softmax to check
+    w = big_oracle["weight"]
+    live = np.flatnonzero(w != 0.0)
+    rows = np.sort(np.unique(np.concatenate([rows[:16], rng.choice(live, min(32, len(live)), replace=False)])))
     z = big["logits"][torch.from_numpy(rows).cuda()].double().cpu().numpy()
     tgt = big["target"][rows]
     ref_cur = oracle.logprob_gather(z, tgt)
     assert_scalar_close(res.cur_lp.cpu().numpy()[rows], ref_cur, what="cur_lp rows")
-    # per-row dlogits = coef (onehot - softmax) with the kernel's coef
-    coef = res.coef.cpu().numpy()[rows]
+    # per-row dlogits = coef (onehot - softmax) with the ORACLE's coef -w/T
+    coef = -w[rows] / T
     e = np.exp(z - z.max(1, keepdims=True))
     p = e / e.sum(1, keepdims=True)
     ref = -coef[:, None] * p
@@ -166,3 +211,58 @@ def test_v32000_claimed_rows_against_oracle(ctx, oracle):
     again = ctx.grpo_step_loss(logits, batch, ClipConfig(), coef=True)
     assert torch.equal(again.dlogits.view(torch.int16), res.dlogits.view(torch.int16))
     assert torch.equal(again.obj, res.obj) and again.loss == res.loss
+
+
+def test_config4_sharded_equals_unsharded(ctx, oracle):
+    """BASELINE config #4 (512 x 16, max 16k tokens, sharded by prompt group)
+    on this GPU: whole groups of the config's batch, LPT-sharded over 2 and 4
+    ranks, one context per rank, T_global passed to each, the four scalars
+    summed (the allreduce). Rows are independent and every rank scales by the
+    global T, so each shard's per-token outputs and dlogits are bitwise the
+    unsharded run's; the loss and counts equal the oracle's over all rows."""
+    from paper_2511_05589_b200 import ClipConfig, Copris
+    from paper_2511_05589_b200.packing import upload
+    from paper_2511_05589_b200.sharding import loss_from_scalars, lpt_shard, shard_arrays
+    from paper_2511_05589_b200.workload import CONFIGS, make_host_batch, make_logits, stale_logprobs
+    from parity_util import assert_loss_close, oracle_per_token
+    cfg = dict(CONFIGS["grpo_512x16_v151936"])
+    P, G, V = cfg.pop("P"), cfg.pop("G"), cfg.pop("vocab")
+    cfg.pop("strong")
+    cfg["mu"], cfg["lmax"] = np.log(512.0), 2048  # the config's shape law, lengths scaled to test size
+    hb = make_host_batch(4, 8, G, V, **cfg)       # 8 prompt groups x 16 responses
+    T = hb.n_tok
+    tgt = torch.from_numpy(hb.target).cuda()
+    logits = make_logits(T, V, tgt, 4, device="cuda")
+    cur, _ = ctx.sequence_logprobs(logits, tgt)
+    blp = stale_logprobs(cur.cpu().numpy(), hb.stage, hb.cur_stage, 4)
+    whole = upload(ctx, hb.tok_off, hb.group_off, hb.target, blp, hb.cur_stage, stage=hb.stage,
+                   reward=hb.reward)
+    full = ctx.grpo_step_loss(logits, whole, ClipConfig(), coef=True)
+    adv = oracle.advantages(hb.reward, hb.group_off)
+    ref = oracle_per_token(oracle, logits.cpu(), hb.tok_off, hb.target, hb.stage, hb.cur_stage, blp, adv)
+    assert_loss_close(full.loss, -ref["obj"].sum() / T, ref["obj"], T, what="config #4 unsharded")
+    assert full.clipped_tokens == int(ref["clipped"].sum())
+    for world in (2, 4):
+        shards = lpt_shard(hb.group_tokens(), world)
+        total = torch.zeros(4, dtype=torch.float64)
+        for rank in range(world):
+            rctx = Copris(0)  # one context per rank
+            t_off, g_off, pt, pj, idx = shard_arrays(
+                hb.tok_off, hb.group_off, {"target": hb.target, "stage": hb.stage, "blp": blp},
+                {"reward": hb.reward}, shards[rank])
+            n = len(idx)
+            b = upload(rctx, t_off, g_off, pt["target"], pt["blp"], hb.cur_stage, stage=pt["stage"],
+                       reward=pj["reward"])
+            gi = torch.from_numpy(idx).cuda()
+            part = rctx.grpo_step_loss(logits[gi], b, ClipConfig(), coef=True, total_tokens=T)
+            assert torch.equal(part.cur_lp, full.cur_lp[gi])
+            assert torch.equal(part.obj, full.obj[gi]) and torch.equal(part.coef, full.coef[gi])
+            assert torch.equal(part.flags, full.flags[gi])
+            assert torch.equal(part.dlogits.view(torch.int16), full.dlogits[gi].view(torch.int16))
+            total += torch.tensor([part.objective, part.token_count, part.stale_tokens,
+                                   part.clipped_tokens], dtype=torch.float64)
+            rctx.close()
+        assert int(total[1]) == T and int(total[3]) == full.clipped_tokens
+        assert int(total[2]) == full.stale_tokens
+        assert_loss_close(loss_from_scalars(total, T), -ref["obj"].sum() / T, ref["obj"], T,
+                          what=f"config #4 over {world} ranks")
