@@ -311,11 +311,12 @@ def run_ours(args):
             n = min(chunk, T - r0)
             if evs is not None:
                 evs[c][0].record()
+            # the last chunk carries out4: the reduction rides along (inside
+            # the loss launch when the step is small, else right behind it)
             run_chunk(logits[:n], batch, clip, outs, dlogits=dl[:n], row_base=r0,
-                      total_tokens=T_global)
+                      total_tokens=T_global, out4=out4 if c == nchunks - 1 else None)
             if evs is not None:
                 evs[c][1].record()
-        ctx.reduce(outs, T, out4)
 
     graph = None
 
@@ -332,6 +333,7 @@ def run_ours(args):
         step()
     ctx.check()
     info = ctx.last_launch()
+    fused_reduce = bool(info.get("fused_reduce")) and not args.unfused
     if args.graph:
         # CUDA graph of one step: the per-launch host cost (Python + C-ABI)
         # leaves the loop; replays are bitwise identical to eager steps
@@ -419,7 +421,8 @@ def run_ours(args):
                          "kernel_ms_per_step": kern_ms / args.steps,
                          "frac_of_8TBs_nominal": achieved / 8000.0},
             "comm": comm,
-            "gpu_launches": args.steps * (nchunks * (3 if args.unfused else 1) + 1),
+            "gpu_launches": args.steps * (nchunks * (3 if args.unfused else 1)
+                                          + (0 if fused_reduce else 1)),
             "clocks": clocks,
         }
 

@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define COPRIS_B200_ABI_VERSION 2
+#define COPRIS_B200_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define COPRIS_API __attribute__((visibility("default")))
@@ -240,6 +240,11 @@ typedef struct {
   double* obj;               /* [T] required: per-token objective */
   double* coef;              /* [T] optional: dlogits row scale -w/T */
   uint8_t* flags;            /* [T] required: COPRIS_FLAG_* */
+  /* optional DEVICE f64[4]: after this chunk, reduce rows [0, row_base + n_rows)
+   * exactly as copris_loss_reduce does (bitwise the same out4); small batches
+   * (<= 8,192 tokens) are reduced by the loss launch itself (its last CTA), so
+   * a one-chunk step is ONE kernel launch. Pass it with the last chunk only. */
+  double* out4;
 } copris_loss_out;
 
 /* Fused single pass: log-softmax+gather, behaviour select, ratio/clip/KL/
@@ -413,6 +418,10 @@ COPRIS_API int copris_engine_stats(const copris_engine* e, int64_t out[7]);
  * name of the last copris_is_loss_* launch on this context. */
 COPRIS_API int copris_ctx_last_launch(const copris_ctx* ctx, int* cluster, int* grid, int* num_sms,
                            const char** kernel_name);
+
+/* Introspection: 1 when the last copris_is_loss_fused launch on this context
+ * also reduced into copris_loss_out.out4 (no separate reduction launch). */
+COPRIS_API int copris_ctx_last_fused_reduce(const copris_ctx* ctx);
 
 /* Diagnostics (not a reference entry point): per-CTA phase-cycle counters of
  * the fused kernels, recorded when the context's `trace` option is on

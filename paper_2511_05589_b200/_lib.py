@@ -39,7 +39,8 @@ class LossCfg(C.Structure):
 
 class LossOut(C.Structure):
     _fields_ = [("dlogits", P), ("ld_dlogits", I64), ("dlogits_dtype", I32), ("_pad", I32),
-                ("cur_lp", P), ("lse", P), ("behav", P), ("obj", P), ("coef", P), ("flags", P)]
+                ("cur_lp", P), ("lse", P), ("behav", P), ("obj", P), ("coef", P), ("flags", P),
+                ("out4", P)]
 
 
 class HostBatch(C.Structure):
@@ -107,6 +108,7 @@ _SIGS = {
                                     C.POINTER(HostResult)], C.c_int),
     "copris_ctx_trace_read": ([P, P, C.c_int], C.c_int),
     "copris_ctx_set_option": ([P, C.c_char_p, I64], C.c_int),
+    "copris_ctx_last_fused_reduce": ([P], C.c_int),
     "copris_ctx_get_option": ([P, C.c_char_p, C.POINTER(I64)], C.c_int),
     "copris_adam_update": ([P, P, P, P, P, I64, I64, C.POINTER(AdamCfg), P], C.c_int),
     "copris_checkpoint_write": ([C.c_char_p, P, P, C.c_uint64, C.c_uint64], C.c_int),

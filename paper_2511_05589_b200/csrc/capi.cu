@@ -111,6 +111,9 @@ LossParams make_params(const copris_ctx* ctx, const copris_loss_batch* b, const 
   p.err = ctx->d_err;
   p.trace = ctx->d_trace;
   p.row_ctr = ctx->d_rowctr;
+  p.out4 = o->out4;
+  p.red_scratch = ctx->d_scratch;
+  p.red_n = b->row_base + b->n_rows;
   return p;
 }
 
@@ -434,6 +437,8 @@ int copris_ctx_last_launch(const copris_ctx* ctx, int* cluster, int* grid, int* 
   if (kernel_name) *kernel_name = ctx->last.kernel ? ctx->last.kernel : "";
   return COPRIS_OK;
 }
+
+int copris_ctx_last_fused_reduce(const copris_ctx* ctx) { return ctx ? ctx->last.reduced : 0; }
 
 int copris_ctx_set_option(copris_ctx* ctx, const char* name, int64_t value) {
   if (!ctx || !name) return fail(COPRIS_E_INVALID, "null argument");

@@ -42,6 +42,162 @@ namespace copris_b200 {
 
 namespace {
 
+// Deterministic reduction of the per-token outputs (obj, flags) of a batch.
+// The token range is cut into TILES whose size depends on n only
+// (reduce_tile); each tile's partial is formed by 256 threads in a fixed order
+// (4-token quads, then a fixed tree), and the final result sums the tile
+// partials in a fixed order (thread i takes partials i, i + 256, ..., then the
+// same tree). The same device code runs in reduce_kernel (blocks take tiles
+// b, b + nb, ...; the last block to finish sums) and in the last CTA of a
+// fused loss launch (it takes every tile): both give bitwise the same out4,
+// and any rerun is bitwise identical. No floating-point atomics.
+constexpr int kReduceBlocks = 512;
+constexpr int kReduceThreads = 256;
+constexpr int kReduceMaxTiles = 8192;
+constexpr int kFuseReduceTiles = 8;  // fused into the loss launch up to 8 tiles (8,192 tokens)
+struct ReduceScratch {
+  double obj[kReduceMaxTiles];
+  unsigned long long stale[kReduceMaxTiles];  // stale | masked << 32
+  unsigned long long clipped[kReduceMaxTiles];
+  unsigned int ticket;        // reduce_kernel blocks done
+  unsigned int fused_ticket;  // fused-launch CTAs done
+};
+
+__host__ __device__ inline int64_t reduce_tile(int64_t n) {
+  const int64_t per = (n + kReduceMaxTiles - 1) / kReduceMaxTiles;
+  const int64_t t = (per + 1023) / 1024 * 1024;
+  return t < 1024 ? 1024 : t;
+}
+
+// Shared-memory arrays of the 256-thread trees.
+struct ReduceSmem {
+  double o[kReduceThreads];
+  unsigned long long s[kReduceThreads], c[kReduceThreads], m[kReduceThreads];
+};
+
+// Tree over the 256 participating threads (named barrier 1: the caller's CTA
+// may have more threads; those do not take part).
+__device__ __forceinline__ void reduce_tree(ReduceSmem& sm, int tid, bool four) {
+  ptx::named_bar_sync(1, kReduceThreads);
+  for (int h = kReduceThreads / 2; h > 0; h >>= 1) {
+    if (tid < h) {
+      sm.o[tid] += sm.o[tid + h];
+      sm.s[tid] += sm.s[tid + h];
+      sm.c[tid] += sm.c[tid + h];
+      if (four) sm.m[tid] += sm.m[tid + h];
+    }
+    ptx::named_bar_sync(1, kReduceThreads);
+  }
+}
+
+// Partial of tile `k` (tokens [k tile, min(n, (k+1) tile))) by threads 0..255,
+// written to sc by thread 0. VEC: obj 16-byte and flags 4-byte aligned.
+template <bool VEC>
+__device__ __forceinline__ void reduce_tile_partial(const double* __restrict__ obj,
+                                                    const uint8_t* __restrict__ flags, int64_t n,
+                                                    int64_t tile, int64_t k, ReduceScratch* sc,
+                                                    ReduceSmem& sm, int tid) {
+  const int64_t t0 = k * tile, t1 = min(n, t0 + tile);
+  double o = 0.0;
+  unsigned long long st = 0, cl = 0, mk = 0;
+  auto tally = [&](uint32_t f) {
+    st += f & FLAG_STALE;
+    cl += (f >> 1) & 1u;
+    mk += (f >> 2) & 1u;
+  };
+  if constexpr (VEC) {
+    const int64_t q1 = t0 + ((t1 - t0) & ~int64_t{3});  // end of whole quads
+    for (int64_t t = t0 + 4 * tid; t < q1; t += 4 * kReduceThreads) {
+      const double2 a0 = *reinterpret_cast<const double2*>(obj + t);
+      const double2 a1 = *reinterpret_cast<const double2*>(obj + t + 2);
+      const uint32_t fa = *reinterpret_cast<const uint32_t*>(flags + t);
+      o += (a0.x + a0.y) + (a1.x + a1.y);
+      tally(fa & 0xFFu); tally((fa >> 8) & 0xFFu); tally((fa >> 16) & 0xFFu); tally(fa >> 24);
+    }
+    for (int64_t u = q1 + tid; u < t1; u += kReduceThreads) {
+      o += obj[u];
+      tally(flags[u]);
+    }
+  } else {
+    for (int64_t t = t0 + tid; t < t1; t += kReduceThreads) {
+      o += obj[t];
+      tally(flags[t]);
+    }
+  }
+  // stale/clipped counts < 2^32 per tile: pack the masked count with stale
+  sm.o[tid] = o;
+  sm.s[tid] = st | (mk << 32);
+  sm.c[tid] = cl;
+  reduce_tree(sm, tid, false);
+  if (tid == 0) {
+    sc->obj[k] = sm.o[0];
+    sc->stale[k] = sm.s[0];
+    sc->clipped[k] = sm.c[0];
+  }
+  ptx::named_bar_sync(1, kReduceThreads);  // sm is reused by the next tile
+}
+
+// The final sum over the tile partials (fixed order) -> out4; resets tickets.
+__device__ __forceinline__ void reduce_final(int64_t n, int64_t ntiles, double* __restrict__ out4,
+                                             ReduceScratch* sc, ReduceSmem& sm, int tid) {
+  double O = 0.0;
+  unsigned long long Sx = 0, Cx = 0, Mx = 0;
+  for (int64_t i = tid; i < ntiles; i += kReduceThreads) {
+    O += *reinterpret_cast<volatile double*>(&sc->obj[i]);
+    const unsigned long long sm2 = *reinterpret_cast<volatile unsigned long long*>(&sc->stale[i]);
+    Sx += sm2 & 0xFFFFFFFFull;
+    Mx += sm2 >> 32;
+    Cx += *reinterpret_cast<volatile unsigned long long*>(&sc->clipped[i]);
+  }
+  sm.o[tid] = O;
+  sm.s[tid] = Sx;
+  sm.c[tid] = Cx;
+  sm.m[tid] = Mx;
+  reduce_tree(sm, tid, true);
+  if (tid == 0) {
+    out4[0] = sm.o[0];
+    out4[1] = static_cast<double>(n - static_cast<int64_t>(sm.m[0]));
+    out4[2] = static_cast<double>(sm.s[0]);
+    out4[3] = static_cast<double>(sm.c[0]);
+    sc->ticket = 0;
+    sc->fused_ticket = 0;
+  }
+}
+
+// All tiles by one CTA (threads 0..255 of it), then the final sum: the last
+// CTA of a fused loss launch (fused_reduce_if_last).
+template <bool VEC>
+__device__ __forceinline__ void reduce_all_in_cta(const double* obj, const uint8_t* flags, int64_t n,
+                                                  double* out4, ReduceScratch* sc, ReduceSmem& sm,
+                                                  int tid) {
+  const int64_t tile = reduce_tile(n), ntiles = (n + tile - 1) / tile;
+  for (int64_t k = 0; k < ntiles; ++k) reduce_tile_partial<VEC>(obj, flags, n, tile, k, sc, sm, tid);
+  reduce_final(n, ntiles, out4, sc, sm, tid);
+}
+
+// End of a fused loss launch with P.out4 set: every CTA, after its rows'
+// outputs are written (by the scalar-phase thread, which fences them), counts
+// itself done; the last one reduces rows [0, P.red_n) into P.out4.
+// `sm_raw` is shared memory the CTA no longer needs (>= sizeof(ReduceSmem)).
+__device__ __forceinline__ void fused_reduce_if_last(const LossParams& P, void* sm_raw) {
+  __shared__ bool last;
+  __threadfence();  // this thread's obj/flags stores, before the ticket
+  __syncthreads();
+  auto* sc = static_cast<ReduceScratch*>(P.red_scratch);
+  if (threadIdx.x == 0) last = atomicAdd(&sc->fused_ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last || threadIdx.x >= kReduceThreads) return;
+  __threadfence();
+  ReduceSmem& sm = *static_cast<ReduceSmem*>(sm_raw);
+  const bool vec = (reinterpret_cast<uintptr_t>(P.obj) % 16 == 0) &&
+                   (reinterpret_cast<uintptr_t>(P.flags) % 4 == 0);
+  if (vec)
+    reduce_all_in_cta<true>(P.obj, P.flags, P.red_n, P.out4, sc, sm, threadIdx.x);
+  else
+    reduce_all_in_cta<false>(P.obj, P.flags, P.red_n, P.out4, sc, sm, threadIdx.x);
+}
+
+
 // ---------------------------------------------------------------------------
 // fused TMA / cluster kernel
 // ---------------------------------------------------------------------------
@@ -391,6 +547,8 @@ __global__ void __launch_bounds__(WARPS * 32, (WARPS == 8 && CL == 1) ? 3 : 1)
   tm.flush(P.trace);
   // no CTA may exit while a peer can still address its shared memory
   if constexpr (CL > 1) ptx::cluster_sync_all();
+  // the row buffer is free now: it holds the trees of the fused reduction
+  if (P.out4) fused_reduce_if_last(P, smem);
 }
 
 // ---------------------------------------------------------------------------
@@ -885,128 +1043,23 @@ __global__ void adam_kernel(double* __restrict__ p, const double* __restrict__ g
   }
 }
 
-// Deterministic two-level reduction: fixed block partition, fixed in-block
-// tree, and the last block sums block partials in index order.
-constexpr int kReduceBlocks = 512;
-constexpr int kReduceThreads = 256;
-struct ReduceScratch {
-  double obj[kReduceBlocks];
-  unsigned long long stale[kReduceBlocks];
-  unsigned long long clipped[kReduceBlocks];
-  unsigned int ticket;
-};
-
-// VEC (obj 16-byte and flags 4-byte aligned): each block's range starts at a
-// multiple of 4 tokens and a thread reads 4 tokens per step (two double2 and
-// one 4-byte flag word), two steps in flight — the scalar form kept too few
-// bytes in flight per SM (0.41 of HBM at 47M tokens). Fixed partition and
-// order either way, so a rerun is bitwise identical.
 template <bool VEC>
 __global__ void __launch_bounds__(kReduceThreads)
     reduce_kernel(const double* __restrict__ obj, const uint8_t* __restrict__ flags, int64_t n,
                   double* __restrict__ out4, ReduceScratch* sc) {
-  __shared__ double so[kReduceThreads];
-  __shared__ unsigned long long ss[kReduceThreads], sk[kReduceThreads], smk[kReduceThreads];
+  __shared__ ReduceSmem sm;
   __shared__ bool last;
-  const int64_t nb = gridDim.x;
-  int64_t b0 = n * blockIdx.x / nb, b1 = n * (blockIdx.x + 1) / nb;
-  double o = 0.0;
-  unsigned long long st = 0, cl = 0, mk = 0;
-  auto tally = [&](uint32_t f) {
-    st += f & FLAG_STALE;
-    cl += (f >> 1) & 1u;
-    mk += (f >> 2) & 1u;
-  };
-  if constexpr (VEC) {
-    b0 &= ~int64_t{3};
-    if (blockIdx.x + 1 < gridDim.x) b1 &= ~int64_t{3};
-    const int64_t q1 = b0 + ((b1 - b0) & ~int64_t{3});  // end of whole quads
-    const int64_t step = 4 * static_cast<int64_t>(blockDim.x);
-    int64_t t = b0 + 4 * static_cast<int64_t>(threadIdx.x);
-    for (; t + step < q1; t += 2 * step) {
-      const double2 a0 = *reinterpret_cast<const double2*>(obj + t);
-      const double2 a1 = *reinterpret_cast<const double2*>(obj + t + 2);
-      const double2 c0 = *reinterpret_cast<const double2*>(obj + t + step);
-      const double2 c1 = *reinterpret_cast<const double2*>(obj + t + step + 2);
-      const uint32_t fa = *reinterpret_cast<const uint32_t*>(flags + t);
-      const uint32_t fc = *reinterpret_cast<const uint32_t*>(flags + t + step);
-      o += ((a0.x + a0.y) + (a1.x + a1.y)) + ((c0.x + c0.y) + (c1.x + c1.y));
-      tally(fa & 0xFFu); tally((fa >> 8) & 0xFFu); tally((fa >> 16) & 0xFFu); tally(fa >> 24);
-      tally(fc & 0xFFu); tally((fc >> 8) & 0xFFu); tally((fc >> 16) & 0xFFu); tally(fc >> 24);
-    }
-    for (; t < q1; t += step) {
-      const double2 a0 = *reinterpret_cast<const double2*>(obj + t);
-      const double2 a1 = *reinterpret_cast<const double2*>(obj + t + 2);
-      const uint32_t fa = *reinterpret_cast<const uint32_t*>(flags + t);
-      o += (a0.x + a0.y) + (a1.x + a1.y);
-      tally(fa & 0xFFu); tally((fa >> 8) & 0xFFu); tally((fa >> 16) & 0xFFu); tally(fa >> 24);
-    }
-    for (int64_t u = q1 + threadIdx.x; u < b1; u += blockDim.x) {
-      o += obj[u];
-      tally(flags[u]);
-    }
-  } else {
-    for (int64_t t = b0 + threadIdx.x; t < b1; t += blockDim.x) {
-      o += obj[t];
-      tally(flags[t]);
-    }
-  }
-  // stale/clipped counts < 2^32 per block: pack them with the masked count
-  so[threadIdx.x] = o;
-  ss[threadIdx.x] = st | (mk << 32);
-  sk[threadIdx.x] = cl;
-  __syncthreads();
-  for (int h = blockDim.x / 2; h > 0; h >>= 1) {
-    if (threadIdx.x < h) {
-      so[threadIdx.x] += so[threadIdx.x + h];
-      ss[threadIdx.x] += ss[threadIdx.x + h];
-      sk[threadIdx.x] += sk[threadIdx.x + h];
-    }
-    __syncthreads();
-  }
+  const int64_t tile = reduce_tile(n), ntiles = (n + tile - 1) / tile;
+  for (int64_t k = blockIdx.x; k < ntiles; k += gridDim.x)
+    reduce_tile_partial<VEC>(obj, flags, n, tile, k, sc, sm, threadIdx.x);
   if (threadIdx.x == 0) {
-    sc->obj[blockIdx.x] = so[0];
-    sc->stale[blockIdx.x] = ss[0];
-    sc->clipped[blockIdx.x] = sk[0];
     __threadfence();
     last = atomicAdd(&sc->ticket, 1u) == gridDim.x - 1;
   }
   __syncthreads();
   if (last) {
-    // the last block sums the per-block partials with all its threads (a
-    // fixed thread-to-partial map and the same tree, so the order is fixed);
-    // one thread walking 512 partials cost ~40 us of dependent L2 loads
     __threadfence();
-    double O = 0.0;
-    unsigned long long Sx = 0, Cx = 0, Mx = 0;
-    for (int i = threadIdx.x; i < gridDim.x; i += blockDim.x) {
-      O += *reinterpret_cast<volatile double*>(&sc->obj[i]);
-      const unsigned long long sm = *reinterpret_cast<volatile unsigned long long*>(&sc->stale[i]);
-      Sx += sm & 0xFFFFFFFFull;
-      Mx += sm >> 32;
-      Cx += *reinterpret_cast<volatile unsigned long long*>(&sc->clipped[i]);
-    }
-    so[threadIdx.x] = O;
-    ss[threadIdx.x] = Sx;
-    sk[threadIdx.x] = Cx;
-    smk[threadIdx.x] = Mx;
-    __syncthreads();
-    for (int h = blockDim.x / 2; h > 0; h >>= 1) {
-      if (threadIdx.x < h) {
-        so[threadIdx.x] += so[threadIdx.x + h];
-        ss[threadIdx.x] += ss[threadIdx.x + h];
-        sk[threadIdx.x] += sk[threadIdx.x + h];
-        smk[threadIdx.x] += smk[threadIdx.x + h];
-      }
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-      out4[0] = so[0];
-      out4[1] = static_cast<double>(n - static_cast<int64_t>(smk[0]));
-      out4[2] = static_cast<double>(ss[0]);
-      out4[3] = static_cast<double>(sk[0]);
-      sc->ticket = 0;
-    }
+    reduce_final(n, ntiles, out4, sc, sm, threadIdx.x);
   }
 }
 
@@ -1039,16 +1092,23 @@ cudaError_t launch_tma(const LossParams& p, int32_t E, int num_sms, cudaStream_t
   const int64_t resident = static_cast<int64_t>(per_sm) * num_sms;
   if (resident < 1) return cudaErrorInvalidConfiguration;
   const int64_t grid = p.n_rows < resident ? p.n_rows : resident;
+  // fused reduction for small steps (<= kFuseReduceTiles tiles): the last CTA
+  // reduces in its row buffer; larger steps keep the separate reduce launch
+  LossParams q = p;
+  const bool fuse = p.out4 && p.red_scratch && smem >= static_cast<int>(sizeof(ReduceSmem)) &&
+                    p.red_n <= kFuseReduceTiles * reduce_tile(p.red_n);
+  if (!fuse) q.out4 = nullptr;
   if (info) {
     info->cluster = CL;
     info->grid = static_cast<int>(grid);
     info->kernel = "fused_tma_kernel";
+    info->reduced = fuse ? 1 : 0;
   }
   if (p.row_ctr) {
     e = cudaMemsetAsync(p.row_ctr, 0, sizeof(unsigned long long), stream);
     if (e != cudaSuccess) return e;
   }
-  kernel<<<static_cast<unsigned>(grid), WARPS * 32, smem, stream>>>(p, E);
+  kernel<<<static_cast<unsigned>(grid), WARPS * 32, smem, stream>>>(q, E);
   return cudaGetLastError();
 }
 
@@ -1158,9 +1218,22 @@ cudaError_t by_types(bool bwd, const LossParams& p, DType in, DType out, int num
 
 }  // namespace
 
+cudaError_t launch_fused_kernel(const LossParams& p, DType in, DType out, int num_sms,
+                                const Tuning& tu, cudaStream_t stream, LaunchInfo* info);
+
 cudaError_t launch_fused(const LossParams& p, DType in, DType out, int num_sms, const Tuning& tu,
                          cudaStream_t stream, LaunchInfo* info) {
-  if (info) info->num_sms = num_sms;
+  LaunchInfo li{};
+  cudaError_t e = launch_fused_kernel(p, in, out, num_sms, tu, stream, &li);
+  li.num_sms = num_sms;
+  if (e == cudaSuccess && p.out4 && !li.reduced)
+    e = launch_reduce(p.obj, p.flags, p.red_n, p.out4, p.red_scratch, num_sms, stream);
+  if (info) *info = li;
+  return e;
+}
+
+cudaError_t launch_fused_kernel(const LossParams& p, DType in, DType out, int num_sms,
+                                const Tuning& tu, cudaStream_t stream, LaunchInfo* info) {
   if (p.n_rows == 0) return cudaSuccess;
   // bf16 rows above 72 KB: the CTA-pair kernel (one HBM read, exponentials
   // staged in TMEM, no L2 re-read) unless another kernel is forced
@@ -1175,10 +1248,15 @@ cudaError_t launch_fused(const LossParams& p, DType in, DType out, int num_sms, 
 cudaError_t launch_bwd(const LossParams& p, DType in, DType out, int num_sms,
                        cudaStream_t stream, LaunchInfo* info) {
   if (info) info->num_sms = num_sms;
-  if (p.n_rows == 0) return cudaSuccess;
-  const Tuning tu{};
-  return p.entropy_coeff != 0.0 ? by_types<true>(true, p, in, out, num_sms, tu, stream, info)
-                                : by_types<false>(true, p, in, out, num_sms, tu, stream, info);
+  cudaError_t e = cudaSuccess;
+  if (p.n_rows > 0) {
+    const Tuning tu{};
+    e = p.entropy_coeff != 0.0 ? by_types<true>(true, p, in, out, num_sms, tu, stream, info)
+                               : by_types<false>(true, p, in, out, num_sms, tu, stream, info);
+  }
+  if (e == cudaSuccess && p.out4)
+    e = launch_reduce(p.obj, p.flags, p.red_n, p.out4, p.red_scratch, num_sms, stream);
+  return e;
 }
 
 // K1 = the fused kernels in gather-only mode: the same TMA/shared-memory
@@ -1363,9 +1441,12 @@ cudaError_t launch_adam(double* p, const double* g, double* m, double* v, int64_
 cudaError_t launch_reduce(const double* obj, const uint8_t* flags, int64_t n_tok, double* out4,
                           void* scratch, int num_sms, cudaStream_t stream) {
   (void)num_sms;
-  int64_t nb = (n_tok + 4 * kReduceThreads - 1) / (4 * kReduceThreads);
-  if (nb > kReduceBlocks) nb = kReduceBlocks;
-  if (nb < 1) nb = 1;
+  if (n_tok == 0) {
+    // an empty batch: zeros (a tile-less reduce would still reset the tickets)
+    return cudaMemsetAsync(out4, 0, 4 * sizeof(double), stream);
+  }
+  const int64_t tile = reduce_tile(n_tok), ntiles = (n_tok + tile - 1) / tile;
+  int64_t nb = ntiles < kReduceBlocks ? ntiles : kReduceBlocks;
   const bool vec = (reinterpret_cast<uintptr_t>(obj) % 16 == 0) &&
                    (reinterpret_cast<uintptr_t>(flags) % 4 == 0);
   if (vec)

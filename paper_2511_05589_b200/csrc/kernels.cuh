@@ -67,6 +67,12 @@ struct LossParams {
   long long* trace;  // optional per-CTA phase-cycle accumulators (COPRIS_TRACE)
   unsigned long long* row_ctr;  // dynamic row claims; zeroed by the launcher before each launch
   int32_t gather_only;  // K1 mode: only (cur_lp, lse) per row — no metadata, no objective
+  // optional fused reduction: the launch also reduces rows [0, red_n) of
+  // obj/flags into out4 (the last CTA to finish does it; kernels that do not
+  // support it leave out4 to a separate reduce launch, see launch_fused)
+  double* out4;
+  void* red_scratch;
+  int64_t red_n;
 };
 
 // Phase accumulators written by the fused kernels when LossParams::trace is
@@ -111,6 +117,7 @@ struct LaunchInfo {
   int cluster;       // CTAs per row chosen by the dispatcher (fused TMA path)
   int grid;          // CTAs launched
   const char* kernel;
+  int reduced;       // 1: the loss launch itself reduced into out4 (no second launch)
 };
 
 // Fused single-pass loss. Chooses the TMA/cluster kernel when rows are 16-byte

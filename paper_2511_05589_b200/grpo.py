@@ -214,7 +214,8 @@ class Copris:
         self._call(self.lib.copris_ctx_last_launch(self.h, C.byref(cl), C.byref(grid),
                                                    C.byref(sms), C.byref(name)))
         return {"cluster": cl.value, "grid": grid.value, "num_sms": sms.value,
-                "kernel": name.value.decode() if name.value else ""}
+                "kernel": name.value.decode() if name.value else "",
+                "fused_reduce": bool(self.lib.copris_ctx_last_fused_reduce(self.h))}
 
     # -- K1 -----------------------------------------------------------------------
     @_on_stream
@@ -349,7 +350,7 @@ class Copris:
 
     # -- K3 -----------------------------------------------------------------------
     def _structs(self, logits, batch: PackedBatch, cfg: ClipConfig, is_enabled, behav_mode,
-                 total_tokens, row_base, dlogits, outs):
+                 total_tokens, row_base, dlogits, outs, out4=None):
         n_rows, v = logits.shape
         b = L.LossBatch(_p(logits), logits.stride(0), _dtype_code(logits.dtype), v, n_rows,
                         row_base, _p(batch.target), _p(batch.stage), _p(batch.buffered_lp),
@@ -360,7 +361,7 @@ class Copris:
         o = L.LossOut(_p(dlogits), dlogits.stride(0) if dlogits is not None else 0,
                       _dtype_code(dlogits.dtype) if dlogits is not None else 0, 0,
                       _p(outs.get("cur_lp")), _p(outs.get("lse")), _p(outs.get("behav")),
-                      _p(outs["obj"]), _p(outs.get("coef")), _p(outs["flags"]))
+                      _p(outs["obj"]), _p(outs.get("coef")), _p(outs["flags"]), _p(out4))
         return b, c, o
 
     def alloc_outputs(self, n_tok: int, device, coef=False, lse=True, behav=True):
@@ -376,18 +377,20 @@ class Copris:
 
     def loss_chunk_fused(self, logits, batch, cfg, outs, *, dlogits=None, row_base=0,
                          total_tokens=None, is_enabled=True,
-                         behav_mode=L.COPRIS_BEHAV_RECOMPUTED, stream=None):
-        """Launch the fused kernel on one chunk of rows (no sync)."""
+                         behav_mode=L.COPRIS_BEHAV_RECOMPUTED, out4=None, stream=None):
+        """Launch the fused kernel on one chunk of rows (no sync). ``out4`` (a
+        device f64[4], with the LAST chunk) also reduces rows [0, row_base + n)
+        — in the same launch for small batches (copris_loss_out.out4)."""
         T = total_tokens if total_tokens is not None else batch.loss_tokens()
         b, c, o = self._structs(logits, batch, cfg, is_enabled, behav_mode, T, row_base, dlogits,
-                                outs)
+                                outs, out4)
         self._call(self.lib.copris_is_loss_fused(self.h, C.byref(b), C.byref(c), C.byref(o),
                                                  self._stream(stream)))
 
     def loss_chunk_unfused(self, logits, batch, cfg, outs, *, dlogits=None, row_base=0,
                            total_tokens=None, is_enabled=True,
-                           behav_mode=L.COPRIS_BEHAV_RECOMPUTED, stream=None):
-        """K1 -> K2 -> K3 on one chunk of rows (no sync)."""
+                           behav_mode=L.COPRIS_BEHAV_RECOMPUTED, out4=None, stream=None):
+        """K1 -> K2 -> K3 on one chunk of rows (no sync); ``out4`` as for the fused path."""
         T = total_tokens if total_tokens is not None else batch.loss_tokens()
         n = logits.shape[0]
         sl = slice(row_base, row_base + n)
@@ -398,7 +401,7 @@ class Copris:
             self.h, _p(batch.stage[sl]), batch.cur_stage, _p(batch.buffered_lp[sl]), _p(cur),
             int(is_enabled), behav_mode, n, _p(behav), None, self._stream(stream)))
         b, c, o = self._structs(logits, batch, cfg, is_enabled, behav_mode, T, row_base, dlogits,
-                                outs)
+                                outs, out4)
         # K3 indexes its per-token inputs by the packed index: pass the full arrays
         self._call(self.lib.copris_is_loss_bwd(self.h, C.byref(b), C.byref(c), _p(outs["cur_lp"]),
                                                _p(outs["lse"]), _p(outs["behav"]), C.byref(o),
@@ -440,10 +443,10 @@ class Copris:
                                   device=logits.device)
         outs = self.alloc_outputs(batch.n_tok, logits.device, coef=coef)
         run = self.loss_chunk_fused if fused else self.loss_chunk_unfused
-        run(logits, batch, cfg, outs, dlogits=dlogits if want_grad else None, row_base=0,
-            total_tokens=T, is_enabled=is_enabled, behav_mode=behav_mode, stream=stream)
         out4 = torch.empty(4, dtype=torch.float64, device=logits.device)
-        self.reduce(outs, batch.n_tok, out4, stream=stream)
+        # one call: the reduction rides along (in the loss launch when small)
+        run(logits, batch, cfg, outs, dlogits=dlogits if want_grad else None, row_base=0,
+            total_tokens=T, is_enabled=is_enabled, behav_mode=behav_mode, out4=out4, stream=stream)
         self.check(stream)
         o = out4.cpu().tolist()
         return GrpoStepResult(loss=-o[0] * (1.0 / T), dlogits=dlogits if want_grad else None,

@@ -20,7 +20,7 @@ def test_library_loads_and_exports_every_declared_symbol():
     for name in declared:
         assert hasattr(lib, name), f"{name} declared in include/copris_b200.h but not exported"
     assert set(declared) == set(L._SIGS), "ctypes signatures out of sync with the header"
-    assert lib.copris_abi_version() == 2
+    assert lib.copris_abi_version() == 3
 
 
 def test_exports_nothing_else():
@@ -44,7 +44,7 @@ int main(void) {
   printf("copris_host_result %zu\n", sizeof(copris_host_result));
   F(copris_loss_batch, cur_stage) F(copris_loss_batch, adv) F(copris_loss_batch, tok_traj)
   F(copris_loss_cfg, total_tokens) F(copris_loss_cfg, behav_mode)
-  F(copris_loss_out, flags) F(copris_loss_out, cur_lp)
+  F(copris_loss_out, flags) F(copris_loss_out, cur_lp) F(copris_loss_out, out4)
   F(copris_host_batch, adv_epsilon) F(copris_host_batch, cur_stage) F(copris_host_batch, group_off)
   F(copris_host_result, loss) F(copris_host_result, clipped_tokens)
   return 0;

@@ -539,3 +539,43 @@ def test_pair_and_ring_kernels_agree(ctx, oracle, impl):
     assert torch.equal(a.flags, b.flags)
     ref = b.dlogits.double().cpu().numpy()
     assert_rows_close(a.dlogits.float().cpu().numpy(), ref, bf16=True, what="pair vs ring dlogits")
+
+
+@pytest.mark.parametrize("n_tok,masked", [(2048, False), (1000, False), (4099, True), (8192, False),
+                                          (8193, False)])
+def test_fused_reduction_bitwise(ctx, oracle, impl, n_tok, masked):
+    """copris_loss_out.out4: a one-chunk step of <= 8,192 tokens is reduced by
+    the loss launch's last CTA (ONE launch); larger ones by the separate
+    reduction. Either way out4 is bitwise copris_loss_reduce's result (same
+    tiles, same fixed order), reruns are bitwise identical, and the loss
+    matches the oracle."""
+    impl(None)
+    case = Case(oracle, seed=n_tok, P=1, G=n_tok // 256 + 1, V=32000, fixed_len=256)
+    hb = case.hb
+    batch = case.upload(ctx)
+    n = min(n_tok, hb.n_tok)
+    logits = case.logits_gpu()[:n]
+    keep = np.random.default_rng(1).random(hb.n_tok) > 0.2
+    if masked:
+        batch.loss_mask = torch.from_numpy(keep.astype(np.uint8)).cuda()
+    outs = ctx.alloc_outputs(hb.n_tok, logits.device)
+    dl = torch.empty((n, case.V), dtype=torch.bfloat16, device="cuda")
+    T = hb.n_tok
+    fused4 = torch.full((4,), -1.0, dtype=torch.float64, device="cuda")
+    ctx.loss_chunk_fused(logits, batch, case.clip(), outs, dlogits=dl, total_tokens=T, out4=fused4)
+    info = ctx.last_launch()
+    assert info["kernel"] == "fused_tma_kernel" and info["fused_reduce"] == (n <= 8192)
+    sep4 = torch.zeros(4, dtype=torch.float64, device="cuda")
+    ctx.reduce(outs, n, sep4)
+    ctx.check()
+    assert torch.equal(fused4, sep4)
+    again = torch.zeros(4, dtype=torch.float64, device="cuda")
+    ctx.loss_chunk_fused(logits, batch, case.clip(), outs, dlogits=dl, total_tokens=T, out4=again)
+    torch.cuda.synchronize()
+    assert torch.equal(again, fused4)
+    k = keep[:n] if masked else np.ones(n, bool)
+    obj = outs["obj"].cpu().numpy()[:n]
+    assert int(fused4[1]) == int(k.sum())
+    assert abs(fused4[0].item() - obj.sum()) <= 1e-12 * max(1.0, np.abs(obj).sum())
+    if n == hb.n_tok and not masked:
+        assert_loss_close(-fused4[0].item() / T, case.ref.loss, case.ref.obj, T, what="fused out4")
