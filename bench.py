@@ -44,6 +44,8 @@ def parse_args():
     ap.add_argument("--config", default="grpo_128x8_v151936")
     ap.add_argument("--chunk-rows", type=int, default=32768)
     ap.add_argument("--unfused", action="store_true", help="K1 -> K2 -> K3 instead of the fused kernel")
+    ap.add_argument("--dlogits", choices=["bf16", "f32"], default="bf16",
+                    help="f32: the parity mode (dlogits within 1e-5; 6V+16 B/token)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-tokens", type=int, default=16384, help="per-rank sample for the host round trip")
@@ -123,13 +125,18 @@ def measured_peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def traffic_per_row(config, unfused):
+def traffic_per_row(config, unfused, kernel, dlogits="bf16"):
     """dram bytes per row of the top kernel from the committed ncu capture
-    (profiles/ncu_traffic.json, written from an `ncu --set full` run)."""
+    (profiles/ncu_traffic.json, written from an `ncu --set full` run); None
+    unless that capture is of the kernel this run launched."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             t = json.load(f)
-        return float(t[("unfused:" if unfused else "") + config]["dram_bytes_per_row"])
+        key = ("unfused:" if unfused else "") + config + (":f32" if dlogits == "f32" else "")
+        rec = t[key]
+        if not unfused and kernel not in rec["kernel"]:
+            return None
+        return float(rec["dram_bytes_per_row"])
     except (OSError, KeyError, ValueError):
         return None
 
@@ -301,7 +308,8 @@ def run_ours(args):
     del cur
     batch = upload(ctx, tok_off, group_off, target, blp, hb.cur_stage, stage=stage, reward=reward)
     outs = ctx.alloc_outputs(T, dev, lse=args.unfused, behav=args.unfused)
-    dl = torch.empty((chunk, V), dtype=torch.bfloat16, device=dev)
+    dl = torch.empty((chunk, V), dtype=torch.float32 if args.dlogits == "f32" else torch.bfloat16,
+                     device=dev)
     out4 = torch.zeros(4, dtype=torch.float64, device=dev)
     run_chunk = ctx.loss_chunk_unfused if args.unfused else ctx.loss_chunk_fused
 
@@ -387,10 +395,10 @@ def run_ours(args):
     else:
         kern_ms = ms * args.steps
     rows_timed = args.steps * T
-    bytes_per_tok = 4 * V + 16
+    bytes_per_tok = (6 if args.dlogits == "f32" else 4) * V + 16
     achieved = rows_timed * bytes_per_tok / (kern_ms / 1e3) / 1e9
     peak, peak_src = measured_peaks()
-    tr = traffic_per_row(args.config, args.unfused)
+    tr = traffic_per_row(args.config, args.unfused, info.get("kernel", ""), args.dlogits)
 
     line = None
     if rank == 0:
@@ -413,6 +421,8 @@ def run_ours(args):
                 "loss": loss,
                 "offpolicy_fraction": out4[2].item() / out4[1].item() if out4[1].item() else 0.0,
                 "clipped_tokens": int(out4[3].item()),
+                "dlogits": ("f32 (parity mode: within 1e-5; 6V+16 B/token)" if args.dlogits == "f32"
+                            else "bf16 (within 1 bf16 ulp; 4V+16 B/token)"),
             },
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_source": peak_src,

@@ -352,6 +352,20 @@ typedef struct {
 COPRIS_API int copris_adam_update(copris_ctx* ctx, double* params, const double* grad, double* m,
                                   double* v, int64_t n, int64_t step, const copris_adam_cfg* cfg,
                                   void* stream);
+/* The whole AdamOptimizer object (grpo.hpp:205-235) for a HOST-side parameter
+ * table: the optimizer owns device copies of the moments (the reference's m_,
+ * v_) and its step count t_; each copris_adam_host_update copies params and
+ * grad in, runs copris_adam_update's kernel and copies params back, on the
+ * optimizer's own stream, synchronously (the reference update is a blocking
+ * call). `n` must equal the size given at creation, else COPRIS_E_CONTRACT
+ * "gradient shape mismatch" (grpo.hpp:210). */
+typedef struct copris_adam_host copris_adam_host;
+COPRIS_API int copris_adam_host_create(copris_ctx* ctx, int64_t n, const copris_adam_cfg* cfg,
+                                       copris_adam_host** out);
+COPRIS_API int copris_adam_host_update(copris_adam_host* opt, double* params, const double* grad,
+                                       int64_t n);
+COPRIS_API int copris_adam_host_steps(const copris_adam_host* opt, int64_t* t);
+COPRIS_API int copris_adam_host_destroy(copris_adam_host* opt);
 COPRIS_API int copris_checkpoint_write(const char* path, const double* logits, const int32_t dims[4],
                                        uint64_t version, uint64_t seed);
 /* Reads the header first: call with logits == NULL to get dims/version/seed,

@@ -179,4 +179,40 @@ class DropIn {
   std::vector<double> adv_;
 };
 
+// Drop-in for AdamOptimizer (grpo.hpp:205-235): replaces
+//     adam_.update(params_, res.grad);                                      // trainer.hpp:177
+// with
+//     gpu_adam_.update<ContractViolation, ConfigError>(params_, res.grad);
+// The moments live on the device (copris_adam_host); each update is one
+// blocking call that leaves params.logits updated and bumps params.version by
+// exactly 1, as the reference does.
+class AdamDropIn {
+ public:
+  // `Cfg` is the reference's AdamConfig (.lr, .beta1, .beta2, .eps, .weight_decay).
+  template <class Cfg>
+  AdamDropIn(copris_ctx* ctx, const Cfg& c) : ctx_(ctx) {
+    cfg_ = copris_adam_cfg{c.lr, c.beta1, c.beta2, c.eps, c.weight_decay};
+  }
+  ~AdamDropIn() {
+    if (opt_) copris_adam_host_destroy(opt_);
+  }
+  AdamDropIn(const AdamDropIn&) = delete;
+  AdamDropIn& operator=(const AdamDropIn&) = delete;
+
+  template <class ContractViolation, class ConfigError, class Params>
+  void update(Params& params, std::span<const double> grad) {
+    if (grad.size() != params.logits.size()) throw ContractViolation("gradient shape mismatch");
+    const int64_t n = static_cast<int64_t>(grad.size());
+    if (!opt_) throw_status<ContractViolation, ConfigError>(copris_adam_host_create(ctx_, n, &cfg_, &opt_));
+    throw_status<ContractViolation, ConfigError>(
+        copris_adam_host_update(opt_, params.logits.data(), grad.data(), n));
+    params.version += 1;
+  }
+
+ private:
+  copris_ctx* ctx_;
+  copris_adam_cfg cfg_{};
+  copris_adam_host* opt_ = nullptr;
+};
+
 }  // namespace copris_b200

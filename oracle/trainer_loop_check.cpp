@@ -1,0 +1,269 @@
+// trainer_loop_check.cpp — TEST INFRASTRUCTURE (built into oracle/_ref/, needs
+// the reference headers at build time; runs on the GPU box).
+//
+// The reference training loop with the GPU IN the loop: GpuLoopTrainer is
+// Trainer::train_step (trainer.hpp:120-178) restated over the reference's own
+// public pieces (run_stage, RolloutEngine, ClusterSim, terminal_reward,
+// compute_advantages, sequence_logprobs, concat_segments), except that the two
+// numeric steps are the drop-ins a maintainer would install:
+//   trainer.hpp:176  grpo_step_loss(params_, items, clip)  -> copris_b200::DropIn
+//   trainer.hpp:177  adam_.update(params_, res.grad)       -> copris_b200::AdamDropIn
+// so the GPU's gradient and update drive the next rollout. It runs beside the
+// UNMODIFIED reference Trainer on the same config and reports, per step, the
+// loss of both runs, whether the batch they formed is the same (ids, tokens,
+// stored log-probs), and the max parameter difference. Until the scheduler
+// first forms a different batch the losses must agree within 1e-5 (relative);
+// the step at which the runs diverge is reported (the two runs are chaotic
+// dynamical systems over token sampling: a gradient that differs in the 7th
+// digit moves a sampled token once a uniform draw lands that close to a CDF
+// boundary).
+//
+// Also the GPU form of acceptance criterion C2 (acceptance_main.cpp:105-121,
+// test_trainer.cpp:25-36): the synchronous GpuLoopTrainer against the
+// reference's standalone on-policy loop (tests/support/reference_loop.hpp),
+// reporting the max per-step parameter difference.
+//
+// Output: one JSON line per step and one summary line per case; exit status 1
+// if any pre-divergence step disagrees.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <optional>
+#include <span>
+#include <string>
+#include <vector>
+
+#include "copris/trainer.hpp"
+#include "copris_b200/grpo_dropin.hpp"
+#include "support/reference_loop.hpp"
+
+using namespace copris;
+
+namespace {
+
+RunConfig desk_config() {  // io.hpp:445-457
+  RunConfig cfg;
+  cfg.mode = SchedulingMode::Copris;
+  cfg.is_enabled = true;
+  cfg.engine = EngineConfig{16, 4, 4, 8, 0};
+  cfg.policy = PolicyShape{4, 8, 6, 4};
+  cfg.cluster = ClusterConfig{4, 1.0, 0.05, 64, 8};
+  cfg.length_model = LengthModel{LengthMode::PolicyDriven, 0.0, 0.0};
+  cfg.total_steps = 200;
+  cfg.seed = 1;
+  cfg.eval_every = 0;
+  return cfg;
+}
+
+// FNV-1a over the batch the scheduler formed: trajectory ids, tokens and
+// segment (version, length), in batch order. The stored log-prob VALUES are
+// left out: they were sampled under slightly different parameters.
+struct Fingerprint {
+  uint64_t h = 1469598103934665603ull;
+  void mix(const void* p, size_t n) {
+    const auto* b = static_cast<const unsigned char*>(p);
+    for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
+  }
+  template <class T>
+  void mix(const T& v) {
+    mix(&v, sizeof(v));
+  }
+};
+
+uint64_t batch_fingerprint(const TrainBatch& batch) {
+  Fingerprint f;
+  for (const auto& g : batch.groups)
+    for (const auto& m : g.members) {
+      f.mix(m.traj_id);
+      for (int t : m.tokens.tokens) f.mix(t);
+      for (const auto& s : m.segments) {
+        f.mix(s.policy_version);
+        f.mix(s.logprobs.size());
+      }
+    }
+  return f.h;
+}
+
+// Trainer (trainer.hpp:100-229) with the loss and the update on the GPU.
+class GpuLoopTrainer {
+ public:
+  explicit GpuLoopTrainer(RunConfig cfg)
+      : cfg_(std::move(cfg)),
+        init_rng_(cfg_.seed, "init"),
+        params_(make_params()),
+        engine_(cfg_.engine, cfg_.mode, cfg_.policy, RngStream(cfg_.seed, "prompt")),
+        cluster_(cfg_.cluster, cfg_.engine.max_response_len, nullptr),
+        gpu_(0),
+        gpu_adam_(gpu_.ctx(), cfg_.adam) {
+    if (cfg_.clip.kl_coeff > 0.0) reference_ = snapshot(params_);
+  }
+
+  struct Step {
+    double loss;
+    uint64_t fingerprint;
+    size_t tokens;
+  };
+
+  Step train_step() {  // trainer.hpp:120-178
+    StageContext sctx;
+    sctx.seed = cfg_.seed;
+    sctx.length_model = cfg_.length_model;
+    sctx.token_streams = &token_streams_;
+    if (cfg_.mode == SchedulingMode::Copris) sctx.expected_in_flight = cfg_.engine.concurrency;
+    StageResult stage = run_stage(params_, engine_, cluster_, sctx);
+    const auto& ev = engine_.evicted_ids();
+    for (; evicted_seen_ < ev.size(); ++evicted_seen_) token_streams_.erase(ev[evicted_seen_]);
+
+    const TrainBatch& batch = stage.batch;
+    const int eos = cfg_.policy.eos_token();
+    std::vector<GrpoItem> items;
+    items.reserve(batch.total_trajectories());
+    for (const auto& g : batch.groups) {
+      std::vector<double> rewards;
+      for (const auto& m : g.members) rewards.push_back(terminal_reward(m, g.question, eos));
+      std::vector<double> adv = compute_advantages(rewards, cfg_.clip.adv_epsilon);
+      for (size_t i = 0; i < g.members.size(); ++i) {
+        GrpoItem item;
+        item.traj = &g.members[i];
+        item.advantage = adv[i];
+        item.current_lp = sequence_logprobs(params_, g.question, g.members[i].tokens);
+        item.stored_lp = cfg_.is_enabled ? concat_segments(g.members[i]) : item.current_lp;
+        if (reference_) item.ref_lp = sequence_logprobs(*reference_, g.question, g.members[i].tokens);
+        items.push_back(std::move(item));
+      }
+    }
+    Step out{0.0, batch_fingerprint(batch), batch.total_tokens()};
+    GrpoStepResult res = gpu_.grpo_step_loss<GrpoStepResult, ContractViolation, ConfigError>(
+        params_, std::span<const GrpoItem>(items), cfg_.clip);
+    out.loss = res.loss;
+    gpu_adam_.update<ContractViolation, ConfigError>(params_, std::span<const double>(res.grad));
+    return out;
+  }
+
+  const PolicyParams& params() const { return params_; }
+
+ private:
+  PolicyParams make_params() {
+    cfg_.validate();
+    return PolicyParams::init_near_uniform(cfg_.policy, init_rng_);
+  }
+
+  RunConfig cfg_;
+  RngStream init_rng_;
+  PolicyParams params_;
+  RolloutEngine engine_;
+  ClusterSim cluster_;
+  std::map<uint64_t, RngStream> token_streams_;
+  std::optional<PolicyParams> reference_;
+  size_t evicted_seen_ = 0;
+  copris_b200::DropIn gpu_;
+  copris_b200::AdamDropIn gpu_adam_;
+};
+
+double max_param_diff(const PolicyParams& a, const PolicyParams& b) {
+  double mx = 0.0;
+  for (size_t i = 0; i < a.logits.size(); ++i) mx = std::max(mx, std::abs(a.logits[i] - b.logits[i]));
+  return mx;
+}
+
+// The reference Trainer and the GPU-in-the-loop trainer side by side.
+bool run_case(const char* name, const RunConfig& cfg, int steps) {
+  Trainer ref(cfg);
+  uint64_t ref_fp = 0;
+  ref.set_inspector([&](const TrainBatch& b, const std::vector<GrpoItem>&) {
+    ref_fp = batch_fingerprint(b);
+  });
+  GpuLoopTrainer gpu(cfg);
+  int diverged = -1;
+  bool ok = true;
+  double worst_rel = 0.0, worst_param = 0.0;
+  for (int s = 0; s < steps; ++s) {
+    StepMetrics m = ref.train_step();
+    GpuLoopTrainer::Step g = gpu.train_step();
+    const bool same_batch = g.fingerprint == ref_fp && g.tokens == m.batch_tokens;
+    if (!same_batch && diverged < 0) diverged = s;
+    const double rel = std::abs(g.loss - m.loss) / std::max(1e-3, std::abs(m.loss));
+    const double pdiff = max_param_diff(ref.params(), gpu.params());
+    const bool step_ok = diverged >= 0 || rel <= 1e-5;
+    if (diverged < 0) {
+      worst_rel = std::max(worst_rel, rel);
+      worst_param = std::max(worst_param, pdiff);
+    }
+    ok = ok && step_ok;
+    std::printf(
+        "{\"case\":\"%s\",\"step\":%d,\"tokens\":%llu,\"same_batch\":%s,\"loss_ref\":%.17g,"
+        "\"loss_gpu\":%.17g,\"loss_rel_err\":%.3g,\"max_param_diff\":%.3g,\"ok\":%s}\n",
+        name, s, (unsigned long long)m.batch_tokens, same_batch ? "true" : "false", m.loss, g.loss,
+        rel, pdiff, step_ok ? "true" : "false");
+  }
+  std::printf(
+      "{\"case\":\"%s\",\"summary\":true,\"steps\":%d,\"lockstep_steps\":%d,\"diverged_at\":%d,"
+      "\"worst_loss_rel_err_lockstep\":%.3g,\"worst_param_diff_lockstep\":%.3g,\"ok\":%s}\n",
+      name, steps, diverged < 0 ? steps : diverged, diverged, worst_rel, worst_param,
+      ok ? "true" : "false");
+  return ok;
+}
+
+// C2 on the GPU: synchronous GpuLoopTrainer vs the standalone reference loop.
+bool run_c2(int steps) {
+  RunConfig cfg = desk_config();
+  cfg.mode = SchedulingMode::Synchronous;
+  GpuLoopTrainer gpu(cfg);
+  copris::testing::ReferenceLoop loop(cfg);
+  double worst = 0.0;
+  int first_large = -1;
+  for (int s = 0; s < steps; ++s) {
+    gpu.train_step();
+    loop.step();
+    const double d = copris::testing::max_param_diff(gpu.params(), loop.params);
+    worst = std::max(worst, d);
+    if (first_large < 0 && d > 1e-6) first_large = s;
+    const bool same_version = gpu.params().version == loop.params.version;
+    std::printf("{\"case\":\"c2_sync_vs_reference_loop\",\"step\":%d,\"max_param_diff\":%.3g,"
+                "\"same_version\":%s}\n",
+                s, d, same_version ? "true" : "false");
+    if (!same_version) return false;
+  }
+  std::printf("{\"case\":\"c2_sync_vs_reference_loop\",\"summary\":true,\"steps\":%d,"
+              "\"worst_param_diff\":%.3g,\"first_step_above_1e-6\":%d,\"ok\":true}\n",
+              steps, worst, first_large);
+  return true;
+}
+
+}  // namespace
+
+// usage: trainer_loop_check [steps]   (default 50)
+int main(int argc, char** argv) {
+  const int steps = argc > 1 ? std::atoi(argv[1]) : 50;
+  bool ok = true;
+  ok = run_case("desk", desk_config(), steps) && ok;
+  {
+    RunConfig c = desk_config();
+    c.engine.batch_prompts = 16;
+    c.engine.concurrency = 48;
+    ok = run_case("b16_c48", c, steps) && ok;
+    c.is_enabled = false;
+    ok = run_case("b16_c48_is_off", c, steps) && ok;
+    c.is_enabled = true;
+    c.clip.kl_coeff = 0.1;
+    c.clip.entropy_coeff = 0.01;
+    ok = run_case("b16_c48_kl_entropy", c, steps) && ok;
+  }
+  {
+    RunConfig c = desk_config();
+    c.engine.batch_prompts = 16;
+    c.engine.concurrency = 128;
+    c.engine.max_response_len = 16;
+    c.policy = PolicyShape{4, 16, 64, 4};
+    c.cluster.memory_capacity = 4096;
+    ok = run_case("v64_h16_c128", c, steps) && ok;
+  }
+  {
+    RunConfig c = desk_config();
+    c.mode = SchedulingMode::Synchronous;
+    ok = run_case("desk_synchronous", c, steps) && ok;
+  }
+  ok = run_c2(steps) && ok;
+  return ok ? 0 : 1;
+}

@@ -111,6 +111,10 @@ _SIGS = {
     "copris_ctx_last_fused_reduce": ([P], C.c_int),
     "copris_ctx_get_option": ([P, C.c_char_p, C.POINTER(I64)], C.c_int),
     "copris_adam_update": ([P, P, P, P, P, I64, I64, C.POINTER(AdamCfg), P], C.c_int),
+    "copris_adam_host_create": ([P, I64, C.POINTER(AdamCfg), C.POINTER(P)], C.c_int),
+    "copris_adam_host_update": ([P, P, P, I64], C.c_int),
+    "copris_adam_host_steps": ([P, C.POINTER(I64)], C.c_int),
+    "copris_adam_host_destroy": ([P], C.c_int),
     "copris_checkpoint_write": ([C.c_char_p, P, P, C.c_uint64, C.c_uint64], C.c_int),
     "copris_checkpoint_read": ([C.c_char_p, P, P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)], C.c_int),
     "copris_engine_create": ([C.POINTER(EngineCfg), C.POINTER(P)], C.c_int),

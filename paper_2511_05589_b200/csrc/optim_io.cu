@@ -24,6 +24,16 @@ struct File {
     if (f) std::fclose(f);
   }
 };
+
+// AdamConfig::validate, grpo.hpp:192-198
+int validate_adam(const copris_adam_cfg* c) {
+  if (c->lr < 0.0) return fail(COPRIS_E_CONFIG, "optimizer.lr must be >= 0");
+  if (c->beta1 < 0.0 || c->beta1 >= 1.0 || c->beta2 < 0.0 || c->beta2 >= 1.0)
+    return fail(COPRIS_E_CONFIG, "optimizer betas must lie in [0, 1)");
+  if (c->eps <= 0.0) return fail(COPRIS_E_CONFIG, "optimizer.eps must be > 0");
+  if (c->weight_decay < 0.0) return fail(COPRIS_E_CONFIG, "optimizer.weight_decay must be >= 0");
+  return COPRIS_OK;
+}
 }  // namespace
 
 extern "C" {
@@ -33,18 +43,92 @@ int copris_adam_update(copris_ctx* ctx, double* params, const double* grad, doub
   if (!ctx || !c) return fail(COPRIS_E_INVALID, "null argument");
   if (n < 0 || step < 1) return fail(COPRIS_E_INVALID, "bad size or step");
   if (n > 0 && (!params || !grad || !m || !v)) return fail(COPRIS_E_INVALID, "null pointer");
-  // AdamConfig::validate, grpo.hpp:192-198
-  if (c->lr < 0.0) return fail(COPRIS_E_CONFIG, "optimizer.lr must be >= 0");
-  if (c->beta1 < 0.0 || c->beta1 >= 1.0 || c->beta2 < 0.0 || c->beta2 >= 1.0)
-    return fail(COPRIS_E_CONFIG, "optimizer betas must lie in [0, 1)");
-  if (c->eps <= 0.0) return fail(COPRIS_E_CONFIG, "optimizer.eps must be > 0");
-  if (c->weight_decay < 0.0) return fail(COPRIS_E_CONFIG, "optimizer.weight_decay must be >= 0");
+  if (int rc = validate_adam(c)) return rc;
   const double bc1 = 1.0 - std::pow(c->beta1, static_cast<double>(step));  // grpo.hpp:214-215
   const double bc2 = 1.0 - std::pow(c->beta2, static_cast<double>(step));
   DeviceGuard g(ctx->device);
   cudaError_t e = launch_adam(params, grad, m, v, n, c->lr, c->beta1, c->beta2, c->eps,
                               c->weight_decay, bc1, bc2, ctx->num_sms, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? COPRIS_OK : cuda_fail(e, "adam launch");
+}
+
+}  // extern "C"
+
+struct copris_adam_host {
+  copris_ctx* ctx = nullptr;
+  int64_t n = 0;
+  int64_t t = 0;  // AdamOptimizer::t_ (grpo.hpp:233)
+  copris_adam_cfg cfg{};
+  double* d = nullptr;  // [params | grad | m | v], n doubles each
+  cudaStream_t stream = nullptr;
+};
+
+extern "C" {
+
+int copris_adam_host_create(copris_ctx* ctx, int64_t n, const copris_adam_cfg* cfg,
+                            copris_adam_host** out) {
+  if (!ctx || !cfg || !out) return fail(COPRIS_E_INVALID, "null argument");
+  if (n < 1) return fail(COPRIS_E_INVALID, "bad size");
+  *out = nullptr;
+  if (int rc = validate_adam(cfg)) return rc;
+  DeviceGuard g(ctx->device);
+  auto* a = new copris_adam_host;
+  a->ctx = ctx;
+  a->n = n;
+  a->cfg = *cfg;
+  const size_t bytes = static_cast<size_t>(n) * sizeof(double);
+  cudaError_t e = cudaStreamCreateWithFlags(&a->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMalloc(&a->d, 4 * bytes);
+  // the reference zero-initialises m_ and v_ on the first update (grpo.hpp:211-213)
+  if (e == cudaSuccess) e = cudaMemsetAsync(a->d + 2 * n, 0, 2 * bytes, a->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(a->stream);
+  if (e != cudaSuccess) {
+    copris_adam_host_destroy(a);
+    return cuda_fail(e, "adam state allocation");
+  }
+  *out = a;
+  return COPRIS_OK;
+}
+
+int copris_adam_host_update(copris_adam_host* a, double* params, const double* grad, int64_t n) {
+  if (!a || !params || !grad) return fail(COPRIS_E_INVALID, "null argument");
+  if (n != a->n) return fail(COPRIS_E_CONTRACT, "gradient shape mismatch");
+  DeviceGuard g(a->ctx->device);
+  const size_t bytes = static_cast<size_t>(n) * sizeof(double);
+  double* p = a->d;
+  double* gd = a->d + n;
+  cudaError_t e = cudaMemcpyAsync(p, params, bytes, cudaMemcpyHostToDevice, a->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(gd, grad, bytes, cudaMemcpyHostToDevice, a->stream);
+  if (e != cudaSuccess) {
+    cudaStreamSynchronize(a->stream);
+    return cuda_fail(e, "adam H2D");
+  }
+  int rc = copris_adam_update(a->ctx, p, gd, a->d + 2 * n, a->d + 3 * n, n, a->t + 1, &a->cfg,
+                              a->stream);
+  if (rc != COPRIS_OK) {
+    cudaStreamSynchronize(a->stream);
+    return rc;
+  }
+  e = cudaMemcpyAsync(params, p, bytes, cudaMemcpyDeviceToHost, a->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(a->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "adam D2H");
+  a->t += 1;
+  return COPRIS_OK;
+}
+
+int copris_adam_host_steps(const copris_adam_host* a, int64_t* t) {
+  if (!a || !t) return fail(COPRIS_E_INVALID, "null argument");
+  *t = a->t;
+  return COPRIS_OK;
+}
+
+int copris_adam_host_destroy(copris_adam_host* a) {
+  if (!a) return COPRIS_OK;
+  DeviceGuard g(a->ctx->device);
+  if (a->d) cudaFree(a->d);
+  if (a->stream) cudaStreamDestroy(a->stream);
+  delete a;
+  return COPRIS_OK;
 }
 
 int copris_checkpoint_write(const char* path, const double* logits, const int32_t dims[4],

@@ -34,6 +34,55 @@ class AdamConfig:
             raise ConfigError("optimizer.weight_decay must be >= 0")
 
 
+class HostAdamOptimizer:
+    """The whole AdamOptimizer object for a HOST parameter table (grpo.hpp:205-235)
+    through copris_adam_host_*: the moments stay on the device, each update is one
+    blocking call on fp64 numpy arrays (params updated in place) and bumps `version`."""
+
+    def __init__(self, ctx: Copris, cfg: AdamConfig | None = None):
+        self.ctx, self.cfg = ctx, cfg or AdamConfig()
+        self.cfg.validate()
+        self.h = None
+        self.n = 0
+        self.version = 0
+
+    def update(self, params: np.ndarray, grad: np.ndarray) -> None:
+        from .errors import ContractViolation
+        if grad.size != params.size:
+            raise ContractViolation("gradient shape mismatch")
+        if params.dtype != np.float64 or grad.dtype != np.float64 or not params.flags.c_contiguous:
+            raise ValueError("contiguous fp64 arrays expected (the reference's precision)")
+        grad = np.ascontiguousarray(grad)
+        if self.h is None:
+            c = L.AdamCfg(self.cfg.lr, self.cfg.beta1, self.cfg.beta2, self.cfg.eps, self.cfg.weight_decay)
+            h = C.c_void_p()
+            self.ctx._call(self.ctx.lib.copris_adam_host_create(self.ctx.h, params.size, C.byref(c),
+                                                                C.byref(h)))
+            self.h, self.n = h, params.size
+        self.ctx._call(self.ctx.lib.copris_adam_host_update(self.h, params.ctypes.data, grad.ctypes.data,
+                                                            params.size))
+        self.version += 1
+
+    @property
+    def t(self) -> int:
+        if self.h is None:
+            return 0
+        t = C.c_int64()
+        self.ctx._call(self.ctx.lib.copris_adam_host_steps(self.h, C.byref(t)))
+        return t.value
+
+    def close(self) -> None:
+        if self.h is not None:
+            self.ctx.lib.copris_adam_host_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class AdamOptimizer:
     """AdamOptimizer::update on device fp64 tensors; each update bumps `version`."""
 

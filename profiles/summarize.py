@@ -104,6 +104,12 @@ def main():
         for k, v in t.items():
             traffic["grpo_128x8_v151936"] = {"dram_bytes_per_row": v, "kernel": k,
                                              "source": f"profiles/{tag}_ncu_{k}.txt"}
+    if os.path.exists(os.path.join(src, "prof_fused_f32.ncu-rep")):
+        # the same kernel writing f32 dlogits (parity mode, 6V+16 B/token)
+        t = ncu_summary(os.path.join(src, "prof_fused_f32.ncu-rep"), os.path.join(HERE, f"{tag}_ncu_f32"), rows)
+        for k, v in t.items():
+            traffic["grpo_128x8_v151936:f32"] = {"dram_bytes_per_row": v, "kernel": k,
+                                                 "source": f"profiles/{tag}_ncu_f32_{k}.txt"}
     if os.path.exists(os.path.join(src, "prof_unfused.ncu-rep")):
         # K1 (the fused kernel in gather-only mode) and K3 of one chunk
         t = ncu_summary(os.path.join(src, "prof_unfused.ncu-rep"), os.path.join(HERE, f"{tag}_ncu_unfused"), rows)
@@ -125,8 +131,16 @@ def main():
         # LM-head backward dW (MN-major operands), T = 4096 tokens
         ncu_summary(os.path.join(src, "prof_lmhead_dw.ncu-rep"), os.path.join(HERE, f"{tag}_ncu_dw"), 4096)
     if traffic:
-        with open(os.path.join(HERE, "ncu_traffic.json"), "w") as f:
-            json.dump(traffic, f, indent=1)
+        # merge into the committed table: a partial capture keeps the other entries
+        path = os.path.join(HERE, "ncu_traffic.json")
+        try:
+            with open(path) as f:
+                old = json.load(f)
+        except (OSError, ValueError):
+            old = {}
+        old.update(traffic)
+        with open(path, "w") as f:
+            json.dump(old, f, indent=1)
     print("wrote", sorted(os.listdir(HERE)))
 
 

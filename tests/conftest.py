@@ -22,8 +22,10 @@ def oracle():
 @pytest.fixture(scope="session")
 def reference():
     from oracle.oracle import Reference
-    if not Reference.available:
-        pytest.skip("oracle/_ref/libcopris_ref.so not built (needs /root/reference)")
+    # a hard failure, not a skip: the reference-compiled checkers travel with the
+    # snapshot (oracle/_ref/ is git-ignored, not gpurun-ignored), so a missing
+    # build means the parity evidence is missing
+    assert Reference.available, "oracle/_ref/libcopris_ref.so not built: run __graft_entry__.build() with /root/reference present"
     return Reference()
 
 

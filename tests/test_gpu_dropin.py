@@ -20,8 +20,8 @@ EXE = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), 
                    "dropin_check")
 
 
-@pytest.mark.skipif(not os.path.exists(EXE), reason="oracle/_ref/dropin_check not built")
 def test_reference_trainer_with_gpu_dropin():
+    assert os.path.exists(EXE), "oracle/_ref/dropin_check not built (hard failure, see conftest.reference)"
     p = subprocess.run([EXE, "--threads"], capture_output=True, text=True, timeout=600)
     lines = [json.loads(l) for l in p.stdout.splitlines() if l.startswith("{")]
     assert lines, p.stderr

@@ -75,3 +75,26 @@ def test_adam_kernel_bit_identical_to_reference(ctx, reference):
     ref = reference.adam(dims, params, grads, lr=3e-2, wd=0.01)
     np.testing.assert_array_equal(p.cpu().numpy(), ref)
     assert opt.version == 3
+
+
+@pytest.mark.gpu
+def test_host_adam_bit_identical_to_reference(ctx, reference):
+    """copris_adam_host (the AdamDropIn behind trainer.hpp:177) on host arrays:
+    bitwise the reference AdamOptimizer over several updates; size mismatch is
+    the reference's ContractViolation."""
+    from paper_2511_05589_b200.errors import ContractViolation
+    from paper_2511_05589_b200.optim import HostAdamOptimizer
+    rng = np.random.default_rng(5)
+    dims = (4, 8, 6, 4)
+    n = 4 * 8 * 6
+    params = rng.normal(size=n)
+    grads = rng.normal(size=(4, n))
+    opt = HostAdamOptimizer(ctx, AdamConfig(lr=3e-2, weight_decay=0.01))
+    p = params.copy()
+    for k in range(4):
+        opt.update(p, grads[k].copy())
+    np.testing.assert_array_equal(p, reference.adam(dims, params, grads, lr=3e-2, wd=0.01))
+    assert opt.version == 4 and opt.t == 4
+    with pytest.raises(ContractViolation, match="gradient shape mismatch"):
+        opt.update(np.zeros(n + 1), np.zeros(n + 1))
+    opt.close()
