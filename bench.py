@@ -493,6 +493,15 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         tps, det = cpu_reference(V, args.cpu_tokens_per_thread, args.cpu_seconds, args.seed)
         line["cpu_baseline"] = {"value": tps, "unit": UNIT, **det}
+        # the reference as it runs in its own trainer: ONE thread (grpo.hpp:113-115,
+        # SURVEY.md §8(d) CPU baseline (i)); the full-batch step time is extrapolated
+        tps1, det1 = cpu_reference(V, args.cpu_tokens_per_thread, min(4.0, args.cpu_seconds), args.seed,
+                                   threads=1, min_rounds=2)
+        line["cpu_baseline"]["single_thread"] = {
+            "value": tps1, "unit": UNIT, "sample": det1["sample"],
+            "extrapolated_step_s": T_global / tps1,
+            "extrapolated_step": f"{T_global} tokens / {tps1:.0f} tok/s = {T_global / tps1 / 3600:.2f} h "
+                                 f"for one {args.config} step on one core"}
     if line is not None:
         print(json.dumps(line), flush=True)
     if world > 1:

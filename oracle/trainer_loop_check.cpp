@@ -8,23 +8,32 @@
 // numeric steps are the drop-ins a maintainer would install:
 //   trainer.hpp:176  grpo_step_loss(params_, items, clip)  -> copris_b200::DropIn
 //   trainer.hpp:177  adam_.update(params_, res.grad)       -> copris_b200::AdamDropIn
-// so the GPU's gradient and update drive the next rollout. It runs beside the
-// UNMODIFIED reference Trainer on the same config and reports, per step, the
-// loss of both runs, whether the batch they formed is the same (ids, tokens,
-// stored log-probs), and the max parameter difference. Until the scheduler
-// first forms a different batch the losses must agree within 1e-5 (relative);
-// the step at which the runs diverge is reported (the two runs are chaotic
-// dynamical systems over token sampling: a gradient that differs in the 7th
-// digit moves a sampled token once a uniform draw lands that close to a CDF
-// boundary).
+// so the GPU's gradient and update drive the next rollout. Three runs side by
+// side on the same config, per case:
+//   ref  the UNMODIFIED reference Trainer;
+//   A    GpuLoopTrainer with the reference loss and the GPU Adam: must be
+//        BITWISE the reference run on every step (loss, parameters, version) —
+//        the Adam kernel is bit-identical, so the whole training trajectory is;
+//   B    GpuLoopTrainer with the GPU loss and the GPU Adam: reported. Its first
+//        step's loss must agree within 1e-5; afterwards the runs separate in
+//        parameter space, because Adam's first update is lr * g / (|g| + eps)
+//        and the table has gradient entries of ~1e-9 (near-cancelling
+//        contributions of a group's members, whose advantages sum to 0) on
+//        which an fp32-level gradient error (~1e-10) is a 10% error — the
+//        update of those entries differs by up to ~0.1 lr. The step at which
+//        the scheduler first forms a different batch is reported.
+// At every reference step the GPU loss is also evaluated on the reference's
+// own items and parameters ("teacher-forced", the dropin_check seam): within
+// 1e-5 on every step, with the gradient error and the count of table entries in
+// Adam's eps regime (|g| below 1000x the gradient error) reported.
 //
 // Also the GPU form of acceptance criterion C2 (acceptance_main.cpp:105-121,
-// test_trainer.cpp:25-36): the synchronous GpuLoopTrainer against the
-// reference's standalone on-policy loop (tests/support/reference_loop.hpp),
-// reporting the max per-step parameter difference.
+// test_trainer.cpp:25-36): the synchronous run A against the reference's
+// standalone on-policy loop (tests/support/reference_loop.hpp), < 1e-12 per
+// step as the reference requires, and run B's parameter difference reported.
 //
 // Output: one JSON line per step and one summary line per case; exit status 1
-// if any pre-divergence step disagrees.
+// if any asserted property fails.
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -88,8 +97,9 @@ uint64_t batch_fingerprint(const TrainBatch& batch) {
 // Trainer (trainer.hpp:100-229) with the loss and the update on the GPU.
 class GpuLoopTrainer {
  public:
-  explicit GpuLoopTrainer(RunConfig cfg)
-      : cfg_(std::move(cfg)),
+  GpuLoopTrainer(RunConfig cfg, bool gpu_loss)
+      : gpu_loss_(gpu_loss),
+        cfg_(std::move(cfg)),
         init_rng_(cfg_.seed, "init"),
         params_(make_params()),
         engine_(cfg_.engine, cfg_.mode, cfg_.policy, RngStream(cfg_.seed, "prompt")),
@@ -134,8 +144,10 @@ class GpuLoopTrainer {
       }
     }
     Step out{0.0, batch_fingerprint(batch), batch.total_tokens()};
-    GrpoStepResult res = gpu_.grpo_step_loss<GrpoStepResult, ContractViolation, ConfigError>(
-        params_, std::span<const GrpoItem>(items), cfg_.clip);
+    GrpoStepResult res =
+        gpu_loss_ ? gpu_.grpo_step_loss<GrpoStepResult, ContractViolation, ConfigError>(
+                        params_, std::span<const GrpoItem>(items), cfg_.clip)
+                  : grpo_step_loss(params_, items, cfg_.clip);
     out.loss = res.loss;
     gpu_adam_.update<ContractViolation, ConfigError>(params_, std::span<const double>(res.grad));
     return out;
@@ -149,6 +161,7 @@ class GpuLoopTrainer {
     return PolicyParams::init_near_uniform(cfg_.policy, init_rng_);
   }
 
+  bool gpu_loss_;
   RunConfig cfg_;
   RngStream init_rng_;
   PolicyParams params_;
@@ -167,68 +180,101 @@ double max_param_diff(const PolicyParams& a, const PolicyParams& b) {
   return mx;
 }
 
-// The reference Trainer and the GPU-in-the-loop trainer side by side.
+// The reference Trainer and the two GPU-in-the-loop trainers side by side.
 bool run_case(const char* name, const RunConfig& cfg, int steps) {
   Trainer ref(cfg);
+  copris_b200::DropIn probe(0);
   uint64_t ref_fp = 0;
-  ref.set_inspector([&](const TrainBatch& b, const std::vector<GrpoItem>&) {
+  double tf_rel = 0.0, tf_gerr = 0.0, tf_gmax = 0.0;
+  long long tf_eps_regime = 0;
+  ref.set_inspector([&](const TrainBatch& b, const std::vector<GrpoItem>& items) {
     ref_fp = batch_fingerprint(b);
+    // teacher-forced: the GPU loss on the reference's own items and parameters
+    GrpoStepResult r = grpo_step_loss(ref.params(), items, cfg.clip);
+    GrpoStepResult g = probe.grpo_step_loss<GrpoStepResult, ContractViolation, ConfigError>(
+        ref.params(), std::span<const GrpoItem>(items), cfg.clip);
+    tf_rel = std::abs(g.loss - r.loss) / std::max(1e-3, std::abs(r.loss));
+    tf_gerr = tf_gmax = 0.0;
+    for (size_t i = 0; i < r.grad.size(); ++i) {
+      tf_gmax = std::max(tf_gmax, std::abs(r.grad[i]));
+      tf_gerr = std::max(tf_gerr, std::abs(r.grad[i] - g.grad[i]));
+    }
+    tf_eps_regime = 0;
+    for (size_t i = 0; i < r.grad.size(); ++i)
+      tf_eps_regime += r.grad[i] != 0.0 && std::abs(r.grad[i]) < 1000.0 * tf_gerr;
   });
-  GpuLoopTrainer gpu(cfg);
+  GpuLoopTrainer a(cfg, false), b(cfg, true);
   int diverged = -1;
-  bool ok = true;
-  double worst_rel = 0.0, worst_param = 0.0;
+  bool ok = true, a_bitwise = true;
+  double worst_tf = 0.0, b_worst_rel = 0.0, b_worst_param = 0.0, b_step0_rel = 0.0;
   for (int s = 0; s < steps; ++s) {
     StepMetrics m = ref.train_step();
-    GpuLoopTrainer::Step g = gpu.train_step();
-    const bool same_batch = g.fingerprint == ref_fp && g.tokens == m.batch_tokens;
-    if (!same_batch && diverged < 0) diverged = s;
-    const double rel = std::abs(g.loss - m.loss) / std::max(1e-3, std::abs(m.loss));
-    const double pdiff = max_param_diff(ref.params(), gpu.params());
-    const bool step_ok = diverged >= 0 || rel <= 1e-5;
+    const uint64_t fp = ref_fp;
+    GpuLoopTrainer::Step ga = a.train_step();
+    GpuLoopTrainer::Step gb = b.train_step();
+    const bool a_same = std::memcmp(&ga.loss, &m.loss, sizeof(double)) == 0 && ga.fingerprint == fp &&
+                        max_param_diff(ref.params(), a.params()) == 0.0 &&
+                        a.params().version == ref.params().version;
+    a_bitwise = a_bitwise && a_same;
+    const bool b_same = gb.fingerprint == fp && gb.tokens == m.batch_tokens;
+    if (!b_same && diverged < 0) diverged = s;
+    const double rel = std::abs(gb.loss - m.loss) / std::max(1e-3, std::abs(m.loss));
+    const double pdiff = max_param_diff(ref.params(), b.params());
+    if (s == 0) b_step0_rel = rel;
     if (diverged < 0) {
-      worst_rel = std::max(worst_rel, rel);
-      worst_param = std::max(worst_param, pdiff);
+      b_worst_rel = std::max(b_worst_rel, rel);
+      b_worst_param = std::max(b_worst_param, pdiff);
     }
+    worst_tf = std::max(worst_tf, tf_rel);
+    const bool step_ok = a_same && tf_rel <= 1e-5 && tf_gerr <= 1e-5 * tf_gmax && (s > 0 || rel <= 1e-5);
     ok = ok && step_ok;
     std::printf(
-        "{\"case\":\"%s\",\"step\":%d,\"tokens\":%llu,\"same_batch\":%s,\"loss_ref\":%.17g,"
-        "\"loss_gpu\":%.17g,\"loss_rel_err\":%.3g,\"max_param_diff\":%.3g,\"ok\":%s}\n",
-        name, s, (unsigned long long)m.batch_tokens, same_batch ? "true" : "false", m.loss, g.loss,
-        rel, pdiff, step_ok ? "true" : "false");
+        "{\"case\":\"%s\",\"step\":%d,\"tokens\":%llu,\"loss_ref\":%.17g,"
+        "\"a_bitwise\":%s,\"teacher_forced_loss_rel_err\":%.3g,\"teacher_forced_grad_err\":%.3g,"
+        "\"grad_max\":%.3g,\"grad_entries_in_adam_eps_regime\":%lld,"
+        "\"b_same_batch\":%s,\"b_loss\":%.17g,\"b_loss_rel_err\":%.3g,\"b_max_param_diff\":%.3g,"
+        "\"ok\":%s}\n",
+        name, s, (unsigned long long)m.batch_tokens, m.loss, a_same ? "true" : "false", tf_rel, tf_gerr,
+        tf_gmax, tf_eps_regime, b_same ? "true" : "false", gb.loss, rel, pdiff, step_ok ? "true" : "false");
   }
   std::printf(
-      "{\"case\":\"%s\",\"summary\":true,\"steps\":%d,\"lockstep_steps\":%d,\"diverged_at\":%d,"
-      "\"worst_loss_rel_err_lockstep\":%.3g,\"worst_param_diff_lockstep\":%.3g,\"ok\":%s}\n",
-      name, steps, diverged < 0 ? steps : diverged, diverged, worst_rel, worst_param,
-      ok ? "true" : "false");
+      "{\"case\":\"%s\",\"summary\":true,\"steps\":%d,\"a_gpu_adam_bitwise_all_steps\":%s,"
+      "\"worst_teacher_forced_loss_rel_err\":%.3g,\"b_step0_loss_rel_err\":%.3g,"
+      "\"b_lockstep_steps\":%d,\"b_diverged_at\":%d,\"b_worst_loss_rel_err_lockstep\":%.3g,"
+      "\"b_worst_param_diff_lockstep\":%.3g,\"ok\":%s}\n",
+      name, steps, a_bitwise ? "true" : "false", worst_tf, b_step0_rel, diverged < 0 ? steps : diverged,
+      diverged, b_worst_rel, b_worst_param, ok ? "true" : "false");
   return ok;
 }
 
-// C2 on the GPU: synchronous GpuLoopTrainer vs the standalone reference loop.
+// C2 on the GPU: the synchronous GPU-in-the-loop trainers vs the standalone
+// reference loop.
 bool run_c2(int steps) {
   RunConfig cfg = desk_config();
   cfg.mode = SchedulingMode::Synchronous;
-  GpuLoopTrainer gpu(cfg);
+  GpuLoopTrainer a(cfg, false), b(cfg, true);
   copris::testing::ReferenceLoop loop(cfg);
-  double worst = 0.0;
-  int first_large = -1;
+  double worst_a = 0.0, worst_b = 0.0;
+  bool ok = true;
   for (int s = 0; s < steps; ++s) {
-    gpu.train_step();
+    a.train_step();
+    b.train_step();
     loop.step();
-    const double d = copris::testing::max_param_diff(gpu.params(), loop.params);
-    worst = std::max(worst, d);
-    if (first_large < 0 && d > 1e-6) first_large = s;
-    const bool same_version = gpu.params().version == loop.params.version;
-    std::printf("{\"case\":\"c2_sync_vs_reference_loop\",\"step\":%d,\"max_param_diff\":%.3g,"
-                "\"same_version\":%s}\n",
-                s, d, same_version ? "true" : "false");
-    if (!same_version) return false;
+    const double da = copris::testing::max_param_diff(a.params(), loop.params);
+    const double db = copris::testing::max_param_diff(b.params(), loop.params);
+    worst_a = std::max(worst_a, da);
+    worst_b = std::max(worst_b, db);
+    const bool step_ok = da < 1e-12 && a.params().version == loop.params.version &&
+                         b.params().version == loop.params.version;
+    ok = ok && step_ok;
+    std::printf("{\"case\":\"c2_sync_vs_reference_loop\",\"step\":%d,\"a_max_param_diff\":%.3g,"
+                "\"b_max_param_diff\":%.3g,\"ok\":%s}\n",
+                s, da, db, step_ok ? "true" : "false");
   }
   std::printf("{\"case\":\"c2_sync_vs_reference_loop\",\"summary\":true,\"steps\":%d,"
-              "\"worst_param_diff\":%.3g,\"first_step_above_1e-6\":%d,\"ok\":true}\n",
-              steps, worst, first_large);
-  return true;
+              "\"a_worst_param_diff\":%.3g,\"b_worst_param_diff\":%.3g,\"ok\":%s}\n",
+              steps, worst_a, worst_b, ok ? "true" : "false");
+  return ok;
 }
 
 }  // namespace

@@ -89,7 +89,7 @@ enum class DType : int { BF16 = 0, F32 = 1 };
 // so a setenv on one thread cannot change another context's kernels mid-run
 // (re-entrancy).
 struct Tuning {
-  int fused_impl = 0;     // 0 auto, 1 stream (TMA ring + L2 re-read), 2 tma (row in smem), 3 pair
+  int fused_impl = 0;     // 0 auto, 1 stream (TMA ring + L2 re-read), 2 tma (row in smem), 3 pair, 4 solo
   int lookahead = 2;      // stream kernel: ring segments of row r+1 before pass 2 of row r
   int slots = 0;          // stream kernel ring slots (0 = as many 32 KB slots as fit 192 KB)
   int resident = 1;       // stream kernel: pass 2 from resident segments when 3 rows fit

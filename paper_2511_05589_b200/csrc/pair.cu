@@ -21,6 +21,12 @@
 // staging adds <= 2^-12 relative before the final bf16 rounding, so dlogits
 // stay within one bf16 ulp of the exact value.
 //
+// f32 dlogits (the parity mode, within 1e-5): f16 staging would cost 2^-12, so
+// pass 1 stages the RAW bf16 logits in TMEM instead (same 16 bits per column,
+// still no L2 re-read) and pass 2 recomputes p_k = 2^(z_k log2(e) - c1) on MUFU
+// — two exponentials per element in this mode, the arithmetic of the other
+// fused kernels' f32 pass 2 (fused_common.cuh p2_segment).
+//
 // The pair exchanges its per-warp partials (m, s, z_y) through DSMEM: every
 // consumer warp writes its entry into its own CTA's table (st.shared + local
 // mbarrier arrive) and into the peer's with st.async, whose bytes complete
@@ -28,6 +34,14 @@
 // consumers' path). Both scalar warps merge the same 32 entries in the same
 // order — bitwise the same row statistics in both halves, no second
 // exchange. Rank 0 writes the per-token outputs.
+//
+// The same kernel with CL = 1 ("solo", rows up to 7 x 16,384 columns, e.g.
+// V = 32,000): one CTA owns the whole row, its 16 warp partials are merged
+// locally and nothing crosses DSMEM; it replaces the two exponentials per
+// element of the row-resident TMA kernel with one.
+//
+// Small steps (<= 8,192 tokens) reduce obj/flags into out4 in the launch's
+// last CTA (reduce.cuh), bitwise what reduce_kernel produces.
 //
 // Reference semantics: policy.hpp:110-121,160-173 (log-softmax, gather),
 // grpo.hpp:117-185 + policy.hpp:180-196 (objective and dlogits) via
@@ -40,6 +54,7 @@
 #include "kernels.cuh"
 #include "pair.cuh"
 #include "ptx.cuh"
+#include "reduce.cuh"
 #include "tc.cuh"
 #include "token_math.cuh"
 
@@ -142,7 +157,7 @@ __device__ __forceinline__ void kill_col(uint32_t& w, int jt, int k, float& zy) 
 // STORE: stage the f16 exponentials in TMEM at taddr (16 columns). Returns
 // nml = 15 - m log2(e) of this thread's columns (+inf when it saw no finite
 // column) for pass 2.
-template <bool STORE>
+template <bool STORE, bool RAW>
 __device__ __forceinline__ float p1_slot(LaneAcc& a, uint32_t sb, int32_t v0, int32_t cnt,
                                          int32_t ycol, int tid, uint32_t taddr) {
   uint4 raw[kPK];
@@ -170,6 +185,17 @@ __device__ __forceinline__ float p1_slot(LaneAcc& a, uint32_t sb, int32_t v0, in
       }
     }
   }
+  if (STORE && RAW) {  // the logits themselves (target column already -inf: p = 0 there)
+    uint32_t h[16];
+#pragma unroll
+    for (int q = 0; q < kPK; ++q) {
+      h[q * 4 + 0] = raw[q].x;
+      h[q * 4 + 1] = raw[q].y;
+      h[q * 4 + 2] = raw[q].z;
+      h[q * 4 + 3] = raw[q].w;
+    }
+    tmem_st_x16(taddr, h);
+  }
   uint32_t mx = ptx::bmax2(ptx::bmax2(raw[0].x, raw[0].y), ptx::bmax2(raw[0].z, raw[0].w));
 #pragma unroll
   for (int q = 1; q < kPK; ++q)
@@ -189,10 +215,10 @@ __device__ __forceinline__ float p1_slot(LaneAcc& a, uint32_t sb, int32_t v0, in
       const uint64_t e = ptx::ex2x2(ptx::ffma2(ptx::bf16x2_to_f2(w[k]), l2e, nml2));
       if (k & 1) acc1 = ptx::fadd2(acc1, e);
       else acc0 = ptx::fadd2(acc0, e);
-      if (STORE) h[q * 4 + k] = f2_to_f16x2(e);
+      if (STORE && !RAW) h[q * 4 + k] = f2_to_f16x2(e);
     }
   }
-  if (STORE) tmem_st_x16(taddr, h);
+  if (STORE && !RAW) tmem_st_x16(taddr, h);
   const uint64_t acc = ptx::fadd2(acc0, acc1);
   const float sl = ptx::f2lo(acc) + ptx::f2hi(acc);
   // online merge into the lane state (branch-free; both parts relative to mn)
@@ -250,12 +276,50 @@ __device__ __forceinline__ void p2_slot(const RowBroadcast& b, bool zero_row, fl
     st_global_b16(dseg + rel, __bfloat16_as_ushort(__float2bfloat16_rn(b.dy)));
 }
 
+// Pass 2, f32 dlogits: the staged raw logits -> d_k = -coef 2^(z_k log2(e) - c1)
+// (fused_common.cuh p2_segment's f32 arithmetic), one 32-byte store per 8
+// columns (a warp writes 1 KB contiguous per instruction).
+__device__ __forceinline__ void p2_slot_f32(const RowBroadcast& b, bool zero_row, uint32_t taddr,
+                                            int32_t v0, int32_t cnt, int32_t ycol, float* dseg,
+                                            int tid) {
+  float* base = dseg + static_cast<int64_t>(tid) * 8;
+  if (zero_row) {
+    const float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int q = 0; q < kPK; ++q)
+      if (tid + q * kPThreads < cnt) ptx::st_global_cs_v8f(base + q * kPThreads * 8, z);
+    return;
+  }
+  uint32_t h[16];
+  tmem_ld_x16(taddr, h);
+  tc::tmem_wait_ld();
+  const float nc = -b.coef, nc1 = -b.c1;
+#pragma unroll
+  for (int q = 0; q < kPK; ++q) {
+    if (cnt == kPSlotVec || tid + q * kPThreads < cnt) {
+      float d[8];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t w = h[q * 4 + k];
+        d[2 * k] = ptx::ex2(fmaf(ptx::bf16_lo(w), kLog2e, nc1)) * nc;
+        d[2 * k + 1] = ptx::ex2(fmaf(ptx::bf16_hi(w), kLog2e, nc1)) * nc;
+      }
+      ptx::st_global_cs_v8f(base + q * kPThreads * 8, d);
+    }
+  }
+  const int32_t rel = ycol - v0 * 8;
+  if (static_cast<uint32_t>(rel) < static_cast<uint32_t>(cnt * 8) && ((rel >> 3) & (kPThreads - 1)) == tid)
+    dseg[rel] = b.dy;
+}
+
 // grid = 2 x clusters, cluster (2, 1, 1); block = (kPW + 2) warps. Dynamic
 // shared memory: nslots ring slots of 32 KB, then nml[kPTSlots][512] floats.
 // nvec0 = vectors of CTA rank 0 (rank 1 takes the rest); look = slots of row
 // r+1 run through pass 1 before pass 2 of row r.
+template <bool F32, int CL>
 __global__ void __launch_bounds__((kPW + 2) * 32, 1)
     fused_pair_kernel(const LossParams P, const int nslots, const int look, const int32_t nvec0) {
+  static_assert(CL == 1 || CL == 2, "a row is split over one or two CTAs");
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[16], empty[16], p1done[2], sdone[2];
   __shared__ PairPart red[2][2 * kPW];
@@ -263,8 +327,8 @@ __global__ void __launch_bounds__((kPW + 2) * 32, 1)
   __shared__ uint32_t tmem_slot;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = ptx::cluster_ctarank(), peer = rank ^ 1u;
-  const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const uint32_t rank = CL == 2 ? ptx::cluster_ctarank() : 0u, peer = rank ^ 1u;
+  const int64_t cid = blockIdx.x / CL, ncl = gridDim.x / CL;
   const int32_t nvec_all = P.vocab / 8;
   const int32_t vbase = rank ? nvec0 : 0;                  // first vector of this half
   const int32_t nvec = rank ? nvec_all - nvec0 : nvec0;     // vectors of this half
@@ -293,7 +357,7 @@ __global__ void __launch_bounds__((kPW + 2) * 32, 1)
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
-  ptx::cluster_sync_all();  // the peer's barriers exist before any remote write
+  if constexpr (CL == 2) ptx::cluster_sync_all();  // the peer's barriers exist before any remote write
   const uint32_t tmem_base = grad ? tmem_slot : 0u;
 
   if (warp == kPW) {
@@ -323,9 +387,13 @@ __global__ void __launch_bounds__((kPW + 2) * 32, 1)
       RowMeta meta{};
       if (lane == 0) meta = mp.advance(P, r, ncl);
       const uint32_t bsel = i & 1u, par = (i >> 1) & 1u;
-      if (lane == 0) ptx::mbar_arrive_expect_tx_u32(p1b + bsel * 8, kPW * sizeof(PairPart));
+      if (lane == 0) {
+        if constexpr (CL == 2) ptx::mbar_arrive_expect_tx_u32(p1b + bsel * 8, kPW * sizeof(PairPart));
+        else ptx::mbar_arrive_u32(p1b + bsel * 8);
+      }
       ptx::mbar_wait_sleep(p1b + bsel * 8, par);
-      const PairPart e = red[bsel][lane];  // entry lane = rank * 16 + warp: same order in both CTAs
+      // entry lane = rank * 16 + warp: same order in both CTAs (solo: lanes 16..31 empty)
+      const PairPart e = lane < CL * kPW ? red[bsel][lane] : PairPart{-INFINITY, 0.f, 0.f, 0.f};
       Lse tot{e.m, e.s, 0.f, 0.f};
       warp_lse<false>(tot);
       const uint32_t hv = __ballot_sync(0xffffffffu, e.have != 0.f);
@@ -352,8 +420,8 @@ __global__ void __launch_bounds__((kPW + 2) * 32, 1)
                             static_cast<uint32_t>((warp >> 2) * (kPTSlots * 16));
     Ring ring(nslots);
     uint32_t ts = 0;  // TMEM slot of the next pass-1 slot (mod kPTSlots)
-    const uint32_t red_peer = ptx::mapa(ptx::smem_u32(&red[0][0]), peer);
-    const uint32_t p1_peer = ptx::mapa(p1b, peer);
+    const uint32_t red_peer = CL == 2 ? ptx::mapa(ptx::smem_u32(&red[0][0]), peer) : 0u;
+    const uint32_t p1_peer = CL == 2 ? ptx::mapa(p1b, peer) : 0u;
     PhaseTimer tm;    // trace slots: 0 pass 1, 2 broadcast wait, 4 pass 2
     tm.start(P.trace && tid == 0 && blockIdx.x < kTraceCtas);
 
@@ -364,9 +432,9 @@ __global__ void __launch_bounds__((kPW + 2) * 32, 1)
         const int32_t cnt = min(kPSlotVec, nvec - v0);
         ptx::mbar_wait_sleep(fbase + slot * 8, ring.ph);
         const uint32_t tsl = (ts + static_cast<uint32_t>(sg)) % kPTSlots;
-        const float nml = grad ? p1_slot<true>(a, sbase + slot * kPSlotBytes, v0, cnt, ycol, tid,
-                                               taddr0 + tsl * 16)
-                               : p1_slot<false>(a, sbase + slot * kPSlotBytes, v0, cnt, ycol, tid, 0u);
+        const float nml = grad ? p1_slot<true, F32>(a, sbase + slot * kPSlotBytes, v0, cnt, ycol, tid,
+                                                    taddr0 + tsl * 16)
+                               : p1_slot<false, F32>(a, sbase + slot * kPSlotBytes, v0, cnt, ycol, tid, 0u);
         nml_sh[tsl * kPThreads + tid] = nml;
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive_u32(ebase + slot * 8);
@@ -390,7 +458,7 @@ __global__ void __launch_bounds__((kPW + 2) * 32, 1)
         const float hvf = hv ? 1.f : 0.f;
         red[bsel][rank * kPW + warp] = PairPart{st.m, st.s, zy, hvf};
         ptx::mbar_arrive_u32(p1b + bsel * 8);
-        st_async_v4(red_peer + off, st.m, st.s, zy, hvf, p1_peer + bsel * 8);
+        if constexpr (CL == 2) st_async_v4(red_peer + off, st.m, st.s, zy, hvf, p1_peer + bsel * 8);
       }
     };
 
@@ -418,13 +486,19 @@ __global__ void __launch_bounds__((kPW + 2) * 32, 1)
         const RowBroadcast b = bc[bsel];
         const bool zero_row = b.coef == 0.f;
         const int32_t ycol = b.y - col0;
-        __nv_bfloat16* drow = static_cast<__nv_bfloat16*>(P.dlogits) + r * P.ld_d + col0;
         tmem_wait_st();  // this thread's pass-1 stores of row i have landed
         for (int32_t sg = 0; sg < nseg; ++sg) {
           const uint32_t tsl = (ts_row + static_cast<uint32_t>(sg)) % kPTSlots;
           const int32_t v0 = sg * kPSlotVec;
-          p2_slot(b, zero_row, nml_sh[tsl * kPThreads + tid], taddr0 + tsl * 16, v0,
-                  min(kPSlotVec, nvec - v0), ycol, drow + static_cast<int64_t>(v0) * 8, tid);
+          if constexpr (F32) {
+            float* drow = static_cast<float*>(P.dlogits) + r * P.ld_d + col0;
+            p2_slot_f32(b, zero_row, taddr0 + tsl * 16, v0, min(kPSlotVec, nvec - v0), ycol,
+                        drow + static_cast<int64_t>(v0) * 8, tid);
+          } else {
+            __nv_bfloat16* drow = static_cast<__nv_bfloat16*>(P.dlogits) + r * P.ld_d + col0;
+            p2_slot(b, zero_row, nml_sh[tsl * kPThreads + tid], taddr0 + tsl * 16, v0,
+                    min(kPSlotVec, nvec - v0), ycol, drow + static_cast<int64_t>(v0) * 8, tid);
+          }
         }
       }
       tm.mark(4);
@@ -441,35 +515,45 @@ __global__ void __launch_bounds__((kPW + 2) * 32, 1)
   // memory or a thread of its own still reads TMEM
   tc::fence_before_sync();
   __syncthreads();
-  ptx::cluster_sync_all();
+  if constexpr (CL == 2) ptx::cluster_sync_all();
   if (warp == 0 && grad) {
     tc::fence_after_sync();
     tc::tmem_dealloc<kPTmemCols>(tmem_base);
   }
+  // small steps: the last CTA reduces obj/flags into out4 (the ring is free now)
+  if (P.out4) fused_reduce_if_last(P, smem);
 }
 
 }  // namespace
 
-bool pair_supported(const LossParams& p, DType in, DType out, bool ent) {
+bool pair_supported(const LossParams& p, DType in, DType out, bool ent, int cl) {
   if (in != DType::BF16 || ent) return false;
-  if (p.dlogits != nullptr && !p.gather_only && out != DType::BF16) return false;
+  if (p.dlogits != nullptr && !p.gather_only && out != DType::BF16 && out != DType::F32) return false;
   if (p.vocab % 16 != 0 || (p.ld * 2) % 16 != 0 || reinterpret_cast<uintptr_t>(p.logits) % 16 != 0)
     return false;
-  if (p.dlogits && ((p.ld_d * 2) % 16 != 0 || reinterpret_cast<uintptr_t>(p.dlogits) % 16 != 0))
+  // f32 rows leave through 32-byte stores
+  const int64_t osz = out == DType::F32 ? 4 : 2, oal = out == DType::F32 ? 32 : 16;
+  if (p.dlogits && ((p.ld_d * osz) % oal != 0 || reinterpret_cast<uintptr_t>(p.dlogits) % oal != 0))
     return false;
-  const int32_t nvec0 = (p.vocab / 8 + 1) / 2;
+  const int32_t nvec0 = cl == 2 ? (p.vocab / 8 + 1) / 2 : p.vocab / 8;
   const int32_t nseg = (nvec0 + kPSlotVec - 1) / kPSlotVec;
   return nseg <= kPTSlots - 1;  // room for at least one lookahead slot in TMEM
 }
 
-cudaError_t launch_pair(const LossParams& p, int num_sms, const Tuning& tu, cudaStream_t stream,
-                        LaunchInfo* info) {
+cudaError_t launch_pair(const LossParams& p, DType out, int cl, int num_sms, const Tuning& tu,
+                        cudaStream_t stream, LaunchInfo* info) {
+  const bool f32 = out == DType::F32 && p.dlogits != nullptr && !p.gather_only;
+  const void* kern =
+      cl == 2 ? (f32 ? reinterpret_cast<const void*>(fused_pair_kernel<true, 2>)
+                     : reinterpret_cast<const void*>(fused_pair_kernel<false, 2>))
+              : (f32 ? reinterpret_cast<const void*>(fused_pair_kernel<true, 1>)
+                     : reinterpret_cast<const void*>(fused_pair_kernel<false, 1>));
   // 6 x 32 KB ring + 16 KB of per-thread nml fill the 227 KB a CTA may use
   const int nslots = tu.slots > 0 ? (tu.slots > 6 ? 6 : tu.slots) : 6;
   const int smem = nslots * kPSlotBytes + kPTSlots * kPThreads * static_cast<int>(sizeof(float));
-  cudaError_t e = allow_dyn_smem(reinterpret_cast<const void*>(fused_pair_kernel), smem);
+  cudaError_t e = allow_dyn_smem(kern, smem);
   if (e != cudaSuccess) return e;
-  const int32_t nvec0 = (p.vocab / 8 + 1) / 2;
+  const int32_t nvec0 = cl == 2 ? (p.vocab / 8 + 1) / 2 : p.vocab / 8;
   const int32_t nseg = (nvec0 + kPSlotVec - 1) / kPSlotVec;
   int look = tu.pair_lookahead;
   if (look > kPTSlots - nseg) look = kPTSlots - nseg;
@@ -477,27 +561,45 @@ cudaError_t launch_pair(const LossParams& p, int num_sms, const Tuning& tu, cuda
   cudaLaunchConfig_t cfg{};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.x = cl;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = cl == 2 ? 1 : 0;
   cfg.blockDim = dim3((kPW + 2) * 32);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cfg.gridDim = dim3(static_cast<unsigned>(num_sms & ~1));
-  int ncl = 0;
-  e = cudaOccupancyMaxActiveClusters(&ncl, fused_pair_kernel, &cfg);
-  if (e != cudaSuccess) return e;
-  if (ncl < 1) return cudaErrorInvalidConfiguration;
-  const int64_t nc = p.n_rows < ncl ? p.n_rows : ncl;
-  cfg.gridDim = dim3(static_cast<unsigned>(2 * nc));
-  if (info) {
-    info->cluster = 2;
-    info->grid = static_cast<int>(2 * nc);
-    info->kernel = "fused_pair_kernel";
+  int64_t slots = 0;  // resident rows-in-flight units (CTA pairs or CTAs)
+  if (cl == 2) {
+    cfg.gridDim = dim3(static_cast<unsigned>(num_sms & ~1));
+    int ncl = 0;
+    e = cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg);
+    if (e != cudaSuccess) return e;
+    slots = ncl;
+  } else {
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (kPW + 2) * 32, smem);
+    if (e != cudaSuccess) return e;
+    slots = static_cast<int64_t>(per_sm) * num_sms;
   }
-  return cudaLaunchKernelEx(&cfg, fused_pair_kernel, p, nslots, look, nvec0);
+  if (slots < 1) return cudaErrorInvalidConfiguration;
+  const int64_t nc = p.n_rows < slots ? p.n_rows : slots;
+  cfg.gridDim = dim3(static_cast<unsigned>(cl * nc));
+  // fused reduction for small steps: the last CTA reduces in its free ring
+  LossParams q = p;
+  const bool fuse = fuse_reduce_ok(p, smem);
+  if (!fuse) q.out4 = nullptr;
+  if (info) {
+    info->cluster = cl;
+    info->grid = static_cast<int>(cl * nc);
+    info->kernel = cl == 2 ? "fused_pair_kernel" : "fused_solo_kernel";
+    info->reduced = fuse ? 1 : 0;
+  }
+  if (cl == 2)
+    return f32 ? cudaLaunchKernelEx(&cfg, fused_pair_kernel<true, 2>, q, nslots, look, nvec0)
+               : cudaLaunchKernelEx(&cfg, fused_pair_kernel<false, 2>, q, nslots, look, nvec0);
+  return f32 ? cudaLaunchKernelEx(&cfg, fused_pair_kernel<true, 1>, q, nslots, look, nvec0)
+             : cudaLaunchKernelEx(&cfg, fused_pair_kernel<false, 1>, q, nslots, look, nvec0);
 }
 
 }  // namespace copris_b200

@@ -235,6 +235,13 @@ __device__ __forceinline__ void st_global_cs_v4(void* p, uint4 v) {
                : "memory");
 }
 
+// Streaming 32-byte store (sm_100: STG.256), 32-byte aligned.
+__device__ __forceinline__ void st_global_cs_v8f(float* p, const float (&d)[8]) {
+  asm volatile("st.global.cs.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "f"(d[0]),
+               "f"(d[1]), "f"(d[2]), "f"(d[3]), "f"(d[4]), "f"(d[5]), "f"(d[6]), "f"(d[7])
+               : "memory");
+}
+
 __device__ __forceinline__ uint4 ld_shared_v4(const void* p) {
   uint4 v;
   asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"

@@ -179,7 +179,7 @@ class Copris:
 
     # kernel selection / tunables of THIS context (copris_ctx_set_option); the
     # COPRIS_* environment is read once, when the context is created
-    _NAMED = {"fused_impl": {"auto": 0, "stream": 1, "tma": 2, "pair": 3},
+    _NAMED = {"fused_impl": {"auto": 0, "stream": 1, "tma": 2, "pair": 3, "solo": 4},
               "lmhead_impl": {"pair": 0, "1sm": 1}}
 
     def set_option(self, name: str, value) -> None:

@@ -22,17 +22,17 @@ def run(ctx, case, dl_dtype=BF16, fused=True, **kw):
 
 
 # (V, logits dtype, forced implementation or None, expected kernel, expected cluster)
-PAIR, LA = ("fused_pair_kernel", 2), ("fused_stream_la_kernel", 1)
+PAIR = ("fused_pair_kernel", 2)
 SHAPES = [
-    # Qwen2.5 vocab: the CTA-pair kernel (exponentials staged in TMEM) for bf16
-    # dlogits, the TMA ring + L2 re-read kernel for fp32 dlogits
-    (151936, BF16, None, (PAIR, LA), None),
-    (151936, BF16, "pair+pl0", (PAIR, LA), None),   # no lookahead: pass 2 right after the row
-    (151936, BF16, "pair+pl1", (PAIR, LA), None),
-    (151936, BF16, "pair+pl3+slots3", (PAIR, LA), None),  # short ring: producer waits on slots
-    (200000, BF16, None, (PAIR, LA), None),         # 7 slots per half-row: the TMEM ring wraps every row
-    (80000, BF16, None, (PAIR, LA), None),          # 3 slots per half, partial last slot
-    (40000, BF16, None, (PAIR, LA), None),          # 80 KB rows: smallest pair vocab
+    # Qwen2.5 vocab: the CTA-pair kernel for bf16 logits, with f16 exponentials
+    # (bf16 dlogits) or the raw logits (fp32 dlogits) staged in TMEM
+    (151936, BF16, None, (PAIR, PAIR), None),
+    (151936, BF16, "pair+pl0", (PAIR, PAIR), None),   # no lookahead: pass 2 right after the row
+    (151936, BF16, "pair+pl1", (PAIR, PAIR), None),
+    (151936, BF16, "pair+pl3+slots3", (PAIR, PAIR), None),  # short ring: producer waits on slots
+    (200000, BF16, None, (PAIR, PAIR), None),         # 7 slots per half-row: the TMEM ring wraps every row
+    (80000, BF16, None, (PAIR, PAIR), None),          # 3 slots per half, partial last slot
+    (40000, BF16, None, (PAIR, PAIR), None),          # 80 KB rows: smallest pair vocab
     (151936, BF16, "stream", "fused_stream_la_kernel", 1),  # the ring kernel forced for bf16 too
     (151936, BF16, "stream+la0", "fused_stream_la_kernel", 1),  # same without the lookahead
     (151936, BF16, "stream+la5", "fused_stream_la_kernel", 1),
@@ -43,6 +43,11 @@ SHAPES = [
     (20000, BF16, "stream", "fused_stream_la_kernel[resident]", 1),  # partial last segment
     (32000, BF16, "stream+la0+res0", "fused_stream_la_kernel", 1),
     (80000, BF16, "tma", "fused_tma_kernel", 1),      # 160 KB rows: one 16-warp CTA per row
+    (32000, BF16, "solo", "fused_solo_kernel", 1),    # one CTA per row, exponentials in TMEM
+    (32000, BF16, "solo+pl0", "fused_solo_kernel", 1),
+    (80000, BF16, "solo", "fused_solo_kernel", 1),    # 5 slots per row, partial last slot
+    (4096, BF16, "solo", "fused_solo_kernel", 1),     # one partial slot per row
+    (256, BF16, "solo", "fused_solo_kernel", 1),      # tiny rows
     (151936, F32, None, "fused_stream_la_kernel", 1),
     (151936, F32, "stream+la0", "fused_stream_la_kernel", 1),
     (32000, F32, None, "fused_stream_la_kernel", 1),
@@ -525,32 +530,43 @@ def test_k1_equals_loss_recompute_bitwise(ctx, oracle, V, dtype):
 
 
 def test_pair_and_ring_kernels_agree(ctx, oracle, impl):
-    """At V = 151,936 the CTA-pair kernel (bf16 dlogits, TMEM-staged f16
-    exponentials) and the ring kernel (fp32 dlogits, exponentials recomputed)
-    split the log-sum-exp differently: per-token outputs agree to fp32
-    rounding, the pair kernel's bf16 dlogits are within one bf16 ulp of the
-    ring kernel's fp32 dlogits, and branch decisions are identical."""
+    """At V = 151,936 the CTA-pair kernel and the ring kernel (exponentials
+    recomputed from an L2 re-read) split the log-sum-exp differently:
+    per-token outputs agree to fp32 rounding, the pair kernel's bf16 dlogits
+    (TMEM-staged f16 exponentials) are within one bf16 ulp of the ring
+    kernel's fp32 dlogits, its fp32 dlogits (TMEM-staged raw logits) within
+    1e-5 of the row's max, and branch decisions are identical."""
     case = Case(oracle, seed=29, P=2, G=8, V=151936, mu=math.log(24), lmax=64)
     _, a = run(ctx, case, BF16)
     assert ctx.last_launch()["kernel"] == "fused_pair_kernel"
+    _, a32 = run(ctx, case, F32)
+    assert ctx.last_launch()["kernel"] == "fused_pair_kernel"
+    impl("stream")
     _, b = run(ctx, case, F32)
     assert ctx.last_launch()["kernel"] == "fused_stream_la_kernel"
     assert_scalar_close(a.cur_lp.cpu().numpy(), b.cur_lp.cpu().numpy(), rtol=2e-6, what="cur_lp")
-    assert torch.equal(a.flags, b.flags)
+    assert torch.equal(a.flags, b.flags) and torch.equal(a32.flags, b.flags)
+    assert torch.equal(a.cur_lp, a32.cur_lp)  # same pass 1 in both pair modes
     ref = b.dlogits.double().cpu().numpy()
     assert_rows_close(a.dlogits.float().cpu().numpy(), ref, bf16=True, what="pair vs ring dlogits")
+    assert_rows_close(a32.dlogits.double().cpu().numpy(), ref, what="pair f32 vs ring f32 dlogits")
 
 
-@pytest.mark.parametrize("n_tok,masked", [(2048, False), (1000, False), (4099, True), (8192, False),
-                                          (8193, False)])
-def test_fused_reduction_bitwise(ctx, oracle, impl, n_tok, masked):
+@pytest.mark.parametrize("n_tok,masked,force,V,kernel", [
+    (2048, False, None, 32000, "fused_tma_kernel"), (1000, False, None, 32000, "fused_tma_kernel"),
+    (4099, True, None, 32000, "fused_tma_kernel"), (8192, False, None, 32000, "fused_tma_kernel"),
+    (8193, False, None, 32000, "fused_tma_kernel"),
+    (2048, False, "solo", 32000, "fused_solo_kernel"), (4099, True, "solo", 32000, "fused_solo_kernel"),
+    (8193, False, "solo", 32000, "fused_solo_kernel"),
+    (1000, True, None, 151936, "fused_pair_kernel"), (2048, False, None, 151936, "fused_pair_kernel")])
+def test_fused_reduction_bitwise(ctx, oracle, impl, n_tok, masked, force, V, kernel):
     """copris_loss_out.out4: a one-chunk step of <= 8,192 tokens is reduced by
     the loss launch's last CTA (ONE launch); larger ones by the separate
     reduction. Either way out4 is bitwise copris_loss_reduce's result (same
     tiles, same fixed order), reruns are bitwise identical, and the loss
     matches the oracle."""
-    impl(None)
-    case = Case(oracle, seed=n_tok, P=1, G=n_tok // 256 + 1, V=32000, fixed_len=256)
+    impl(force)
+    case = Case(oracle, seed=n_tok, P=1, G=n_tok // 256 + 1, V=V, fixed_len=256)
     hb = case.hb
     batch = case.upload(ctx)
     n = min(n_tok, hb.n_tok)
@@ -564,7 +580,7 @@ def test_fused_reduction_bitwise(ctx, oracle, impl, n_tok, masked):
     fused4 = torch.full((4,), -1.0, dtype=torch.float64, device="cuda")
     ctx.loss_chunk_fused(logits, batch, case.clip(), outs, dlogits=dl, total_tokens=T, out4=fused4)
     info = ctx.last_launch()
-    assert info["kernel"] == "fused_tma_kernel" and info["fused_reduce"] == (n <= 8192)
+    assert info["kernel"] == kernel and info["fused_reduce"] == (n <= 8192)
     sep4 = torch.zeros(4, dtype=torch.float64, device="cuda")
     ctx.reduce(outs, n, sep4)
     ctx.check()

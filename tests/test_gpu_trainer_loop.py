@@ -5,13 +5,16 @@ grpo_dropin.hpp, linked against libcopris_b200.so) restates Trainer::train_step
 (trainer.hpp:120-178) with grpo_step_loss -> DropIn (trainer.hpp:176) and
 adam_.update -> AdamDropIn (trainer.hpp:177), so the GPU gradient and update
 drive the next rollout, and runs it beside the UNMODIFIED reference Trainer.
-While the two runs form the same batches (ids, tokens, segment versions and
-lengths) the losses must agree within 1e-5 (relative); the step at which the
-scheduler first forms a different batch is reported, not asserted — the runs
-are chaotic in the sampled tokens (a gradient that differs in the 7th digit
-moves a token once a uniform draw lands that close to a CDF boundary). Plus
-the GPU form of acceptance criterion C2 (acceptance_main.cpp:105-121): the
-synchronous GPU loop against the reference's standalone on-policy loop."""
+Asserted: with the reference loss and the GPU Adam the whole run is BITWISE the
+reference Trainer's (loss, parameters, version, batches) on every step; the
+GPU loss on the reference's own items is within 1e-5 on every step; with the
+GPU loss AND the GPU Adam driving the rollouts the first step agrees within
+1e-5. Reported, not asserted: how many steps that run keeps forming the same
+batches — Adam's first update lr g / (|g| + eps) turns the ~1e-10 fp32 error of
+~1e-9 near-cancelling table-gradient entries into a ~0.1 lr parameter
+difference, and the sampled tokens follow. Plus the GPU form of acceptance
+criterion C2 (acceptance_main.cpp:105-121): the synchronous loop with the GPU
+Adam against the reference's standalone on-policy loop, < 1e-12 per step."""
 import json
 import os
 import subprocess
@@ -32,12 +35,16 @@ def test_reference_trainer_loop_with_gpu_loss_and_adam():
     assert lines, p.stderr
     summaries = {l["case"]: l for l in lines if l.get("summary")}
     assert set(summaries) == CASES | {"c2_sync_vs_reference_loop"}, sorted(summaries)
-    bad = [l for l in lines if not l["ok"]] if lines else []
+    bad = [l for l in lines if not l["ok"]]
     assert not bad, bad[:3]
     assert p.returncode == 0, p.stderr
     for name in CASES:
         s = summaries[name]
-        # the first batch is formed before any update: identical by construction
-        assert s["lockstep_steps"] >= 1, s
-        assert s["worst_loss_rel_err_lockstep"] <= 1e-5, s
+        # GPU Adam in the reference loop: the whole training run is bitwise the reference's
+        assert s["a_gpu_adam_bitwise_all_steps"], s
+        # GPU loss on the reference's items and parameters, every step
+        assert s["worst_teacher_forced_loss_rel_err"] <= 1e-5, s
+        # GPU loss + GPU Adam driving the rollouts: the first step agrees
+        assert s["b_step0_loss_rel_err"] <= 1e-5 and s["b_lockstep_steps"] >= 1, s
+    assert summaries["c2_sync_vs_reference_loop"]["a_worst_param_diff"] < 1e-12
     print(json.dumps(list(summaries.values())))
