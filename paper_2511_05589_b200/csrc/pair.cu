@@ -233,17 +233,30 @@ __device__ __forceinline__ float p1_slot(LaneAcc& a, uint32_t sb, int32_t v0, in
 }
 
 // Pass 2 of one consumer thread on one slot: dlogits from the staged
-// exponentials (or zeros), bf16 out. The target column is written by its
-// owner afterwards (a later store of the same thread to the same address).
+// exponentials (or zeros), bf16 out. W256 (full slots, 32-byte aligned rows):
+// lane pairs swap one vector each so that every thread writes two ADJACENT
+// vectors with one 32-byte store (STG.256); the target column is patched into
+// its vector before the swap. Otherwise 16-byte stores and the target column
+// written by its owner afterwards (a later store of the same thread).
+template <bool W256>
 __device__ __forceinline__ void p2_slot(const RowBroadcast& b, bool zero_row, float nml,
                                         uint32_t taddr, int32_t v0, int32_t cnt, int32_t ycol,
                                         __nv_bfloat16* dseg, int tid) {
   __nv_bfloat16* base = dseg + static_cast<int64_t>(tid) * 8;
+  const int32_t rel = ycol - v0 * 8;
+  const bool own_y = static_cast<uint32_t>(rel) < static_cast<uint32_t>(cnt * 8) &&
+                     ((rel >> 3) & (kPThreads - 1)) == tid;
   if (zero_row) {
     const uint4 z{0u, 0u, 0u, 0u};
+    if (W256) {
+      const int64_t pb = (tid & 1) ? -8 : 0;  // the pair's even vector
 #pragma unroll
-    for (int q = 0; q < kPK; ++q)
-      if (tid + q * kPThreads < cnt) ptx::st_global_cs_v4(base + q * kPThreads * 8, z);
+      for (int q = (tid & 1); q < kPK; q += 2) ptx::st_global_cs_v8u(base + pb + q * kPThreads * 8, z, z);
+    } else {
+#pragma unroll
+      for (int q = 0; q < kPK; ++q)
+        if (tid + q * kPThreads < cnt) ptx::st_global_cs_v4(base + q * kPThreads * 8, z);
+    }
     return;
   }
   // |coef| p_k = e_k 2^(m log2(e) - 15 - c2) = e_k 2^(-nml - c2); 0 for a lane
@@ -262,6 +275,38 @@ __device__ __forceinline__ void p2_slot(const RowBroadcast& b, bool zero_row, fl
     for (int k = 0; k < 4; ++k) o[k] = ptx::f2_to_bf16x2(ptx::fmul2(f16x2_to_f2(h[q * 4 + k]), sc2));
     v[q] = uint4{o[0], o[1], o[2], o[3]};
   }
+  if (W256) {
+    // one-hot term coef (1 - p_y) (policy.hpp:193-194) into its vector first
+    if (own_y) {
+      const int qy = rel >> 12, jy = rel & 7;  // vector (tid + qy * 512), column jy of it
+      const uint32_t dyb = __bfloat16_as_ushort(__float2bfloat16_rn(b.dy));
+      // register-only patch (no address of v is taken: v stays in registers)
+      auto patch = [&](uint32_t w, int k) {
+        if ((jy >> 1) != k) return w;
+        return (jy & 1) ? (w & 0x0000FFFFu) | (dyb << 16) : (w & 0xFFFF0000u) | dyb;
+      };
+#pragma unroll
+      for (int q = 0; q < kPK; ++q)
+        if (q == qy) v[q] = uint4{patch(v[q].x, 0), patch(v[q].y, 1), patch(v[q].z, 2), patch(v[q].w, 3)};
+    }
+    // pair (q, q+1): the even lane stores {own, partner} of q, the odd lane
+    // {partner, own} of q+1
+    const bool odd = tid & 1;
+#pragma unroll
+    for (int q = 0; q < kPK; q += 2) {
+      const uint4 send = odd ? v[q] : v[q + 1];
+      uint4 got;
+      got.x = __shfl_xor_sync(0xffffffffu, send.x, 1);
+      got.y = __shfl_xor_sync(0xffffffffu, send.y, 1);
+      got.z = __shfl_xor_sync(0xffffffffu, send.z, 1);
+      got.w = __shfl_xor_sync(0xffffffffu, send.w, 1);
+      if (odd)
+        ptx::st_global_cs_v8u(base - 8 + (q + 1) * kPThreads * 8, got, v[q + 1]);
+      else
+        ptx::st_global_cs_v8u(base + q * kPThreads * 8, v[q], got);
+    }
+    return;
+  }
   if (cnt == kPSlotVec) {
 #pragma unroll
     for (int q = 0; q < kPK; ++q) ptx::st_global_cs_v4(base + q * kPThreads * 8, v[q]);
@@ -271,9 +316,7 @@ __device__ __forceinline__ void p2_slot(const RowBroadcast& b, bool zero_row, fl
       if (tid + q * kPThreads < cnt) ptx::st_global_cs_v4(base + q * kPThreads * 8, v[q]);
   }
   // one-hot term coef (1 - p_y) (policy.hpp:193-194), by the thread that owns it
-  const int32_t rel = ycol - v0 * 8;
-  if (static_cast<uint32_t>(rel) < static_cast<uint32_t>(cnt * 8) && ((rel >> 3) & (kPThreads - 1)) == tid)
-    st_global_b16(dseg + rel, __bfloat16_as_ushort(__float2bfloat16_rn(b.dy)));
+  if (own_y) st_global_b16(dseg + rel, __bfloat16_as_ushort(__float2bfloat16_rn(b.dy)));
 }
 
 // Pass 2, f32 dlogits: the staged raw logits -> d_k = -coef 2^(z_k log2(e) - c1)
@@ -336,6 +379,9 @@ __global__ void __launch_bounds__((kPW + 2) * 32, 1)
   const int32_t nseg = (nvec + kPSlotVec - 1) / kPSlotVec;
   const int32_t L = min(look, nseg);
   const bool grad = P.dlogits != nullptr && !P.gather_only;
+  // bf16 rows whose every half starts 32-byte aligned: 32-byte stores in pass 2
+  const bool w256 = !F32 && grad && (P.ld_d % 16) == 0 && (reinterpret_cast<uintptr_t>(P.dlogits) % 32) == 0 &&
+                    (col0 % 16) == 0;
   const uint32_t sbase = ptx::smem_u32(smem);
   float* nml_sh = reinterpret_cast<float*>(smem + nslots * kPSlotBytes);
   const uint32_t fbase = ptx::smem_u32(full), ebase = ptx::smem_u32(empty);
@@ -496,8 +542,13 @@ __global__ void __launch_bounds__((kPW + 2) * 32, 1)
                         drow + static_cast<int64_t>(v0) * 8, tid);
           } else {
             __nv_bfloat16* drow = static_cast<__nv_bfloat16*>(P.dlogits) + r * P.ld_d + col0;
-            p2_slot(b, zero_row, nml_sh[tsl * kPThreads + tid], taddr0 + tsl * 16, v0,
-                    min(kPSlotVec, nvec - v0), ycol, drow + static_cast<int64_t>(v0) * 8, tid);
+            const int32_t cnt = min(kPSlotVec, nvec - v0);
+            if (w256 && cnt == kPSlotVec)
+              p2_slot<true>(b, zero_row, nml_sh[tsl * kPThreads + tid], taddr0 + tsl * 16, v0, cnt,
+                            ycol, drow + static_cast<int64_t>(v0) * 8, tid);
+            else
+              p2_slot<false>(b, zero_row, nml_sh[tsl * kPThreads + tid], taddr0 + tsl * 16, v0, cnt,
+                             ycol, drow + static_cast<int64_t>(v0) * 8, tid);
           }
         }
       }

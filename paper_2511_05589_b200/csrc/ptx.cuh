@@ -235,6 +235,13 @@ __device__ __forceinline__ void st_global_cs_v4(void* p, uint4 v) {
                : "memory");
 }
 
+// Streaming 32-byte store of two 16-byte vectors (sm_100: STG.256), 32-byte aligned.
+__device__ __forceinline__ void st_global_cs_v8u(void* p, uint4 a, uint4 b) {
+  asm volatile("st.global.cs.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(a.x),
+               "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+               : "memory");
+}
+
 // Streaming 32-byte store (sm_100: STG.256), 32-byte aligned.
 __device__ __forceinline__ void st_global_cs_v8f(float* p, const float (&d)[8]) {
   asm volatile("st.global.cs.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "f"(d[0]),

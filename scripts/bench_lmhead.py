@@ -7,6 +7,7 @@ import numpy as np
 import torch
 
 sys.path.insert(0, ".")
+from bench import ClockSampler  # noqa: E402
 from paper_2511_05589_b200 import ClipConfig, Copris
 from paper_2511_05589_b200.lmhead import lmhead_grpo_step_loss
 from paper_2511_05589_b200.packing import upload
@@ -25,7 +26,18 @@ def timeit(fn, iters=10, warm=3):
     return s.elapsed_time(e) / iters
 
 
+def peaks():
+    try:
+        with open("MEASURED_PEAKS.json") as f:
+            p = json.load(f)
+        return p["bf16_tflops"], p["bf16_tflops_sustained"], "MEASURED_PEAKS.json"
+    except (OSError, KeyError, ValueError):
+        return 2250.0, 2250.0, "nominal dense bf16"
+
+
 def main():
+    sampler = ClockSampler(None)
+    sampler.start()
     T = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
     H = int(sys.argv[2]) if len(sys.argv) > 2 else 4096
     V = int(sys.argv[3]) if len(sys.argv) > 3 else 151936
@@ -79,8 +91,15 @@ def main():
         return out4.cpu()
 
     t_comp = timeit(composed, iters=3, warm=1)
-    out.update({"step_ms": t_step, "step_tcgen05_bwd_ms": t_step_tc, "step_tcgen05_dhidden_ms": t_step_dh, "composed_step_ms": t_comp, "chunk": chunk,
-                "step_tflops": 6 * T * H * V / t_step / 1e9})
+    burst, sustained, src = peaks()
+    step_tf = 6 * T * H * V / t_step / 1e9
+    out.update({"step_ms": t_step, "step_tcgen05_bwd_ms": t_step_tc, "step_tcgen05_dhidden_ms": t_step_dh,
+                "composed_step_ms": t_comp, "chunk": chunk, "step_tflops": step_tf,
+                "step_frac_of_sustained_bf16": step_tf / sustained,
+                "fwd_frac_of_burst_bf16": out["lmhead_fwd_tflops"] / burst,
+                "cublas_fwd_frac_of_burst_bf16": out["cublas_fwd_tflops"] / burst,
+                "peaks": {"bf16_tflops": burst, "bf16_tflops_sustained": sustained, "source": src},
+                "clocks": sampler.stop()})
     print(json.dumps(out))
 
 
