@@ -67,6 +67,7 @@ class ClockSampler:
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
     NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+    LOAD_W = 400.0  # a sample counts as "under load" at or above this board power
 
     def __init__(self, bus_id: str | None):
         self.bus = (bus_id or "").upper()
@@ -111,9 +112,17 @@ class ClockSampler:
         reasons = sorted({self.NAMES[i] for r in self.rows for i in range(4)
                           if r[4 + i].lower().startswith("active")})
         pw = [float(r[3]) for r in self.rows if r[3].replace(".", "").isdigit()]
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows),
-                "power_w": statistics.median(pw) if pw else None}
+        out = {"sm_mhz": statistics.median(sm) if sm else None,
+               "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows),
+               "power_w": statistics.median(pw) if pw else None}
+        # samples under load only (a sampler that also covers setup phases)
+        load = [(float(r[1]), float(r[3])) for r in self.rows
+                if r[1].replace(".", "").isdigit() and r[3].replace(".", "").isdigit()
+                and float(r[3]) >= self.LOAD_W]
+        if load and len(load) < len(self.rows):
+            out["under_load"] = {"samples": len(load), "sm_mhz": statistics.median(a for a, _ in load),
+                                 "power_w": statistics.median(b for _, b in load)}
+        return out
 
 
 def measured_peaks():

@@ -147,6 +147,9 @@ int copris_ctx_create(int device, copris_ctx** out) {
   e = cudaMalloc(&ctx->d_err, sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMemset(ctx->d_err, 0, sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMalloc(&ctx->d_rowctr, sizeof(unsigned long long));
+  // the claim counter starts at 0; every launch that claims rows leaves it at 0
+  // again (its last CTA resets it, reduce.cuh end_of_launch)
+  if (e == cudaSuccess) e = cudaMemset(ctx->d_rowctr, 0, sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMalloc(&ctx->d_scratch, reduce_scratch_bytes());
   if (e == cudaSuccess) e = cudaMemset(ctx->d_scratch, 0, reduce_scratch_bytes());
   if (e == cudaSuccess && ctx->tuning.trace) {
@@ -208,8 +211,8 @@ int copris_logprob_gather(copris_ctx* ctx, const void* logits, int64_t ld, int32
   if (vocab < 1 || ld < vocab) return fail(COPRIS_E_INVALID, "bad vocab/ld");
   DeviceGuard g(ctx->device);
   cudaError_t e = launch_logprob_gather(logits, ld, dt(dtype), target, n_tok, vocab, out_lp,
-                                        out_lse, ctx->d_err, ctx->d_rowctr, ctx->num_sms,
-                                        ctx->tuning, as_stream(stream));
+                                        out_lse, ctx->d_err, ctx->d_rowctr, ctx->d_scratch,
+                                        ctx->num_sms, ctx->tuning, as_stream(stream));
   return e == cudaSuccess ? COPRIS_OK : cuda_fail(e, "logprob_gather launch");
 }
 

@@ -392,8 +392,10 @@ __global__ void __launch_bounds__(WARPS * 32, (WARPS == 8 && CL == 1) ? 3 : 1)
   tm.flush(P.trace);
   // no CTA may exit while a peer can still address its shared memory
   if constexpr (CL > 1) ptx::cluster_sync_all();
-  // the row buffer is free now: it holds the trees of the fused reduction
-  if (P.out4) fused_reduce_if_last(P, smem);
+  // the row buffer is free now: it holds the trees of the fused reduction; the
+  // last CTA also rearms the claim counter
+  const bool self_reset = dyn && P.red_scratch != nullptr;
+  if (P.out4 || self_reset) end_of_launch(P, smem, self_reset);
 }
 
 // ---------------------------------------------------------------------------
@@ -948,7 +950,9 @@ cudaError_t launch_tma(const LossParams& p, int32_t E, int num_sms, cudaStream_t
     info->kernel = "fused_tma_kernel";
     info->reduced = fuse ? 1 : 0;
   }
-  if (p.row_ctr) {
+  // without the reduction scratch (its ticket) the kernel cannot rearm the claim
+  // counter itself: zero it here
+  if (p.row_ctr && (CL != 1 || !p.red_scratch)) {
     e = cudaMemsetAsync(p.row_ctr, 0, sizeof(unsigned long long), stream);
     if (e != cudaSuccess) return e;
   }
@@ -1112,8 +1116,8 @@ cudaError_t launch_bwd(const LossParams& p, DType in, DType out, int num_sms,
 // test_policy.cpp:157-172), without metadata, objective or dlogits.
 cudaError_t launch_logprob_gather(const void* logits, int64_t ld, DType in, const int32_t* target,
                                   int64_t n_tok, int32_t vocab, float* out_lp, float* out_lse,
-                                  uint32_t* err, unsigned long long* row_ctr, int num_sms,
-                                  const Tuning& tu, cudaStream_t stream) {
+                                  uint32_t* err, unsigned long long* row_ctr, void* red_scratch,
+                                  int num_sms, const Tuning& tu, cudaStream_t stream) {
   if (n_tok == 0) return cudaSuccess;
   LossParams p{};
   p.logits = logits;
@@ -1126,6 +1130,7 @@ cudaError_t launch_logprob_gather(const void* logits, int64_t ld, DType in, cons
   p.lse = out_lse;
   p.err = err;
   p.row_ctr = row_ctr;
+  p.red_scratch = red_scratch;  // its ticket lets the last CTA rearm row_ctr
   p.gather_only = 1;
   p.clamp_lo = 0.8;
   p.clamp_hi = 1.28;
@@ -1152,6 +1157,7 @@ const TuneField kFields[] = {
     {"slots", "COPRIS_TUNE_SLOTS", 0, 32, &Tuning::slots, nullptr},
     {"resident", "COPRIS_TUNE_RESIDENT", 0, 1, &Tuning::resident, nullptr},
     {"pair_lookahead", "COPRIS_PAIR_LOOKAHEAD", 0, 7, &Tuning::pair_lookahead, nullptr},
+    {"pair_st256", "COPRIS_PAIR_ST256", 0, 1, &Tuning::pair_st256, nullptr},
     {"lmhead_impl", "COPRIS_LMHEAD_IMPL", 0, 1, &Tuning::lmhead_impl, nullptr},
     {"lmhead_group", "COPRIS_LMHEAD_GROUP", 1, 1 << 20, &Tuning::lmhead_group, nullptr},
     {"lmhead_tma_store", "COPRIS_LMHEAD_TMA_STORE", 0, 1, &Tuning::lmhead_tma_store, nullptr},

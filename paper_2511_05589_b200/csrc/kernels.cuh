@@ -65,7 +65,7 @@ struct LossParams {
   uint8_t* flags;
   uint32_t* err;
   long long* trace;  // optional per-CTA phase-cycle accumulators (COPRIS_TRACE)
-  unsigned long long* row_ctr;  // dynamic row claims; zeroed by the launcher before each launch
+  unsigned long long* row_ctr;  // dynamic row claims: 0 at launch; the last CTA rearms it (reduce.cuh)
   int32_t gather_only;  // K1 mode: only (cur_lp, lse) per row — no metadata, no objective
   // optional fused reduction: the launch also reduces rows [0, red_n) of
   // obj/flags into out4 (the last CTA to finish does it; kernels that do not
@@ -94,6 +94,7 @@ struct Tuning {
   int slots = 0;          // stream kernel ring slots (0 = as many 32 KB slots as fit 192 KB)
   int resident = 1;       // stream kernel: pass 2 from resident segments when 3 rows fit
   int pair_lookahead = 3; // pair kernel: slots of row r+1 through pass 1 before pass 2 of row r
+  int pair_st256 = 1;     // pair kernel, bf16 dlogits: 32-byte stores (lane-pair swap) in pass 2
   int lmhead_impl = 0;    // 0 CTA pair (cta_group::2), 1 single SM
   int lmhead_group = 16;  // LM-head raster group (token pairs per vocab sweep)
   int lmhead_tma_store = 1;
@@ -130,8 +131,8 @@ cudaError_t launch_bwd(const LossParams& p, DType in, DType out, int num_sms,
 // K1.
 cudaError_t launch_logprob_gather(const void* logits, int64_t ld, DType in, const int32_t* target,
                                   int64_t n_tok, int32_t vocab, float* out_lp, float* out_lse,
-                                  uint32_t* err, unsigned long long* row_ctr, int num_sms,
-                                  const Tuning& tu, cudaStream_t stream);
+                                  uint32_t* err, unsigned long long* row_ctr, void* red_scratch,
+                                  int num_sms, const Tuning& tu, cudaStream_t stream);
 // K2.
 cudaError_t launch_expand_segments(const int64_t* seg_off, const uint32_t* seg_ver, int64_t n_seg,
                                    uint32_t* out_stage, cudaStream_t stream);

@@ -361,7 +361,8 @@ __device__ __forceinline__ void p2_slot_f32(const RowBroadcast& b, bool zero_row
 // r+1 run through pass 1 before pass 2 of row r.
 template <bool F32, int CL>
 __global__ void __launch_bounds__((kPW + 2) * 32, 1)
-    fused_pair_kernel(const LossParams P, const int nslots, const int look, const int32_t nvec0) {
+    fused_pair_kernel(const LossParams P, const int nslots, const int look, const int32_t nvec0,
+                      const int st256) {
   static_assert(CL == 1 || CL == 2, "a row is split over one or two CTAs");
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[16], empty[16], p1done[2], sdone[2];
@@ -380,7 +381,7 @@ __global__ void __launch_bounds__((kPW + 2) * 32, 1)
   const int32_t L = min(look, nseg);
   const bool grad = P.dlogits != nullptr && !P.gather_only;
   // bf16 rows whose every half starts 32-byte aligned: 32-byte stores in pass 2
-  const bool w256 = !F32 && grad && (P.ld_d % 16) == 0 && (reinterpret_cast<uintptr_t>(P.dlogits) % 32) == 0 &&
+  const bool w256 = st256 && !F32 && grad && (P.ld_d % 16) == 0 && (reinterpret_cast<uintptr_t>(P.dlogits) % 32) == 0 &&
                     (col0 % 16) == 0;
   const uint32_t sbase = ptx::smem_u32(smem);
   float* nml_sh = reinterpret_cast<float*>(smem + nslots * kPSlotBytes);
@@ -647,10 +648,10 @@ cudaError_t launch_pair(const LossParams& p, DType out, int cl, int num_sms, con
     info->reduced = fuse ? 1 : 0;
   }
   if (cl == 2)
-    return f32 ? cudaLaunchKernelEx(&cfg, fused_pair_kernel<true, 2>, q, nslots, look, nvec0)
-               : cudaLaunchKernelEx(&cfg, fused_pair_kernel<false, 2>, q, nslots, look, nvec0);
-  return f32 ? cudaLaunchKernelEx(&cfg, fused_pair_kernel<true, 1>, q, nslots, look, nvec0)
-             : cudaLaunchKernelEx(&cfg, fused_pair_kernel<false, 1>, q, nslots, look, nvec0);
+    return f32 ? cudaLaunchKernelEx(&cfg, fused_pair_kernel<true, 2>, q, nslots, look, nvec0, tu.pair_st256)
+               : cudaLaunchKernelEx(&cfg, fused_pair_kernel<false, 2>, q, nslots, look, nvec0, tu.pair_st256);
+  return f32 ? cudaLaunchKernelEx(&cfg, fused_pair_kernel<true, 1>, q, nslots, look, nvec0, tu.pair_st256)
+             : cudaLaunchKernelEx(&cfg, fused_pair_kernel<false, 1>, q, nslots, look, nvec0, tu.pair_st256);
 }
 
 }  // namespace copris_b200

@@ -155,11 +155,13 @@ inline bool fuse_reduce_ok(const LossParams& p, int smem_bytes) {
          p.red_n <= kFuseReduceTiles * reduce_tile(p.red_n);
 }
 
-// End of a fused loss launch with P.out4 set: every CTA, after its rows'
-// outputs are written (by the scalar-phase thread, which fences them), counts
-// itself done; the last one reduces rows [0, P.red_n) into P.out4.
-// `sm_raw` is shared memory the CTA no longer needs (>= sizeof(ReduceSmem)).
-__device__ __forceinline__ void fused_reduce_if_last(const LossParams& P, void* sm_raw) {
+// End of a fused loss launch (every CTA, after its rows' outputs are written by
+// the scalar-phase thread, which fences them): the CTA counts itself done and the
+// LAST one (a) resets the row-claim counter when `reset_ctr` (so the next launch —
+// or a CUDA-graph replay of this one — starts at 0 without a memset node) and
+// (b) with P.out4 set, reduces rows [0, P.red_n) into P.out4. `sm_raw` is shared
+// memory the CTA no longer needs (>= sizeof(ReduceSmem)).
+__device__ __forceinline__ void end_of_launch(const LossParams& P, void* sm_raw, bool reset_ctr) {
   __shared__ bool last;
   __threadfence();  // this thread's obj/flags stores, before the ticket
   __syncthreads();
@@ -168,6 +170,11 @@ __device__ __forceinline__ void fused_reduce_if_last(const LossParams& P, void* 
   __syncthreads();
   if (!last || threadIdx.x >= kReduceThreads) return;
   __threadfence();
+  if (threadIdx.x == 0) {
+    if (reset_ctr) *P.row_ctr = 0ull;  // every CTA has made its last claim
+    if (!P.out4) sc->fused_ticket = 0;  // else reduce_final resets it
+  }
+  if (!P.out4) return;
   ReduceSmem& sm = *static_cast<ReduceSmem*>(sm_raw);
   const bool vec = (reinterpret_cast<uintptr_t>(P.obj) % 16 == 0) &&
                    (reinterpret_cast<uintptr_t>(P.flags) % 4 == 0);
@@ -177,6 +184,9 @@ __device__ __forceinline__ void fused_reduce_if_last(const LossParams& P, void* 
     reduce_all_in_cta<false>(P.obj, P.flags, P.red_n, P.out4, sc, sm, threadIdx.x);
 }
 
+__device__ __forceinline__ void fused_reduce_if_last(const LossParams& P, void* sm_raw) {
+  end_of_launch(P, sm_raw, false);
+}
 
 }  // namespace
 }  // namespace copris_b200

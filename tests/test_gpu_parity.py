@@ -29,6 +29,7 @@ SHAPES = [
     (151936, BF16, None, (PAIR, PAIR), None),
     (151936, BF16, "pair+pl0", (PAIR, PAIR), None),   # no lookahead: pass 2 right after the row
     (151936, BF16, "pair+pl1", (PAIR, PAIR), None),
+    (151936, BF16, "pair+st0", (PAIR, PAIR), None),  # 16-byte stores in pass 2
     (151936, BF16, "pair+pl3+slots3", (PAIR, PAIR), None),  # short ring: producer waits on slots
     (200000, BF16, None, (PAIR, PAIR), None),
     (151952, BF16, None, (PAIR, PAIR), None),       # second half not 32-byte aligned: 16-byte stores there         # 7 slots per half-row: the TMEM ring wraps every row
@@ -59,7 +60,7 @@ SHAPES = [
 ]
 
 # the context options every test starts from (copris_ctx_set_option)
-DEFAULT_OPTS = dict(fused_impl=0, lookahead=2, resident=1, slots=0, pair_lookahead=3)
+DEFAULT_OPTS = dict(fused_impl=0, lookahead=2, resident=1, slots=0, pair_lookahead=3, pair_st256=1)
 
 
 @pytest.fixture
@@ -79,6 +80,8 @@ def impl(ctx):
                     opts["pair_lookahead"] = int(o[2:])
                 elif o.startswith("slots"):
                     opts["slots"] = int(o[5:])
+                elif o.startswith("st"):
+                    opts["pair_st256"] = int(o[2:])
         if name:
             opts["fused_impl"] = name
         for k, v in opts.items():
@@ -596,3 +599,27 @@ def test_fused_reduction_bitwise(ctx, oracle, impl, n_tok, masked, force, V, ker
     assert abs(fused4[0].item() - obj.sum()) <= 1e-12 * max(1.0, np.abs(obj).sum())
     if n == hb.n_tok and not masked:
         assert_loss_close(-fused4[0].item() / T, case.ref.loss, case.ref.obj, T, what="fused out4")
+
+
+def test_claim_counter_rearmed_across_launch_kinds(ctx, oracle, impl):
+    """The TMA kernel claims rows from a per-context counter that the launch's
+    last CTA rearms (no memset node). K1 (gather-only) and loss launches of
+    more rows than resident CTAs, interleaved, must each give bitwise what a
+    fresh context gives."""
+    from paper_2511_05589_b200 import Copris
+    impl(None)
+    case = Case(oracle, seed=41, P=2, G=8, V=32000, fixed_len=256)   # 4,096 rows > 444 CTAs
+    logits = case.logits_gpu()
+    tgt = torch.from_numpy(case.hb.target).cuda()
+    fresh = Copris(0)
+    lp0, _ = fresh.sequence_logprobs(logits, tgt)
+    _, r0 = run(fresh, case, BF16)
+    for _ in range(3):
+        lp, _ = ctx.sequence_logprobs(logits, tgt)
+        _, r = run(ctx, case, BF16)
+        assert ctx.last_launch()["kernel"] == "fused_tma_kernel"
+        assert torch.equal(lp, lp0)
+        assert torch.equal(r.cur_lp, r0.cur_lp) and torch.equal(r.flags, r0.flags)
+        assert torch.equal(r.dlogits.view(torch.int16), r0.dlogits.view(torch.int16))
+        assert r.loss == r0.loss
+    case.check(r0, BF16, what="claim counter")
