@@ -94,7 +94,7 @@ struct Tuning {
   int slots = 0;          // stream kernel ring slots (0 = as many 32 KB slots as fit 192 KB)
   int resident = 1;       // stream kernel: pass 2 from resident segments when 3 rows fit
   int pair_lookahead = 3; // pair kernel: slots of row r+1 through pass 1 before pass 2 of row r
-  int pair_st256 = 1;     // pair kernel, bf16 dlogits: 32-byte stores (lane-pair swap) in pass 2
+  int pair_st256 = 0;     // pair kernel, bf16 dlogits: 32-byte stores (lane-pair swap) in pass 2
   int lmhead_impl = 0;    // 0 CTA pair (cta_group::2), 1 single SM
   int lmhead_group = 16;  // LM-head raster group (token pairs per vocab sweep)
   int lmhead_tma_store = 1;

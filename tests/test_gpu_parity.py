@@ -29,10 +29,11 @@ SHAPES = [
     (151936, BF16, None, (PAIR, PAIR), None),
     (151936, BF16, "pair+pl0", (PAIR, PAIR), None),   # no lookahead: pass 2 right after the row
     (151936, BF16, "pair+pl1", (PAIR, PAIR), None),
-    (151936, BF16, "pair+st0", (PAIR, PAIR), None),  # 16-byte stores in pass 2
+    (151936, BF16, "pair+st1", (PAIR, PAIR), None),  # 32-byte stores in pass 2 (lane-pair swap)
+    (200000, BF16, "pair+st1", (PAIR, PAIR), None),
     (151936, BF16, "pair+pl3+slots3", (PAIR, PAIR), None),  # short ring: producer waits on slots
     (200000, BF16, None, (PAIR, PAIR), None),
-    (151952, BF16, None, (PAIR, PAIR), None),       # second half not 32-byte aligned: 16-byte stores there         # 7 slots per half-row: the TMEM ring wraps every row
+    (151952, BF16, "pair+st1", (PAIR, PAIR), None),  # second half not 32-byte aligned: 16-byte stores there         # 7 slots per half-row: the TMEM ring wraps every row
     (80000, BF16, None, (PAIR, PAIR), None),          # 3 slots per half, partial last slot
     (40000, BF16, None, (PAIR, PAIR), None),          # 80 KB rows: smallest pair vocab
     (151936, BF16, "stream", "fused_stream_la_kernel", 1),  # the ring kernel forced for bf16 too
@@ -60,7 +61,7 @@ SHAPES = [
 ]
 
 # the context options every test starts from (copris_ctx_set_option)
-DEFAULT_OPTS = dict(fused_impl=0, lookahead=2, resident=1, slots=0, pair_lookahead=3, pair_st256=1)
+DEFAULT_OPTS = dict(fused_impl=0, lookahead=2, resident=1, slots=0, pair_lookahead=3, pair_st256=0)
 
 
 @pytest.fixture
