@@ -897,8 +897,16 @@ __global__ void __launch_bounds__(kReduceThreads)
   __shared__ ReduceSmem sm;
   __shared__ bool last;
   const int64_t tile = reduce_tile(n), ntiles = (n + tile - 1) / tile;
-  for (int64_t k = blockIdx.x; k < ntiles; k += gridDim.x)
-    reduce_tile_partial<VEC>(obj, flags, n, tile, k, sc, sm, threadIdx.x);
+  for (int64_t k = blockIdx.x; k < ntiles; k += gridDim.x) {
+    double po;
+    unsigned long long ps, pc;
+    reduce_tile_partial<VEC>(obj, flags, n, tile, k, sm, threadIdx.x, po, ps, pc);
+    if (threadIdx.x == 0) {
+      sc->obj[k] = po;
+      sc->stale[k] = ps;
+      sc->clipped[k] = pc;
+    }
+  }
   if (threadIdx.x == 0) {
     __threadfence();
     last = atomicAdd(&sc->ticket, 1u) == gridDim.x - 1;
@@ -906,7 +914,11 @@ __global__ void __launch_bounds__(kReduceThreads)
   __syncthreads();
   if (last) {
     __threadfence();
-    reduce_final(n, ntiles, out4, sc, sm, threadIdx.x);
+    reduce_final(n, ntiles, out4, sm, threadIdx.x,
+                 [&](int64_t i, double& o, unsigned long long& s, unsigned long long& c) {
+                   scratch_part(sc, i, o, s, c);
+                 });
+    if (threadIdx.x == 0) sc->ticket = 0;
   }
 }
 
@@ -1087,7 +1099,7 @@ cudaError_t launch_fused_kernel(const LossParams& p, DType in, DType out, int nu
   // staged in TMEM, no L2 re-read) unless another kernel is forced; the solo
   // kernel (the same with one CTA per row) only when forced (fused_impl 4)
   const bool ent = p.entropy_coeff != 0.0;
-  if ((tu.fused_impl == 0 || tu.fused_impl == 3) && static_cast<int64_t>(p.vocab) * 2 > 72 * 1024 &&
+  if ((tu.fused_impl == 3 || (tu.fused_impl == 0 && static_cast<int64_t>(p.vocab) * 2 > 72 * 1024)) &&
       pair_supported(p, in, out, ent, 2))
     return launch_pair(p, out, 2, num_sms, tu, stream, info);
   if (tu.fused_impl == 4 && pair_supported(p, in, out, ent, 1))

@@ -42,34 +42,65 @@ __host__ __device__ inline int64_t reduce_tile(int64_t n) {
   return t < 1024 ? 1024 : t;
 }
 
-// Shared-memory arrays of the 256-thread trees.
+// Shared memory of the 256-thread trees: one slot per warp, plus the tile
+// partials of the in-CTA path (at most kFuseReduceTiles tiles).
 struct ReduceSmem {
-  double o[kReduceThreads];
-  unsigned long long s[kReduceThreads], c[kReduceThreads], m[kReduceThreads];
+  double o[kReduceThreads / 32];
+  unsigned long long s[kReduceThreads / 32], c[kReduceThreads / 32], m[kReduceThreads / 32];
+  double po[kFuseReduceTiles];
+  unsigned long long ps[kFuseReduceTiles], pc[kFuseReduceTiles];
 };
 
-// Tree over the 256 participating threads (named barrier 1: the caller's CTA
-// may have more threads; those do not take part).
-__device__ __forceinline__ void reduce_tree(ReduceSmem& sm, int tid, bool four) {
-  ptx::named_bar_sync(1, kReduceThreads);
-  for (int h = kReduceThreads / 2; h > 0; h >>= 1) {
-    if (tid < h) {
-      sm.o[tid] += sm.o[tid + h];
-      sm.s[tid] += sm.s[tid + h];
-      sm.c[tid] += sm.c[tid + h];
-      if (four) sm.m[tid] += sm.m[tid + h];
-    }
-    ptx::named_bar_sync(1, kReduceThreads);
+// Fixed-order tree over the 256 participating threads (named barrier 1: the
+// caller's CTA may have more threads; those do not take part): a shuffle
+// butterfly inside each warp (a + b == b + a exactly, so every lane holds the
+// same bits), the 8 warp results through shared memory, the same butterfly in
+// warp 0. The result is valid in thread 0. Two barriers instead of a
+// shared-memory tree's nine: the reduction is on the tail of every small step.
+template <bool FOUR>
+__device__ __forceinline__ void reduce_tree(ReduceSmem& sm, int tid, double& o, unsigned long long& s,
+                                            unsigned long long& c, unsigned long long& m) {
+  constexpr unsigned kAll = 0xffffffffu;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    o += __shfl_xor_sync(kAll, o, off);
+    s += __shfl_xor_sync(kAll, s, off);
+    c += __shfl_xor_sync(kAll, c, off);
+    if (FOUR) m += __shfl_xor_sync(kAll, m, off);
   }
+  const int w = tid >> 5, lane = tid & 31;
+  if (lane == 0) {
+    sm.o[w] = o;
+    sm.s[w] = s;
+    sm.c[w] = c;
+    if (FOUR) sm.m[w] = m;
+  }
+  ptx::named_bar_sync(1, kReduceThreads);
+  if (w == 0) {
+    constexpr int NW = kReduceThreads / 32;
+    o = lane < NW ? sm.o[lane] : 0.0;
+    s = lane < NW ? sm.s[lane] : 0ull;
+    c = lane < NW ? sm.c[lane] : 0ull;
+    if (FOUR) m = lane < NW ? sm.m[lane] : 0ull;
+#pragma unroll
+    for (int off = NW / 2; off > 0; off >>= 1) {
+      o += __shfl_xor_sync(kAll, o, off);
+      s += __shfl_xor_sync(kAll, s, off);
+      c += __shfl_xor_sync(kAll, c, off);
+      if (FOUR) m += __shfl_xor_sync(kAll, m, off);
+    }
+  }
+  ptx::named_bar_sync(1, kReduceThreads);  // sm is reused by the next tree
 }
 
-// Partial of tile `k` (tokens [k tile, min(n, (k+1) tile))) by threads 0..255,
-// written to sc by thread 0. VEC: obj 16-byte and flags 4-byte aligned.
+// Partial of tile `k` (tokens [k tile, min(n, (k+1) tile))) by threads 0..255;
+// valid in thread 0. VEC: obj 16-byte and flags 4-byte aligned.
 template <bool VEC>
 __device__ __forceinline__ void reduce_tile_partial(const double* __restrict__ obj,
                                                     const uint8_t* __restrict__ flags, int64_t n,
-                                                    int64_t tile, int64_t k, ReduceScratch* sc,
-                                                    ReduceSmem& sm, int tid) {
+                                                    int64_t tile, int64_t k, ReduceSmem& sm, int tid,
+                                                    double& po, unsigned long long& ps,
+                                                    unsigned long long& pc) {
   const int64_t t0 = k * tile, t1 = min(n, t0 + tile);
   double o = 0.0;
   unsigned long long st = 0, cl = 0, mk = 0;
@@ -98,54 +129,71 @@ __device__ __forceinline__ void reduce_tile_partial(const double* __restrict__ o
     }
   }
   // stale/clipped counts < 2^32 per tile: pack the masked count with stale
-  sm.o[tid] = o;
-  sm.s[tid] = st | (mk << 32);
-  sm.c[tid] = cl;
-  reduce_tree(sm, tid, false);
-  if (tid == 0) {
-    sc->obj[k] = sm.o[0];
-    sc->stale[k] = sm.s[0];
-    sc->clipped[k] = sm.c[0];
-  }
-  ptx::named_bar_sync(1, kReduceThreads);  // sm is reused by the next tile
+  unsigned long long sv = st | (mk << 32), unused = 0;
+  reduce_tree<false>(sm, tid, o, sv, cl, unused);
+  po = o;
+  ps = sv;
+  pc = cl;
 }
 
-// The final sum over the tile partials (fixed order) -> out4; resets tickets.
+// The final sum over the tile partials (fixed order: thread i takes partials
+// i, i + 256, ... starting from 0, then the tree) -> out4. `part(i, o, s, c)`
+// yields partial i (global scratch in reduce_kernel, shared memory in the
+// in-CTA path: the same values, so the same bits).
+template <typename Part>
 __device__ __forceinline__ void reduce_final(int64_t n, int64_t ntiles, double* __restrict__ out4,
-                                             ReduceScratch* sc, ReduceSmem& sm, int tid) {
+                                             ReduceSmem& sm, int tid, Part part) {
   double O = 0.0;
   unsigned long long Sx = 0, Cx = 0, Mx = 0;
   for (int64_t i = tid; i < ntiles; i += kReduceThreads) {
-    O += *reinterpret_cast<volatile double*>(&sc->obj[i]);
-    const unsigned long long sm2 = *reinterpret_cast<volatile unsigned long long*>(&sc->stale[i]);
-    Sx += sm2 & 0xFFFFFFFFull;
-    Mx += sm2 >> 32;
-    Cx += *reinterpret_cast<volatile unsigned long long*>(&sc->clipped[i]);
+    double po;
+    unsigned long long ps, pc;
+    part(i, po, ps, pc);
+    O += po;
+    Sx += ps & 0xFFFFFFFFull;
+    Mx += ps >> 32;
+    Cx += pc;
   }
-  sm.o[tid] = O;
-  sm.s[tid] = Sx;
-  sm.c[tid] = Cx;
-  sm.m[tid] = Mx;
-  reduce_tree(sm, tid, true);
+  reduce_tree<true>(sm, tid, O, Sx, Cx, Mx);
   if (tid == 0) {
-    out4[0] = sm.o[0];
-    out4[1] = static_cast<double>(n - static_cast<int64_t>(sm.m[0]));
-    out4[2] = static_cast<double>(sm.s[0]);
-    out4[3] = static_cast<double>(sm.c[0]);
-    sc->ticket = 0;
-    sc->fused_ticket = 0;
+    out4[0] = O;
+    out4[1] = static_cast<double>(n - static_cast<int64_t>(Mx));
+    out4[2] = static_cast<double>(Sx);
+    out4[3] = static_cast<double>(Cx);
   }
 }
 
-// All tiles by one CTA (threads 0..255 of it), then the final sum: the last
-// CTA of a fused loss launch (fused_reduce_if_last).
+// Partials in the global scratch (reduce_kernel: written by other blocks).
+__device__ __forceinline__ void scratch_part(const ReduceScratch* sc, int64_t i, double& o,
+                                             unsigned long long& s, unsigned long long& c) {
+  o = *reinterpret_cast<const volatile double*>(&sc->obj[i]);
+  s = *reinterpret_cast<const volatile unsigned long long*>(&sc->stale[i]);
+  c = *reinterpret_cast<const volatile unsigned long long*>(&sc->clipped[i]);
+}
+
+// All tiles by one CTA (threads 0..255 of it), partials kept in shared memory,
+// then the final sum: the last CTA of a fused loss launch (<= kFuseReduceTiles).
 template <bool VEC>
 __device__ __forceinline__ void reduce_all_in_cta(const double* obj, const uint8_t* flags, int64_t n,
-                                                  double* out4, ReduceScratch* sc, ReduceSmem& sm,
-                                                  int tid) {
+                                                  double* out4, ReduceSmem& sm, int tid) {
   const int64_t tile = reduce_tile(n), ntiles = (n + tile - 1) / tile;
-  for (int64_t k = 0; k < ntiles; ++k) reduce_tile_partial<VEC>(obj, flags, n, tile, k, sc, sm, tid);
-  reduce_final(n, ntiles, out4, sc, sm, tid);
+  for (int64_t k = 0; k < ntiles; ++k) {
+    double po;
+    unsigned long long ps, pc;
+    reduce_tile_partial<VEC>(obj, flags, n, tile, k, sm, tid, po, ps, pc);
+    if (tid == 0) {
+      sm.po[k] = po;
+      sm.ps[k] = ps;
+      sm.pc[k] = pc;
+    }
+  }
+  ptx::named_bar_sync(1, kReduceThreads);
+  reduce_final(n, ntiles, out4, sm, tid, [&](int64_t i, double& o, unsigned long long& s,
+                                             unsigned long long& c) {
+    o = sm.po[i];
+    s = sm.ps[i];
+    c = sm.pc[i];
+  });
 }
 
 // Whether a launch over p.red_n tokens reduces in its last CTA (<= 8 tiles, and
@@ -163,25 +211,28 @@ inline bool fuse_reduce_ok(const LossParams& p, int smem_bytes) {
 // memory the CTA no longer needs (>= sizeof(ReduceSmem)).
 __device__ __forceinline__ void end_of_launch(const LossParams& P, void* sm_raw, bool reset_ctr) {
   __shared__ bool last;
-  __threadfence();  // this thread's obj/flags stores, before the ticket
+  // every thread's stores (the per-token outputs) are ordered before thread 0's
+  // release fence by the barrier (fence cumulativity), as in a grid barrier
   __syncthreads();
   auto* sc = static_cast<ReduceScratch*>(P.red_scratch);
-  if (threadIdx.x == 0) last = atomicAdd(&sc->fused_ticket, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (!last || threadIdx.x >= kReduceThreads) return;
-  __threadfence();
   if (threadIdx.x == 0) {
-    if (reset_ctr) *P.row_ctr = 0ull;  // every CTA has made its last claim
-    if (!P.out4) sc->fused_ticket = 0;  // else reduce_final resets it
+    __threadfence();
+    last = atomicAdd(&sc->fused_ticket, 1u) == gridDim.x - 1;
+    if (last) {
+      __threadfence();  // acquire: the other CTAs' outputs, before this CTA reads them
+      if (reset_ctr) *P.row_ctr = 0ull;  // every CTA has made its last claim
+      sc->fused_ticket = 0;
+    }
   }
-  if (!P.out4) return;
+  __syncthreads();
+  if (!last || !P.out4 || threadIdx.x >= kReduceThreads) return;
   ReduceSmem& sm = *static_cast<ReduceSmem*>(sm_raw);
   const bool vec = (reinterpret_cast<uintptr_t>(P.obj) % 16 == 0) &&
                    (reinterpret_cast<uintptr_t>(P.flags) % 4 == 0);
   if (vec)
-    reduce_all_in_cta<true>(P.obj, P.flags, P.red_n, P.out4, sc, sm, threadIdx.x);
+    reduce_all_in_cta<true>(P.obj, P.flags, P.red_n, P.out4, sm, threadIdx.x);
   else
-    reduce_all_in_cta<false>(P.obj, P.flags, P.red_n, P.out4, sc, sm, threadIdx.x);
+    reduce_all_in_cta<false>(P.obj, P.flags, P.red_n, P.out4, sm, threadIdx.x);
 }
 
 __device__ __forceinline__ void fused_reduce_if_last(const LossParams& P, void* sm_raw) {
