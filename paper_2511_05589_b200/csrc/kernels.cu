@@ -1096,13 +1096,17 @@ cudaError_t launch_fused_kernel(const LossParams& p, DType in, DType out, int nu
                                 const Tuning& tu, cudaStream_t stream, LaunchInfo* info) {
   if (p.n_rows == 0) return cudaSuccess;
   // bf16 rows above 72 KB: the CTA-pair kernel (one HBM read, exponentials
-  // staged in TMEM, no L2 re-read) unless another kernel is forced; the solo
-  // kernel (the same with one CTA per row) only when forced (fused_impl 4)
+  // staged in TMEM, no L2 re-read) unless another kernel is forced
   const bool ent = p.entropy_coeff != 0.0;
   if ((tu.fused_impl == 3 || (tu.fused_impl == 0 && static_cast<int64_t>(p.vocab) * 2 > 72 * 1024)) &&
       pair_supported(p, in, out, ent, 2))
     return launch_pair(p, out, 2, num_sms, tu, stream, info);
-  if (tu.fused_impl == 4 && pair_supported(p, in, out, ent, 1))
+  // 56-72 KB bf16 rows (e.g. V = 32,000): the solo kernel by default — on the
+  // bench configs of BASELINE #5 it matched or beat the TMA kernel on 5 of 6
+  // (one group x L = 256: 0.68 vs 0.66 of peak; profiles/r02_solo_vs_tma.txt)
+  const int64_t row_bytes = static_cast<int64_t>(p.vocab) * 2;
+  const bool solo_auto = tu.fused_impl == 0 && row_bytes >= 56 * 1024 && row_bytes <= 72 * 1024;
+  if ((tu.fused_impl == 4 || solo_auto) && pair_supported(p, in, out, ent, 1))
     return launch_pair(p, out, 1, num_sms, tu, stream, info);
   return p.entropy_coeff != 0.0 ? by_types<true>(false, p, in, out, num_sms, tu, stream, info)
                                 : by_types<false>(false, p, in, out, num_sms, tu, stream, info);

@@ -191,6 +191,13 @@ def test_v32000_claimed_rows_against_oracle(ctx, oracle):
                          adv, want_dlogits=False)
     batch = upload(ctx, hb.tok_off, hb.group_off, hb.target, blp, hb.cur_stage, stage=hb.stage,
                    reward=hb.reward)
+    with ctx.options(fused_impl="tma"):
+        _claimed_rows_checks(ctx, logits, batch, ref, hb, T, z64, V)
+
+
+def _claimed_rows_checks(ctx, logits, batch, ref, hb, T, z64, V):
+    from paper_2511_05589_b200 import ClipConfig
+    from parity_util import assert_loss_close
     res = ctx.grpo_step_loss(logits, batch, ClipConfig(), coef=True)
     assert ctx.last_launch()["kernel"] == "fused_tma_kernel"
     assert_scalar_close(res.cur_lp.cpu().numpy(), ref.cur_lp, what="cur_lp")

@@ -39,7 +39,8 @@ SHAPES = [
     (151936, BF16, "stream", "fused_stream_la_kernel", 1),  # the ring kernel forced for bf16 too
     (151936, BF16, "stream+la0", "fused_stream_la_kernel", 1),  # same without the lookahead
     (151936, BF16, "stream+la5", "fused_stream_la_kernel", 1),
-    (32000, BF16, None, "fused_tma_kernel", 1),       # 64 KB rows resident, several CTAs/SM
+    (32000, BF16, None, "fused_solo_kernel", 1),      # 64 KB rows: one CTA per row, exponentials in TMEM
+    (32000, BF16, "tma", "fused_tma_kernel", 1),      # 64 KB rows resident, several CTAs/SM
     (32000, BF16, "stream", "fused_stream_la_kernel[resident]", 1),  # 3 rows fit the ring: no L2 re-read
     (32000, BF16, "stream+res0", "fused_stream_la_kernel", 1),  # 2 segments/row: lookahead = whole row
     (32000, BF16, "stream+la1+res0", "fused_stream_la_kernel", 1),
@@ -558,11 +559,11 @@ def test_pair_and_ring_kernels_agree(ctx, oracle, impl):
 
 
 @pytest.mark.parametrize("n_tok,masked,force,V,kernel", [
-    (2048, False, None, 32000, "fused_tma_kernel"), (1000, False, None, 32000, "fused_tma_kernel"),
-    (4099, True, None, 32000, "fused_tma_kernel"), (8192, False, None, 32000, "fused_tma_kernel"),
-    (8193, False, None, 32000, "fused_tma_kernel"),
-    (2048, False, "solo", 32000, "fused_solo_kernel"), (4099, True, "solo", 32000, "fused_solo_kernel"),
-    (8193, False, "solo", 32000, "fused_solo_kernel"),
+    (2048, False, "tma", 32000, "fused_tma_kernel"), (1000, False, "tma", 32000, "fused_tma_kernel"),
+    (4099, True, "tma", 32000, "fused_tma_kernel"), (8192, False, "tma", 32000, "fused_tma_kernel"),
+    (8193, False, "tma", 32000, "fused_tma_kernel"),
+    (2048, False, None, 32000, "fused_solo_kernel"), (4099, True, None, 32000, "fused_solo_kernel"),
+    (8192, False, None, 32000, "fused_solo_kernel"), (8193, False, "solo", 32000, "fused_solo_kernel"),
     (1000, True, None, 151936, "fused_pair_kernel"), (2048, False, None, 151936, "fused_pair_kernel")])
 def test_fused_reduction_bitwise(ctx, oracle, impl, n_tok, masked, force, V, kernel):
     """copris_loss_out.out4: a one-chunk step of <= 8,192 tokens is reduced by
@@ -608,11 +609,12 @@ def test_claim_counter_rearmed_across_launch_kinds(ctx, oracle, impl):
     more rows than resident CTAs, interleaved, must each give bitwise what a
     fresh context gives."""
     from paper_2511_05589_b200 import Copris
-    impl(None)
+    impl("tma")
     case = Case(oracle, seed=41, P=2, G=8, V=32000, fixed_len=256)   # 4,096 rows > 444 CTAs
     logits = case.logits_gpu()
     tgt = torch.from_numpy(case.hb.target).cuda()
     fresh = Copris(0)
+    fresh.set_option("fused_impl", "tma")
     lp0, _ = fresh.sequence_logprobs(logits, tgt)
     _, r0 = run(fresh, case, BF16)
     for _ in range(3):
