@@ -495,7 +495,10 @@ def run_ours(args):
                            "d2h_bytes_per_step": d2h,
                            "api": "copris_grpo_step_loss_host (host pinned buffers, 3-stream chunked pipeline)",
                            "sample": f"first {n_tr} trajectories ({Ts} tokens) of each rank's batch, "
-                                     f"{e2e_steps} timed calls", "loss": res["loss"]}
+                                     f"{e2e_steps} timed calls", "loss": res["loss"],
+                           "bound": (f"PCIe: host bf16 logits in and host dlogits out, {2 * V} B per token "
+                                     f"each way; the per-token cost does not depend on the sample size, "
+                                     f"so the sample's tok/s is the config's")}
         ws.close()
         del h_logits, h_dl
 

@@ -342,6 +342,7 @@ def test_lmhead_dweight_errors(ctx):
         ctx.lmhead_dweight(dl, x, out=torch.zeros((64, 66), device="cuda")[:, :64])
 
 
+@pytest.mark.parametrize("impl", ["pair"], indirect=True)  # the TMA-store epilogue is the pair kernel's
 @pytest.mark.parametrize("T,H,V", [(1, 64, 256), (130, 64, 300), (257, 192, 1000), (300, 520, 4099),
                                    (129, 64, 1064), (1024, 4096, 151936)])
 def test_lmhead_tma_store_epilogue_bitwise(ctx, T, H, V, impl, monkeypatch):
@@ -350,8 +351,6 @@ def test_lmhead_tma_store_epilogue_bitwise(ctx, T, H, V, impl, monkeypatch):
     register-store epilogue's (lmhead_tma_store = 0), ragged T included; at
     V % 8 != 0 the register-store epilogue runs (TMA would clip at 16-byte
     granularity and write the row padding)."""
-    if impl == "1sm":
-        pytest.skip("pair kernel only")
     x, w, tgt = _inputs(T, H, V, 23)
     ldv = (V + 7) // 8 * 8
     lg0 = torch.full((T, ldv), 3.0, dtype=torch.bfloat16, device="cuda")

@@ -268,7 +268,7 @@ def test_deterministic_and_chunk_invariant(ctx, oracle):
 
 
 def test_padded_rows(ctx, oracle):
-    for ld, kernel in ((32008, "fused_tma_kernel"), (32001, "fused_generic_kernel")):
+    for ld, kernel in ((32008, "fused_solo_kernel"), (32001, "fused_generic_kernel")):
         case = Case(oracle, seed=16, P=2, G=4, V=32000, ld=ld)
         _, res = run(ctx, case, F32)
         assert ctx.last_launch()["kernel"] == kernel
