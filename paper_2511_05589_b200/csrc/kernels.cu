@@ -1174,6 +1174,7 @@ const TuneField kFields[] = {
     {"resident", "COPRIS_TUNE_RESIDENT", 0, 1, &Tuning::resident, nullptr},
     {"pair_lookahead", "COPRIS_PAIR_LOOKAHEAD", 0, 7, &Tuning::pair_lookahead, nullptr},
     {"pair_st256", "COPRIS_PAIR_ST256", 0, 1, &Tuning::pair_st256, nullptr},
+    {"pair_bf16_stage", "COPRIS_PAIR_BF16_STAGE", 0, 1, &Tuning::pair_bf16_stage, nullptr},
     {"lmhead_impl", "COPRIS_LMHEAD_IMPL", 0, 1, &Tuning::lmhead_impl, nullptr},
     {"lmhead_group", "COPRIS_LMHEAD_GROUP", 1, 1 << 20, &Tuning::lmhead_group, nullptr},
     {"lmhead_tma_store", "COPRIS_LMHEAD_TMA_STORE", 0, 1, &Tuning::lmhead_tma_store, nullptr},

@@ -157,7 +157,7 @@ __device__ __forceinline__ void kill_col(uint32_t& w, int jt, int k, float& zy) 
 // STORE: stage the f16 exponentials in TMEM at taddr (16 columns). Returns
 // nml = 15 - m log2(e) of this thread's columns (+inf when it saw no finite
 // column) for pass 2.
-template <bool STORE, bool RAW>
+template <bool STORE, bool RAW, bool BST>
 __device__ __forceinline__ float p1_slot(LaneAcc& a, uint32_t sb, int32_t v0, int32_t cnt,
                                          int32_t ycol, int tid, uint32_t taddr) {
   uint4 raw[kPK];
@@ -215,7 +215,7 @@ __device__ __forceinline__ float p1_slot(LaneAcc& a, uint32_t sb, int32_t v0, in
       const uint64_t e = ptx::ex2x2(ptx::ffma2(ptx::bf16x2_to_f2(w[k]), l2e, nml2));
       if (k & 1) acc1 = ptx::fadd2(acc1, e);
       else acc0 = ptx::fadd2(acc0, e);
-      if (STORE && !RAW) h[q * 4 + k] = f2_to_f16x2(e);
+      if (STORE && !RAW) h[q * 4 + k] = BST ? ptx::f2_to_bf16x2(e) : f2_to_f16x2(e);
     }
   }
   if (STORE && !RAW) tmem_st_x16(taddr, h);
@@ -238,7 +238,7 @@ __device__ __forceinline__ float p1_slot(LaneAcc& a, uint32_t sb, int32_t v0, in
 // vectors with one 32-byte store (STG.256); the target column is patched into
 // its vector before the swap. Otherwise 16-byte stores and the target column
 // written by its owner afterwards (a later store of the same thread).
-template <bool W256>
+template <bool W256, bool BST>
 __device__ __forceinline__ void p2_slot(const RowBroadcast& b, bool zero_row, float nml,
                                         uint32_t taddr, int32_t v0, int32_t cnt, int32_t ycol,
                                         __nv_bfloat16* dseg, int tid) {
@@ -268,12 +268,21 @@ __device__ __forceinline__ void p2_slot(const RowBroadcast& b, bool zero_row, fl
   tmem_ld_x16(taddr, h);
   tc::tmem_wait_ld();
   uint4 v[kPK];
+  if (BST) {
+    // bf16 staging: one packed bf16 multiply per two columns (sc rounded to bf16)
+    const uint32_t sb = ptx::f2_to_bf16x2(sc2);
 #pragma unroll
-  for (int q = 0; q < kPK; ++q) {
-    uint32_t o[4];
+    for (int q = 0; q < kPK; ++q)
+      v[q] = uint4{ptx::bmul2(h[q * 4 + 0], sb), ptx::bmul2(h[q * 4 + 1], sb), ptx::bmul2(h[q * 4 + 2], sb),
+                   ptx::bmul2(h[q * 4 + 3], sb)};
+  } else {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) o[k] = ptx::f2_to_bf16x2(ptx::fmul2(f16x2_to_f2(h[q * 4 + k]), sc2));
-    v[q] = uint4{o[0], o[1], o[2], o[3]};
+    for (int q = 0; q < kPK; ++q) {
+      uint32_t o[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) o[k] = ptx::f2_to_bf16x2(ptx::fmul2(f16x2_to_f2(h[q * 4 + k]), sc2));
+      v[q] = uint4{o[0], o[1], o[2], o[3]};
+    }
   }
   if (W256) {
     // one-hot term coef (1 - p_y) (policy.hpp:193-194) into its vector first
@@ -359,7 +368,7 @@ __device__ __forceinline__ void p2_slot_f32(const RowBroadcast& b, bool zero_row
 // shared memory: nslots ring slots of 32 KB, then nml[kPTSlots][512] floats.
 // nvec0 = vectors of CTA rank 0 (rank 1 takes the rest); look = slots of row
 // r+1 run through pass 1 before pass 2 of row r.
-template <bool F32, int CL>
+template <bool F32, int CL, bool BST>
 __global__ void __launch_bounds__((kPW + 2) * 32, 1)
     fused_pair_kernel(const LossParams P, const int nslots, const int look, const int32_t nvec0,
                       const int st256) {
@@ -479,9 +488,9 @@ __global__ void __launch_bounds__((kPW + 2) * 32, 1)
         const int32_t cnt = min(kPSlotVec, nvec - v0);
         ptx::mbar_wait_sleep(fbase + slot * 8, ring.ph);
         const uint32_t tsl = (ts + static_cast<uint32_t>(sg)) % kPTSlots;
-        const float nml = grad ? p1_slot<true, F32>(a, sbase + slot * kPSlotBytes, v0, cnt, ycol, tid,
-                                                    taddr0 + tsl * 16)
-                               : p1_slot<false, F32>(a, sbase + slot * kPSlotBytes, v0, cnt, ycol, tid, 0u);
+        const float nml = grad ? p1_slot<true, F32, BST>(a, sbase + slot * kPSlotBytes, v0, cnt, ycol, tid,
+                                                         taddr0 + tsl * 16)
+                               : p1_slot<false, F32, BST>(a, sbase + slot * kPSlotBytes, v0, cnt, ycol, tid, 0u);
         nml_sh[tsl * kPThreads + tid] = nml;
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive_u32(ebase + slot * 8);
@@ -545,10 +554,10 @@ __global__ void __launch_bounds__((kPW + 2) * 32, 1)
             __nv_bfloat16* drow = static_cast<__nv_bfloat16*>(P.dlogits) + r * P.ld_d + col0;
             const int32_t cnt = min(kPSlotVec, nvec - v0);
             if (w256 && cnt == kPSlotVec)
-              p2_slot<true>(b, zero_row, nml_sh[tsl * kPThreads + tid], taddr0 + tsl * 16, v0, cnt,
+              p2_slot<true, BST>(b, zero_row, nml_sh[tsl * kPThreads + tid], taddr0 + tsl * 16, v0, cnt,
                             ycol, drow + static_cast<int64_t>(v0) * 8, tid);
             else
-              p2_slot<false>(b, zero_row, nml_sh[tsl * kPThreads + tid], taddr0 + tsl * 16, v0, cnt,
+              p2_slot<false, BST>(b, zero_row, nml_sh[tsl * kPThreads + tid], taddr0 + tsl * 16, v0, cnt,
                              ycol, drow + static_cast<int64_t>(v0) * 8, tid);
           }
         }
@@ -595,15 +604,17 @@ bool pair_supported(const LossParams& p, DType in, DType out, bool ent, int cl) 
 cudaError_t launch_pair(const LossParams& p, DType out, int cl, int num_sms, const Tuning& tu,
                         cudaStream_t stream, LaunchInfo* info) {
   const bool f32 = out == DType::F32 && p.dlogits != nullptr && !p.gather_only;
-  const void* kern =
-      cl == 2 ? (f32 ? reinterpret_cast<const void*>(fused_pair_kernel<true, 2>)
-                     : reinterpret_cast<const void*>(fused_pair_kernel<false, 2>))
-              : (f32 ? reinterpret_cast<const void*>(fused_pair_kernel<true, 1>)
-                     : reinterpret_cast<const void*>(fused_pair_kernel<false, 1>));
+  const bool bst = !f32 && tu.pair_bf16_stage;
+  using Kern = void (*)(const LossParams, const int, const int, const int32_t, const int);
+  const Kern kern =
+      cl == 2 ? (f32 ? fused_pair_kernel<true, 2, false>
+                     : (bst ? fused_pair_kernel<false, 2, true> : fused_pair_kernel<false, 2, false>))
+              : (f32 ? fused_pair_kernel<true, 1, false>
+                     : (bst ? fused_pair_kernel<false, 1, true> : fused_pair_kernel<false, 1, false>));
   // 6 x 32 KB ring + 16 KB of per-thread nml fill the 227 KB a CTA may use
   const int nslots = tu.slots > 0 ? (tu.slots > 6 ? 6 : tu.slots) : 6;
   const int smem = nslots * kPSlotBytes + kPTSlots * kPThreads * static_cast<int>(sizeof(float));
-  cudaError_t e = allow_dyn_smem(kern, smem);
+  cudaError_t e = allow_dyn_smem(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) return e;
   const int32_t nvec0 = cl == 2 ? (p.vocab / 8 + 1) / 2 : p.vocab / 8;
   const int32_t nseg = (nvec0 + kPSlotVec - 1) / kPSlotVec;
@@ -625,12 +636,13 @@ cudaError_t launch_pair(const LossParams& p, DType out, int cl, int num_sms, con
   if (cl == 2) {
     cfg.gridDim = dim3(static_cast<unsigned>(num_sms & ~1));
     int ncl = 0;
-    e = cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg);
+    e = cudaOccupancyMaxActiveClusters(&ncl, reinterpret_cast<const void*>(kern), &cfg);
     if (e != cudaSuccess) return e;
     slots = ncl;
   } else {
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (kPW + 2) * 32, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(kern),
+                                                      (kPW + 2) * 32, smem);
     if (e != cudaSuccess) return e;
     slots = static_cast<int64_t>(per_sm) * num_sms;
   }
@@ -647,11 +659,7 @@ cudaError_t launch_pair(const LossParams& p, DType out, int cl, int num_sms, con
     info->kernel = cl == 2 ? "fused_pair_kernel" : "fused_solo_kernel";
     info->reduced = fuse ? 1 : 0;
   }
-  if (cl == 2)
-    return f32 ? cudaLaunchKernelEx(&cfg, fused_pair_kernel<true, 2>, q, nslots, look, nvec0, tu.pair_st256)
-               : cudaLaunchKernelEx(&cfg, fused_pair_kernel<false, 2>, q, nslots, look, nvec0, tu.pair_st256);
-  return f32 ? cudaLaunchKernelEx(&cfg, fused_pair_kernel<true, 1>, q, nslots, look, nvec0, tu.pair_st256)
-             : cudaLaunchKernelEx(&cfg, fused_pair_kernel<false, 1>, q, nslots, look, nvec0, tu.pair_st256);
+  return cudaLaunchKernelEx(&cfg, kern, q, nslots, look, nvec0, tu.pair_st256);
 }
 
 }  // namespace copris_b200

@@ -374,6 +374,13 @@ __device__ __forceinline__ uint32_t f2_to_bf16x2(uint64_t a) {
   return r;
 }
 
+// packed bf16 multiply (HMUL2.BF16): both halves of a by the halves of b
+__device__ __forceinline__ uint32_t bmul2(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+
 // bf16 word -> (lo, hi) fp32 pair
 __device__ __forceinline__ uint64_t bf16x2_to_f2(uint32_t w) {
   return f2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));

@@ -30,6 +30,9 @@ SHAPES = [
     (151936, BF16, "pair+pl0", (PAIR, PAIR), None),   # no lookahead: pass 2 right after the row
     (151936, BF16, "pair+pl1", (PAIR, PAIR), None),
     (151936, BF16, "pair+st1", (PAIR, PAIR), None),  # 32-byte stores in pass 2 (lane-pair swap)
+    (151936, BF16, "pair+bst0", (PAIR, PAIR), None),  # f16 exponentials in TMEM (round-2 first version)
+    (151936, BF16, "pair+bst0+st1", (PAIR, PAIR), None),
+    (32000, BF16, "solo+bst0", "fused_solo_kernel", 1),
     (200000, BF16, "pair+st1", (PAIR, PAIR), None),
     (151936, BF16, "pair+pl3+slots3", (PAIR, PAIR), None),  # short ring: producer waits on slots
     (200000, BF16, None, (PAIR, PAIR), None),
@@ -62,7 +65,8 @@ SHAPES = [
 ]
 
 # the context options every test starts from (copris_ctx_set_option)
-DEFAULT_OPTS = dict(fused_impl=0, lookahead=2, resident=1, slots=0, pair_lookahead=3, pair_st256=0)
+DEFAULT_OPTS = dict(fused_impl=0, lookahead=2, resident=1, slots=0, pair_lookahead=3, pair_st256=0,
+                    pair_bf16_stage=1)
 
 
 @pytest.fixture
@@ -84,6 +88,8 @@ def impl(ctx):
                     opts["slots"] = int(o[5:])
                 elif o.startswith("st"):
                     opts["pair_st256"] = int(o[2:])
+                elif o.startswith("bst"):
+                    opts["pair_bf16_stage"] = int(o[3:])
         if name:
             opts["fused_impl"] = name
         for k, v in opts.items():
