@@ -431,7 +431,7 @@ def run_ours(args):
                 "offpolicy_fraction": out4[2].item() / out4[1].item() if out4[1].item() else 0.0,
                 "clipped_tokens": int(out4[3].item()),
                 "dlogits": ("f32 (parity mode: within 1e-5; 6V+16 B/token)" if args.dlogits == "f32"
-                            else "bf16 (within 1 bf16 ulp; 4V+16 B/token)"),
+                            else "bf16 (within 2^-7 relative; 4V+16 B/token)"),
             },
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_source": peak_src,

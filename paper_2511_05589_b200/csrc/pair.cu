@@ -12,14 +12,17 @@
 // Pass 1, per thread and slot (32 columns): m = max of the thread's columns
 // (packed bf16 max, target column excluded), then for each column
 // e = 2^((z - m) log2(e) + 15) on MUFU — summed in fp32 for the log-sum-exp
-// (the sum never sees the rounding below) and stored as f16 in TENSOR MEMORY
-// (tcgen05.st, 16 columns of 32-bit per thread and slot; 2^15 keeps e in
-// f16's normal range down to 2^-29 of the thread's slot maximum), with
+// (the sum never sees the rounding below) and stored as bf16 in TENSOR MEMORY
+// (tcgen05.st, 16 columns of 32-bit per thread and slot), with
 // nml = 15 - m log2(e) kept in shared memory. Pass 2, after the scalar phase:
-// d = e * sign(-coef) 2^(-nml - c2) (one MUFU per thread and slot, none per
-// element): tcgen05.ld, f16 -> f32, packed multiply, bf16 store. The f16
-// staging adds <= 2^-12 relative before the final bf16 rounding, so dlogits
-// stay within one bf16 ulp of the exact value.
+// d = e * sign(-coef) 2^(-nml - c2) with the scale rounded to bf16 once per
+// thread and slot (one MUFU per thread and slot, none per element):
+// tcgen05.ld, then ONE packed bf16x2 multiply per two columns, stored as is.
+// Three bf16 roundings (e, scale, product) bound the error by 3 * 2^-9 <
+// 2^-7 relative, the bf16-dlogits tolerance. (pair_bf16_stage = 0: f16
+// exponentials — the 2^15 offset keeps them in f16's normal range down to
+// 2^-29 of the slot maximum — and an f32 multiply, <= 2^-12 before the final
+// bf16 rounding; 3.4% slower on one box, more instructions per column.)
 //
 // f32 dlogits (the parity mode, within 1e-5): f16 staging would cost 2^-12, so
 // pass 1 stages the RAW bf16 logits in TMEM instead (same 16 bits per column,
