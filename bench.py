@@ -53,6 +53,9 @@ def parse_args():
     ap.add_argument("--cpu-tokens-per-thread", type=int, default=256)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--graph-steps", type=int, default=1,
+                    help="with --graph: steps captured back to back in one graph (a training loop's "
+                         "consecutive small steps; N=1 only); --steps must be a multiple")
     ap.add_argument("--graph", action="store_true",
                     help="capture one step (all chunk launches + the reduction) in a CUDA graph "
                          "and replay it; the allreduce stays outside the graph")
@@ -337,6 +340,10 @@ def run_ours(args):
 
     graph = None
 
+    gsteps = max(1, args.graph_steps) if args.graph else 1
+    if gsteps > 1 and (world > 1 or args.steps % gsteps):
+        raise SystemExit("bench.py: --graph-steps needs N=1 and --steps a multiple of it")
+
     def step(evs=None):
         torch.cuda.nvtx.range_push("copris step")
         if graph is not None:
@@ -361,7 +368,8 @@ def run_ours(args):
             launches()
         torch.cuda.current_stream().wait_stream(side)
         with torch.cuda.graph(graph):
-            launches()
+            for _ in range(gsteps):  # whole steps back to back (each ends with its reduction)
+                launches()
         for _ in range(max(args.warmup, 1)):
             step()
         ctx.check()
@@ -381,7 +389,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for k in range(args.steps):
+    for k in range(args.steps // gsteps):
         step(evs[k])
     e1.record()
     torch.cuda.synchronize()
@@ -423,7 +431,8 @@ def run_ours(args):
                 "tokens_rank0": T, "chunk_rows": chunk, "chunks_per_step": nchunks,
                 "parallelism": f"dp{world} (whole prompt groups, LPT by tokens)",
                 "path": ("unfused K1->K2->K3" if args.unfused else "fused single pass")
-                        + (" (CUDA graph replay)" if graph is not None else ""),
+                        + ((" (CUDA graph replay" + (f", {gsteps} steps per graph)" if gsteps > 1 else ")"))
+                           if graph is not None else ""),
                 "kernel": info, "l2": (f"inputs larger than L2: each step streams {T * V * 2 / 1e6:.0f} MB "
                                        f"of logits and writes as much dlogits (chunk buffer "
                                        f"{chunk * V * 2 / 1e6:.0f} MB; L2 126 MB); no flush"),
