@@ -112,7 +112,11 @@ COPRIS_API int copris_logprob_gather(copris_ctx* ctx, const void* logits, int64_
  * copris_lse_merge then yields exactly what copris_logprob_gather computes
  * from the stored logits — (cur_lp, lse) — reading only the partials and the
  * target logit; the loss continues with copris_behaviour_concat +
- * copris_is_loss_bwd (one streaming pass). */
+ * copris_is_loss_bwd (one streaming pass). partials == NULL (target may then
+ * be NULL): logits only, no statistics — for a step whose loss runs the
+ * one-pass fused kernel (copris_is_loss_fused) on the logits; needs the
+ * default CTA-pair kernel with TMA stores (vocab % 8 == 0), else
+ * COPRIS_E_INVALID. */
 COPRIS_API int32_t copris_lmhead_num_vtiles(int32_t vocab);
 COPRIS_API int copris_lmhead_logits(copris_ctx* ctx, const void* hidden, int64_t ld_hidden,
                                     const void* weight, int64_t ld_weight, int64_t n_rows,

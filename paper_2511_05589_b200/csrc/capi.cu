@@ -227,7 +227,7 @@ int copris_lmhead_logits(copris_ctx* ctx, const void* hidden, int64_t ld_hidden,
   if (!ctx) return fail(COPRIS_E_INVALID, "null ctx");
   if (n_rows < 0) return fail(COPRIS_E_INVALID, "negative n_rows");
   if (n_rows == 0) return COPRIS_OK;
-  if (!hidden || !weight || !target || !logits || !partials)
+  if (!hidden || !weight || !logits || (partials && !target))
     return fail(COPRIS_E_INVALID, "null pointer");
   if (vocab < 1 || hidden_dim < 1) return fail(COPRIS_E_INVALID, "bad vocab/hidden_dim");
   if (ld_hidden < hidden_dim || ld_weight < hidden_dim || ld_hidden % 8 || ld_weight % 8)
@@ -241,6 +241,8 @@ int copris_lmhead_logits(copris_ctx* ctx, const void* hidden, int64_t ld_hidden,
   cudaError_t e = launch_lmhead_fwd(hidden, ld_hidden, weight, ld_weight, n_rows, hidden_dim, vocab,
                                     target, logits, ld_logits, partials, ctx->num_sms,
                                     ctx->tuning, as_stream(stream), &ctx->last);
+  if (e == cudaErrorInvalidValue && !partials)
+    return fail(COPRIS_E_INVALID, "logits-only mode needs the CTA-pair kernel with TMA stores (vocab % 8 == 0)");
   return e == cudaSuccess ? COPRIS_OK : cuda_fail(e, "lmhead_logits launch");
 }
 

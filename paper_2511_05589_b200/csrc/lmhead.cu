@@ -136,7 +136,7 @@ __device__ __forceinline__ float2 epilogue_row(uint32_t taddr, int64_t row, bool
 __device__ __forceinline__ float2 epilogue_row_tma(uint32_t taddr, int32_t row0, int32_t n0,
                                                    int32_t ncols, int32_t yrel,
                                                    const CUtensorMap* tm_l, uint32_t box0,
-                                                   int& buf, uint64_t st_pol) {
+                                                   int& buf, uint64_t st_pol, bool stats) {
   const int lane = threadIdx.x & 31;
   float m = -INFINITY, s = 0.f;
 #pragma unroll 1
@@ -158,7 +158,7 @@ __device__ __forceinline__ float2 epilogue_row_tma(uint32_t taddr, int32_t row0,
         z[j] = bf16_round(__uint_as_float(r[j]));
         if (cc + j < ncols) cm = fmaxf(cm, z[j]);
       }
-      if (cc < ncols) {
+      if (stats && cc < ncols) {  // logits-only mode: no statistics, no exponentials
         if (cm > m) {
           s *= ptx::ex2((m - cm) * kLog2e);
           m = cm;
@@ -654,15 +654,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive_remote(ptx::mapa(tempty_bar(acc), lrank));
       } else if constexpr (EPI == 3) {
-        const int32_t yrel = row_ok ? P.target[row] - n0 : -1;
+        const bool stats = P.partials != nullptr;  // nullptr: logits only (uniform)
+        const int32_t yrel = row_ok && stats ? P.target[row] - n0 : -1;
         const int32_t row0 = static_cast<int32_t>(mp * 256 + 128 * prank + sub * 32);
         const float2 part = epilogue_row_tma(taddr, row0, n0, ncols, yrel, &tm_c,
                                              stg + static_cast<uint32_t>(sub) * 8192u, dw_buf,
-                                             st_pol);
+                                             st_pol, stats);
         tc::fence_before_sync();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive_remote(ptx::mapa(tempty_bar(acc), lrank));
-        if (row_ok) P.partials[row * P.n_vt + vt] = part;
+        if (row_ok && stats) P.partials[row * P.n_vt + vt] = part;
       } else {
       const int32_t yrel = row_ok ? P.target[row] - n0 : -1;
       const float2 part = epilogue_row(taddr, row, row_ok, n0, ncols, yrel, P, st_pol);
@@ -847,6 +848,10 @@ cudaError_t launch_lmhead_fwd(const void* hidden, int64_t ld_h, const void* weig
   p.partials = reinterpret_cast<float2*>(partials);
   p.target = target;
   p.group = std::max(1, tu.lmhead_group);
+  // logits only (no partials): the CTA-pair kernel's TMA-store epilogue skips the
+  // statistics; the other epilogues always produce them
+  if (!partials && (tu.lmhead_impl == 1 || tu.lmhead_tma_store == 0 || V % 8 != 0))
+    return cudaErrorInvalidValue;
   if (tu.lmhead_impl == 1) {
     cudaError_t ea = allow_dyn_smem(reinterpret_cast<const void*>(lmhead_fwd_kernel), static_cast<int>(kSmemBytes));
     if (ea != cudaSuccess) return ea;

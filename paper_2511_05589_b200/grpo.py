@@ -232,11 +232,12 @@ class Copris:
 
     # -- LM-head forward + log-softmax partials (tcgen05) ---------------------------
     @_on_stream
-    def lmhead_logits(self, hidden: torch.Tensor, weight: torch.Tensor, target: torch.Tensor,
+    def lmhead_logits(self, hidden: torch.Tensor, weight: torch.Tensor, target: Optional[torch.Tensor],
                       logits: Optional[torch.Tensor] = None,
-                      partials: Optional[torch.Tensor] = None, stream=None):
+                      partials: Optional[torch.Tensor] = None, stream=None, stats: bool = True):
         """logits = bf16(hidden @ weight^T) and per-256-column LSE partials
-        (float2 per (token, tile), target column excluded)."""
+        (float2 per (token, tile), target column excluded); ``stats=False``:
+        logits only (no partials, ``target`` unused)."""
         n, h = hidden.shape
         v = weight.shape[0]
         if hidden.dtype != torch.bfloat16 or weight.dtype != torch.bfloat16:
@@ -245,11 +246,14 @@ class Copris:
         if logits is None:
             ld = (v + 7) // 8 * 8
             logits = torch.empty((n, ld), dtype=torch.bfloat16, device=hidden.device)[:, :v]
-        if partials is None:
+        if stats and partials is None:
             partials = torch.empty((n, nvt, 2), dtype=torch.float32, device=hidden.device)
+        if not stats:
+            partials = None
         self._call(self.lib.copris_lmhead_logits(
             self.h, _p(hidden), hidden.stride(0), _p(weight), weight.stride(0), n, h, v,
-            _p(target), _p(logits), logits.stride(0), _p(partials), self._stream(stream)))
+            _p(target) if stats else None, _p(logits), logits.stride(0),
+            _p(partials) if stats else None, self._stream(stream)))
         return logits, partials
 
     @_on_stream

@@ -6,16 +6,17 @@ module runs the loss path of grpo.hpp:117-185 with that producer in front and
 its backward behind, chunked over tokens so the [T x V] logits exist only one
 chunk at a time:
 
-  per chunk of rows
-    copris_lmhead_logits   tcgen05 GEMM -> bf16 logits + LSE partials   (fwd, fused)
-    copris_lse_merge       (cur_lp, lse) from partials                   (replaces K1's read)
-    copris_behaviour_concat                                             (K2)
-    copris_is_loss_bwd     objective/coef + dlogits IN PLACE over logits (one pass)
-    dhidden = dlogits @ W  and  dW += dlogits^T @ hidden                 (cuBLAS: plain GEMMs)
+  per chunk of rows (default: loss_impl="fused", fwd_impl="cublas")
+    logits = hidden @ W^T  (plain GEMM; or copris_lmhead_logits, tcgen05, logits only)
+    copris_is_loss_fused   the one-pass loss: cur_lp, behaviour, objective,
+                           dlogits IN PLACE over the logits (CTA-pair kernel)
+    dhidden = dlogits @ W  and  dW += dlogits^T @ hidden   (plain GEMMs, or tcgen05)
   copris_loss_reduce -> loss, counts
+  loss_impl="lse" instead: copris_lmhead_logits (tcgen05, logits + LSE partials in
+  the epilogue) -> copris_lse_merge -> copris_behaviour_concat -> copris_is_loss_bwd.
 
-Every step is a kernel in libcopris_b200.so except the two backward GEMMs,
-which are plain library GEMMs.
+The loss is a kernel in libcopris_b200.so; the GEMMs are plain library GEMMs by
+default, or this library's tcgen05 kernels (DESIGN.md §3b for the measurements).
 """
 from __future__ import annotations
 
@@ -60,7 +61,8 @@ def _lmhead_grpo_step_loss(ctx: Copris, hidden: torch.Tensor, weight: torch.Tens
                           total_tokens: Optional[int] = None, want_grad: bool = True,
                           dweight: Optional[torch.Tensor] = None, coef: bool = False,
                           dhidden_impl: str = "cublas", weight_t: Optional[torch.Tensor] = None,
-                          dweight_impl: str = "cublas", stream=None) -> LmHeadStepResult:
+                          dweight_impl: str = "cublas", loss_impl: str = "fused",
+                          fwd_impl: str = "cublas", stream=None) -> LmHeadStepResult:
     """grpo.hpp:117-185 with logits = hidden @ weight^T (bf16 in, fp32 accumulate).
 
     ``dweight`` (fp32 [V x H]) is accumulated into when given (zeros otherwise).
@@ -72,6 +74,17 @@ def _lmhead_grpo_step_loss(ctx: Copris, hidden: torch.Tensor, weight: torch.Tens
     within a few percent of cuBLAS (dhidden faster at 8K-token chunks); inside
     this power-capped step the cuBLAS GEMMs measured faster, so they are the
     default.
+
+    ``loss_impl``: "fused" (default) — the forward stores the logits only and
+    the one-pass fused loss kernel (copris_is_loss_fused: the CTA-pair kernel,
+    one exponential per element) writes dlogits in place; "lse" — the tcgen05
+    forward's epilogue emits the softmax statistics, then lse_merge -> K2 -> K3
+    (one streaming pass that recomputes the exponentials).
+    ``fwd_impl``: "cublas" (default) — the forward is a plain library GEMM;
+    "tcgen05" — copris_lmhead_logits (the CTA-pair tcgen05 kernel). Defaults
+    are the fastest measured combination in a sustained, power-capped step
+    (cuBLAS GEMMs around the one-pass loss kernel; the tcgen05
+    kernels run 2-10% slower there, at lower clocks for the same power).
     """
     cfg = cfg or ClipConfig()
     cfg.validate()
@@ -94,7 +107,7 @@ def _lmhead_grpo_step_loss(ctx: Copris, hidden: torch.Tensor, weight: torch.Tens
     ldv = (V + 7) // 8 * 8
     buf = torch.empty((chunk, ldv), dtype=torch.bfloat16, device=dev)[:, :V]
     nvt = int(ctx.lib.copris_lmhead_num_vtiles(V))
-    part = torch.empty((chunk, nvt, 2), dtype=torch.float32, device=dev)
+    part = torch.empty((chunk, nvt, 2), dtype=torch.float32, device=dev) if loss_impl == "lse" else None
     outs = ctx.alloc_outputs(T, dev, coef=coef)
     dhidden = torch.empty_like(hidden) if want_grad else None
     if want_grad and dweight is None:
@@ -106,21 +119,38 @@ def _lmhead_grpo_step_loss(ctx: Copris, hidden: torch.Tensor, weight: torch.Tens
         raise ValueError("dhidden_impl must be 'cublas' or 'tcgen05'")
     if dweight_impl not in ("cublas", "tcgen05"):
         raise ValueError("dweight_impl must be 'cublas' or 'tcgen05'")
+    if loss_impl not in ("lse", "fused"):
+        raise ValueError("loss_impl must be 'lse' or 'fused'")
+    if fwd_impl not in ("cublas", "tcgen05"):
+        raise ValueError("fwd_impl must be 'cublas' or 'tcgen05'")
+    if loss_impl == "lse" and fwd_impl != "tcgen05":
+        raise ValueError("loss_impl='lse' needs the statistics of fwd_impl='tcgen05'")
     for a in range(0, T, chunk):
         n = min(chunk, T - a)
         sl = slice(a, a + n)
         lg = buf[:n]
-        ctx.lmhead_logits(hidden[sl], weight, batch.target[sl], logits=lg, partials=part[:n],
-                          stream=stream)
-        ctx.lse_merge(part[:n], lg, batch.target[sl], out_lp=outs["cur_lp"][sl],
-                      out_lse=outs["lse"][sl], stream=stream)
-        ctx._call(ctx.lib.copris_behaviour_concat(
-            ctx.h, _p(batch.stage[sl]), batch.cur_stage, _p(batch.buffered_lp[sl]),
-            _p(outs["cur_lp"][sl]), int(is_enabled), behav_mode, n, _p(outs["behav"][sl]), None, s))
-        b, c, o = ctx._structs(lg, batch, cfg, is_enabled, behav_mode, T_glob, a,
-                               lg if want_grad else None, outs)
-        ctx._call(ctx.lib.copris_is_loss_bwd(ctx.h, C.byref(b), C.byref(c), _p(outs["cur_lp"]),
-                                             _p(outs["lse"]), _p(outs["behav"]), C.byref(o), s))
+        if loss_impl == "fused":
+            if fwd_impl == "tcgen05":
+                ctx.lmhead_logits(hidden[sl], weight, None, logits=lg, stats=False, stream=stream)
+            else:
+                with torch.cuda.stream(stream) if stream is not None else _null():
+                    torch.mm(hidden[sl], weight.t(), out=lg)
+            ctx.loss_chunk_fused(lg, batch, cfg, outs, dlogits=lg if want_grad else None, row_base=a,
+                                 total_tokens=T_glob, is_enabled=is_enabled, behav_mode=behav_mode,
+                                 stream=stream)
+        else:
+            ctx.lmhead_logits(hidden[sl], weight, batch.target[sl], logits=lg, partials=part[:n],
+                              stream=stream)
+            ctx.lse_merge(part[:n], lg, batch.target[sl], out_lp=outs["cur_lp"][sl],
+                          out_lse=outs["lse"][sl], stream=stream)
+            ctx._call(ctx.lib.copris_behaviour_concat(
+                ctx.h, _p(batch.stage[sl]), batch.cur_stage, _p(batch.buffered_lp[sl]),
+                _p(outs["cur_lp"][sl]), int(is_enabled), behav_mode, n, _p(outs["behav"][sl]), None,
+                s))
+            b, c, o = ctx._structs(lg, batch, cfg, is_enabled, behav_mode, T_glob, a,
+                                   lg if want_grad else None, outs)
+            ctx._call(ctx.lib.copris_is_loss_bwd(ctx.h, C.byref(b), C.byref(c), _p(outs["cur_lp"]),
+                                                 _p(outs["lse"]), _p(outs["behav"]), C.byref(o), s))
         if want_grad:
             # dlogits now sits in `lg`: the LM-head backward (plain GEMMs)
             if dhidden_impl == "tcgen05":

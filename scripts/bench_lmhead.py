@@ -1,5 +1,10 @@
 """LM-head forward (tcgen05 + fused LSE partials) vs cuBLAS, and the chunked
-LM-head IS-loss step vs the composition cuBLAS GEMM -> fused loss -> cuBLAS."""
+LM-head IS-loss step in its variants: step_default (cuBLAS forward -> one-pass
+fused loss in place -> cuBLAS backward), step_fused_loss (the same with the
+tcgen05 forward, logits only), step_lse (tcgen05 forward with LSE partials ->
+merge -> K2 -> K3), step_tcgen05_* (backward GEMMs on the tcgen05 kernels);
+composed = the default written out by hand. Every timing is a loop of >= 1.5 s
+with its own nvidia-smi clock record (sustained, at the power cap)."""
 import json
 import sys
 
@@ -13,7 +18,12 @@ from paper_2511_05589_b200.lmhead import lmhead_grpo_step_loss
 from paper_2511_05589_b200.packing import upload
 
 
-def timeit(fn, iters=10, warm=3):
+CLOCKS = {}
+
+
+def timeit(fn, iters=10, warm=3, name=None, seconds=1.5):
+    """Mean ms per call over a timed loop of at least `seconds` (so the clock
+    sampler sees it under load); nvidia-smi clocks of the loop in CLOCKS[name]."""
     for _ in range(warm):
         fn()
     torch.cuda.synchronize()
@@ -23,7 +33,17 @@ def timeit(fn, iters=10, warm=3):
         fn()
     e.record()
     torch.cuda.synchronize()
-    return s.elapsed_time(e) / iters
+    ms = s.elapsed_time(e) / iters
+    reps = max(iters, int(seconds * 1e3 / max(ms, 1e-3)))
+    sampler = ClockSampler(None)
+    sampler.start()
+    s.record()
+    for _ in range(reps):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    CLOCKS[name or getattr(fn, "__name__", "?")] = sampler.stop()
+    return s.elapsed_time(e) / reps
 
 
 def peaks():
@@ -50,8 +70,8 @@ def main():
     buf = torch.empty((T, ldv), dtype=torch.bfloat16, device="cuda")[:, :V]
     part = torch.empty((T, ctx.lib.copris_lmhead_num_vtiles(V), 2), dtype=torch.float32, device="cuda")
     flops = 2.0 * T * H * V
-    t_ours = timeit(lambda: ctx.lmhead_logits(x, w, tgt, logits=buf, partials=part))
-    t_cublas = timeit(lambda: torch.mm(x, w.t(), out=buf))
+    t_ours = timeit(lambda: ctx.lmhead_logits(x, w, tgt, logits=buf, partials=part), name="lmhead_fwd")
+    t_cublas = timeit(lambda: torch.mm(x, w.t(), out=buf), name="cublas_fwd")
     out = {"T": T, "H": H, "V": V,
            "lmhead_fwd_ms": t_ours, "lmhead_fwd_tflops": flops / t_ours / 1e9,
            "cublas_fwd_ms": t_cublas, "cublas_fwd_tflops": flops / t_cublas / 1e9}
@@ -66,14 +86,24 @@ def main():
     dW = torch.zeros((V, H), dtype=torch.float32, device="cuda")
     chunk = int(sys.argv[4]) if len(sys.argv) > 4 else 8192
     t_step = timeit(lambda: lmhead_grpo_step_loss(ctx, x, w, batch, ClipConfig(), chunk_rows=chunk,
-                                                  dweight=dW), iters=3, warm=1)
+                                                  dweight=dW, loss_impl="lse", fwd_impl="tcgen05"),
+                    iters=3, warm=1, name="step_lse")
     wt = w.t().contiguous()
     t_step_tc = timeit(lambda: lmhead_grpo_step_loss(ctx, x, w, batch, ClipConfig(), chunk_rows=chunk,
                                                      dweight=dW, dhidden_impl="tcgen05", weight_t=wt,
-                                                     dweight_impl="tcgen05"), iters=3, warm=1)
+                                                     dweight_impl="tcgen05", fwd_impl="tcgen05"),
+                       iters=3, warm=1,
+                       name="step_tcgen05_bwd")
     t_step_dh = timeit(lambda: lmhead_grpo_step_loss(ctx, x, w, batch, ClipConfig(), chunk_rows=chunk,
-                                                     dweight=dW, dhidden_impl="tcgen05", weight_t=wt),
-                       iters=3, warm=1)
+                                                     dweight=dW, dhidden_impl="tcgen05", weight_t=wt,
+                                                     fwd_impl="tcgen05"),
+                       iters=3, warm=1, name="step_tcgen05_dhidden")
+    t_step_fused = timeit(lambda: lmhead_grpo_step_loss(ctx, x, w, batch, ClipConfig(), chunk_rows=chunk,
+                                                        dweight=dW, loss_impl="fused", fwd_impl="tcgen05"),
+                          iters=3, warm=1, name="step_fused_loss")
+    t_step_default = timeit(lambda: lmhead_grpo_step_loss(ctx, x, w, batch, ClipConfig(), chunk_rows=chunk,
+                                                          dweight=dW),
+                            iters=3, warm=1, name="step_default")
     dh = torch.empty_like(x)
     outs = ctx.alloc_outputs(T, x.device)
     out4 = torch.empty(4, dtype=torch.float64, device="cuda")
@@ -90,16 +120,16 @@ def main():
         ctx.check()
         return out4.cpu()
 
-    t_comp = timeit(composed, iters=3, warm=1)
+    t_comp = timeit(composed, iters=3, warm=1, name="composed_step")
     burst, sustained, src = peaks()
-    step_tf = 6 * T * H * V / t_step / 1e9
-    out.update({"step_ms": t_step, "step_tcgen05_bwd_ms": t_step_tc, "step_tcgen05_dhidden_ms": t_step_dh,
+    step_tf = 6 * T * H * V / t_step_default / 1e9  # the default step (cuBLAS GEMMs + one-pass loss)
+    out.update({"step_lse_ms": t_step, "step_fused_loss_ms": t_step_fused, "step_default_ms": t_step_default, "step_tcgen05_bwd_ms": t_step_tc, "step_tcgen05_dhidden_ms": t_step_dh,
                 "composed_step_ms": t_comp, "chunk": chunk, "step_tflops": step_tf,
                 "step_frac_of_sustained_bf16": step_tf / sustained,
                 "fwd_frac_of_burst_bf16": out["lmhead_fwd_tflops"] / burst,
                 "cublas_fwd_frac_of_burst_bf16": out["cublas_fwd_tflops"] / burst,
                 "peaks": {"bf16_tflops": burst, "bf16_tflops_sustained": sustained, "source": src},
-                "clocks": sampler.stop()})
+                "clocks_per_measurement": CLOCKS, "clocks_whole_script": sampler.stop()})
     print(json.dumps(out))
 
 

@@ -83,8 +83,25 @@ def test_lmhead_saturated_rows(ctx):
 
 
 @pytest.mark.parametrize("chunk", [4096, 100])
-@pytest.mark.parametrize("dhidden_impl,dweight_impl", [("cublas", "cublas"), ("tcgen05", "tcgen05")])
-def test_lmhead_loss_path_against_oracle(ctx, oracle, chunk, dhidden_impl, dweight_impl):
+@pytest.mark.parametrize("dhidden_impl,dweight_impl,loss_impl,fwd_impl", [
+    ("cublas", "cublas", "lse", "tcgen05"), ("tcgen05", "tcgen05", "lse", "tcgen05"),
+    ("cublas", "cublas", "fused", "tcgen05"), ("tcgen05", "tcgen05", "fused", "tcgen05"),
+    ("cublas", "cublas", "fused", "cublas"), ("tcgen05", "tcgen05", "fused", "cublas")])
+def test_lmhead_loss_path_against_oracle(ctx, oracle, chunk, dhidden_impl, dweight_impl, loss_impl,
+                                         fwd_impl, impl):
+    """The LM-head step against the oracle on the logits the step computed.
+    loss_impl "fused": the forward stores logits only and the one-pass fused
+    loss kernel runs on them (the CTA-pair tcgen05 forward's TMA-store epilogue
+    has the logits-only mode; the 1-SM forward runs the "lse" path only);
+    fwd_impl "cublas": a plain library GEMM forward (the step's default)."""
+    if loss_impl == "fused" and fwd_impl == "tcgen05" and impl == "1sm":
+        with pytest.raises(Exception, match="logits-only"):
+            _lmhead_oracle_case(ctx, oracle, chunk, dhidden_impl, dweight_impl, loss_impl, fwd_impl)
+        return
+    _lmhead_oracle_case(ctx, oracle, chunk, dhidden_impl, dweight_impl, loss_impl, fwd_impl)
+
+
+def _lmhead_oracle_case(ctx, oracle, chunk, dhidden_impl, dweight_impl, loss_impl, fwd_impl):
     from paper_2511_05589_b200 import ClipConfig
     from paper_2511_05589_b200.lmhead import lmhead_grpo_step_loss
     from paper_2511_05589_b200.packing import upload
@@ -102,14 +119,19 @@ def test_lmhead_loss_path_against_oracle(ctx, oracle, chunk, dhidden_impl, dweig
         a, b = tok_off[i], tok_off[i + 1]
         stage[a:a + (b - a) // 2] = 1 if i % 2 else 2
         stage[a + (b - a) // 2:b] = 2
-    lg_full, _ = ctx.lmhead_logits(x, w, tgt)
+    if fwd_impl == "cublas":
+        # the step's own chunking, so the library GEMM picks the same kernels
+        lg_full = torch.cat([torch.mm(x[a:a + chunk], w.t()) for a in range(0, T, chunk)])
+    else:
+        lg_full, _ = ctx.lmhead_logits(x, w, tgt)
     cur, _ = ctx.sequence_logprobs(lg_full, tgt)
     blp = stale_logprobs(cur.cpu().numpy(), stage, 2, 7)
     reward = (rng.random(n_traj) < 0.5).astype(np.float64)
     group_off = np.arange(0, n_traj + 1, G, dtype=np.int64)
     batch = upload(ctx, tok_off, group_off, target, blp, 2, stage=stage, reward=reward)
     res = lmhead_grpo_step_loss(ctx, x, w, batch, ClipConfig(), chunk_rows=chunk, coef=True,
-                                dhidden_impl=dhidden_impl, dweight_impl=dweight_impl)
+                                dhidden_impl=dhidden_impl, dweight_impl=dweight_impl,
+                                loss_impl=loss_impl, fwd_impl=fwd_impl)
     z = lg_full.double().cpu().numpy()
     adv = batch.adv.cpu().numpy()
     ref = oracle.is_loss(z, tok_off, target, stage, 2, blp.astype(np.float64), adv)
@@ -146,7 +168,8 @@ def test_lmhead_matches_logits_path(ctx):
     blp = stale_logprobs(cur.cpu().numpy(), stage, 2, 3)
     reward = (np.arange(16) % 3 == 0).astype(np.float64)
     batch = upload(ctx, tok_off, group_off, tgt.cpu().numpy(), blp, 2, stage=stage, reward=reward)
-    a = lmhead_grpo_step_loss(ctx, x, w, batch, ClipConfig(), chunk_rows=777)
+    a = lmhead_grpo_step_loss(ctx, x, w, batch, ClipConfig(), chunk_rows=777, loss_impl="lse",
+                              fwd_impl="tcgen05")
     b = ctx.grpo_step_loss(lg.contiguous(), batch, ClipConfig())
     assert a.stale_tokens == b.stale_tokens and a.clipped_tokens == b.clipped_tokens
     assert abs(a.loss - b.loss) <= 1e-6 * max(1e-12, float(b.obj.abs().sum()) / T)
@@ -176,7 +199,8 @@ def test_lmhead_loss_mask_equals_deletion(ctx, oracle):
     batch = upload(ctx, tok_off, group_off, tgt.cpu().numpy(), blp, 2, stage=stage, reward=reward)
     keep = np.random.default_rng(3).random(T) > 0.35
     batch.loss_mask = torch.from_numpy(keep.astype(np.uint8)).cuda()
-    res = lmhead_grpo_step_loss(ctx, x, w, batch, ClipConfig(), chunk_rows=250)
+    res = lmhead_grpo_step_loss(ctx, x, w, batch, ClipConfig(), chunk_rows=250, loss_impl="lse",
+                                fwd_impl="tcgen05")
     csum = np.concatenate([[0], np.cumsum(keep)])
     adv = oracle.advantages(reward, group_off)
     ref = oracle.is_loss(z64[keep], csum[tok_off].astype(np.int64), tgt.cpu().numpy()[keep],
@@ -368,3 +392,16 @@ def test_lmhead_tma_store_epilogue_bitwise(ctx, T, H, V, impl, monkeypatch):
     torch.cuda.synchronize()
     assert torch.equal(lg1.view(torch.int16), lg0.view(torch.int16))  # padding untouched too
     assert torch.equal(p1.view(torch.int32), p0.view(torch.int32))
+
+
+@pytest.mark.parametrize("impl", ["pair"], indirect=True)
+@pytest.mark.parametrize("T,H,V", [(130, 64, 1000), (1024, 4096, 151936)])
+def test_lmhead_logits_only_bitwise(ctx, T, H, V, impl):
+    """partials = NULL: the forward stores the logits only (no exponentials in
+    the epilogue) — bitwise the logits of the statistics-producing call."""
+    x, w, tgt = _inputs(T, H, V, 29)
+    a, pa = ctx.lmhead_logits(x, w, tgt)
+    b, pb = ctx.lmhead_logits(x, w, None, stats=False)
+    torch.cuda.synchronize()
+    assert pb is None and pa is not None
+    assert torch.equal(a.view(torch.int16), b.view(torch.int16))
