@@ -101,6 +101,7 @@ __device__ __forceinline__ void online_update(const float* x, Lse& st, int jt) {
     st.s *= r;
     st.m = vm;
   }
+  if (st.m == -INFINITY) return;  // every column so far is -inf (masked vocabulary): adds 0
   if (jt < 0) {
 #pragma unroll
     for (int j = 0; j < N; ++j) {
@@ -108,7 +109,7 @@ __device__ __forceinline__ void online_update(const float* x, Lse& st, int jt) {
       const float e = ptx::ex2(d * kLog2e);
       st.s += e;
       if (ENT) {
-        st.u = fmaf(e, d, st.u);
+        st.u = fmaf(e, e > 0.f ? d : 0.f, st.u);  // exp(-inf) * -inf = 0, not NaN
         st.a += e;
       }
     }
@@ -119,7 +120,7 @@ __device__ __forceinline__ void online_update(const float* x, Lse& st, int jt) {
       const float e = ptx::ex2(d * kLog2e);
       if (j != jt) st.s += e;
       if (ENT) {
-        st.u = fmaf(e, d, st.u);
+        st.u = fmaf(e, e > 0.f ? d : 0.f, st.u);
         st.a += e;
       }
     }
@@ -261,7 +262,7 @@ __device__ __forceinline__ void row_grad(const float* x, float* d, int32_t c,
     const float p = ptx::ex2(fmaf(xm, kLog2e, -b.log2s));
     float v = -b.coef * p;
     if (c + j == b.y) v = b.dy;  // one-hot term: coef*(1 - p_y) (policy.hpp:193-194)
-    if (ENT) v = fmaf(b.eg * p, xm + b.k0, v);
+    if (ENT && p > 0.f) v = fmaf(b.eg * p, xm + b.k0, v);  // p = 0 at -inf: no entropy term
     d[j] = v;
   }
 }
@@ -331,7 +332,7 @@ struct Ring {
 // between their two passes for about one row plus L segments.
 // ---------------------------------------------------------------------------
 struct P1Acc {
-  float m = -INFINITY, nml = INFINITY;
+  float m = -INFINITY, nml = -INFINITY;  // -inf until a finite column: -inf columns add 0
   float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
   float zy = 0.f;
   bool have_zy = false;

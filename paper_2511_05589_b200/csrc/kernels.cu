@@ -188,7 +188,8 @@ __global__ void __launch_bounds__(WARPS * 32, (WARPS == 8 && CL == 1) ? 3 : 1)
         }
       }
     } else {
-      float m = -INFINITY, nml = INFINITY;
+      // nml = -inf until a finite column is seen: an all -inf vector adds 2^-inf = 0
+      float m = -INFINITY, nml = -INFINITY;
       float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
       for (int p = 0; p < npieces; ++p) {
         ptx::mbar_wait_u32(barbase + p * 8, par);

@@ -97,6 +97,10 @@ __device__ __forceinline__ LogProb finish_logprob(float M, float s_excl, float z
     q.cur = __int_as_float(0x7fc00000);
     return q;
   }
+  if (M == -INFINITY) {  // every other column is -inf (masked vocabulary): p_y = 1
+    M = zy;
+    s_excl = 0.f;
+  }
   const float dz = zy - M;
   const float r = s_excl * expf(-dz);
   const float l1 = log1pf(r);

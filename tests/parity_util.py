@@ -65,7 +65,7 @@ class Case:
     def __init__(self, oracle, seed=1, P=2, G=4, V=512, fixed_len=None, mu=math.log(12),
                  sigma=0.6, lmax=48, stages=(1, 2), stale_prob=0.6, dtype=torch.bfloat16,
                  ld=None, clip_low=0.2, clip_high=0.28, kl_coeff=0.0, entropy_coeff=0.0,
-                 is_enabled=True, behav_mode=0, reward=None):
+                 is_enabled=True, behav_mode=0, reward=None, edit_logits=None):
         hb = make_host_batch(seed, P, G, V, mu=mu, sigma=sigma, lmax=lmax, fixed_len=fixed_len,
                              stages=stages, stale_prob=stale_prob)
         if reward is not None:
@@ -75,6 +75,8 @@ class Case:
         self.dtype = dtype
         self.ld = ld
         logits = make_logits(hb.n_tok, V, hb.target, seed, "cpu", dtype, ld=ld)
+        if edit_logits is not None:  # e.g. masked vocabulary entries (-inf)
+            edit_logits(logits, hb)
         self.logits_cpu = logits  # may be a padded view
         self.z64 = logits.double().numpy()
         cur = oracle.logprob_gather(self.z64, hb.target)

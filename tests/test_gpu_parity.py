@@ -632,3 +632,47 @@ def test_claim_counter_rearmed_across_launch_kinds(ctx, oracle, impl):
         assert torch.equal(r.dlogits.view(torch.int16), r0.dlogits.view(torch.int16))
         assert r.loss == r0.loss
     case.check(r0, BF16, what="claim counter")
+
+
+
+def _mask_vocab(logits, hb):
+    """-inf logits (a masked vocabulary): ~10% of each row's non-target columns,
+    row 0 everything but the target (p_y = 1 exactly), row 1 everything but the
+    target and one other column."""
+    g = torch.Generator().manual_seed(5)
+    T, V = logits.shape[0], logits.shape[1]
+    m = torch.rand((T, V), generator=g) < 0.1
+    m[0, :] = True
+    m[1, :] = True
+    m[1, (int(hb.target[1]) + 7) % V] = False
+    m[torch.arange(T), torch.from_numpy(hb.target).long()] = False
+    logits.masked_fill_(m, float("-inf"))
+
+
+@pytest.mark.parametrize("V,force,kernel", [(151936, None, "fused_pair_kernel"),
+                                            (32000, None, "fused_solo_kernel"),
+                                            (32000, "tma", "fused_tma_kernel"),
+                                            (151936, "stream", "fused_stream_la_kernel")])
+@pytest.mark.parametrize("dl_dtype", [BF16, F32])
+def test_masked_vocabulary_minus_inf(ctx, oracle, impl, V, force, kernel, dl_dtype):
+    """-inf logits: zero probability, zero dlogits, and a row whose only finite
+    logit is the target has log-prob exactly 0 (policy.hpp:114-120 with
+    exp(-inf) = 0); every kernel, K1 and the unfused path against the oracle.
+    (With the entropy term on, the reference's h -= p log p is NaN at p = 0,
+    grpo.hpp:172; the kernels take the limit 0 there.)"""
+    impl(force)
+    case = Case(oracle, seed=43, P=2, G=4, V=V, mu=math.log(10), lmax=24, edit_logits=_mask_vocab)
+    _, res = run(ctx, case, dl_dtype)
+    assert ctx.last_launch()["kernel"] == kernel
+    case.check(res, dl_dtype, what=f"masked vocab V={V} {force}")
+    assert res.cur_lp[0].item() == 0.0
+    dl = res.dlogits.float()
+    inf_cols = torch.isinf(case.logits_gpu().float())
+    assert torch.all(dl[inf_cols] == 0)
+    # K1 (sequence_logprobs) and the unfused path on the same rows
+    lp, lse = ctx.sequence_logprobs(case.logits_gpu(), torch.from_numpy(case.hb.target).cuda())
+    assert_scalar_close(lp.cpu().numpy(), case.ref.cur_lp, what="K1 masked vocab")
+    assert torch.isfinite(lse).all()
+    if force is None:
+        _, ru = run(ctx, case, F32, fused=False)
+        case.check(ru, F32, what=f"unfused masked vocab V={V}")
