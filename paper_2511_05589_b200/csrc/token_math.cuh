@@ -102,6 +102,17 @@ __device__ __forceinline__ LogProb finish_logprob(float M, float s_excl, float z
     s_excl = 0.f;
   }
   const float dz = zy - M;
+  if (dz < -64.f) {
+    // target far below the row maximum (p_y < e^-64): s_excl e^-dz would
+    // overflow fp32; s_excl >= 1 (it holds the max column's e^0), so
+    // ln S = ln s_excl + log1p(e^dz / s_excl) is exact to rounding
+    const float ey = expf(dz);
+    q.ln_s = logf(s_excl) + log1pf(ey / s_excl);
+    q.cur = dz - q.ln_s;
+    q.S = s_excl + ey;
+    q.lse = static_cast<double>(M) + static_cast<double>(q.ln_s);
+    return q;
+  }
   const float r = s_excl * expf(-dz);
   const float l1 = log1pf(r);
   q.cur = -l1;

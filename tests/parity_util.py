@@ -59,15 +59,35 @@ def assert_loss_close(gpu_loss, ref_loss, ref_obj, T, rtol=RTOL, what="loss"):
         f"{what}: gpu {gpu_loss!r} ref {ref_loss!r} (scale {scale:.3e})"
 
 
+def with_empty_trajectories(hb, idx):
+    """The batch with every token of trajectories `idx` removed (zero-length
+    trajectories stay in their groups: they count for the group advantage but
+    contribute no token)."""
+    from dataclasses import replace
+    idx = set(int(i) for i in idx)
+    keep = np.ones(hb.n_tok, bool)
+    for i in idx:
+        keep[hb.tok_off[i]:hb.tok_off[i + 1]] = False
+    before = np.concatenate([[0], np.cumsum(~keep)])  # dropped tokens before each offset
+    tok_off = hb.tok_off - before[hb.tok_off]
+    seg_off = hb.seg_off - before[hb.seg_off]
+    nonempty = np.diff(seg_off) > 0
+    seg_off = np.concatenate([[0], seg_off[1:][nonempty]]).astype(np.int64)
+    return replace(hb, tok_off=tok_off.astype(np.int64), target=hb.target[keep], stage=hb.stage[keep],
+                   seg_off=seg_off, seg_ver=hb.seg_ver[nonempty])
+
+
 class Case:
     """A seeded synthetic batch plus its oracle result."""
 
     def __init__(self, oracle, seed=1, P=2, G=4, V=512, fixed_len=None, mu=math.log(12),
                  sigma=0.6, lmax=48, stages=(1, 2), stale_prob=0.6, dtype=torch.bfloat16,
                  ld=None, clip_low=0.2, clip_high=0.28, kl_coeff=0.0, entropy_coeff=0.0,
-                 is_enabled=True, behav_mode=0, reward=None, edit_logits=None):
+                 is_enabled=True, behav_mode=0, reward=None, edit_logits=None, empty=None):
         hb = make_host_batch(seed, P, G, V, mu=mu, sigma=sigma, lmax=lmax, fixed_len=fixed_len,
                              stages=stages, stale_prob=stale_prob)
+        if empty is not None:
+            hb = with_empty_trajectories(hb, empty)
         if reward is not None:
             hb.reward[:] = reward
         self.hb = hb

@@ -676,3 +676,41 @@ def test_masked_vocabulary_minus_inf(ctx, oracle, impl, V, force, kernel, dl_dty
     if force is None:
         _, ru = run(ctx, case, F32, fused=False)
         case.check(ru, F32, what=f"unfused masked vocab V={V}")
+
+
+
+def _special_rows(logits, hb):
+    """Rows the reference's own KATs single out (test_policy.cpp:52-65): an
+    all-equal row (p = 1/V), a row spanning +-300 (LSE stability), a row whose
+    target is far below the rest (log-prob ~ -600; the reference takes log(p), so
+    its log-prob is only finite while p > 1e-308: no further)."""
+    T, V = logits.shape
+    y = torch.from_numpy(hb.target).long()
+    for r in range(0, T, 5):
+        logits[r] = 0.0
+    for r in range(1, T, 5):
+        logits[r] = torch.linspace(-300.0, 300.0, V)
+    for r in range(2, T, 5):
+        logits[r, y[r]] = -600.0
+
+
+@pytest.mark.parametrize("V,force,kernel", [(151936, None, "fused_pair_kernel"),
+                                            (32000, None, "fused_solo_kernel"),
+                                            (32000, "tma", "fused_tma_kernel"),
+                                            (151936, "stream", "fused_stream_la_kernel"),
+                                            (4099, None, "fused_generic_kernel")])
+def test_empty_trajectories_and_special_rows(ctx, oracle, impl, V, force, kernel):
+    """Zero-length trajectories inside groups (they count for the group's
+    advantages, grpo.hpp:51-65, and add no token), uniform rows, +-300 rows and
+    targets far below the row maximum, through every kernel against the oracle."""
+    impl(force)
+    case = Case(oracle, seed=47, P=3, G=4, V=V, mu=math.log(8), lmax=16, empty=[1, 4, 5, 10],
+                edit_logits=_special_rows)
+    assert np.any(np.diff(case.hb.tok_off) == 0)
+    for dl_dtype in (BF16, F32):
+        _, res = run(ctx, case, dl_dtype)
+        assert ctx.last_launch()["kernel"] == kernel
+        case.check(res, dl_dtype, what=f"empty trajectories / special rows V={V} {force}")
+    uni = np.arange(0, case.hb.n_tok, 5)
+    assert_scalar_close(res.cur_lp.cpu().numpy()[uni], np.full(len(uni), -math.log(V)), rtol=2e-6,
+                        what="uniform rows: -log V")
