@@ -83,7 +83,8 @@ class Case:
     def __init__(self, oracle, seed=1, P=2, G=4, V=512, fixed_len=None, mu=math.log(12),
                  sigma=0.6, lmax=48, stages=(1, 2), stale_prob=0.6, dtype=torch.bfloat16,
                  ld=None, clip_low=0.2, clip_high=0.28, kl_coeff=0.0, entropy_coeff=0.0,
-                 is_enabled=True, behav_mode=0, reward=None, edit_logits=None, empty=None):
+                 is_enabled=True, behav_mode=0, reward=None, edit_logits=None, empty=None,
+                 edit_blp=None):
         hb = make_host_batch(seed, P, G, V, mu=mu, sigma=sigma, lmax=lmax, fixed_len=fixed_len,
                              stages=stages, stale_prob=stale_prob)
         if empty is not None:
@@ -101,6 +102,8 @@ class Case:
         self.z64 = logits.double().numpy()
         cur = oracle.logprob_gather(self.z64, hb.target)
         self.blp = stale_logprobs(cur, hb.stage, hb.cur_stage, seed, clip_low, clip_high)
+        if edit_blp is not None:  # e.g. tokens far off policy
+            edit_blp(self.blp, cur, hb)
         self.adv = oracle.advantages(hb.reward, hb.group_off)
         self.ref_lp = None
         if kl_coeff > 0.0:

@@ -714,3 +714,32 @@ def test_empty_trajectories_and_special_rows(ctx, oracle, impl, V, force, kernel
     uni = np.arange(0, case.hb.n_tok, 5)
     assert_scalar_close(res.cur_lp.cpu().numpy()[uni], np.full(len(uni), -math.log(V)), rtol=2e-6,
                         what="uniform rows: -log V")
+
+
+
+def _far_off_policy(blp, cur, hb):
+    """Stale tokens whose behaviour log-prob is 120 below / above the current
+    one: ratios e^120 and e^-120 (fp32 exp overflows at e^88)."""
+    stale = np.nonzero(hb.stage < hb.cur_stage)[0]
+    blp[stale[0::4]] = cur[stale[0::4]] - 120.0
+    blp[stale[1::4]] = cur[stale[1::4]] + 120.0
+
+
+def test_far_off_policy_ratios(ctx, oracle, impl):
+    """Ratios e^+-120 (grpo.hpp:71 takes exp in fp64): the objective, the fp64
+    coefficient and the loss match the reference's; positive advantages take
+    the clipped branch (zero gradient), negative ones the unclipped branch with
+    |w| ~ e^120 (beyond any f32/bf16 dlogits, whose rows are not compared)."""
+    impl(None)
+    case = Case(oracle, seed=53, P=2, G=4, V=151936, mu=math.log(12), lmax=24, stale_prob=1.0,
+                edit_blp=_far_off_policy)
+    _, res = run(ctx, case, F32)
+    ref = case.ref
+    assert_scalar_close(res.obj.cpu().numpy(), ref.obj, what="obj")
+    np.testing.assert_array_equal((res.flags.cpu().numpy() >> 1) & 1, ref.clipped)
+    coef = res.coef.cpu().numpy()
+    want = -ref.weight / case.hb.n_tok
+    assert_scalar_close(coef, want, what="coef")
+    assert np.isfinite(res.loss) and np.isfinite(ref.loss)
+    assert_loss_close(res.loss, ref.loss, ref.obj, case.hb.n_tok, what="far off-policy loss")
+    assert np.abs(coef).max() > 1e40  # the e^120 rows are there
