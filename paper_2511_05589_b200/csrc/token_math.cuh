@@ -32,11 +32,11 @@ struct TokenResult {
 };
 
 // grpo.hpp:147-162 (+ 170-171 when `ent`): cur/beh are the f32 log-probs,
-// H the row entropy in nats (only read when ent). The ratio and the KL term
-// are fp64 from the f32 log-probs (one exp per row: off the element loop), and
-// the products and sums that decide the branch and form w, obj and coef are
-// fp64 in the reference's order, so a current-stage token (ratio exactly 1)
-// gets w = A and coef = -A/T bit for bit.
+// H the row entropy in nats (only read when ent). The ratio and the KL
+// exponential are fp32 expf (fp64 exp beyond |x| >= 80, where expf would
+// overflow), and the products and sums that decide the branch and form w, obj
+// and coef are fp64 in the reference's order, so a current-stage token (ratio
+// exactly 1) gets w = A and coef = -A/T bit for bit.
 __device__ __forceinline__ TokenResult token_objective(const LossParams& P, float cur, float beh,
                                                        double adv, float ref, bool stale,
                                                        float H, bool ent) {
@@ -49,10 +49,13 @@ __device__ __forceinline__ TokenResult token_objective(const LossParams& P, floa
     r.err = ERR_NONFINITE_LP;
     return r;
   }
-  // fp64 exp, as the reference (grpo.hpp:71): finite up to e^709, so a token far
-  // off policy (|cur - beh| > 88) keeps the reference's objective and coef
-  // (fp64 outputs); cur == beh still gives exactly 1 (acceptance C3)
-  const double ratio = exp(static_cast<double>(cur) - static_cast<double>(beh));
+  // exp in fp32 (<= 2 ulp, on the scalar phase's critical path) unless the token
+  // is far off policy (|cur - beh| >= 80, where expf would overflow at 88): then
+  // fp64, as the reference (grpo.hpp:71), finite up to e^709, so the objective
+  // and the fp64 coef keep the reference's values; cur == beh gives exactly 1
+  const float dr = cur - beh;
+  const double ratio = fabsf(dr) < 80.f ? static_cast<double>(expf(dr))
+                                        : exp(static_cast<double>(cur) - static_cast<double>(beh));
   // std::clamp(ratio, 1 - clip_low, 1 + clip_high), grpo.hpp:149
   const double clamped = ratio < P.clamp_lo ? P.clamp_lo : (P.clamp_hi < ratio ? P.clamp_hi : ratio);
   const double unclipped = __dmul_rn(ratio, adv);
@@ -66,8 +69,10 @@ __device__ __forceinline__ TokenResult token_objective(const LossParams& P, floa
     r.flags |= FLAG_CLIPPED;
   }
   if (P.kl_coeff > 0.0) {  // grpo.hpp:158-162
-    const double d = static_cast<double>(ref) - static_cast<double>(cur);
-    const double ed = exp(d);
+    const float df = ref - cur;
+    const double d = static_cast<double>(df);
+    const double ed = fabsf(df) < 80.f ? static_cast<double>(expf(df))
+                                       : exp(static_cast<double>(ref) - static_cast<double>(cur));
     obj = __dadd_rn(obj, -__dmul_rn(P.kl_coeff, __dadd_rn(__dadd_rn(ed, -d), -1.0)));
     w = __dadd_rn(w, __dmul_rn(P.kl_coeff, __dadd_rn(ed, -1.0)));
   }

@@ -1,9 +1,9 @@
 """GPU: clip-branch flips, fp32 device arithmetic vs the reference's fp64
 (grpo.hpp:147-152), on inputs WITHOUT the synthetic guard band.
 
-The device computes the log-probs in fp32 and the ratio exp(cur - behav) and
-the branch `u <= c` in fp64 from them (token_math.cuh); the reference does
-everything in fp64. A token whose ratio lies within a few fp32 ulps of
+The device computes the ratio as expf(cur - behav) in fp32 from fp32 log-probs
+(token_math.cuh) and the branch `u <= c` in fp64 on that ratio; the reference
+does everything in fp64. A token whose ratio lies within a few fp32 ulps of
 1 - eps_lo or 1 + eps_hi can take the other branch. The parity tests keep a
 1e-4 guard band around the thresholds (workload.stale_logprobs) so their clip
 masks are bit-exact; these tests drop it and COUNT the flips:
