@@ -84,9 +84,12 @@ class Case:
                  sigma=0.6, lmax=48, stages=(1, 2), stale_prob=0.6, dtype=torch.bfloat16,
                  ld=None, clip_low=0.2, clip_high=0.28, kl_coeff=0.0, entropy_coeff=0.0,
                  is_enabled=True, behav_mode=0, reward=None, edit_logits=None, empty=None,
-                 edit_blp=None):
+                 edit_blp=None, targets=None):
         hb = make_host_batch(seed, P, G, V, mu=mu, sigma=sigma, lmax=lmax, fixed_len=fixed_len,
                              stages=stages, stale_prob=stale_prob)
+        if targets is not None:  # chosen target columns, cycled over the tokens
+            t = np.asarray(targets, np.int32)
+            hb.target[:] = t[np.arange(hb.n_tok) % len(t)]
         if empty is not None:
             hb = with_empty_trajectories(hb, empty)
         if reward is not None:

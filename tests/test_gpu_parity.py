@@ -361,18 +361,20 @@ def test_expand_segments(ctx):
     np.testing.assert_array_equal(tt, np.repeat(np.arange(hb.n_traj), np.diff(hb.tok_off)))
 
 
-def test_host_buffer_dropin(ctx, oracle):
+@pytest.mark.parametrize("V,dl_dtype", [(32000, F32), (151936, BF16)])
+def test_host_buffer_dropin(ctx, oracle, V, dl_dtype):
     """copris_grpo_step_loss_host: host arrays in (pinned), 3-stream chunked
-    pipeline, host loss/counts/dlogits out — same numbers as the oracle."""
+    pipeline, host loss/counts/dlogits out — same numbers as the oracle (bf16
+    dlogits at V = 151,936: the bench's e2e path)."""
     from paper_2511_05589_b200.grpo import HostWorkspace
-    case = Case(oracle, seed=19, P=4, G=4, V=32000, mu=math.log(20), lmax=64)
+    case = Case(oracle, seed=19, P=4, G=4, V=V, mu=math.log(20), lmax=64)
     hb = case.hb
     T = hb.n_tok
-    ws = HostWorkspace(ctx, chunk_rows=29, vocab=32000, max_tokens=T, max_traj=hb.n_traj,
-                       dlogits_dtype=F32)
+    ws = HostWorkspace(ctx, chunk_rows=29, vocab=V, max_tokens=T, max_traj=hb.n_traj,
+                       dlogits_dtype=dl_dtype)
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
     logits = case.logits_cpu.pin_memory()
-    dl = torch.empty((T, 32000), dtype=F32).pin_memory()
+    dl = torch.empty((T, V), dtype=dl_dtype).pin_memory()
     cur = torch.empty(T, dtype=F32).pin_memory()
     out = ws.grpo_step_loss(logits, pin(hb.tok_off), pin(hb.target), pin(hb.stage.view(np.int32)),
                             pin(case.blp), hb.cur_stage, rewards=pin(hb.reward),
@@ -384,8 +386,9 @@ def test_host_buffer_dropin(ctx, oracle):
     assert_scalar_close(cur.numpy(), ref.cur_lp, what="host cur_lp")
     from parity_util import assert_loss_close
     assert_loss_close(out["loss"], ref.loss, ref.obj, T, what="host loss")
-    atol = (32000 + 8) * 2.0 ** -52 * np.abs(ref.weight) / T
-    assert_rows_close(dl.numpy(), ref.dlogits, what="host dlogits", row_atol=atol)
+    atol = (V + 8) * 2.0 ** -52 * np.abs(ref.weight) / T
+    assert_rows_close(dl.float().numpy(), ref.dlogits, bf16=dl_dtype == BF16, what="host dlogits",
+                      row_atol=atol)
     # errors keep the reference's semantics
     from paper_2511_05589_b200 import ConfigError
     bad = pin(np.array([0, 1, 3], np.int64))
@@ -743,3 +746,26 @@ def test_far_off_policy_ratios(ctx, oracle, impl):
     assert np.isfinite(res.loss) and np.isfinite(ref.loss)
     assert_loss_close(res.loss, ref.loss, ref.obj, case.hb.n_tok, what="far off-policy loss")
     assert np.abs(coef).max() > 1e40  # the e^120 rows are there
+
+
+
+@pytest.mark.parametrize("V,force,kernel,targets", [
+    # pair: half boundary at column 75,968 (nvec0 = 9,496 vectors), slots of 16,384 columns
+    (151936, None, "fused_pair_kernel", [0, 1, 7, 8, 16383, 16384, 75959, 75967, 75968, 75969,
+                                         75968 + 16383, 75968 + 16384, 151935, 151934]),
+    (151952, None, "fused_pair_kernel", [0, 75975, 75976, 75977, 151951]),  # odd nvec0
+    (32000, None, "fused_solo_kernel", [0, 1, 16383, 16384, 31999, 31998]),
+    (32000, "tma", "fused_tma_kernel", [0, 1, 16383, 16384, 31999]),
+])
+@pytest.mark.parametrize("dl_dtype", [BF16, F32])
+def test_target_at_vector_slot_and_half_boundaries(ctx, oracle, impl, V, force, kernel, targets,
+                                                   dl_dtype):
+    """Target columns on every boundary the kernels split rows at (16-byte
+    vector, ring slot, CTA-pair half, last column): the target is kept out of
+    the running sums by the thread that owns it, and its one-hot term is
+    written by that thread — against the oracle, bf16 and f32 dlogits."""
+    impl(force)
+    case = Case(oracle, seed=59, P=2, G=4, V=V, mu=math.log(10), lmax=24, targets=targets)
+    _, res = run(ctx, case, dl_dtype)
+    assert ctx.last_launch()["kernel"] == kernel
+    case.check(res, dl_dtype, what=f"boundary targets V={V} {force}")
