@@ -159,6 +159,16 @@ class Case:
             # the reference's p_y = e_y / sum_k e_k carries up to ~V ulps of error,
             # which its one-hot entry w - w*p_y inherits (policy.hpp:193-194)
             atol = (self.V + 8) * 2.0 ** -52 * (np.abs(ref.weight) + self.cfg["entropy_coeff"]) / T
+            beta = self.cfg["kl_coeff"]
+            if beta > 0.0:
+                # w = r A + beta (e^d - 1) can cancel; its error follows the
+                # conditioning of its terms in cur (an fp32 log-prob on the
+                # device): dw ~ (|r A| + beta e^d) dcur, dcur ~ 2e-6 max(1, |cur|)
+                cur = ref.cur_lp
+                r = np.exp(cur - ref.behav)
+                adv_t = np.repeat(self.adv, np.diff(hb.tok_off))
+                ed = np.exp(self.ref_lp.astype(np.float64) - cur)
+                atol = atol + (np.abs(r * adv_t) + beta * ed) * 2e-6 * np.maximum(1.0, np.abs(cur)) / T
             assert_rows_close(dl, ref.dlogits, bf16=(dl_dtype == torch.bfloat16),
                               what=f"{what} dlogits", row_atol=atol)
 

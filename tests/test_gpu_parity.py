@@ -769,3 +769,20 @@ def test_target_at_vector_slot_and_half_boundaries(ctx, oracle, impl, V, force, 
     _, res = run(ctx, case, dl_dtype)
     assert ctx.last_launch()["kernel"] == kernel
     case.check(res, dl_dtype, what=f"boundary targets V={V} {force}")
+
+
+@pytest.mark.parametrize("V,kernel", [(151936, "fused_pair_kernel"), (32000, "fused_solo_kernel")])
+@pytest.mark.parametrize("mode", ["kl", "is_off", "recorded", "kl_recorded"])
+def test_pair_and_solo_token_math_modes(ctx, oracle, impl, V, kernel, mode):
+    """The default kernels at both vocabularies in every token-math mode they
+    take (the entropy term goes to the other kernels): KL against the
+    version-0 snapshot's log-probs (grpo.hpp:158-162), IS off (trainer.hpp:149),
+    recorded behaviour (concat_segments verbatim), KL with recorded behaviour."""
+    impl(None)
+    kw = dict(kl_coeff=0.1 if mode.startswith("kl") else 0.0, is_enabled=mode != "is_off",
+              behav_mode=1 if mode.endswith("recorded") else 0)
+    case = Case(oracle, seed=61, P=2, G=4, V=V, mu=math.log(12), lmax=24, **kw)
+    for dl_dtype in (BF16, F32):
+        _, res = run(ctx, case, dl_dtype)
+        assert ctx.last_launch()["kernel"] == kernel
+        case.check(res, dl_dtype, what=f"{mode} V={V}")
