@@ -51,6 +51,7 @@
 // token_math.cuh, exactly as the other fused kernels.
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "fused_common.cuh"
@@ -64,14 +65,30 @@
 namespace copris_b200 {
 namespace {
 
-constexpr int kPW = 16;                     // consumer warps per CTA
 constexpr int kPK = 4;                      // 16-byte vectors per consumer thread per slot
-constexpr int kPThreads = kPW * 32;         // 512 consumer threads
-constexpr int kPSlotVec = kPThreads * kPK;  // 2048 vectors = 16,384 bf16 columns per slot
-constexpr int kPSlotBytes = kPSlotVec * 16; // 32 KB
 constexpr int kPTSlots = 8;                 // TMEM slots per thread (16 columns each)
-constexpr int kPTmemCols = 512;             // the whole tensor memory of the SM
 constexpr uint32_t kNegInf2 = 0xFF80FF80u;  // bf16x2 (-inf, -inf)
+
+// Shape of a CTA with PW consumer warps: PW = 16 for the CTA pair (one CTA per
+// SM, 32 KB slots, the SM's whole 512-column TMEM), PW = 8 for the solo kernel
+// (16 KB slots, 256 TMEM columns, 104 KB of shared memory: TWO CTAs per SM,
+// whose independent row pipelines overlap one CTA's exponentials with the
+// other's stores).
+template <int PW>
+struct PShape {
+  static constexpr int kPW = PW;                      // consumer warps per CTA
+  static constexpr int kPThreads = PW * 32;           // consumer threads
+  static constexpr int kPSlotVec = kPThreads * kPK;   // 16-byte vectors per slot
+  static constexpr int kPSlotBytes = kPSlotVec * 16;  // 32 KB (PW 16) / 16 KB (PW 8)
+  static constexpr int kPTmemCols = PW * 32;          // 4 lane quarters x PW/4 warps x 128 columns
+};
+#define COPRIS_PSHAPE(PW)                                       \
+  constexpr int kPW = PShape<PW>::kPW;                          \
+  constexpr int kPThreads = PShape<PW>::kPThreads;              \
+  constexpr int kPSlotVec = PShape<PW>::kPSlotVec;              \
+  constexpr int kPSlotBytes = PShape<PW>::kPSlotBytes;          \
+  constexpr int kPTmemCols = PShape<PW>::kPTmemCols;            \
+  (void)kPW; (void)kPThreads; (void)kPSlotVec; (void)kPSlotBytes; (void)kPTmemCols
 
 __device__ __forceinline__ uint32_t f2_to_f16x2(uint64_t a) {
   uint32_t r;
@@ -160,9 +177,10 @@ __device__ __forceinline__ void kill_col(uint32_t& w, int jt, int k, float& zy) 
 // STORE: stage the f16 exponentials in TMEM at taddr (16 columns). Returns
 // nml = 15 - m log2(e) of this thread's columns (+inf when it saw no finite
 // column) for pass 2.
-template <bool STORE, bool RAW, bool BST>
+template <bool STORE, bool RAW, bool BST, int PW>
 __device__ __forceinline__ float p1_slot(LaneAcc& a, uint32_t sb, int32_t v0, int32_t cnt,
                                          int32_t ycol, int tid, uint32_t taddr) {
+  COPRIS_PSHAPE(PW);
   uint4 raw[kPK];
   if (cnt == kPSlotVec) {
 #pragma unroll
@@ -241,10 +259,11 @@ __device__ __forceinline__ float p1_slot(LaneAcc& a, uint32_t sb, int32_t v0, in
 // vectors with one 32-byte store (STG.256); the target column is patched into
 // its vector before the swap. Otherwise 16-byte stores and the target column
 // written by its owner afterwards (a later store of the same thread).
-template <bool W256, bool BST>
+template <bool W256, bool BST, int PW>
 __device__ __forceinline__ void p2_slot(const RowBroadcast& b, bool zero_row, float nml,
                                         uint32_t taddr, int32_t v0, int32_t cnt, int32_t ycol,
                                         __nv_bfloat16* dseg, int tid) {
+  COPRIS_PSHAPE(PW);
   __nv_bfloat16* base = dseg + static_cast<int64_t>(tid) * 8;
   const int32_t rel = ycol - v0 * 8;
   const bool own_y = static_cast<uint32_t>(rel) < static_cast<uint32_t>(cnt * 8) &&
@@ -334,9 +353,11 @@ __device__ __forceinline__ void p2_slot(const RowBroadcast& b, bool zero_row, fl
 // Pass 2, f32 dlogits: the staged raw logits -> d_k = -coef 2^(z_k log2(e) - c1)
 // (fused_common.cuh p2_segment's f32 arithmetic), one 32-byte store per 8
 // columns (a warp writes 1 KB contiguous per instruction).
+template <int PW>
 __device__ __forceinline__ void p2_slot_f32(const RowBroadcast& b, bool zero_row, uint32_t taddr,
                                             int32_t v0, int32_t cnt, int32_t ycol, float* dseg,
                                             int tid) {
+  COPRIS_PSHAPE(PW);
   float* base = dseg + static_cast<int64_t>(tid) * 8;
   if (zero_row) {
     const float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -371,14 +392,15 @@ __device__ __forceinline__ void p2_slot_f32(const RowBroadcast& b, bool zero_row
 // shared memory: nslots ring slots of 32 KB, then nml[kPTSlots][512] floats.
 // nvec0 = vectors of CTA rank 0 (rank 1 takes the rest); look = slots of row
 // r+1 run through pass 1 before pass 2 of row r.
-template <bool F32, int CL, bool BST>
-__global__ void __launch_bounds__((kPW + 2) * 32, 1)
+template <bool F32, int CL, bool BST, int PW>
+__global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
     fused_pair_kernel(const LossParams P, const int nslots, const int look, const int32_t nvec0,
                       const int st256) {
+  COPRIS_PSHAPE(PW);
   static_assert(CL == 1 || CL == 2, "a row is split over one or two CTAs");
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[16], empty[16], p1done[2], sdone[2];
-  __shared__ PairPart red[2][2 * kPW];
+  __shared__ PairPart red[2][2 * PW];
   __shared__ RowBroadcast bc[2];
   __shared__ uint32_t tmem_slot;
 
@@ -491,9 +513,9 @@ __global__ void __launch_bounds__((kPW + 2) * 32, 1)
         const int32_t cnt = min(kPSlotVec, nvec - v0);
         ptx::mbar_wait_sleep(fbase + slot * 8, ring.ph);
         const uint32_t tsl = (ts + static_cast<uint32_t>(sg)) % kPTSlots;
-        const float nml = grad ? p1_slot<true, F32, BST>(a, sbase + slot * kPSlotBytes, v0, cnt, ycol, tid,
+        const float nml = grad ? p1_slot<true, F32, BST, PW>(a, sbase + slot * kPSlotBytes, v0, cnt, ycol, tid,
                                                          taddr0 + tsl * 16)
-                               : p1_slot<false, F32, BST>(a, sbase + slot * kPSlotBytes, v0, cnt, ycol, tid, 0u);
+                               : p1_slot<false, F32, BST, PW>(a, sbase + slot * kPSlotBytes, v0, cnt, ycol, tid, 0u);
         nml_sh[tsl * kPThreads + tid] = nml;
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive_u32(ebase + slot * 8);
@@ -551,16 +573,16 @@ __global__ void __launch_bounds__((kPW + 2) * 32, 1)
           const int32_t v0 = sg * kPSlotVec;
           if constexpr (F32) {
             float* drow = static_cast<float*>(P.dlogits) + r * P.ld_d + col0;
-            p2_slot_f32(b, zero_row, taddr0 + tsl * 16, v0, min(kPSlotVec, nvec - v0), ycol,
+            p2_slot_f32<PW>(b, zero_row, taddr0 + tsl * 16, v0, min(kPSlotVec, nvec - v0), ycol,
                         drow + static_cast<int64_t>(v0) * 8, tid);
           } else {
             __nv_bfloat16* drow = static_cast<__nv_bfloat16*>(P.dlogits) + r * P.ld_d + col0;
             const int32_t cnt = min(kPSlotVec, nvec - v0);
             if (w256 && cnt == kPSlotVec)
-              p2_slot<true, BST>(b, zero_row, nml_sh[tsl * kPThreads + tid], taddr0 + tsl * 16, v0, cnt,
+              p2_slot<true, BST, PW>(b, zero_row, nml_sh[tsl * kPThreads + tid], taddr0 + tsl * 16, v0, cnt,
                             ycol, drow + static_cast<int64_t>(v0) * 8, tid);
             else
-              p2_slot<false, BST>(b, zero_row, nml_sh[tsl * kPThreads + tid], taddr0 + tsl * 16, v0, cnt,
+              p2_slot<false, BST, PW>(b, zero_row, nml_sh[tsl * kPThreads + tid], taddr0 + tsl * 16, v0, cnt,
                              ycol, drow + static_cast<int64_t>(v0) * 8, tid);
           }
         }
@@ -599,22 +621,47 @@ bool pair_supported(const LossParams& p, DType in, DType out, bool ent, int cl) 
   const int64_t osz = out == DType::F32 ? 4 : 2, oal = out == DType::F32 ? 32 : 16;
   if (p.dlogits && ((p.ld_d * osz) % oal != 0 || reinterpret_cast<uintptr_t>(p.dlogits) % oal != 0))
     return false;
+  const int32_t slot_vec = cl == 2 ? PShape<16>::kPSlotVec : PShape<8>::kPSlotVec;
   const int32_t nvec0 = cl == 2 ? (p.vocab / 8 + 1) / 2 : p.vocab / 8;
-  const int32_t nseg = (nvec0 + kPSlotVec - 1) / kPSlotVec;
+  const int32_t nseg = (nvec0 + slot_vec - 1) / slot_vec;
   return nseg <= kPTSlots - 1;  // room for at least one lookahead slot in TMEM
 }
 
-cudaError_t launch_pair(const LossParams& p, DType out, int cl, int num_sms, const Tuning& tu,
-                        cudaStream_t stream, LaunchInfo* info) {
+namespace {
+// CTAs of `kern` that fit one SM: shared memory (dynamic + static + the 1 KB the
+// runtime reserves per CTA), registers, threads and TMEM columns. The occupancy
+// API answered 1 for the 104 KB solo CTA where two fit and run (measured: 296
+// co-resident CTAs, one group x L = 256 at 0.78 instead of 0.66 of peak).
+int ctas_per_sm(const void* kern, int threads, int dyn_smem, int tmem_cols) {
+  int dev = 0, smem_sm = 0, regs_sm = 0, thr_sm = 0;
+  cudaFuncAttributes fa{};
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaFuncGetAttributes(&fa, kern) != cudaSuccess) return 1;
+  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
+  cudaDeviceGetAttribute(&thr_sm, cudaDevAttrMaxThreadsPerMultiProcessor, dev);
+  const int per_cta = dyn_smem + static_cast<int>(fa.sharedSizeBytes) + 1024;
+  int n = smem_sm / per_cta;
+  const int regs = ((fa.numRegs + 7) / 8) * 8 * threads;
+  if (regs > 0) n = std::min(n, regs_sm / regs);
+  n = std::min(n, thr_sm / threads);
+  n = std::min(n, 512 / tmem_cols);
+  return n < 1 ? 1 : n;
+}
+
+template <int PW>
+cudaError_t launch_pair_pw(const LossParams& p, DType out, int cl, int num_sms, const Tuning& tu,
+                           cudaStream_t stream, LaunchInfo* info) {
+  COPRIS_PSHAPE(PW);
   const bool f32 = out == DType::F32 && p.dlogits != nullptr && !p.gather_only;
   const bool bst = !f32 && tu.pair_bf16_stage;
   using Kern = void (*)(const LossParams, const int, const int, const int32_t, const int);
   const Kern kern =
-      cl == 2 ? (f32 ? fused_pair_kernel<true, 2, false>
-                     : (bst ? fused_pair_kernel<false, 2, true> : fused_pair_kernel<false, 2, false>))
-              : (f32 ? fused_pair_kernel<true, 1, false>
-                     : (bst ? fused_pair_kernel<false, 1, true> : fused_pair_kernel<false, 1, false>));
-  // 6 x 32 KB ring + 16 KB of per-thread nml fill the 227 KB a CTA may use
+      cl == 2 ? (f32 ? fused_pair_kernel<true, 2, false, PW>
+                     : (bst ? fused_pair_kernel<false, 2, true, PW> : fused_pair_kernel<false, 2, false, PW>))
+              : (f32 ? fused_pair_kernel<true, 1, false, PW>
+                     : (bst ? fused_pair_kernel<false, 1, true, PW> : fused_pair_kernel<false, 1, false, PW>));
+  // PW 16: 6 x 32 KB ring + 16 KB of per-thread nml fill the 227 KB a CTA may
+  // use; PW 8: 6 x 16 KB + 8 KB = 104 KB, two CTAs per SM
   const int nslots = tu.slots > 0 ? (tu.slots > 6 ? 6 : tu.slots) : 6;
   const int smem = nslots * kPSlotBytes + kPTSlots * kPThreads * static_cast<int>(sizeof(float));
   cudaError_t e = allow_dyn_smem(reinterpret_cast<const void*>(kern), smem);
@@ -647,6 +694,8 @@ cudaError_t launch_pair(const LossParams& p, DType out, int cl, int num_sms, con
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(kern),
                                                       (kPW + 2) * 32, smem);
     if (e != cudaSuccess) return e;
+    per_sm = std::max(per_sm, ctas_per_sm(reinterpret_cast<const void*>(kern), (kPW + 2) * 32, smem,
+                                          kPTmemCols));
     slots = static_cast<int64_t>(per_sm) * num_sms;
   }
   if (slots < 1) return cudaErrorInvalidConfiguration;
@@ -663,6 +712,13 @@ cudaError_t launch_pair(const LossParams& p, DType out, int cl, int num_sms, con
     info->reduced = fuse ? 1 : 0;
   }
   return cudaLaunchKernelEx(&cfg, kern, q, nslots, look, nvec0, tu.pair_st256);
+}
+}  // namespace
+
+cudaError_t launch_pair(const LossParams& p, DType out, int cl, int num_sms, const Tuning& tu,
+                        cudaStream_t stream, LaunchInfo* info) {
+  return cl == 2 ? launch_pair_pw<16>(p, out, cl, num_sms, tu, stream, info)
+                 : launch_pair_pw<8>(p, out, cl, num_sms, tu, stream, info);
 }
 
 }  // namespace copris_b200

@@ -52,7 +52,7 @@ SHAPES = [
     (80000, BF16, "tma", "fused_tma_kernel", 1),      # 160 KB rows: one 16-warp CTA per row
     (32000, BF16, "solo", "fused_solo_kernel", 1),    # one CTA per row, exponentials in TMEM
     (32000, BF16, "solo+pl0", "fused_solo_kernel", 1),
-    (80000, BF16, "solo", "fused_solo_kernel", 1),    # 5 slots per row, partial last slot
+    (48000, BF16, "solo", "fused_solo_kernel", 1),    # 6 slots per row (PW 8: 16 KB slots), partial last slot
     (4096, BF16, "solo", "fused_solo_kernel", 1),     # one partial slot per row
     (256, BF16, "solo", "fused_solo_kernel", 1),      # tiny rows
     (151936, F32, None, "fused_stream_la_kernel", 1),
