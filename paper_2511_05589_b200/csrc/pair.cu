@@ -648,18 +648,16 @@ int ctas_per_sm(const void* kern, int threads, int dyn_smem, int tmem_cols) {
   return n < 1 ? 1 : n;
 }
 
-template <int PW>
-cudaError_t launch_pair_pw(const LossParams& p, DType out, int cl, int num_sms, const Tuning& tu,
+template <int PW, int CL>
+cudaError_t launch_pair_pw(const LossParams& p, DType out, int num_sms, const Tuning& tu,
                            cudaStream_t stream, LaunchInfo* info) {
   COPRIS_PSHAPE(PW);
+  constexpr int cl = CL;
   const bool f32 = out == DType::F32 && p.dlogits != nullptr && !p.gather_only;
   const bool bst = !f32 && tu.pair_bf16_stage;
   using Kern = void (*)(const LossParams, const int, const int, const int32_t, const int);
-  const Kern kern =
-      cl == 2 ? (f32 ? fused_pair_kernel<true, 2, false, PW>
-                     : (bst ? fused_pair_kernel<false, 2, true, PW> : fused_pair_kernel<false, 2, false, PW>))
-              : (f32 ? fused_pair_kernel<true, 1, false, PW>
-                     : (bst ? fused_pair_kernel<false, 1, true, PW> : fused_pair_kernel<false, 1, false, PW>));
+  const Kern kern = f32 ? fused_pair_kernel<true, CL, false, PW>
+                        : (bst ? fused_pair_kernel<false, CL, true, PW> : fused_pair_kernel<false, CL, false, PW>);
   // PW 16: 6 x 32 KB ring + 16 KB of per-thread nml fill the 227 KB a CTA may
   // use; PW 8: 6 x 16 KB + 8 KB = 104 KB, two CTAs per SM
   const int nslots = tu.slots > 0 ? (tu.slots > 6 ? 6 : tu.slots) : 6;
@@ -717,8 +715,8 @@ cudaError_t launch_pair_pw(const LossParams& p, DType out, int cl, int num_sms, 
 
 cudaError_t launch_pair(const LossParams& p, DType out, int cl, int num_sms, const Tuning& tu,
                         cudaStream_t stream, LaunchInfo* info) {
-  return cl == 2 ? launch_pair_pw<16>(p, out, cl, num_sms, tu, stream, info)
-                 : launch_pair_pw<8>(p, out, cl, num_sms, tu, stream, info);
+  return cl == 2 ? launch_pair_pw<16, 2>(p, out, num_sms, tu, stream, info)
+                 : launch_pair_pw<8, 1>(p, out, num_sms, tu, stream, info);
 }
 
 }  // namespace copris_b200

@@ -16,3 +16,8 @@ ncu --set full --clock-control none --import-source on -k regex:fused_ -s 3 -c 1
     -o $OUT/prof_fused_f32 -f \
     python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --chunk-rows 8192 --dlogits f32 \
     > $OUT/prof_fused_f32.log 2>&1
+# V = 32,000 (config #5): the solo kernel, 16,384-row launch
+ncu --set full --clock-control none --import-source on -k regex:fused_ -s 3 -c 1 \
+    -o $OUT/prof_tma -f \
+    python bench.py --config grpo_128x8_v32000_L1024 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline \
+    --chunk-rows 16384 > $OUT/prof_tma.log 2>&1
