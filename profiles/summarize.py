@@ -61,6 +61,11 @@ def ncu_summary(rep, dst_prefix, rows_per_launch):
         name = r[hdr.index("Kernel Name")]
         short = name.replace("(anonymous namespace)::", "").split("(")[0].split("<")[0]
         short = short.split("::")[-1].replace("void ", "").strip()
+        if short == "fused_pair_kernel" and "<" in name:
+            # fused_pair_kernel<F32, CL, BST, PW>: CL = 1 is the solo kernel
+            targs = [a.strip() for a in name.split("<", 1)[1].split(">")[0].split(",")]
+            if len(targs) >= 2 and targs[1] == "1":
+                short = "fused_solo_kernel"
         lines = [f"kernel: {name}"]
         for k in KEYS:
             if k in hdr:
