@@ -5,7 +5,7 @@
 // A 2-CTA cluster owns a row; CTA h of the pair owns half of its columns.
 // Per CTA: 1 producer warp streams the half-row HBM -> shared memory through a
 // ring of 32 KB slots (cp.async.bulk + mbarrier complete_tx, read once,
-// evict_first); 16 consumer warps run pass 1 on each slot as it lands and
+// evict_first); 16 consumer warps (PShape<16>) run pass 1 on each slot as it lands and
 // release it at once; 1 scalar warp merges the row's partials and runs the
 // token math. Nothing is re-read from L2: the slot ring is pure streaming.
 //
@@ -38,10 +38,12 @@
 // order — bitwise the same row statistics in both halves, no second
 // exchange. Rank 0 writes the per-token outputs.
 //
-// The same kernel with CL = 1 ("solo", rows up to 7 x 16,384 columns, e.g.
-// V = 32,000): one CTA owns the whole row, its 16 warp partials are merged
+// The same kernel with CL = 1 ("solo", rows up to 7 x 8,192 columns, e.g.
+// V = 32,000): one CTA owns the whole row, its warp partials are merged
 // locally and nothing crosses DSMEM; it replaces the two exponentials per
-// element of the row-resident TMA kernel with one.
+// element of the row-resident TMA kernel with one. The solo CTA has 8
+// consumer warps and 16 KB slots (PShape<8>: 104 KB of shared memory, 256
+// TMEM columns), so two CTAs share an SM and overlap each other's phases.
 //
 // Small steps (<= 8,192 tokens) reduce obj/flags into out4 in the launch's
 // last CTA (reduce.cuh), bitwise what reduce_kernel produces.
