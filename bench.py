@@ -44,6 +44,8 @@ def parse_args():
     ap.add_argument("--config", default="grpo_128x8_v151936")
     ap.add_argument("--chunk-rows", type=int, default=32768)
     ap.add_argument("--unfused", action="store_true", help="K1 -> K2 -> K3 instead of the fused kernel")
+    ap.add_argument("--vocab", type=int, default=None,
+                    help="override the config's vocabulary (a vocabulary sweep; not a BASELINE config)")
     ap.add_argument("--dlogits", choices=["bf16", "f32"], default="bf16",
                     help="f32: the parity mode (dlogits within 1e-5; 6V+16 B/token)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -289,6 +291,8 @@ def run_ours(args):
             raise SystemExit(f"bench.py: communicator has {comm} ranks, --gpus {args.gpus}")
 
     cfgd = dict(CONFIGS[args.config])
+    if args.vocab:
+        cfgd["vocab"] = args.vocab
     V = cfgd["vocab"]
     strong = cfgd.pop("strong", False)
     P_cfg = cfgd.pop("P")
@@ -415,7 +419,7 @@ def run_ours(args):
     bytes_per_tok = (6 if args.dlogits == "f32" else 4) * V + 16
     achieved = rows_timed * bytes_per_tok / (kern_ms / 1e3) / 1e9
     peak, peak_src = measured_peaks()
-    tr = traffic_per_row(args.config, args.unfused, info.get("kernel", ""), args.dlogits)
+    tr = None if args.vocab else traffic_per_row(args.config, args.unfused, info.get("kernel", ""), args.dlogits)
 
     line = None
     if rank == 0:
@@ -426,7 +430,7 @@ def run_ours(args):
             "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic",
             "config": {
-                "workload": describe(args.config),
+                "workload": describe(args.config) + (f" [vocab overridden: {V}]" if args.vocab else ""),
                 "prompts": P_global, "responses": G, "vocab": V, "tokens_global": T_global,
                 "tokens_rank0": T, "chunk_rows": chunk, "chunks_per_step": nchunks,
                 "parallelism": f"dp{world} (whole prompt groups, LPT by tokens)",

@@ -1096,19 +1096,22 @@ cudaError_t launch_fused(const LossParams& p, DType in, DType out, int num_sms, 
 cudaError_t launch_fused_kernel(const LossParams& p, DType in, DType out, int num_sms,
                                 const Tuning& tu, cudaStream_t stream, LaunchInfo* info) {
   if (p.n_rows == 0) return cudaSuccess;
-  // bf16 rows above 72 KB: the CTA-pair kernel (one HBM read, exponentials
-  // staged in TMEM, no L2 re-read) unless another kernel is forced
+  // bf16 rows, by size (fused_impl 0; 3 forces the pair kernel, 4 the solo):
+  //   56 KB .. 112 KB (V 28,672 .. 57,344, e.g. 32,000 / 50,304): the solo
+  //     kernel — one CTA per row, two 8-warp CTAs per SM;
+  //   above (e.g. 65,536 .. 229,376): the CTA-pair kernel, with 8-warp CTAs
+  //     (two per SM) while the half row fits them (V <= 114,688), else 16;
+  //   below, unaligned or with the entropy term: the TMA / ring / generic kernels.
+  // Same-box A/B in profiles/r02_vocab_sweep.txt (solo at V = 50,304: 0.92 vs
+  // 0.74 for the 16-warp pair; V = 32,000 sustained: solo 0.90 vs pair 0.86).
   const bool ent = p.entropy_coeff != 0.0;
-  if ((tu.fused_impl == 3 || (tu.fused_impl == 0 && static_cast<int64_t>(p.vocab) * 2 > 72 * 1024)) &&
-      pair_supported(p, in, out, ent, 2))
-    return launch_pair(p, out, 2, num_sms, tu, stream, info);
-  // 56-72 KB bf16 rows (e.g. V = 32,000): the solo kernel by default — on the
-  // bench configs of BASELINE #5 it matched or beat the TMA kernel on 5 of 6
-  // (one group x L = 256: 0.68 vs 0.66 of peak; profiles/r02_solo_vs_tma.txt)
   const int64_t row_bytes = static_cast<int64_t>(p.vocab) * 2;
-  const bool solo_auto = tu.fused_impl == 0 && row_bytes >= 56 * 1024 && row_bytes <= 72 * 1024;
+  const bool solo_auto = tu.fused_impl == 0 && row_bytes >= 56 * 1024 && pair_fits(p.vocab, 1, 8);
   if ((tu.fused_impl == 4 || solo_auto) && pair_supported(p, in, out, ent, 1))
     return launch_pair(p, out, 1, num_sms, tu, stream, info);
+  if ((tu.fused_impl == 3 || (tu.fused_impl == 0 && row_bytes > 72 * 1024)) &&
+      pair_supported(p, in, out, ent, 2))
+    return launch_pair(p, out, 2, num_sms, tu, stream, info);
   return p.entropy_coeff != 0.0 ? by_types<true>(false, p, in, out, num_sms, tu, stream, info)
                                 : by_types<false>(false, p, in, out, num_sms, tu, stream, info);
 }
@@ -1176,6 +1179,7 @@ const TuneField kFields[] = {
     {"pair_lookahead", "COPRIS_PAIR_LOOKAHEAD", 0, 7, &Tuning::pair_lookahead, nullptr},
     {"pair_st256", "COPRIS_PAIR_ST256", 0, 1, &Tuning::pair_st256, nullptr},
     {"pair_bf16_stage", "COPRIS_PAIR_BF16_STAGE", 0, 1, &Tuning::pair_bf16_stage, nullptr},
+    {"pair_pw8", "COPRIS_PAIR_PW8", 0, 1, &Tuning::pair_pw8, nullptr},
     {"lmhead_impl", "COPRIS_LMHEAD_IMPL", 0, 1, &Tuning::lmhead_impl, nullptr},
     {"lmhead_group", "COPRIS_LMHEAD_GROUP", 1, 1 << 20, &Tuning::lmhead_group, nullptr},
     {"lmhead_tma_store", "COPRIS_LMHEAD_TMA_STORE", 0, 1, &Tuning::lmhead_tma_store, nullptr},

@@ -623,10 +623,17 @@ bool pair_supported(const LossParams& p, DType in, DType out, bool ent, int cl) 
   const int64_t osz = out == DType::F32 ? 4 : 2, oal = out == DType::F32 ? 32 : 16;
   if (p.dlogits && ((p.ld_d * osz) % oal != 0 || reinterpret_cast<uintptr_t>(p.dlogits) % oal != 0))
     return false;
-  const int32_t slot_vec = cl == 2 ? PShape<16>::kPSlotVec : PShape<8>::kPSlotVec;
-  const int32_t nvec0 = cl == 2 ? (p.vocab / 8 + 1) / 2 : p.vocab / 8;
+  return pair_fits(p.vocab, cl, cl == 2 ? 16 : 8);
+}
+
+// Whether a row's part per CTA (half for cl = 2) fits the TMEM staging of a
+// CTA with `pw` consumer warps: at most kPTSlots - 1 slots, one left for the
+// lookahead.
+bool pair_fits(int32_t vocab, int cl, int pw) {
+  const int32_t slot_vec = pw == 16 ? PShape<16>::kPSlotVec : PShape<8>::kPSlotVec;
+  const int32_t nvec0 = cl == 2 ? (vocab / 8 + 1) / 2 : vocab / 8;
   const int32_t nseg = (nvec0 + slot_vec - 1) / slot_vec;
-  return nseg <= kPTSlots - 1;  // room for at least one lookahead slot in TMEM
+  return nseg <= kPTSlots - 1;
 }
 
 namespace {
@@ -688,7 +695,9 @@ cudaError_t launch_pair_pw(const LossParams& p, DType out, int num_sms, const Tu
     int ncl = 0;
     e = cudaOccupancyMaxActiveClusters(&ncl, reinterpret_cast<const void*>(kern), &cfg);
     if (e != cudaSuccess) return e;
-    slots = ncl;
+    // two 8-warp CTAs per SM: the API under-counts them as for the solo kernel
+    const int per_sm = ctas_per_sm(reinterpret_cast<const void*>(kern), (kPW + 2) * 32, smem, kPTmemCols);
+    slots = std::max<int64_t>(ncl, static_cast<int64_t>(per_sm) * (num_sms & ~1) / 2);
   } else {
     int per_sm = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(kern),
@@ -717,8 +726,10 @@ cudaError_t launch_pair_pw(const LossParams& p, DType out, int num_sms, const Tu
 
 cudaError_t launch_pair(const LossParams& p, DType out, int cl, int num_sms, const Tuning& tu,
                         cudaStream_t stream, LaunchInfo* info) {
-  return cl == 2 ? launch_pair_pw<16, 2>(p, out, num_sms, tu, stream, info)
-                 : launch_pair_pw<8, 1>(p, out, num_sms, tu, stream, info);
+  if (cl == 1) return launch_pair_pw<8, 1>(p, out, num_sms, tu, stream, info);
+  // half rows that fit the 8-warp shape (V <= 114,688) run two CTAs per SM
+  return pair_fits(p.vocab, 2, 8) && tu.pair_pw8 ? launch_pair_pw<8, 2>(p, out, num_sms, tu, stream, info)
+                                                 : launch_pair_pw<16, 2>(p, out, num_sms, tu, stream, info);
 }
 
 }  // namespace copris_b200

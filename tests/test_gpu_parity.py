@@ -37,8 +37,13 @@ SHAPES = [
     (151936, BF16, "pair+pl3+slots3", (PAIR, PAIR), None),  # short ring: producer waits on slots
     (200000, BF16, None, (PAIR, PAIR), None),
     (151952, BF16, "pair+st1", (PAIR, PAIR), None),  # second half not 32-byte aligned: 16-byte stores there         # 7 slots per half-row: the TMEM ring wraps every row
-    (80000, BF16, None, (PAIR, PAIR), None),          # 3 slots per half, partial last slot
-    (40000, BF16, None, (PAIR, PAIR), None),          # 80 KB rows: smallest pair vocab
+    (80000, BF16, None, (PAIR, PAIR), None),          # 8-warp pair CTAs (2 per SM): 5 slots per half
+    (40000, BF16, "pair", (PAIR, PAIR), None),        # 80 KB rows, forced pair (the solo's range)
+    (40000, BF16, None, "fused_solo_kernel", 1),      # 80 KB rows: solo by default
+    (57344, BF16, None, "fused_solo_kernel", 1),      # largest solo row: 7 slots of 8,192 columns
+    (57360, BF16, None, (PAIR, PAIR), None),          # one vector more: the pair kernel
+    (114688, BF16, None, (PAIR, PAIR), None),         # largest half row for 8-warp pair CTAs
+    (114704, BF16, None, (PAIR, PAIR), None),         # first 16-warp pair width
     (151936, BF16, "stream", "fused_stream_la_kernel", 1),  # the ring kernel forced for bf16 too
     (151936, BF16, "stream+la0", "fused_stream_la_kernel", 1),  # same without the lookahead
     (151936, BF16, "stream+la5", "fused_stream_la_kernel", 1),
