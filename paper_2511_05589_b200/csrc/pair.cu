@@ -390,28 +390,32 @@ __device__ __forceinline__ void p2_slot_f32(const RowBroadcast& b, bool zero_row
     dseg[rel] = b.dy;
 }
 
-// grid = 2 x clusters, cluster (2, 1, 1); block = (kPW + 2) warps. Dynamic
-// shared memory: nslots ring slots of 32 KB, then nml[kPTSlots][512] floats.
-// nvec0 = vectors of CTA rank 0 (rank 1 takes the rest); look = slots of row
-// r+1 run through pass 1 before pass 2 of row r.
+// grid = CL x clusters, cluster (CL, 1, 1); block = (PW + 2) warps. Dynamic
+// shared memory: nslots ring slots, then nml[kPTSlots][kPThreads] floats.
+// nvec0 = vectors of CTA ranks 0 .. CL-2 (the last rank takes the rest);
+// look = slots of row r+1 run through pass 1 before pass 2 of row r.
+// CL = 4 ("quad", rows too wide for a pair's TMEM staging, V > 229,376): every
+// consumer warp sends its partial to the three other CTAs; each scalar warp
+// merges the 64 entries in rank order (two per lane, then a butterfly).
 template <bool F32, int CL, bool BST, int PW>
 __global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
     fused_pair_kernel(const LossParams P, const int nslots, const int look, const int32_t nvec0,
                       const int st256) {
   COPRIS_PSHAPE(PW);
-  static_assert(CL == 1 || CL == 2, "a row is split over one or two CTAs");
+  static_assert(CL == 1 || CL == 2 || CL == 4, "a row is split over one, two or four CTAs");
+  constexpr int kNE = CL * PW;  // warp partials per row (entries of the exchange table)
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[16], empty[16], p1done[2], sdone[2];
-  __shared__ PairPart red[2][2 * PW];
+  __shared__ PairPart red[2][kNE];
   __shared__ RowBroadcast bc[2];
   __shared__ uint32_t tmem_slot;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = CL == 2 ? ptx::cluster_ctarank() : 0u, peer = rank ^ 1u;
+  const uint32_t rank = CL > 1 ? ptx::cluster_ctarank() : 0u;
   const int64_t cid = blockIdx.x / CL, ncl = gridDim.x / CL;
   const int32_t nvec_all = P.vocab / 8;
-  const int32_t vbase = rank ? nvec0 : 0;                  // first vector of this half
-  const int32_t nvec = rank ? nvec_all - nvec0 : nvec0;     // vectors of this half
+  const int32_t vbase = static_cast<int32_t>(rank) * nvec0;       // first vector of this part
+  const int32_t nvec = min(nvec0, nvec_all - vbase);               // vectors of this part
   const int32_t col0 = vbase * 8;
   const int32_t nseg = (nvec + kPSlotVec - 1) / kPSlotVec;
   const int32_t L = min(look, nseg);
@@ -430,7 +434,7 @@ __global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
       ptx::mbar_init(&empty[i], kPW);
     }
     for (int i = 0; i < 2; ++i) {
-      // 16 local warps + the scalar warp's arrive that expects the peer's 16 st.async entries
+      // the local warps + the scalar warp's arrive that expects the peers' st.async entries
       ptx::mbar_init(&p1done[i], kPW + 1);
       ptx::mbar_init(&sdone[i], 1);
     }
@@ -440,7 +444,7 @@ __global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
-  if constexpr (CL == 2) ptx::cluster_sync_all();  // the peer's barriers exist before any remote write
+  if constexpr (CL > 1) ptx::cluster_sync_all();  // the peers' barriers exist before any remote write
   const uint32_t tmem_base = grad ? tmem_slot : 0u;
 
   if (warp == kPW) {
@@ -471,16 +475,28 @@ __global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
       if (lane == 0) meta = mp.advance(P, r, ncl);
       const uint32_t bsel = i & 1u, par = (i >> 1) & 1u;
       if (lane == 0) {
-        if constexpr (CL == 2) ptx::mbar_arrive_expect_tx_u32(p1b + bsel * 8, kPW * sizeof(PairPart));
+        if constexpr (CL > 1) ptx::mbar_arrive_expect_tx_u32(p1b + bsel * 8, (CL - 1) * kPW * sizeof(PairPart));
         else ptx::mbar_arrive_u32(p1b + bsel * 8);
       }
       ptx::mbar_wait_sleep(p1b + bsel * 8, par);
-      // entry lane = rank * 16 + warp: same order in both CTAs (solo: lanes 16..31 empty)
-      const PairPart e = lane < CL * kPW ? red[bsel][lane] : PairPart{-INFINITY, 0.f, 0.f, 0.f};
+      // entry = rank * PW + warp: the same order in every CTA of the cluster
+      // (solo: lanes PW..31 empty; 4 x 16 entries: lane l merges l, then l + 32)
+      const PairPart e = lane < kNE ? red[bsel][lane] : PairPart{-INFINITY, 0.f, 0.f, 0.f};
       Lse tot{e.m, e.s, 0.f, 0.f};
+      bool have = e.have != 0.f;
+      float ezy = e.zy;
+      if constexpr (kNE > 32) {
+        static_assert(kNE <= 64, "two entries per lane at most");
+        const PairPart e2 = red[bsel][lane + 32];
+        lse_merge<false>(tot, Lse{e2.m, e2.s, 0.f, 0.f});
+        if (e2.have != 0.f) {
+          have = true;
+          ezy = e2.zy;
+        }
+      }
       warp_lse<false>(tot);
-      const uint32_t hv = __ballot_sync(0xffffffffu, e.have != 0.f);
-      float zy = __shfl_sync(0xffffffffu, e.zy, hv ? __ffs(hv) - 1 : 0);
+      const uint32_t hv = __ballot_sync(0xffffffffu, have);
+      float zy = __shfl_sync(0xffffffffu, ezy, hv ? __ffs(hv) - 1 : 0);
       if (lane == 0) {
         const bool ok = static_cast<uint32_t>(meta.y) < static_cast<uint32_t>(P.vocab);
         if (!ok) zy = 0.f;
@@ -503,8 +519,13 @@ __global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
                             static_cast<uint32_t>((warp >> 2) * (kPTSlots * 16));
     Ring ring(nslots);
     uint32_t ts = 0;  // TMEM slot of the next pass-1 slot (mod kPTSlots)
-    const uint32_t red_peer = CL == 2 ? ptx::mapa(ptx::smem_u32(&red[0][0]), peer) : 0u;
-    const uint32_t p1_peer = CL == 2 ? ptx::mapa(p1b, peer) : 0u;
+    uint32_t red_peer[CL > 1 ? CL - 1 : 1], p1_peer[CL > 1 ? CL - 1 : 1];
+#pragma unroll
+    for (int c = 1; c < CL; ++c) {  // the other CTAs of the cluster, in rank order after this one
+      const uint32_t pr = (rank + static_cast<uint32_t>(c)) % CL;
+      red_peer[c - 1] = ptx::mapa(ptx::smem_u32(&red[0][0]), pr);
+      p1_peer[c - 1] = ptx::mapa(p1b, pr);
+    }
     PhaseTimer tm;    // trace slots: 0 pass 1, 2 broadcast wait, 4 pass 2
     tm.start(P.trace && tid == 0 && blockIdx.x < kTraceCtas);
 
@@ -537,11 +558,13 @@ __global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
       const float zy = __shfl_sync(0xffffffffu, a.zy, hv ? __ffs(hv) - 1 : 0);
       if (lane == 0) {
         const uint32_t bsel = i & 1u;
-        const uint32_t off = (bsel * 2 * kPW + rank * kPW + warp) * sizeof(PairPart);
+        const uint32_t off = (bsel * kNE + rank * kPW + warp) * sizeof(PairPart);
         const float hvf = hv ? 1.f : 0.f;
         red[bsel][rank * kPW + warp] = PairPart{st.m, st.s, zy, hvf};
         ptx::mbar_arrive_u32(p1b + bsel * 8);
-        if constexpr (CL == 2) st_async_v4(red_peer + off, st.m, st.s, zy, hvf, p1_peer + bsel * 8);
+#pragma unroll
+        for (int c = 0; c < CL - 1; ++c)
+          st_async_v4(red_peer[c] + off, st.m, st.s, zy, hvf, p1_peer[c] + bsel * 8);
       }
     };
 
@@ -603,7 +626,7 @@ __global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
   // memory or a thread of its own still reads TMEM
   tc::fence_before_sync();
   __syncthreads();
-  if constexpr (CL == 2) ptx::cluster_sync_all();
+  if constexpr (CL > 1) ptx::cluster_sync_all();
   if (warp == 0 && grad) {
     tc::fence_after_sync();
     tc::tmem_dealloc<kPTmemCols>(tmem_base);
@@ -623,7 +646,9 @@ bool pair_supported(const LossParams& p, DType in, DType out, bool ent, int cl) 
   const int64_t osz = out == DType::F32 ? 4 : 2, oal = out == DType::F32 ? 32 : 16;
   if (p.dlogits && ((p.ld_d * osz) % oal != 0 || reinterpret_cast<uintptr_t>(p.dlogits) % oal != 0))
     return false;
-  return pair_fits(p.vocab, cl, cl == 2 ? 16 : 8);
+  // cl = 2: a CTA pair, or (rows too wide for the pair's TMEM staging, e.g.
+  // V = 256,000) a 4-CTA cluster
+  return cl == 2 ? pair_fits(p.vocab, 2, 16) || pair_fits(p.vocab, 4, 16) : pair_fits(p.vocab, 1, 8);
 }
 
 // Whether a row's part per CTA (half for cl = 2) fits the TMEM staging of a
@@ -631,7 +656,7 @@ bool pair_supported(const LossParams& p, DType in, DType out, bool ent, int cl) 
 // lookahead.
 bool pair_fits(int32_t vocab, int cl, int pw) {
   const int32_t slot_vec = pw == 16 ? PShape<16>::kPSlotVec : PShape<8>::kPSlotVec;
-  const int32_t nvec0 = cl == 2 ? (vocab / 8 + 1) / 2 : vocab / 8;
+  const int32_t nvec0 = (vocab / 8 + cl - 1) / cl;
   const int32_t nseg = (nvec0 + slot_vec - 1) / slot_vec;
   return nseg <= kPTSlots - 1;
 }
@@ -673,7 +698,7 @@ cudaError_t launch_pair_pw(const LossParams& p, DType out, int num_sms, const Tu
   const int smem = nslots * kPSlotBytes + kPTSlots * kPThreads * static_cast<int>(sizeof(float));
   cudaError_t e = allow_dyn_smem(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) return e;
-  const int32_t nvec0 = cl == 2 ? (p.vocab / 8 + 1) / 2 : p.vocab / 8;
+  const int32_t nvec0 = (p.vocab / 8 + cl - 1) / cl;  // vectors per CTA (the last takes the rest)
   const int32_t nseg = (nvec0 + kPSlotVec - 1) / kPSlotVec;
   int look = tu.pair_lookahead;
   if (look > kPTSlots - nseg) look = kPTSlots - nseg;
@@ -685,19 +710,25 @@ cudaError_t launch_pair_pw(const LossParams& p, DType out, int num_sms, const Tu
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = cl == 2 ? 1 : 0;
+  cfg.numAttrs = cl > 1 ? 1 : 0;
   cfg.blockDim = dim3((kPW + 2) * 32);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   int64_t slots = 0;  // resident rows-in-flight units (CTA pairs or CTAs)
-  if (cl == 2) {
-    cfg.gridDim = dim3(static_cast<unsigned>(num_sms & ~1));
+  if (cl > 1) {
+    const int sms = num_sms / cl * cl;
+    cfg.gridDim = dim3(static_cast<unsigned>(sms));
     int ncl = 0;
     e = cudaOccupancyMaxActiveClusters(&ncl, reinterpret_cast<const void*>(kern), &cfg);
     if (e != cudaSuccess) return e;
-    // two 8-warp CTAs per SM: the API under-counts them as for the solo kernel
-    const int per_sm = ctas_per_sm(reinterpret_cast<const void*>(kern), (kPW + 2) * 32, smem, kPTmemCols);
-    slots = std::max<int64_t>(ncl, static_cast<int64_t>(per_sm) * (num_sms & ~1) / 2);
+    slots = ncl;
+    if (PW == 8) {
+      // two 8-warp CTAs per SM: the API under-counts them as for the solo kernel
+      const int per_sm = ctas_per_sm(reinterpret_cast<const void*>(kern), (kPW + 2) * 32, smem, kPTmemCols);
+      slots = std::max<int64_t>(ncl, static_cast<int64_t>(per_sm) * sms / cl);
+    }
+    // (4-CTA clusters: the API's count is the truth — GPC placement leaves some
+    // SMs without a whole cluster, and launching more than fit runs a second wave)
   } else {
     int per_sm = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(kern),
@@ -717,7 +748,7 @@ cudaError_t launch_pair_pw(const LossParams& p, DType out, int num_sms, const Tu
   if (info) {
     info->cluster = cl;
     info->grid = static_cast<int>(cl * nc);
-    info->kernel = cl == 2 ? "fused_pair_kernel" : "fused_solo_kernel";
+    info->kernel = cl == 4 ? "fused_quad_kernel" : cl == 2 ? "fused_pair_kernel" : "fused_solo_kernel";
     info->reduced = fuse ? 1 : 0;
   }
   return cudaLaunchKernelEx(&cfg, kern, q, nslots, look, nvec0, tu.pair_st256);
@@ -727,9 +758,11 @@ cudaError_t launch_pair_pw(const LossParams& p, DType out, int num_sms, const Tu
 cudaError_t launch_pair(const LossParams& p, DType out, int cl, int num_sms, const Tuning& tu,
                         cudaStream_t stream, LaunchInfo* info) {
   if (cl == 1) return launch_pair_pw<8, 1>(p, out, num_sms, tu, stream, info);
-  // half rows that fit the 8-warp shape (V <= 114,688) run two CTAs per SM
-  return pair_fits(p.vocab, 2, 8) && tu.pair_pw8 ? launch_pair_pw<8, 2>(p, out, num_sms, tu, stream, info)
-                                                 : launch_pair_pw<16, 2>(p, out, num_sms, tu, stream, info);
+  // half rows that fit the 8-warp shape (V <= 114,688) run two CTAs per SM;
+  // rows too wide for a 16-warp pair (V > 229,376) split over 4 CTAs
+  if (pair_fits(p.vocab, 2, 8) && tu.pair_pw8) return launch_pair_pw<8, 2>(p, out, num_sms, tu, stream, info);
+  if (pair_fits(p.vocab, 2, 16)) return launch_pair_pw<16, 2>(p, out, num_sms, tu, stream, info);
+  return launch_pair_pw<16, 4>(p, out, num_sms, tu, stream, info);
 }
 
 }  // namespace copris_b200

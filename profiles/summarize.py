@@ -66,6 +66,8 @@ def ncu_summary(rep, dst_prefix, rows_per_launch):
             targs = [a.strip() for a in name.split("<", 1)[1].split(">")[0].split(",")]
             if len(targs) >= 2 and targs[1] == "1":
                 short = "fused_solo_kernel"
+            elif len(targs) >= 2 and targs[1] == "4":
+                short = "fused_quad_kernel"
         lines = [f"kernel: {name}"]
         for k in KEYS:
             if k in hdr:

@@ -23,6 +23,7 @@ def run(ctx, case, dl_dtype=BF16, fused=True, **kw):
 
 # (V, logits dtype, forced implementation or None, expected kernel, expected cluster)
 PAIR = ("fused_pair_kernel", 2)
+QUAD = ("fused_quad_kernel", 4)
 SHAPES = [
     # Qwen2.5 vocab: the CTA-pair kernel for bf16 logits, with f16 exponentials
     # (bf16 dlogits) or the raw logits (fp32 dlogits) staged in TMEM
@@ -44,6 +45,10 @@ SHAPES = [
     (57360, BF16, None, (PAIR, PAIR), None),          # one vector more: the pair kernel
     (114688, BF16, None, (PAIR, PAIR), None),         # largest half row for 8-warp pair CTAs
     (114704, BF16, None, (PAIR, PAIR), None),         # first 16-warp pair width
+    (229376, BF16, None, (PAIR, PAIR), None),         # widest pair row: 7 slots per half
+    (229392, BF16, None, (QUAD, QUAD), None),         # one vector more: a 4-CTA cluster per row
+    (256000, BF16, None, (QUAD, QUAD), None),         # Gemma-size vocabulary
+    (458752, BF16, None, (QUAD, QUAD), None),         # widest quad row: 7 slots per quarter
     (151936, BF16, "stream", "fused_stream_la_kernel", 1),  # the ring kernel forced for bf16 too
     (151936, BF16, "stream+la0", "fused_stream_la_kernel", 1),  # same without the lookahead
     (151936, BF16, "stream+la5", "fused_stream_la_kernel", 1),
@@ -761,6 +766,9 @@ def test_far_off_policy_ratios(ctx, oracle, impl):
     (151952, None, "fused_pair_kernel", [0, 75975, 75976, 75977, 151951]),  # odd nvec0
     (32000, None, "fused_solo_kernel", [0, 1, 16383, 16384, 31999, 31998]),
     (32000, "tma", "fused_tma_kernel", [0, 1, 16383, 16384, 31999]),
+    # quad: quarters of 8,000 vectors (64,000 columns)
+    (256000, None, "fused_quad_kernel", [0, 63999, 64000, 64001, 127999, 128000, 191999, 192000,
+                                         192000 + 16384, 255999]),
 ])
 @pytest.mark.parametrize("dl_dtype", [BF16, F32])
 def test_target_at_vector_slot_and_half_boundaries(ctx, oracle, impl, V, force, kernel, targets,
