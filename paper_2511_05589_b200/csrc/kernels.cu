@@ -1097,16 +1097,18 @@ cudaError_t launch_fused_kernel(const LossParams& p, DType in, DType out, int nu
                                 const Tuning& tu, cudaStream_t stream, LaunchInfo* info) {
   if (p.n_rows == 0) return cudaSuccess;
   // bf16 rows, by size (fused_impl 0; 3 forces the pair kernel, 4 the solo):
-  //   56 KB .. 112 KB (V 28,672 .. 57,344, e.g. 32,000 / 50,304): the solo
+  //   4 KB .. 112 KB (V 2,048 .. 57,344, e.g. 32,000 / 50,304): the solo
   //     kernel — one CTA per row, two 8-warp CTAs per SM;
   //   above (e.g. 65,536 .. 229,376): the CTA-pair kernel, with 8-warp CTAs
   //     (two per SM) while the half row fits them (V <= 114,688), else 16;
   //   below, unaligned or with the entropy term: the TMA / ring / generic kernels.
   // Same-box A/B in profiles/r02_vocab_sweep.txt (solo at V = 50,304: 0.92 vs
-  // 0.74 for the 16-warp pair; V = 32,000 sustained: solo 0.90 vs pair 0.86).
+  // 0.74 for the 16-warp pair; V = 32,000 sustained: solo 0.90 vs pair 0.86;
+  // solo vs the TMA kernel at V = 2,048 / 8,192 / 16,384 / 24,576: 136 / 128 /
+  // 91 / 57 M rows/s vs 119 / 97 / 71 / 52).
   const bool ent = p.entropy_coeff != 0.0;
   const int64_t row_bytes = static_cast<int64_t>(p.vocab) * 2;
-  const bool solo_auto = tu.fused_impl == 0 && row_bytes >= 56 * 1024 && pair_fits(p.vocab, 1, 8);
+  const bool solo_auto = tu.fused_impl == 0 && row_bytes >= 4 * 1024 && pair_fits(p.vocab, 1, 8);
   if ((tu.fused_impl == 4 || solo_auto) && pair_supported(p, in, out, ent, 1))
     return launch_pair(p, out, 1, num_sms, tu, stream, info);
   if ((tu.fused_impl == 3 || (tu.fused_impl == 0 && row_bytes > 72 * 1024)) &&
