@@ -55,6 +55,9 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "fused_common.cuh"
 #include "kernels.cuh"
@@ -668,8 +671,18 @@ namespace {
 // co-resident CTAs, one group x L = 256 at 0.78 instead of 0.66 of peak).
 int ctas_per_sm(const void* kern, int threads, int dyn_smem, int tmem_cols) {
   int dev = 0, smem_sm = 0, regs_sm = 0, thr_sm = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 1;
+  // cached per (kernel, device, shared memory): the answer is static
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, int>, int> cache;
+  const auto key = std::make_tuple(kern, dev, dyn_smem);
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    const auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
   cudaFuncAttributes fa{};
-  if (cudaGetDevice(&dev) != cudaSuccess || cudaFuncGetAttributes(&fa, kern) != cudaSuccess) return 1;
+  if (cudaFuncGetAttributes(&fa, kern) != cudaSuccess) return 1;
   cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
   cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
   cudaDeviceGetAttribute(&thr_sm, cudaDevAttrMaxThreadsPerMultiProcessor, dev);
@@ -679,7 +692,10 @@ int ctas_per_sm(const void* kern, int threads, int dyn_smem, int tmem_cols) {
   if (regs > 0) n = std::min(n, regs_sm / regs);
   n = std::min(n, thr_sm / threads);
   n = std::min(n, 512 / tmem_cols);
-  return n < 1 ? 1 : n;
+  n = n < 1 ? 1 : n;
+  std::lock_guard<std::mutex> lock(mu);
+  cache[key] = n;
+  return n;
 }
 
 template <int PW, int CL>
