@@ -49,6 +49,8 @@ SHAPES = [
     (229392, BF16, None, (QUAD, QUAD), None),         # one vector more: a 4-CTA cluster per row
     (256000, BF16, None, (QUAD, QUAD), None),         # Gemma-size vocabulary
     (458752, BF16, None, (QUAD, QUAD), None),         # widest quad row: 7 slots per quarter
+    (458768, BF16, None, "fused_stream_la_kernel", 1),  # wider: the ring kernel (any width)
+    (151944, BF16, None, "fused_stream_la_kernel", 1),  # 16-byte rows but V % 16 != 0: the ring kernel
     (151936, BF16, "stream", "fused_stream_la_kernel", 1),  # the ring kernel forced for bf16 too
     (151936, BF16, "stream+la0", "fused_stream_la_kernel", 1),  # same without the lookahead
     (151936, BF16, "stream+la5", "fused_stream_la_kernel", 1),
