@@ -1102,6 +1102,8 @@ cudaError_t launch_fused_kernel(const LossParams& p, DType in, DType out, int nu
   //   above (e.g. 65,536 .. 229,376): the CTA-pair kernel, with 8-warp CTAs
   //     (two per SM) while the half row fits them (V <= 114,688), else 16;
   //   below, unaligned or with the entropy term: the TMA / ring / generic kernels.
+  // K1 (gather-only) takes the same shape as the loss at its vocabulary: its
+  // log-probs are bitwise the loss kernel's recomputation.
   // Same-box A/B in profiles/r02_vocab_sweep.txt (solo at V = 50,304: 0.92 vs
   // 0.74 for the 16-warp pair; V = 32,000 sustained: solo 0.90 vs pair 0.86;
   // solo vs the TMA kernel at V = 2,048 / 8,192 / 16,384 / 24,576: 136 / 128 /

@@ -650,7 +650,10 @@ bool pair_supported(const LossParams& p, DType in, DType out, bool ent, int cl) 
   if (p.dlogits && ((p.ld_d * osz) % oal != 0 || reinterpret_cast<uintptr_t>(p.dlogits) % oal != 0))
     return false;
   // cl = 2: a CTA pair, or (rows too wide for the pair's TMEM staging, e.g.
-  // V = 256,000) a 4-CTA cluster
+  // V = 256,000) a 4-CTA cluster. K1 (gather-only) and forward-only launches
+  // take the SAME kernel shape as the loss at their vocabulary, so their
+  // log-probs are bitwise the loss kernel's recomputation (test_policy.cpp:157-172;
+  // a solo K1 at V = 151,936 was also slower: 0.73 vs 0.80)
   return cl == 2 ? pair_fits(p.vocab, 2, 16) || pair_fits(p.vocab, 4, 16) : pair_fits(p.vocab, 1, 8);
 }
 
@@ -719,6 +722,10 @@ cudaError_t launch_pair_pw(const LossParams& p, DType out, int num_sms, const Tu
   int look = tu.pair_lookahead;
   if (look > kPTSlots - nseg) look = kPTSlots - nseg;
   if (look < 0) look = 0;
+  // no dlogits (K1's gather-only mode, forward-only losses): nothing is staged
+  // in TMEM, so pass 1 of the whole next row may run before this row's scalar
+  // phase is awaited
+  if (p.dlogits == nullptr || p.gather_only) look = nseg;
   cudaLaunchConfig_t cfg{};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
