@@ -48,6 +48,8 @@ def parse_args():
                     help="override the config's vocabulary (a vocabulary sweep; not a BASELINE config)")
     ap.add_argument("--dlogits", choices=["bf16", "f32"], default="bf16",
                     help="f32: the parity mode (dlogits within 1e-5; 6V+16 B/token)")
+    ap.add_argument("--entropy-coeff", type=float, default=0.0,
+                    help="grpo.entropy_coeff (grpo.hpp:168-181); the headline configs use 0 (desk.json)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-tokens", type=int, default=16384, help="per-rank sample for the host round trip")
@@ -309,7 +311,7 @@ def run_ours(args):
     nchunks = (T + chunk - 1) // chunk
 
     ctx = Copris(local)
-    clip = ClipConfig()
+    clip = ClipConfig(entropy_coeff=args.entropy_coeff)
     # resident logits chunk buffer; token t of the local batch reads buffer row
     # t % chunk, whose target column is the boosted one.
     g = torch.Generator(device="cpu")
@@ -419,7 +421,7 @@ def run_ours(args):
     bytes_per_tok = (6 if args.dlogits == "f32" else 4) * V + 16
     achieved = rows_timed * bytes_per_tok / (kern_ms / 1e3) / 1e9
     peak, peak_src = measured_peaks()
-    tr = None if args.vocab else traffic_per_row(args.config, args.unfused, info.get("kernel", ""), args.dlogits)
+    tr = None if args.vocab or args.entropy_coeff else traffic_per_row(args.config, args.unfused, info.get("kernel", ""), args.dlogits)
 
     line = None
     if rank == 0:
@@ -441,6 +443,7 @@ def run_ours(args):
                                        f"of logits and writes as much dlogits (chunk buffer "
                                        f"{chunk * V * 2 / 1e6:.0f} MB; L2 126 MB); no flush"),
                 "loss": loss,
+                **({"entropy_coeff": args.entropy_coeff} if args.entropy_coeff else {}),
                 "offpolicy_fraction": out4[2].item() / out4[1].item() if out4[1].item() else 0.0,
                 "clipped_tokens": int(out4[3].item()),
                 "dlogits": ("f32 (parity mode: within 1e-5; 6V+16 B/token)" if args.dlogits == "f32"

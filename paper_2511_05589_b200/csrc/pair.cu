@@ -58,6 +58,7 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <type_traits>
 
 #include "fused_common.cuh"
 #include "kernels.cuh"
@@ -155,11 +156,21 @@ __device__ __forceinline__ void tmem_wait_st() {
 struct __align__(16) PairPart {
   float m, s, zy, have;
 };
+// The entropy term's extra per-warp partial: u = sum e (z - m) (same frame as s).
+struct __align__(16) PairPartU {
+  float u, pad0, pad1, pad2;
+};
+
+constexpr float kLn2 = 0.69314718055994531f;
+// bf16x2 {-9.9e29, -9.9e29}: -inf columns clamped to it stay finite through
+// (z - m) log2(e) (the lowest finite bf16 would overflow to -inf there)
+constexpr uint32_t kClampLo2 = 0xF149F149u;
 
 // Lane state of pass 1: running max and the lane's sum of 2^15-scaled
 // exponentials relative to it.
 struct LaneAcc {
   float m = -INFINITY, s = 0.f;
+  float u = 0.f;  // entropy term only: sum e (z - m), natural-log units
   float zy = 0.f;
   bool have = false;
 };
@@ -182,7 +193,7 @@ __device__ __forceinline__ void kill_col(uint32_t& w, int jt, int k, float& zy) 
 // STORE: stage the f16 exponentials in TMEM at taddr (16 columns). Returns
 // nml = 15 - m log2(e) of this thread's columns (+inf when it saw no finite
 // column) for pass 2.
-template <bool STORE, bool RAW, bool BST, int PW>
+template <bool STORE, bool RAW, bool BST, int PW, bool ENT = false>
 __device__ __forceinline__ float p1_slot(LaneAcc& a, uint32_t sb, int32_t v0, int32_t cnt,
                                          int32_t ycol, int tid, uint32_t taddr) {
   COPRIS_PSHAPE(PW);
@@ -196,6 +207,19 @@ __device__ __forceinline__ float p1_slot(LaneAcc& a, uint32_t sb, int32_t v0, in
       const int32_t j = tid + q * kPThreads;
       raw[q] = j < cnt ? ptx::lds_v4(sb + j * 16) : uint4{kNegInf2, kNegInf2, kNegInf2, kNegInf2};
     }
+  }
+  if (STORE && RAW) {
+    // the logits themselves, target column included (pass 2 overwrites it with
+    // the one-hot term; the entropy term there needs p_y)
+    uint32_t h[16];
+#pragma unroll
+    for (int q = 0; q < kPK; ++q) {
+      h[q * 4 + 0] = raw[q].x;
+      h[q * 4 + 1] = raw[q].y;
+      h[q * 4 + 2] = raw[q].z;
+      h[q * 4 + 3] = raw[q].w;
+    }
+    tmem_st_x16(taddr, h);
   }
   // the target column: record z_y, then keep it out of the max and the sum
   if (static_cast<uint32_t>(ycol - v0 * 8) < static_cast<uint32_t>(cnt * 8)) {
@@ -211,17 +235,6 @@ __device__ __forceinline__ float p1_slot(LaneAcc& a, uint32_t sb, int32_t v0, in
       }
     }
   }
-  if (STORE && RAW) {  // the logits themselves (target column already -inf: p = 0 there)
-    uint32_t h[16];
-#pragma unroll
-    for (int q = 0; q < kPK; ++q) {
-      h[q * 4 + 0] = raw[q].x;
-      h[q * 4 + 1] = raw[q].y;
-      h[q * 4 + 2] = raw[q].z;
-      h[q * 4 + 3] = raw[q].w;
-    }
-    tmem_st_x16(taddr, h);
-  }
   uint32_t mx = ptx::bmax2(ptx::bmax2(raw[0].x, raw[0].y), ptx::bmax2(raw[0].z, raw[0].w));
 #pragma unroll
   for (int q = 1; q < kPK; ++q)
@@ -232,15 +245,20 @@ __device__ __forceinline__ float p1_slot(LaneAcc& a, uint32_t sb, int32_t v0, in
   const float nml = fmaf(-(fin ? ml : 0.f), kLog2e, 15.f);
   const uint64_t l2e = ptx::f2(kLog2e, kLog2e), nml2 = ptx::f2(nml, nml);
   uint64_t acc0 = 0, acc1 = 0;  // two packed fp32 partial sums (0.0f bits)
+  uint64_t accu = 0;            // entropy: sum e d, d = (z - ml) log2(e) + 15
   uint32_t h[16];
 #pragma unroll
   for (int q = 0; q < kPK; ++q) {
     const uint32_t w[4] = {raw[q].x, raw[q].y, raw[q].z, raw[q].w};
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const uint64_t e = ptx::ex2x2(ptx::ffma2(ptx::bf16x2_to_f2(w[k]), l2e, nml2));
+      // entropy: -inf columns clamped to a huge finite negative (after the max):
+      // e is still 0 there and e d = 0 instead of NaN
+      const uint64_t d = ptx::ffma2(ptx::bf16x2_to_f2(ENT ? ptx::bmax2(w[k], kClampLo2) : w[k]), l2e, nml2);
+      const uint64_t e = ptx::ex2x2(d);
       if (k & 1) acc1 = ptx::fadd2(acc1, e);
       else acc0 = ptx::fadd2(acc0, e);
+      if (ENT) accu = ptx::ffma2(e, d, accu);
       if (STORE && !RAW) h[q * 4 + k] = BST ? ptx::f2_to_bf16x2(e) : f2_to_f16x2(e);
     }
   }
@@ -252,6 +270,12 @@ __device__ __forceinline__ float p1_slot(LaneAcc& a, uint32_t sb, int32_t v0, in
   if (mn != -INFINITY) {
     const float ra = a.m == -INFINITY ? 0.f : ptx::ex2((a.m - mn) * kLog2e);
     const float rl = fin ? ptx::ex2((ml - mn) * kLog2e) : 0.f;
+    if (ENT) {
+      // slot: u_l = sum e (z - ml) = ln2 (sum e d - 15 sl); both parts to frame mn
+      const float ul = fin ? kLn2 * ((ptx::f2lo(accu) + ptx::f2hi(accu)) - 15.f * sl) : 0.f;
+      const float ua = a.m == -INFINITY ? 0.f : ra * fmaf(a.s, a.m - mn, a.u);
+      a.u = ua + (fin ? rl * fmaf(sl, ml - mn, ul) : 0.f);
+    }
     a.s = fmaf(a.s, ra, sl * rl);
     a.m = mn;
   }
@@ -393,6 +417,72 @@ __device__ __forceinline__ void p2_slot_f32(const RowBroadcast& b, bool zero_row
     dseg[rel] = b.dy;
 }
 
+// Pass 2 with the entropy term (entropy_coeff != 0): the staged raw logits
+// through row_grad (fused_common.cuh), the same per-column arithmetic as the
+// other fused kernels, f32 or bf16 out; c0 = absolute column of vector v0.
+template <int PW, typename TOut>
+__device__ __forceinline__ void p2_slot_ent(const RowBroadcast& b, bool zero_row, uint32_t taddr,
+                                            int32_t v0, int32_t cnt, int32_t ycol, TOut* dseg, int tid) {
+  COPRIS_PSHAPE(PW);
+  constexpr bool kF32 = sizeof(TOut) == 4;
+  TOut* base = dseg + static_cast<int64_t>(tid) * 8;
+  uint32_t h[16];
+  if (!zero_row) {
+    tmem_ld_x16(taddr, h);
+    tc::tmem_wait_ld();
+  }
+  // d_k = p_k (eg (x_k + k0) - coef), x = z - m, p = 2^(x log2(e) - log2 S):
+  // row_grad's arithmetic, two columns per packed op; -inf columns clamped
+  // (kClampLo2) give p = 0 and d = 0 (row_grad's p > 0 guard)
+  const uint64_t nm2 = ptx::f2(-b.m, -b.m), l2e = ptx::f2(kLog2e, kLog2e);
+  const uint64_t nls2 = ptx::f2(-b.log2s, -b.log2s), eg2 = ptx::f2(b.eg, b.eg);
+  const float c0 = fmaf(b.eg, b.k0, -b.coef);
+  const uint64_t c02 = ptx::f2(c0, c0);
+  const int32_t rel = ycol - v0 * 8;
+  const bool own_y = static_cast<uint32_t>(rel) < static_cast<uint32_t>(cnt * 8) &&
+                     ((rel >> 3) & (kPThreads - 1)) == tid;
+#pragma unroll
+  for (int q = 0; q < kPK; ++q) {
+    if (cnt == kPSlotVec || tid + q * kPThreads < cnt) {
+      uint64_t d2[4] = {0, 0, 0, 0};
+      if (!zero_row) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint64_t x = ptx::fadd2(ptx::bf16x2_to_f2(ptx::bmax2(h[q * 4 + k], kClampLo2)), nm2);
+          const uint64_t pk = ptx::ex2x2(ptx::ffma2(x, l2e, nls2));
+          d2[k] = ptx::fmul2(pk, ptx::ffma2(eg2, x, c02));
+        }
+        // the target column: coef (1 - p_y) + the entropy term (row_grad)
+        if (own_y && (rel >> 3) == tid + q * kPThreads) {
+          // register-only selects (a dynamic index would put h and d2 in local memory)
+          const int jy = rel & 7, ky = jy >> 1;
+          uint32_t wy = h[q * 4];
+#pragma unroll
+          for (int k = 1; k < 4; ++k) wy = ky == k ? h[q * 4 + k] : wy;
+          const float zy = (jy & 1) ? ptx::bf16_hi(wy) : ptx::bf16_lo(wy);
+          const float xm = zy - b.m;
+          const float py = ptx::ex2(fmaf(xm, kLog2e, -b.log2s));
+          const float vy = py > 0.f ? fmaf(b.eg * py, xm + b.k0, b.dy) : b.dy;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t pk = (jy & 1) ? ptx::f2(ptx::f2lo(d2[k]), vy) : ptx::f2(vy, ptx::f2hi(d2[k]));
+            d2[k] = ky == k ? pk : d2[k];
+          }
+        }
+      }
+      if constexpr (kF32) {
+        const float d[8] = {ptx::f2lo(d2[0]), ptx::f2hi(d2[0]), ptx::f2lo(d2[1]), ptx::f2hi(d2[1]),
+                            ptx::f2lo(d2[2]), ptx::f2hi(d2[2]), ptx::f2lo(d2[3]), ptx::f2hi(d2[3])};
+        ptx::st_global_cs_v8f(reinterpret_cast<float*>(base) + q * kPThreads * 8, d);
+      } else {
+        const uint4 o{ptx::f2_to_bf16x2(d2[0]), ptx::f2_to_bf16x2(d2[1]), ptx::f2_to_bf16x2(d2[2]),
+                      ptx::f2_to_bf16x2(d2[3])};
+        ptx::st_global_cs_v4(reinterpret_cast<__nv_bfloat16*>(base) + q * kPThreads * 8, o);
+      }
+    }
+  }
+}
+
 // grid = CL x clusters, cluster (CL, 1, 1); block = (PW + 2) warps. Dynamic
 // shared memory: nslots ring slots, then nml[kPTSlots][kPThreads] floats.
 // nvec0 = vectors of CTA ranks 0 .. CL-2 (the last rank takes the rest);
@@ -400,7 +490,7 @@ __device__ __forceinline__ void p2_slot_f32(const RowBroadcast& b, bool zero_row
 // CL = 4 ("quad", rows too wide for a pair's TMEM staging, V > 229,376): every
 // consumer warp sends its partial to the three other CTAs; each scalar warp
 // merges the 64 entries in rank order (two per lane, then a butterfly).
-template <bool F32, int CL, bool BST, int PW>
+template <bool F32, int CL, bool BST, int PW, bool ENT>
 __global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
     fused_pair_kernel(const LossParams P, const int nslots, const int look, const int32_t nvec0,
                       const int st256) {
@@ -410,6 +500,8 @@ __global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[16], empty[16], p1done[2], sdone[2];
   __shared__ PairPart red[2][kNE];
+  __shared__ PairPartU redu[2][ENT ? kNE : 1];  // entropy: the u of each entry
+  constexpr bool kRaw = F32 || ENT;             // stage the raw logits for pass 2
   __shared__ RowBroadcast bc[2];
   __shared__ uint32_t tmem_slot;
 
@@ -478,26 +570,29 @@ __global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
       if (lane == 0) meta = mp.advance(P, r, ncl);
       const uint32_t bsel = i & 1u, par = (i >> 1) & 1u;
       if (lane == 0) {
-        if constexpr (CL > 1) ptx::mbar_arrive_expect_tx_u32(p1b + bsel * 8, (CL - 1) * kPW * sizeof(PairPart));
+        if constexpr (CL > 1)
+          ptx::mbar_arrive_expect_tx_u32(p1b + bsel * 8,
+                                         (CL - 1) * kPW * (sizeof(PairPart) + (ENT ? sizeof(PairPartU) : 0)));
         else ptx::mbar_arrive_u32(p1b + bsel * 8);
       }
       ptx::mbar_wait_sleep(p1b + bsel * 8, par);
       // entry = rank * PW + warp: the same order in every CTA of the cluster
       // (solo: lanes PW..31 empty; 4 x 16 entries: lane l merges l, then l + 32)
+      // (entropy: u and a = s of the non-target columns; the target joins below)
       const PairPart e = lane < kNE ? red[bsel][lane] : PairPart{-INFINITY, 0.f, 0.f, 0.f};
-      Lse tot{e.m, e.s, 0.f, 0.f};
+      Lse tot{e.m, e.s, ENT && lane < kNE ? redu[bsel][lane % kNE].u : 0.f, ENT ? e.s : 0.f};
       bool have = e.have != 0.f;
       float ezy = e.zy;
       if constexpr (kNE > 32) {
         static_assert(kNE <= 64, "two entries per lane at most");
         const PairPart e2 = red[bsel][lane + 32];
-        lse_merge<false>(tot, Lse{e2.m, e2.s, 0.f, 0.f});
+        lse_merge<ENT>(tot, Lse{e2.m, e2.s, ENT ? redu[bsel][(lane + 32) % kNE].u : 0.f, ENT ? e2.s : 0.f});
         if (e2.have != 0.f) {
           have = true;
           ezy = e2.zy;
         }
       }
-      warp_lse<false>(tot);
+      warp_lse<ENT>(tot);
       const uint32_t hv = __ballot_sync(0xffffffffu, have);
       float zy = __shfl_sync(0xffffffffu, ezy, hv ? __ffs(hv) - 1 : 0);
       if (lane == 0) {
@@ -506,10 +601,22 @@ __global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
         // the target column stayed out of every thread's max: fold it into M
         // so that M >= z_y as finish_logprob assumes
         if (ok && hv && zy > tot.m) {
-          tot.s = tot.m == -INFINITY ? 0.f : tot.s * ptx::ex2((tot.m - zy) * kLog2e);
+          const float rz = ptx::ex2((tot.m - zy) * kLog2e);
+          if (ENT) {
+            tot.u = tot.m == -INFINITY ? 0.f : rz * fmaf(tot.a, tot.m - zy, tot.u);
+            tot.a = tot.m == -INFINITY ? 0.f : tot.a * rz;
+          }
+          tot.s = tot.m == -INFINITY ? 0.f : tot.s * rz;
           tot.m = zy;
         }
-        bc[bsel] = row_scalar_phase<false>(P, P.row_base + r, meta.y, meta.st, meta.blp, meta.rl,
+        if (ENT && ok && hv) {  // u and a run over every column (fused_common.cuh Lse)
+          const float ey = ptx::ex2((zy - tot.m) * kLog2e);
+          if (ey > 0.f) {
+            tot.a += ey;
+            tot.u = fmaf(ey, zy - tot.m, tot.u);
+          }
+        }
+        bc[bsel] = row_scalar_phase<ENT>(P, P.row_base + r, meta.y, meta.st, meta.blp, meta.rl,
                                            meta.adv, tot, zy, rank == 0, meta.keep);
         ptx::mbar_arrive_u32(sdb + bsel * 8);
       }
@@ -522,11 +629,12 @@ __global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
                             static_cast<uint32_t>((warp >> 2) * (kPTSlots * 16));
     Ring ring(nslots);
     uint32_t ts = 0;  // TMEM slot of the next pass-1 slot (mod kPTSlots)
-    uint32_t red_peer[CL > 1 ? CL - 1 : 1], p1_peer[CL > 1 ? CL - 1 : 1];
+    uint32_t red_peer[CL > 1 ? CL - 1 : 1], redu_peer[CL > 1 ? CL - 1 : 1], p1_peer[CL > 1 ? CL - 1 : 1];
 #pragma unroll
     for (int c = 1; c < CL; ++c) {  // the other CTAs of the cluster, in rank order after this one
       const uint32_t pr = (rank + static_cast<uint32_t>(c)) % CL;
       red_peer[c - 1] = ptx::mapa(ptx::smem_u32(&red[0][0]), pr);
+      if (ENT) redu_peer[c - 1] = ptx::mapa(ptx::smem_u32(&redu[0][0]), pr);
       p1_peer[c - 1] = ptx::mapa(p1b, pr);
     }
     PhaseTimer tm;    // trace slots: 0 pass 1, 2 broadcast wait, 4 pass 2
@@ -539,9 +647,10 @@ __global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
         const int32_t cnt = min(kPSlotVec, nvec - v0);
         ptx::mbar_wait_sleep(fbase + slot * 8, ring.ph);
         const uint32_t tsl = (ts + static_cast<uint32_t>(sg)) % kPTSlots;
-        const float nml = grad ? p1_slot<true, F32, BST, PW>(a, sbase + slot * kPSlotBytes, v0, cnt, ycol, tid,
-                                                         taddr0 + tsl * 16)
-                               : p1_slot<false, F32, BST, PW>(a, sbase + slot * kPSlotBytes, v0, cnt, ycol, tid, 0u);
+        const float nml = grad ? p1_slot<true, kRaw, BST, PW, ENT>(a, sbase + slot * kPSlotBytes, v0, cnt, ycol,
+                                                                  tid, taddr0 + tsl * 16)
+                               : p1_slot<false, kRaw, BST, PW, ENT>(a, sbase + slot * kPSlotBytes, v0, cnt, ycol,
+                                                                   tid, 0u);
         nml_sh[tsl * kPThreads + tid] = nml;
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive_u32(ebase + slot * 8);
@@ -557,6 +666,13 @@ __global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) sv += __shfl_xor_sync(0xffffffffu, sv, o);
       const Lse st{M, sv * (1.f / 32768.f), 0.f, 0.f};
+      float uv = 0.f;
+      if (ENT) {  // u to the warp frame M: r (u + s (m - M)), 2^15-scaled like s
+        uv = a.m == -INFINITY ? 0.f : ptx::ex2((a.m - M) * kLog2e) * fmaf(a.s, a.m - M, a.u);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) uv += __shfl_xor_sync(0xffffffffu, uv, o);
+        uv *= 1.f / 32768.f;
+      }
       const uint32_t hv = __ballot_sync(0xffffffffu, a.have);
       const float zy = __shfl_sync(0xffffffffu, a.zy, hv ? __ffs(hv) - 1 : 0);
       if (lane == 0) {
@@ -564,10 +680,15 @@ __global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
         const uint32_t off = (bsel * kNE + rank * kPW + warp) * sizeof(PairPart);
         const float hvf = hv ? 1.f : 0.f;
         red[bsel][rank * kPW + warp] = PairPart{st.m, st.s, zy, hvf};
+        if (ENT) redu[bsel][(rank * kPW + warp) % (ENT ? kNE : 1)] = PairPartU{uv, 0.f, 0.f, 0.f};
         ptx::mbar_arrive_u32(p1b + bsel * 8);
 #pragma unroll
-        for (int c = 0; c < CL - 1; ++c)
+        for (int c = 0; c < CL - 1; ++c) {
           st_async_v4(red_peer[c] + off, st.m, st.s, zy, hvf, p1_peer[c] + bsel * 8);
+          if (ENT)
+            st_async_v4(redu_peer[c] + (off / sizeof(PairPart)) * sizeof(PairPartU), uv, 0.f, 0.f, 0.f,
+                        p1_peer[c] + bsel * 8);
+        }
       }
     };
 
@@ -593,13 +714,18 @@ __global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
       tm.mark(2);
       if (grad) {
         const RowBroadcast b = bc[bsel];
-        const bool zero_row = b.coef == 0.f;
+        const bool zero_row = b.coef == 0.f && (!ENT || b.eg == 0.f);
         const int32_t ycol = b.y - col0;
         tmem_wait_st();  // this thread's pass-1 stores of row i have landed
         for (int32_t sg = 0; sg < nseg; ++sg) {
           const uint32_t tsl = (ts_row + static_cast<uint32_t>(sg)) % kPTSlots;
           const int32_t v0 = sg * kPSlotVec;
-          if constexpr (F32) {
+          if constexpr (ENT) {
+            using TO = typename std::conditional<F32, float, __nv_bfloat16>::type;
+            TO* drow = static_cast<TO*>(P.dlogits) + r * P.ld_d + col0;
+            p2_slot_ent<PW, TO>(b, zero_row, taddr0 + tsl * 16, v0, min(kPSlotVec, nvec - v0), ycol,
+                                drow + static_cast<int64_t>(v0) * 8, tid);
+          } else if constexpr (F32) {
             float* drow = static_cast<float*>(P.dlogits) + r * P.ld_d + col0;
             p2_slot_f32<PW>(b, zero_row, taddr0 + tsl * 16, v0, min(kPSlotVec, nvec - v0), ycol,
                         drow + static_cast<int64_t>(v0) * 8, tid);
@@ -641,7 +767,8 @@ __global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
 }  // namespace
 
 bool pair_supported(const LossParams& p, DType in, DType out, bool ent, int cl) {
-  if (in != DType::BF16 || ent) return false;
+  (void)ent;  // entropy: the ENT instantiations (raw staging, u exchanged with the partials)
+  if (in != DType::BF16) return false;
   if (p.dlogits != nullptr && !p.gather_only && out != DType::BF16 && out != DType::F32) return false;
   if (p.vocab % 16 != 0 || (p.ld * 2) % 16 != 0 || reinterpret_cast<uintptr_t>(p.logits) % 16 != 0)
     return false;
@@ -707,10 +834,13 @@ cudaError_t launch_pair_pw(const LossParams& p, DType out, int num_sms, const Tu
   COPRIS_PSHAPE(PW);
   constexpr int cl = CL;
   const bool f32 = out == DType::F32 && p.dlogits != nullptr && !p.gather_only;
-  const bool bst = !f32 && tu.pair_bf16_stage;
+  const bool ent = p.entropy_coeff != 0.0;
+  const bool bst = !f32 && !ent && tu.pair_bf16_stage;
   using Kern = void (*)(const LossParams, const int, const int, const int32_t, const int);
-  const Kern kern = f32 ? fused_pair_kernel<true, CL, false, PW>
-                        : (bst ? fused_pair_kernel<false, CL, true, PW> : fused_pair_kernel<false, CL, false, PW>);
+  // entropy: raw logits staged (pass 2 needs z for the p log p term), f32 or bf16 out
+  const Kern kern = ent ? (f32 ? fused_pair_kernel<true, CL, false, PW, true> : fused_pair_kernel<false, CL, false, PW, true>)
+                  : f32 ? fused_pair_kernel<true, CL, false, PW, false>
+                        : (bst ? fused_pair_kernel<false, CL, true, PW, false> : fused_pair_kernel<false, CL, false, PW, false>);
   // PW 16: 6 x 32 KB ring + 16 KB of per-thread nml fill the 227 KB a CTA may
   // use; PW 8: 6 x 16 KB + 8 KB = 104 KB, two CTAs per SM
   const int nslots = tu.slots > 0 ? (tu.slots > 6 ? 6 : tu.slots) : 6;

@@ -790,7 +790,7 @@ def test_target_at_vector_slot_and_half_boundaries(ctx, oracle, impl, V, force, 
 @pytest.mark.parametrize("mode", ["kl", "is_off", "recorded", "kl_recorded"])
 def test_pair_and_solo_token_math_modes(ctx, oracle, impl, V, kernel, mode):
     """The default kernels at both vocabularies in every token-math mode they
-    take (the entropy term goes to the other kernels): KL against the
+    take: KL against the
     version-0 snapshot's log-probs (grpo.hpp:158-162), IS off (trainer.hpp:149),
     recorded behaviour (concat_segments verbatim), KL with recorded behaviour."""
     impl(None)
@@ -801,3 +801,51 @@ def test_pair_and_solo_token_math_modes(ctx, oracle, impl, V, kernel, mode):
         _, res = run(ctx, case, dl_dtype)
         assert ctx.last_launch()["kernel"] == kernel
         case.check(res, dl_dtype, what=f"{mode} V={V}")
+
+
+@pytest.mark.parametrize("V,kernel,cluster", [(32000, "fused_solo_kernel", 1),
+                                              (80000, "fused_pair_kernel", 2),
+                                              (151936, "fused_pair_kernel", 2),
+                                              (256000, "fused_quad_kernel", 4)])
+def test_entropy_on_pair_family(ctx, oracle, impl, V, kernel, cluster):
+    """The entropy bonus (grpo.hpp:168-181) in the solo / pair / quad kernels:
+    raw logits staged in TMEM, u = sum e (z - m) exchanged with each warp's
+    (m, s) partial, pass 2 through row_grad's p (log p + H) term; with KL on
+    too, bf16 and fp32 dlogits, against the oracle."""
+    impl(None)
+    P, G = (2, 4) if V > 50000 else (4, 4)
+    case = Case(oracle, seed=V % 89 + 7, P=P, G=G, V=V, mu=math.log(12), lmax=24, kl_coeff=0.1,
+                entropy_coeff=0.01)
+    for dl_dtype in (BF16, F32):
+        _, res = run(ctx, case, dl_dtype)
+        info = ctx.last_launch()
+        assert info["kernel"] == kernel and info["cluster"] == cluster, info
+        case.check(res, dl_dtype, what=f"entropy V={V} {dl_dtype}")
+    # forward only (no dlogits): the same objective
+    _, rf = run(ctx, case, BF16, want_grad=False)
+    assert ctx.last_launch()["kernel"] == kernel and rf.dlogits is None
+    assert_loss_close(rf.loss, case.ref.loss, case.ref.obj, case.hb.n_tok, what=f"entropy fwd V={V}")
+
+
+@pytest.mark.parametrize("V,kernel", [(151936, "fused_pair_kernel"), (32000, "fused_solo_kernel")])
+def test_entropy_masked_vocabulary_pair_vs_stream(ctx, oracle, impl, V, kernel):
+    """-inf logits with the entropy term on: the reference's h -= p log p is NaN
+    at p = 0 (grpo.hpp:172), the kernels take the limit 0 there. The pair-family
+    kernel against the streaming kernel (the same limit, its entropy arithmetic
+    pinned to the oracle on finite rows): finite, and equal within fp32 rounding."""
+    case = Case(oracle, seed=43, P=2, G=4, V=V, mu=math.log(10), lmax=24, edit_logits=_mask_vocab,
+                entropy_coeff=0.01)
+    out = {}
+    for force, kern in ((None, kernel), ("stream", "fused_stream_la_kernel")):
+        impl(force)
+        _, res = run(ctx, case, F32)
+        assert ctx.last_launch()["kernel"].startswith(kern)
+        out[kern] = res
+    a, b = out[kernel], out["fused_stream_la_kernel"]
+    for r in (a, b):
+        assert math.isfinite(r.loss) and torch.isfinite(r.dlogits).all() and torch.isfinite(r.obj).all()
+    np.testing.assert_allclose(a.cur_lp.cpu().numpy(), b.cur_lp.cpu().numpy(), rtol=0, atol=2e-5)
+    np.testing.assert_allclose(a.obj.cpu().numpy(), b.obj.cpu().numpy(), rtol=1e-4, atol=1e-6)
+    np.testing.assert_allclose(a.dlogits.cpu().numpy(), b.dlogits.cpu().numpy(), rtol=1e-4, atol=1e-9)
+    inf_cols = torch.isinf(case.logits_gpu().float())
+    assert torch.all(a.dlogits[inf_cols] == 0)
