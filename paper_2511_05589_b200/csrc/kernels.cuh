@@ -77,7 +77,8 @@ struct LossParams {
 
 // Phase accumulators written by the fused kernels when LossParams::trace is
 // set: [cta * kTraceSlots + k], k = pass B, wait A, scalar, wait B, pass C, rows,
-// ring waits (2), lifetime ns, lifetime cycles.
+// ring waits (2), lifetime ns, lifetime cycles (the pair family: slots 6/7 =
+// start globaltimer ns and SM id instead of the ring waits).
 constexpr int kTraceSlots = 10;
 constexpr int kTraceCtas = 2048;
 

@@ -505,6 +505,7 @@ __global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
   __shared__ RowBroadcast bc[2];
   __shared__ uint32_t tmem_slot;
 
+  const unsigned long long t_entry = P.trace ? PhaseTimer::gtimer() : 0ull;  // trace slot 6
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = CL > 1 ? ptx::cluster_ctarank() : 0u;
   const int64_t cid = blockIdx.x / CL, ncl = gridDim.x / CL;
@@ -535,7 +536,10 @@ __global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
     }
     ptx::fence_mbarrier_init();
   }
-  if (warp == 0 && grad) tc::tmem_alloc<kPTmemCols>(ptx::smem_u32(&tmem_slot));
+  if (warp == 0) {
+    if (grad) tc::tmem_alloc<kPTmemCols>(ptx::smem_u32(&tmem_slot));
+    else tc::tmem_relinquish();  // else the next CTA on this SM waits for this one to exit
+  }
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
@@ -637,8 +641,14 @@ __global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
       if (ENT) redu_peer[c - 1] = ptx::mapa(ptx::smem_u32(&redu[0][0]), pr);
       p1_peer[c - 1] = ptx::mapa(p1b, pr);
     }
-    PhaseTimer tm;    // trace slots: 0 pass 1, 2 broadcast wait, 4 pass 2
+    PhaseTimer tm;    // trace slots: 0 pass 1, 2 broadcast wait, 4 pass 2, 6 kernel entry (globaltimer ns), 7 SM id
     tm.start(P.trace && tid == 0 && blockIdx.x < kTraceCtas);
+    if (tm.on) {
+      uint32_t smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      tm.acc[6] = static_cast<long long>(t_entry);
+      tm.acc[7] = smid;
+    }
 
     auto run_p1 = [&](LaneAcc& a, int32_t ycol, int32_t sg0, int32_t sg1) {
       for (int32_t sg = sg0; sg < sg1; ++sg, ring.next()) {

@@ -73,6 +73,14 @@ __device__ __forceinline__ void tmem_alloc(uint32_t slot_smem) {
   asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
 }
 
+// A CTA of a kernel that uses TMEM but allocates none in this launch (gather-only
+// or forward-only): give up the allocation right anyway. Until a CTA has
+// relinquished it, no further CTA of the kernel starts on that SM — measured:
+// the 2-per-SM solo grid ran in two waves without this (scripts/k1_residency.py).
+__device__ __forceinline__ void tmem_relinquish() {
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_dealloc(uint32_t taddr) {
   asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols)
