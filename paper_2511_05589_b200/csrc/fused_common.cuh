@@ -250,6 +250,29 @@ struct MetaPipe {
     }
     return cur;
   }
+  // The same over an explicit row sequence (rows claimed at run time): r0 and r1
+  // are the first two rows, -1 past the end.
+  __device__ __forceinline__ void init_ids(const LossParams& P, int64_t r0, int64_t r1) {
+    if (r0 >= 0) next = load_meta(P, P.row_base + r0);
+    if (!P.gather_only && r1 >= 0) traj_ahead = P.tok_traj[P.row_base + r1];
+  }
+  // Returns the current row's metadata; r1 = the next row, r2 = the one after.
+  __device__ __forceinline__ RowMeta advance_ids(const LossParams& P, int64_t r1, int64_t r2) {
+    const RowMeta cur = next;
+    if (r1 >= 0 && P.gather_only) {
+      next.y = P.target[P.row_base + r1];
+    } else if (r1 >= 0) {
+      const int64_t t1 = P.row_base + r1;
+      next.y = P.target[t1];
+      next.st = P.stage[t1];
+      next.blp = P.buffered_lp[t1];
+      next.rl = P.ref_lp ? P.ref_lp[t1] : 0.f;
+      next.adv = P.adv[traj_ahead];
+      next.keep = P.loss_mask ? P.loss_mask[t1] != 0 : true;
+      if (r2 >= 0) traj_ahead = P.tok_traj[P.row_base + r2];
+    }
+    return cur;
+  }
 };
 
 // dlogits for N consecutive columns starting at column c.

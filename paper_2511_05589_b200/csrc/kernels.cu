@@ -1184,6 +1184,7 @@ const TuneField kFields[] = {
     {"pair_st256", "COPRIS_PAIR_ST256", 0, 1, &Tuning::pair_st256, nullptr},
     {"pair_bf16_stage", "COPRIS_PAIR_BF16_STAGE", 0, 1, &Tuning::pair_bf16_stage, nullptr},
     {"pair_pw8", "COPRIS_PAIR_PW8", 0, 1, &Tuning::pair_pw8, nullptr},
+    {"pair_dynamic", "COPRIS_PAIR_DYNAMIC", 0, 1, &Tuning::pair_dynamic, nullptr},
     {"lmhead_impl", "COPRIS_LMHEAD_IMPL", 0, 1, &Tuning::lmhead_impl, nullptr},
     {"lmhead_group", "COPRIS_LMHEAD_GROUP", 1, 1 << 20, &Tuning::lmhead_group, nullptr},
     {"lmhead_tma_store", "COPRIS_LMHEAD_TMA_STORE", 0, 1, &Tuning::lmhead_tma_store, nullptr},

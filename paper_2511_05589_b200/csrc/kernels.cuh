@@ -98,6 +98,7 @@ struct Tuning {
   int pair_st256 = 0;     // pair kernel, bf16 dlogits: 32-byte stores (lane-pair swap) in pass 2
   int pair_bf16_stage = 1; // pair kernel, bf16 dlogits: bf16 (not f16) exponentials in TMEM, bf16x2 pass 2
   int pair_pw8 = 1;       // pair kernel: 8-warp CTAs, two per SM, when the half row fits (V <= 114,688)
+  int pair_dynamic = 1;   // pair kernels: rows after the first claimed from the context's counter
   int lmhead_impl = 0;    // 0 CTA pair (cta_group::2), 1 single SM
   int lmhead_group = 16;  // LM-head raster group (token pairs per vocab sweep)
   int lmhead_tma_store = 1;

@@ -162,6 +162,13 @@ struct __align__(16) PairPartU {
 };
 
 constexpr float kLn2 = 0.69314718055994531f;
+// Row sequence of a cluster: entry j = the j-th row it processes (-1 past the
+// end), published by rank 0's producer kRowAhead entries ahead of its own use.
+// Every role lags the publisher by a few rows (the ring, the lookahead and the
+// two-row scalar pipeline), far fewer than kRowQ, so an entry is never rewritten
+// while a CTA of the cluster can still wait on its previous phase.
+constexpr int kRowQ = 16;
+constexpr uint32_t kRowAhead = 3;
 // bf16x2 {-9.9e29, -9.9e29}: -inf columns clamped to it stay finite through
 // (z - m) log2(e) (the lowest finite bf16 would overflow to -inf there)
 constexpr uint32_t kClampLo2 = 0xF149F149u;
@@ -493,7 +500,7 @@ __device__ __forceinline__ void p2_slot_ent(const RowBroadcast& b, bool zero_row
 template <bool F32, int CL, bool BST, int PW, bool ENT>
 __global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
     fused_pair_kernel(const LossParams P, const int nslots, const int look, const int32_t nvec0,
-                      const int st256) {
+                      const int st256, const int dyn) {
   COPRIS_PSHAPE(PW);
   static_assert(CL == 1 || CL == 2 || CL == 4, "a row is split over one, two or four CTAs");
   constexpr int kNE = CL * PW;  // warp partials per row (entries of the exchange table)
@@ -504,6 +511,8 @@ __global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
   constexpr bool kRaw = F32 || ENT;             // stage the raw logits for pass 2
   __shared__ RowBroadcast bc[2];
   __shared__ uint32_t tmem_slot;
+  __shared__ __align__(8) uint64_t rqfull[kRowQ];
+  __shared__ __align__(8) int64_t rq[kRowQ];
 
   const unsigned long long t_entry = P.trace ? PhaseTimer::gtimer() : 0ull;  // trace slot 6
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -523,6 +532,14 @@ __global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
   float* nml_sh = reinterpret_cast<float*>(smem + nslots * kPSlotBytes);
   const uint32_t fbase = ptx::smem_u32(full), ebase = ptx::smem_u32(empty);
   const uint32_t p1b = ptx::smem_u32(p1done), sdb = ptx::smem_u32(sdone);
+  const uint32_t rqb = ptx::smem_u32(rqfull), rqa = ptx::smem_u32(rq);
+  // entry j of the row sequence (waits until rank 0 has published it)
+  auto rq_get = [&](uint32_t j) -> int64_t {
+    const uint32_t k = j % kRowQ, par = (j / kRowQ) & 1u;
+    if constexpr (CL > 1) ptx::mbar_wait_acq_cluster(rqb + k * 8, par);
+    else ptx::mbar_wait_u32(rqb + k * 8, par);
+    return *reinterpret_cast<volatile int64_t*>(&rq[k]);
+  };
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < nslots; ++i) {
@@ -534,6 +551,7 @@ __global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
       ptx::mbar_init(&p1done[i], kPW + 1);
       ptx::mbar_init(&sdone[i], 1);
     }
+    for (int i = 0; i < kRowQ; ++i) ptx::mbar_init(&rqfull[i], 1);  // rank 0's producer arrives
     ptx::fence_mbarrier_init();
   }
   if (warp == 0) {
@@ -551,7 +569,40 @@ __global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
     if (lane == 0) {
       const uint64_t pol = ptx::policy_evict_first();  // read once
       Ring ring(nslots);
-      for (int64_t r = cid; r < P.n_rows; r += ncl) {
+      // rank 0: the cluster's first row is cid, every later one is claimed from
+      // the context's counter (rows ncl, ncl + 1, ...): clusters that run faster
+      // take more rows and all finish within about a row of each other (a static
+      // stride ended the slowest CTAs 7% (pair) to 17% (solo) of the launch after
+      // the mean, scripts/cta_tail.py). The last CTA rearms the counter.
+      bool done = false;
+      auto publish = [&](uint32_t j) {
+        int64_t r = -1;
+        if (!done) {
+          r = j == 0 ? cid
+                     : (dyn ? ncl + static_cast<int64_t>(atomicAdd(P.row_ctr, 1ull))
+                            : cid + static_cast<int64_t>(j) * ncl);
+          if (r >= P.n_rows) {
+            done = true;
+            r = -1;
+          }
+        }
+        const uint32_t k = j % kRowQ;
+        if constexpr (CL > 1) {
+#pragma unroll
+          for (uint32_t c = 0; c < static_cast<uint32_t>(CL); ++c) {
+            ptx::st_cluster_b64(ptx::mapa(rqa + k * 8, c), r);
+            ptx::mbar_arrive_remote(ptx::mapa(rqb + k * 8, c));  // releases the store
+          }
+        } else {
+          rq[k] = r;
+          ptx::mbar_arrive_u32(rqb + k * 8);
+        }
+      };
+      if (rank == 0)
+        for (uint32_t j = 0; j < kRowAhead; ++j) publish(j);
+      for (uint32_t j = 0;; ++j) {
+        const int64_t r = rq_get(j);
+        if (r < 0) break;
         const __nv_bfloat16* row = static_cast<const __nv_bfloat16*>(P.logits) + r * P.ld + col0;
         for (int32_t sg = 0; sg < nseg; ++sg, ring.next()) {
           const uint32_t slot = ring.slot;
@@ -562,16 +613,20 @@ __global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
           ptx::bulk_g2s_u32(sbase + slot * kPSlotBytes, row + static_cast<int64_t>(v0) * 8, bytes,
                             fbase + slot * 8, pol);
         }
+        if (rank == 0) publish(j + kRowAhead);
       }
     }
   } else if (warp == kPW + 1) {
     // ---------------- scalar warp: merge the pair's 32 partials, token math ------
     MetaPipe mp;
-    if (lane == 0) mp.init(P, cid, ncl);
+    int64_t r = rq_get(0);
+    int64_t r1 = r >= 0 ? rq_get(1) : -1;
+    if (lane == 0) mp.init_ids(P, r, r1);
     uint32_t i = 0;
-    for (int64_t r = cid; r < P.n_rows; r += ncl, ++i) {
+    for (; r >= 0; ++i) {
+      const int64_t r2 = r1 >= 0 ? rq_get(i + 2) : -1;
       RowMeta meta{};
-      if (lane == 0) meta = mp.advance(P, r, ncl);
+      if (lane == 0) meta = mp.advance_ids(P, r1, r2);
       const uint32_t bsel = i & 1u, par = (i >> 1) & 1u;
       if (lane == 0) {
         if constexpr (CL > 1)
@@ -625,6 +680,8 @@ __global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
         ptx::mbar_arrive_u32(sdb + bsel * 8);
       }
       __syncwarp();
+      r = r1;
+      r1 = r2;
     }
   } else {
     // ---------------- consumers ------------------------------------------------------
@@ -702,16 +759,16 @@ __global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
       }
     };
 
-    int64_t r = cid;
+    int64_t r = rq_get(0);
     uint32_t i = 0;
-    if (r < P.n_rows) {
+    if (r >= 0) {
       LaneAcc a0;
       run_p1(a0, P.target[P.row_base + r] - col0, 0, nseg);
       finish_p1(a0, 0);
     }
-    for (; r < P.n_rows; r += ncl, ++i) {
-      const int64_t rn = r + ncl;
-      const bool nx = rn < P.n_rows;
+    for (; r >= 0; ++i) {
+      const int64_t rn = rq_get(i + 1);
+      const bool nx = rn >= 0;
       const uint32_t ts_row = ts;  // TMEM slots of row i: ts_row .. ts_row + nseg - 1
       LaneAcc an;
       const int32_t ycn = nx ? P.target[P.row_base + rn] - col0 : -1;
@@ -758,6 +815,7 @@ __global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
       }
       tm.mark(0);
       tm.acc[5] += 1;
+      r = rn;
     }
     tm.flush(P.trace);
   }
@@ -770,8 +828,9 @@ __global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
     tc::fence_after_sync();
     tc::tmem_dealloc<kPTmemCols>(tmem_base);
   }
-  // small steps: the last CTA reduces obj/flags into out4 (the ring is free now)
-  if (P.out4) fused_reduce_if_last(P, smem);
+  // the last CTA rearms the row counter and, for small steps, reduces obj/flags
+  // into out4 (the ring is free now)
+  if (P.red_scratch) end_of_launch(P, smem, dyn != 0);
 }
 
 }  // namespace
@@ -846,7 +905,7 @@ cudaError_t launch_pair_pw(const LossParams& p, DType out, int num_sms, const Tu
   const bool f32 = out == DType::F32 && p.dlogits != nullptr && !p.gather_only;
   const bool ent = p.entropy_coeff != 0.0;
   const bool bst = !f32 && !ent && tu.pair_bf16_stage;
-  using Kern = void (*)(const LossParams, const int, const int, const int32_t, const int);
+  using Kern = void (*)(const LossParams, const int, const int, const int32_t, const int, const int);
   // entropy: raw logits staged (pass 2 needs z for the p log p term), f32 or bf16 out
   const Kern kern = ent ? (f32 ? fused_pair_kernel<true, CL, false, PW, true> : fused_pair_kernel<false, CL, false, PW, true>)
                   : f32 ? fused_pair_kernel<true, CL, false, PW, false>
@@ -914,7 +973,9 @@ cudaError_t launch_pair_pw(const LossParams& p, DType out, int num_sms, const Tu
     info->kernel = cl == 4 ? "fused_quad_kernel" : cl == 2 ? "fused_pair_kernel" : "fused_solo_kernel";
     info->reduced = fuse ? 1 : 0;
   }
-  return cudaLaunchKernelEx(&cfg, kern, q, nslots, look, nvec0, tu.pair_st256);
+  // claimed rows need the counter and the ticket that lets the last CTA rearm it
+  const int dyn = tu.pair_dynamic && p.row_ctr && p.red_scratch ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, q, nslots, look, nvec0, tu.pair_st256, dyn);
 }
 }  // namespace
 
