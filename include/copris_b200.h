@@ -82,7 +82,7 @@ COPRIS_API int copris_ctx_destroy(copris_ctx* ctx);
  * launches never read the environment again. Change an option between
  * launches (not concurrently with a launch on the same context). Names:
  * fused_impl (0 auto, 1 stream, 2 tma, 3 pair, 4 solo), lookahead, slots, resident,
- * pair_lookahead, pair_st256, pair_bf16_stage, pair_pw8, lmhead_impl (0 pair, 1 single SM), lmhead_group, lmhead_tma_store,
+ * pair_lookahead, pair_st256, pair_bf16_stage, pair_pw8, pair_dynamic, lmhead_impl (0 pair, 1 single SM), lmhead_group, lmhead_tma_store,
  * gemm_wide, gemm_mc, gemm_splits, gemm_a_evict_first, dw_group, dw_policy,
  * dw_kchunk, trace. COPRIS_E_INVALID for an unknown name or out-of-range value. */
 COPRIS_API int copris_ctx_set_option(copris_ctx* ctx, const char* name, int64_t value);

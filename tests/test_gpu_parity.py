@@ -624,30 +624,45 @@ def test_fused_reduction_bitwise(ctx, oracle, impl, n_tok, masked, force, V, ker
         assert_loss_close(-fused4[0].item() / T, case.ref.loss, case.ref.obj, T, what="fused out4")
 
 
-def test_claim_counter_rearmed_across_launch_kinds(ctx, oracle, impl):
-    """The TMA kernel claims rows from a per-context counter that the launch's
-    last CTA rearms (no memset node). K1 (gather-only) and loss launches of
-    more rows than resident CTAs, interleaved, must each give bitwise what a
-    fresh context gives."""
+@pytest.mark.parametrize("V,force,kernel", [(32000, "tma", "fused_tma_kernel"),
+                                            (32000, None, "fused_solo_kernel"),
+                                            (80000, None, "fused_pair_kernel"),
+                                            (151936, None, "fused_pair_kernel"),
+                                            (256000, None, "fused_quad_kernel")])
+def test_claim_counter_rearmed_across_launch_kinds(ctx, oracle, impl, V, force, kernel):
+    """Rows after each CTA's (cluster's) first are CLAIMED from a per-context
+    counter that the launch's last CTA rearms (no memset node): the TMA kernel
+    and the pair family (solo / pair / quad, whose rank-0 producer publishes the
+    cluster's row sequence through DSMEM). K1 (gather-only) and loss launches of
+    more rows than resident CTAs, interleaved with the other kernel kind on the
+    same context, must each give bitwise what a fresh context with the static
+    row stride (pair_dynamic = 0) gives."""
     from paper_2511_05589_b200 import Copris
-    impl("tma")
-    case = Case(oracle, seed=41, P=2, G=8, V=32000, fixed_len=256)   # 4,096 rows > 444 CTAs
+    impl(force)
+    P, G, L = (2, 8, 256) if V <= 32000 else (2, 4, 256)   # 4,096 / 2,048 rows > resident CTAs
+    case = Case(oracle, seed=41, P=P, G=G, V=V, fixed_len=L)
     logits = case.logits_gpu()
     tgt = torch.from_numpy(case.hb.target).cuda()
     fresh = Copris(0)
-    fresh.set_option("fused_impl", "tma")
+    if force:
+        fresh.set_option("fused_impl", force)
+    fresh.set_option("pair_dynamic", 0)
     lp0, _ = fresh.sequence_logprobs(logits, tgt)
     _, r0 = run(fresh, case, BF16)
+    other = "solo" if force == "tma" else "tma"
     for _ in range(3):
         lp, _ = ctx.sequence_logprobs(logits, tgt)
         _, r = run(ctx, case, BF16)
-        assert ctx.last_launch()["kernel"] == "fused_tma_kernel"
+        assert ctx.last_launch()["kernel"] == kernel
         assert torch.equal(lp, lp0)
         assert torch.equal(r.cur_lp, r0.cur_lp) and torch.equal(r.flags, r0.flags)
         assert torch.equal(r.dlogits.view(torch.int16), r0.dlogits.view(torch.int16))
         assert r.loss == r0.loss
-    case.check(r0, BF16, what="claim counter")
-
+        # the other kind on the same counter in between
+        ctx.set_option("fused_impl", other)
+        run(ctx, case, BF16)
+        ctx.set_option("fused_impl", force or "auto")
+    case.check(r0, BF16, what=f"claim counter V={V}")
 
 
 def _mask_vocab(logits, hb):
