@@ -160,6 +160,32 @@ def traffic_per_row(config, unfused, kernel, dlogits="bf16"):
 # ---------------------------------------------------------------------------
 # CPU: the reference's own path (oracle/_ref) on the host cores
 # ---------------------------------------------------------------------------
+def pcie_probe(h_src, h_dst, d_dst, d_src, reps=3):
+    """Pinned host<->device copy rates on this box (GB/s): H2D alone, D2H alone,
+    and both at once on two streams (the e2e pipeline's situation). Wall clock
+    around synchronised copies of ~GBs, so launch overhead is negligible."""
+    n = min(h_src.shape[0], h_dst.shape[0], d_dst.shape[0], d_src.shape[0])
+    nb = n * h_src.shape[1] * h_src.element_size()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def timed(h2d, d2h):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            if h2d:
+                with torch.cuda.stream(s1):
+                    d_dst[:n].copy_(h_src[:n], non_blocking=True)
+            if d2h:
+                with torch.cuda.stream(s2):
+                    h_dst[:n].copy_(d_src[:n], non_blocking=True)
+        torch.cuda.synchronize()
+        return reps * nb / (time.perf_counter() - t0) / 1e9
+
+    timed(True, True)
+    return {"h2d_gbs": timed(True, False), "d2h_gbs": timed(False, True),
+            "duplex_gbs_each_way": timed(True, True), "bytes_per_copy": nb}
+
+
 def cpu_reference(V, tokens_per_thread, seconds, seed, threads=None, min_rounds=1, max_rounds=None):
     """Times the UNMODIFIED reference hot path (sequence_logprobs ->
     concat_segments -> grpo_step_loss, compiled from /root/reference) with one
@@ -515,6 +541,11 @@ def run_ours(args):
                            "bound": (f"PCIe: host bf16 logits in and host dlogits out, {2 * V} B per token "
                                      f"each way; the per-token cost does not depend on the sample size, "
                                      f"so the sample's tok/s is the config's")}
+            if world == 1 and args.dlogits == "bf16":
+                pc = pcie_probe(h_logits, h_dl, dl, logits)
+                e2e_gbs = Ts_all / el * 2 * V / 1e9
+                line["e2e"]["pcie"] = {**pc, "e2e_gbs_each_way": e2e_gbs,
+                                       "frac_of_duplex": e2e_gbs / pc["duplex_gbs_each_way"]}
         ws.close()
         del h_logits, h_dl
 
