@@ -164,6 +164,7 @@ def pcie_probe(h_src, h_dst, d_dst, d_src, reps=3):
     """Pinned host<->device copy rates on this box (GB/s): H2D alone, D2H alone,
     and both at once on two streams (the e2e pipeline's situation). Wall clock
     around synchronised copies of ~GBs, so launch overhead is negligible."""
+    import torch
     n = min(h_src.shape[0], h_dst.shape[0], d_dst.shape[0], d_src.shape[0])
     nb = n * h_src.shape[1] * h_src.element_size()
     s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
