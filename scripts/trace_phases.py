@@ -39,7 +39,7 @@ print(f"V={V} rows={T} kernel={info} {ms:.3f} ms, {T * (4*V+16) / ms / 1e6:.0f} 
 for name, v in zip(["passB", "waitA", "scalar", "waitB", "passC"], per):
     print(f"  {name:8s} {v:9.0f} cycles/row ({100*v/per.sum():.1f}%)")
 print(f"  total    {per.sum():9.0f} cycles/row; CTAs traced {len(a)}")
-if not info["kernel"].startswith("fused_tma_kernel"):
+if info["kernel"].startswith("fused_stream"):  # the pair family keeps entry time / SM id in slots 6/7
     print(f"  of which waiting for ring data: passB {waits[0]:.0f}, passC {waits[1]:.0f} cycles/row")
 life_ns, life_cyc = a[:, 8], a[:, 9]
 print(f"  CTA lifetime: {life_cyc.mean():.0f} cycles, {life_ns.mean() / 1e3:.1f} us "
