@@ -92,7 +92,7 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
+@pytest.mark.parametrize("world", [2, 4])
 def test_sharded_scalar_allreduce_gloo(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
