@@ -429,6 +429,20 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     clocks = sampler.stop()
+    if world > 1:
+        # every rank sampled its own GPU over the same timed region: rank 0
+        # reports all of them (reasons are the union; sm_mhz the lowest rank's
+        # median, the clock the max-over-ranks time was set by)
+        per_rank = [None] * world
+        dist.all_gather_object(per_rank, clocks)
+        ok = [c for c in per_rank if c and c.get("sm_mhz") is not None]
+        if ok:
+            clocks = dict(min(ok, key=lambda c: c["sm_mhz"]))
+            clocks["reasons"] = sorted({x for c in ok for x in c["reasons"]})
+            clocks["per_rank"] = [{k: c.get(k) for k in ("sm_mhz", "reasons", "power_w", "samples")}
+                                  if c else None for c in per_rank]
+            clocks["busy_gpus"] = sum(1 for c in ok if (c.get("under_load") or {}).get("samples", 0) > 0
+                                      or (c.get("power_w") or 0.0) >= ClockSampler.LOAD_W)
     ctx.check()
     ms = e0.elapsed_time(e1) / args.steps
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
