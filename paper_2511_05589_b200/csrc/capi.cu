@@ -148,7 +148,8 @@ int copris_ctx_create(int device, copris_ctx** out) {
   if (e == cudaSuccess) e = cudaMemset(ctx->d_err, 0, sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMalloc(&ctx->d_rowctr, sizeof(unsigned long long));
   // the claim counter starts at 0; every launch that claims rows leaves it at 0
-  // again (its last CTA resets it, reduce.cuh end_of_launch)
+  // again (the TMA kernel's last CTA resets it, reduce.cuh end_of_launch; in
+  // the pair family the last cluster whose row claim comes back empty)
   if (e == cudaSuccess) e = cudaMemset(ctx->d_rowctr, 0, sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMalloc(&ctx->d_scratch, reduce_scratch_bytes());
   if (e == cudaSuccess) e = cudaMemset(ctx->d_scratch, 0, reduce_scratch_bytes());

@@ -45,8 +45,11 @@
 // consumer warps and 16 KB slots (PShape<8>: 104 KB of shared memory, 256
 // TMEM columns), so two CTAs share an SM and overlap each other's phases.
 //
-// Small steps (<= 8,192 tokens) reduce obj/flags into out4 in the launch's
-// last CTA (reduce.cuh), bitwise what reduce_kernel produces.
+// Small steps (<= 8,192 tokens) reduce obj/flags into out4 in the CTA whose
+// scalar warp finishes the launch's scalar phases last (a per-launch count off
+// the consumers' path), with its consumer warps once their own dlogits are out
+// (reduce.cuh), bitwise what reduce_kernel produces. Nothing global runs on the
+// CTAs' exit path: the row counter is rearmed by the last failing claim.
 //
 // Reference semantics: policy.hpp:110-121,160-173 (log-softmax, gather),
 // grpo.hpp:117-185 + policy.hpp:180-196 (objective and dlogits) via
@@ -511,6 +514,7 @@ __global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
   constexpr bool kRaw = F32 || ENT;             // stage the raw logits for pass 2
   __shared__ RowBroadcast bc[2];
   __shared__ uint32_t tmem_slot;
+  __shared__ bool red_mine;  // small step: this CTA reduces obj/flags into out4
   __shared__ __align__(8) uint64_t rqfull[kRowQ];
   __shared__ __align__(8) int64_t rq[kRowQ];
 
@@ -573,7 +577,7 @@ __global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
       // the context's counter (rows ncl, ncl + 1, ...): clusters that run faster
       // take more rows and all finish within about a row of each other (a static
       // stride ended the slowest CTAs 7% (pair) to 17% (solo) of the launch after
-      // the mean, scripts/cta_tail.py). The last CTA rearms the counter.
+      // the mean, scripts/cta_tail.py). The last failing claim rearms the counter.
       bool done = false;
       auto publish = [&](uint32_t j) {
         int64_t r = -1;
@@ -584,6 +588,18 @@ __global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
           if (r >= P.n_rows) {
             done = true;
             r = -1;
+            // every cluster makes exactly one failing claim (its first row is
+            // cid < n_rows); the last of them rearms the counter for the next
+            // launch or graph replay — no ticket on the CTAs' exit path
+            if (dyn && j > 0) {
+              auto* sc = static_cast<ReduceScratch*>(P.red_scratch);
+              __threadfence();  // this claim before the count
+              if (atomicAdd(&sc->claims_failed, 1u) == static_cast<unsigned>(ncl - 1)) {
+                __threadfence();
+                *P.row_ctr = 0ull;
+                sc->claims_failed = 0u;
+              }
+            }
           }
         }
         const uint32_t k = j % kRowQ;
@@ -683,6 +699,24 @@ __global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
       r = r1;
       r1 = r2;
     }
+    // small step: this CTA's rows have all written obj/flags (rank 0 writes
+    // them); the CTA whose count completes the launch reduces, with its consumer
+    // warps once their last dlogits are out — the count is off their path and
+    // the other CTAs may still be writing dlogits
+    if (P.out4 && lane == 0) {
+      bool last = false;
+      if (rank == 0) {
+        __threadfence();  // release this CTA's obj/flags
+        auto* sc = static_cast<ReduceScratch*>(P.red_scratch);
+        last = atomicAdd(&sc->rows_done, 1u) == static_cast<unsigned>(ncl - 1);
+        if (last) {
+          __threadfence();  // acquire: every CTA's obj/flags
+          sc->rows_done = 0u;
+        }
+      }
+      red_mine = last;
+    }
+    if (P.out4) ptx::named_bar_sync(2, (kPW + 1) * 32);  // the consumers read red_mine
   } else {
     // ---------------- consumers ------------------------------------------------------
     const int tid = threadIdx.x;
@@ -818,6 +852,18 @@ __global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
       r = rn;
     }
     tm.flush(P.trace);
+    if (P.out4) {
+      // the scalar warp has counted this CTA; the ring is idle (every slot it
+      // was filled for has been through pass 1)
+      ptx::named_bar_sync(2, (kPW + 1) * 32);
+      if (red_mine && tid < kReduceThreads) {
+        ReduceSmem& rsm = *reinterpret_cast<ReduceSmem*>(smem);
+        if ((reinterpret_cast<uintptr_t>(P.obj) % 16 == 0) && (reinterpret_cast<uintptr_t>(P.flags) % 4 == 0))
+          reduce_all_in_cta<true>(P.obj, P.flags, P.red_n, P.out4, rsm, tid);
+        else
+          reduce_all_in_cta<false>(P.obj, P.flags, P.red_n, P.out4, rsm, tid);
+      }
+    }
   }
   // no CTA may exit (or free TMEM) while its peer can still address its shared
   // memory or a thread of its own still reads TMEM
@@ -828,9 +874,9 @@ __global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
     tc::fence_after_sync();
     tc::tmem_dealloc<kPTmemCols>(tmem_base);
   }
-  // the last CTA rearms the row counter and, for small steps, reduces obj/flags
-  // into out4 (the ring is free now)
-  if (P.red_scratch) end_of_launch(P, smem, dyn != 0);
+  // (the row counter was rearmed by the last failing claim, the small-step
+  // reduction done by the scalar warp of the last scalar phase: nothing global
+  // on the exit path)
 }
 
 }  // namespace

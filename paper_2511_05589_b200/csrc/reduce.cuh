@@ -1,7 +1,8 @@
 // reduce.cuh — deterministic reduction of the per-token loss outputs (obj,
 // flags) into out4 = {objective, tokens, stale, clipped}, shared by
-// reduce_kernel and the last CTA of every fused loss launch (kernels.cu,
-// pair.cu). Reference: grpo.hpp:113-115,183 (one ordered fp64 accumulation);
+// reduce_kernel and one CTA of every small fused loss launch (kernels.cu: the
+// last CTA to exit; pair.cu: the CTA whose scalar warp completes the launch's
+// scalar phases). Reference: grpo.hpp:113-115,183 (one ordered fp64 accumulation);
 // here a fixed tile partition and fixed-order trees, so reruns and chunkings
 // are bitwise identical and no floating-point atomics are used.
 #pragma once
@@ -34,6 +35,8 @@ struct ReduceScratch {
   unsigned long long clipped[kReduceMaxTiles];
   unsigned int ticket;        // reduce_kernel blocks done
   unsigned int fused_ticket;  // fused-launch CTAs done
+  unsigned int rows_done;     // pair family: clusters whose rows have all written obj/flags
+  unsigned int claims_failed; // pair family: clusters whose row claim has come back empty
 };
 
 __host__ __device__ inline int64_t reduce_tile(int64_t n) {
