@@ -614,8 +614,10 @@ __global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
           ptx::mbar_arrive_u32(rqb + k * 8);
         }
       };
-      if (rank == 0)
-        for (uint32_t j = 0; j < kRowAhead; ++j) publish(j);
+      // row 0 (the cluster index, no claim) goes out first; the claims for rows
+      // 1 .. kRowAhead (global atomics, ~1 us each at launch) are made once row
+      // 0's loads are in flight, so they are not on the first row's path
+      if (rank == 0) publish(0);
       for (uint32_t j = 0;; ++j) {
         const int64_t r = rq_get(j);
         if (r < 0) break;
@@ -629,7 +631,11 @@ __global__ void __launch_bounds__((PW + 2) * 32, 16 / PW)
           ptx::bulk_g2s_u32(sbase + slot * kPSlotBytes, row + static_cast<int64_t>(v0) * 8, bytes,
                             fbase + slot * 8, pol);
         }
-        if (rank == 0) publish(j + kRowAhead);
+        if (rank == 0) {
+          if (j == 0)
+            for (uint32_t k = 1; k < kRowAhead; ++k) publish(k);
+          publish(j + kRowAhead);
+        }
       }
     }
   } else if (warp == kPW + 1) {
