@@ -444,9 +444,12 @@ __device__ __forceinline__ void p2_slot_ent(const RowBroadcast& b, bool zero_row
   // d_k = p_k (eg (x_k + k0) - coef), x = z - m, p = 2^(x log2(e) - log2 S):
   // row_grad's arithmetic, two columns per packed op; -inf columns clamped
   // (kClampLo2) give p = 0 and d = 0 (row_grad's p > 0 guard)
-  const uint64_t nm2 = ptx::f2(-b.m, -b.m), l2e = ptx::f2(kLog2e, kLog2e);
-  const uint64_t nls2 = ptx::f2(-b.log2s, -b.log2s), eg2 = ptx::f2(b.eg, b.eg);
-  const float c0 = fmaf(b.eg, b.k0, -b.coef);
+  // folded: 2^(z log2(e) + A) with A = -m log2(e) - log2 S, and eg z + C with
+  // C = eg (k0 - m) - coef — no separate x = z - m per column
+  const uint64_t l2e = ptx::f2(kLog2e, kLog2e), eg2 = ptx::f2(b.eg, b.eg);
+  const float A = fmaf(-b.m, kLog2e, -b.log2s);
+  const uint64_t A2 = ptx::f2(A, A);
+  const float c0 = fmaf(b.eg, b.k0 - b.m, -b.coef);
   const uint64_t c02 = ptx::f2(c0, c0);
   const int32_t rel = ycol - v0 * 8;
   const bool own_y = static_cast<uint32_t>(rel) < static_cast<uint32_t>(cnt * 8) &&
@@ -458,9 +461,9 @@ __device__ __forceinline__ void p2_slot_ent(const RowBroadcast& b, bool zero_row
       if (!zero_row) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          const uint64_t x = ptx::fadd2(ptx::bf16x2_to_f2(ptx::bmax2(h[q * 4 + k], kClampLo2)), nm2);
-          const uint64_t pk = ptx::ex2x2(ptx::ffma2(x, l2e, nls2));
-          d2[k] = ptx::fmul2(pk, ptx::ffma2(eg2, x, c02));
+          const uint64_t z = ptx::bf16x2_to_f2(ptx::bmax2(h[q * 4 + k], kClampLo2));
+          const uint64_t pk = ptx::ex2x2(ptx::ffma2(z, l2e, A2));
+          d2[k] = ptx::fmul2(pk, ptx::ffma2(eg2, z, c02));
         }
         // the target column: coef (1 - p_y) + the entropy term (row_grad)
         if (own_y && (rel >> 3) == tid + q * kPThreads) {
